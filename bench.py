@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""bench.py — LLM-Pilot GPU-recommendation hot path on B200 (arxiv 2410.02425).
+
+Metric (BASELINE.json): GBDT train row-iters/s (+ predict rows/s), 1/2/4/8 B200, % of HBM peak.
+
+One STEP = one pass of the whole hot path over the resident synthetic batch:
+  llmpilot_fit      Eq. (4) weights, quantile cuts, bin codes, 2 targets x 500 trees x depth 8
+                    (root histogram, partitions, smaller-child histograms, split scans, updates)
+  llmpilot_recommend  assemble [unseen-LLM | profile | users] rows, predict both targets,
+                    Eq. (1)-(3) cheapest-feasible argmin per LLM.
+Workload: C3 shape per GPU — 10,000,000 rows = 78,125 LLMs x 8 GPU profiles x 16 user levels,
+32 features, 256 bins — weak-scaled over N ranks (C4 family: N x 78,125 LLMs, contiguous row
+shards, NCCL histogram all-reduce per level).  value = row-iters (2 targets x global rows x trees
+x steps) / max-over-ranks device time of the K timed steps.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+Under torchrun each rank drives one GPU; rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+L1, L2, U = 100.0, 50.0, 200
+LLMS_PER_GPU = 78125                  # C3: 78,125 x 8 x 16 = 10,000,000 rows per GPU
+SWEEP_LLMS_PER_GPU = 6554             # C5-sized unseen-LLM batch per GPU
+METRIC = "GBDT train row-iters/s & predict rows/s, 1/2/4/8 B200, % HBM peak"
+UNIT = "row-iters/s"
+
+# algorithmic bytes per unit: unit = one row processed by that kernel
+BYTES_PER_UNIT = {
+    "hist_root": 48.0,    # 32 B code row + y, w, p (12 B) read + 4 B packed gradient pair written
+    "hist_level": 40.0,   # 32 B code row (gathered by row index) + 8 B (row index, gradient pair)
+    "partition": 17.0,    # 8 B state read + 1 B split-feature code + 8 B state written
+    "update": 48.0,       # 32 B code row + y, w, p read (12 B) + p written (4 B)
+    "codes": 160.0,       # 32 f32 features read (128 B) + 32 B row-major + 32 B column-major codes... (see DESIGN)
+}
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--trees", type=int, default=500)
+    ap.add_argument("--depth", type=int, default=8)
+    ap.add_argument("--llms-per-gpu", type=int, default=LLMS_PER_GPU)
+    ap.add_argument("--sweep-llms", type=int, default=SWEEP_LLMS_PER_GPU)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-rows", type=int, default=2_000_000, help="oracle sample rows (cpu_baseline)")
+    ap.add_argument("--ref-rows", type=int, default=1_000_000, help="oracle sample rows per reference step")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the profiled kernels (profiles/ncu_traffic.json, from ncu --set full)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+# ------------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        if self.proc is None:
+            return out
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx.append(float(parts[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        os.unlink(self.path)
+        if sm:
+            out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                   "samples": len(sm)}
+        return out
+
+
+# ---------------------------------------------------------------------------------- reference
+def run_reference(args, rank, world):
+    """The reference arm for this tier is the CPU oracle, as it stands, on a bounded sample."""
+    if rank != 0:
+        return 0
+    import oracle
+    import synth
+    n_llm = max(1, args.ref_rows // 128)
+    d = synth.make_scaled(n_llm)
+    hp = oracle.hparams(n_trees=args.trees, max_depth=args.depth)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.fit(d.X, d.y, hp, d.users_col, d.llm_id, d.prof_id, d.n_llm, d.n_prof, L1, L2, n_trees_limit=1)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    total = sum(times)
+    row_iters = 2.0 * d.n * 1 * len(times)
+    value = row_iters / total
+    sample = ("oracle fit of the first tree of each target (depth %d, 256 bins) on the first %d rows "
+              "(%d LLMs x 8 profiles x 16 levels) of the C3 workload, incl. its binning" % (args.depth, d.n, n_llm))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/i64",
+        "data": "synthetic (seeded, synth/)",
+        "config": {"workload": "C3 scaled synthetic fit (oracle sample)", "rows": d.n, "features": 32,
+                   "bins": 256, "trees_timed": 1, "depth": args.depth, "targets": 2},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------- ours
+def main():
+    args = parse()
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local_rank = _env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2410_02425_b200 as lp
+    import synth
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    uid = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        t = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            t.copy_(torch.frombuffer(bytearray(lp.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(t, 0)
+        uid = bytes(t.cpu().numpy().tobytes())
+
+    # ---- synthetic inputs (seeded), resident in HBM before the timed region
+    n_llm_total = args.llms_per_gpu * world
+    d = synth.make_scaled(n_llm_total, rank, world)
+    lf, pf, cost, levels = synth.sweep_tables(n_llm=args.sweep_llms, seed=1, profiles=synth.PROFILES_C3,
+                                              params_lo=1.0, params_hi=16.0, first_id=rank * args.sweep_llms)
+    stream = torch.cuda.current_stream()
+    Xd = torch.from_numpy(d.X).to(dev)
+    yd = torch.from_numpy(d.y).to(dev)
+    ld = torch.from_numpy(d.llm_id).to(dev)
+    pd = torch.from_numpy(d.prof_id).to(dev)
+    lfd = torch.from_numpy(lf).to(dev)
+    pfd = torch.from_numpy(pf).to(dev)
+    torch.cuda.synchronize()
+    ctx = lp.Context(local_rank, stream, uid, rank, world)
+    hp = lp.hparams(n_trees=args.trees, max_depth=args.depth, max_bin=256)
+    n_global = d.n_global
+    sweep_rows = lf.shape[0] * pf.shape[0] * len(levels)
+
+    ev = []
+
+    def step(X, y, li, pi, lfx, pfx, record=None):
+        if record is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e2 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        m = lp.fit(ctx, X, y, hp, d.users_col, li, pi, d.n_llm, d.n_prof, L1, L2, row_offset=d.row_offset,
+                   n_global=n_global)
+        if record is not None:
+            e1.record(stream)
+        recs = lp.recommend(ctx, m, lfx, pfx, cost, levels, L1, L2, U)
+        if record is not None:
+            e2.record(stream)
+            record.append((e0, e1, e2))
+        m.free()
+        return recs
+
+    for _ in range(args.warmup):
+        step(Xd, yd, ld, pd, lfd, pfd)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, device-resident inputs, CUDA events on the context stream
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctx.reset_stats()
+    ctx.set_timing(True)
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for _ in range(args.steps):
+        step(Xd, yd, ld, pd, lfd, pfd, record=ev)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    stats = ctx.stats()
+    ctx.set_timing(False)
+    clk = clocks.stop()
+    fit_ms = sum(a.elapsed_time(b) for a, b, c in ev)
+    pred_ms = sum(b.elapsed_time(c) for a, b, c in ev)
+    agg = torch.tensor([elapsed_ms, fit_ms, pred_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(agg, op=dist.ReduceOp.MAX)
+    elapsed_ms, fit_ms, pred_ms = agg.tolist()
+
+    row_iters = 2.0 * n_global * args.trees * args.steps
+    value = row_iters / (elapsed_ms / 1000.0)
+    predict_rows = float(sweep_rows) * world * args.steps
+
+    # ---- per-kernel roofline from the live event timings
+    peak, peak_src = measured_peaks()
+    traffic = ncu_traffic()
+    kernels = {}
+    for name, c in stats["classes"].items():
+        if c["ms"] <= 0:
+            continue
+        k = {"launches": c["launches"], "ms_total": round(c["ms"], 3), "ms_avg": c["ms"] / c["launches"],
+             "share_of_step": c["ms"] / elapsed_ms}
+        if name in BYTES_PER_UNIT and c["rows"] > 0:
+            gbs = BYTES_PER_UNIT[name] * c["rows"] / (c["ms"] / 1000.0) / 1e9
+            k.update({"units": c["rows"], "bytes_per_unit": BYTES_PER_UNIT[name], "achieved_gbs": gbs,
+                      "frac_hbm": gbs / peak})
+        kernels[name] = k
+    dom = max((n for n in kernels if n in BYTES_PER_UNIT and "achieved_gbs" in kernels[n]),
+              key=lambda n: kernels[n]["ms_total"], default=None)
+    roofline = None
+    if dom:
+        kd = kernels[dom]
+        tr = traffic.get(dom)
+        roofline = {"kernel": dom, "bound": "hbm", "achieved": kd["achieved_gbs"], "peak": peak, "unit": "GB/s",
+                    "frac": kd["achieved_gbs"] / peak, "peak_source": peak_src,
+                    "bytes_per_unit": kd["bytes_per_unit"], "units_per_launch": kd["units"] / kd["launches"],
+                    "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+                    "traffic_note": tr.get("note") if tr else "no ncu capture committed"}
+
+    # ---- end to end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.from_numpy(d.X).pin_memory()
+        yh = torch.from_numpy(d.y).pin_memory()
+        lh = torch.from_numpy(d.llm_id).pin_memory()
+        ph = torch.from_numpy(d.prof_id).pin_memory()
+        lfh = torch.from_numpy(lf).pin_memory()
+        pfh = torch.from_numpy(pf).pin_memory()
+        step(Xh, yh, lh, ph, lfh, pfh)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step(Xh, yh, lh, ph, lfh, pfh)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        nn = (1 << (args.depth + 1)) - 1
+        h2d = d.X.nbytes + d.y.nbytes + d.llm_id.nbytes + d.prof_id.nbytes + lf.nbytes + pf.nbytes
+        d2h = 2 * args.trees * nn * 16 + 8 + lf.shape[0] * 24
+        e2e = {"value": row_iters / (e2e_ms.item() / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms.item() / args.steps}
+
+    # ---- CPU baseline: the oracle as it stands, rank 0, N = 1, bounded sample
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        nl = max(1, args.cpu_rows // 128)
+        ds = synth.make_scaled(nl)
+        ohp = oracle.hparams(n_trees=args.trees, max_depth=args.depth)
+        t0 = time.perf_counter()
+        oracle.fit(ds.X, ds.y, ohp, ds.users_col, ds.llm_id, ds.prof_id, ds.n_llm, ds.n_prof, L1, L2,
+                   n_trees_limit=1)
+        dt = time.perf_counter() - t0
+        cpu = {"value": 2.0 * ds.n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": "first tree of each target (depth %d) on the first %d rows of this workload, single-threaded "
+                         "C oracle incl. its binning; %.1f s" % (args.depth, ds.n, dt)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u8/i64",
+            "data": "synthetic (seeded counter-based generator, synth/; shapes of the paper's dataset)",
+            "config": {"workload": "C3 per GPU (C4 family when N > 1): %d rows/GPU = %d LLMs x 8 profiles x 16 user "
+                                   "levels, 32 features, 256 bins, 2 targets x %d trees, depth %d; recommend sweep %d "
+                                   "unseen LLMs/GPU" % (d.n, args.llms_per_gpu, args.trees, args.depth,
+                                                        args.sweep_llms),
+                       "rows_global": n_global, "rows_per_gpu": d.n, "features": 32, "bins": 256,
+                       "trees": args.trees, "depth": args.depth, "targets": 2,
+                       "sweep_rows_per_gpu": sweep_rows, "global_batch": n_global,
+                       "parallelism": "row-sharded dp%d, NCCL int64 histogram all-reduce" % world,
+                       "l2": "inputs larger than L2 (codes %d MB + state per GPU), no flush" % (d.n * 32 // 2 ** 20)},
+            "predict": {"value": predict_rows / (pred_ms / 1000.0), "unit": "rows/s", "rows_per_step": sweep_rows * world,
+                        "ms_per_step": pred_ms / args.steps},
+            "fit": {"value": row_iters / (fit_ms / 1000.0), "unit": UNIT, "ms_per_step": fit_ms / args.steps},
+            "roofline": roofline,
+            "kernels": kernels,
+            "gpu_launches": stats["total_launches"],
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

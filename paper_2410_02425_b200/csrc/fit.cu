@@ -1,0 +1,1154 @@
+// fit.cu — LLM-Pilot performance-model training on B200 (§IV-B).
+//
+// Two gradient-boosted regression-tree ensembles (nTTFT, ITL) with Eq. (4) sample weights and
+// a monotone constraint on users, grown level-wise with quantised integer gradients so every
+// histogram is an exact, order-free integer sum:
+//
+//   per tree t:   k_hist<ROOT>   root histogram over all rows (identity order), fused with the
+//                                gradient computation + quantisation (writes gp_root)
+//                 k_split(0)
+//                 for d = 1..D-1:
+//                   k_partition(d)  stable partition of the split parents' rows into children
+//                                   (decoupled look-back over tiles), zeroes the child hists
+//                   k_hist<LEVEL>   histogram of the smaller child of each split parent
+//                   k_split(d)      sibling = parent - built; prefix scan; fp64 gains; argmax
+//                 k_update(t)    route every row to its leaf, p += v, next tree's max|g|
+//
+// No host synchronisation happens inside the tree loop; all decisions live on the device.
+#include <float.h>
+#include <math.h>
+
+#include <algorithm>
+
+#include "internal.cuh"
+
+namespace llmp {
+
+// ---------------------------------------------------------------------------------------------
+constexpr int HIST_THREADS = 512;
+constexpr int HIST_WARPS = HIST_THREADS / 32;
+constexpr int HIST_CHUNK = 65536;          // rows per CTA between flushes: |sum q_g| < 2^30 in int32
+constexpr int ROWBUF_STRIDE = 48;          // bytes per staged code row (conflict-free 16B stores)
+constexpr int MAX_PIECES = 512;            // built children per level (2^(kMaxDepth-1))
+constexpr int HIST_SMEM = 2 * kHistBins * 4 + HIST_WARPS * 32 * ROWBUF_STRIDE;  // 64 KB + 24 KB
+
+constexpr int PART_THREADS = 256;
+constexpr int PART_ITEMS = 8;
+constexpr int TILE = PART_THREADS * PART_ITEMS;  // 2048 rows per look-back tile
+
+constexpr int SPLIT_THREADS = 256;
+constexpr int SLOT = 2 * kHistBins;        // int64 per histogram slot (g then h)
+
+constexpr uint64_t FLAG_AGG = 1ull << 62;
+constexpr uint64_t FLAG_INCL = 2ull << 62;
+constexpr uint64_t FLAG_MASK = (1ull << 62) - 1;
+
+__device__ __forceinline__ double exp2i(int e) {  // exact 2^e for e in [-1022, 1023]
+  return __longlong_as_double((long long)(e + 1023) << 52);
+}
+
+struct LevelView {
+  int64_t* start;    // [2^d] segment start in the 2n state buffer (A = [0,n), B = [n,2n))
+  int64_t* cnt;      // [2^d] local rows
+  int64_t* gcnt;     // [2^d] global rows (== cnt for one rank)
+  double* lo;        // [2^d] monotone bounds
+  double* hi;
+  int32_t* split_f;  // [2^d] -1 = leaf / absent
+  int32_t* split_b;
+  int32_t* built;    // [2^(d-1)] which child of parent j was histogrammed (0 left, 1 right)
+  uint64_t* flags;   // look-back tile flags
+  int32_t* ticket;
+};
+
+struct FitArgs {
+  int64_t n, row_offset;
+  int F, users_col, D, K, T, target;
+  const uint8_t* codes;
+  const uint8_t* codesT;
+  const float* y;
+  const float* w;
+  float* p;
+  uint32_t* gp_root;
+  uint2* st[2];
+  int64_t* H[2];
+  LevelView lv[kMaxDepth + 1];
+  uint32_t* maxg;    // [T+1] float bits of max |g| per tree (slot T: base score)
+  uint32_t* maxh;
+  const float* cuts;     // [32][255]
+  const int32_t* ncuts;  // [32]
+  int32_t* tfeat;        // [T][nn] this target's trees
+  int32_t* tbin;
+  float* tthr;
+  float* tval;
+  double eta, lambda, mcw;
+  float subsample, colsample;
+  uint64_t seed;
+  int monotone;
+  int nn;
+  unsigned long long* units;  // device counters of rows processed per kernel class (instrumentation)
+};
+
+// debug-mode inputs of the histogram kernel
+struct DbgArgs {
+  const int32_t* idx;
+  const int32_t* qg;
+  const int32_t* qh;
+  int64_t m;
+  int64_t* out;  // one slot
+};
+
+// row sampling decision: keep iff u < subsample, u = top 53 bits / 2^53
+__device__ __forceinline__ bool row_sampled_out(uint64_t seed, int target, int t, int64_t gi, float subsample) {
+  if (subsample >= 1.0f) return false;
+  uint64_t r = rng4(seed, (uint64_t)(2 * target), (uint64_t)t, (uint64_t)gi);
+  double u = (double)(r >> 11) * 0x1.0p-53;
+  return u >= (double)subsample;
+}
+
+// slot of node k at level d inside H[d&1]: built child of parent j -> j, sibling -> 2^(d-1)+j
+__device__ __forceinline__ int node_slot(const FitArgs& a, int d, int k) {
+  if (d == 0) return 0;
+  int j = k >> 1;
+  int side = a.lv[d].built[j];
+  return ((k & 1) == side) ? j : (1 << (d - 1)) + j;
+}
+
+// ---------------------------------------------------------------------------------------------
+// histogram kernel: lane = feature, one row per warp step, run-length aggregation of equal
+// consecutive codes in registers, 32-bit shared atomics on change, zero-skipping int64 flush
+enum { HM_ROOT = 0, HM_LEVEL = 1, HM_DEBUG = 2 };
+
+template <int MODE>
+__global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const int d, const int t, const DbgArgs dbg) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  int32_t* sg = reinterpret_cast<int32_t*>(smem);                 // [256 bins][32 features]
+  uint32_t* sh = reinterpret_cast<uint32_t*>(smem + kHistBins * 4);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint8_t* rowbuf = smem + 2 * kHistBins * 4 + warp * 32 * ROWBUF_STRIDE;
+
+  __shared__ int64_t s_vstart[MAX_PIECES + 1];
+  __shared__ int64_t s_pstart[MAX_PIECES];
+  __shared__ int32_t s_slot[MAX_PIECES];
+  __shared__ int s_np;
+
+  for (int i = tid; i < kHistBins; i += HIST_THREADS) {
+    sg[i] = 0;
+    sh[i] = 0;
+  }
+  // ---- piece list (virtual concatenation of the rows to histogram)
+  if (MODE == HM_LEVEL) {
+    const int NP = 1 << (d - 1);
+    const LevelView& P = a.lv[d - 1];
+    const LevelView& C = a.lv[d];
+    // one parent per thread (NP <= 512 <= HIST_THREADS)
+    int64_t len = 0, pst = 0;
+    int side = 0;
+    bool sp = false;
+    if (tid < NP) {
+      sp = P.split_f[tid] >= 0;
+      if (sp) {
+        int64_t nL = C.gcnt[2 * tid], nR = C.gcnt[2 * tid + 1];
+        side = (nL <= nR) ? 0 : 1;       // build the smaller child (by global count), ties -> left
+        len = C.cnt[2 * tid + side];
+        pst = C.start[2 * tid + side];
+        if (blockIdx.x == 0) C.built[tid] = side;
+      }
+    }
+    // block exclusive scan of len over 512 threads
+    __shared__ int64_t s_wsum[HIST_WARPS];
+    int64_t v = len;
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    if (lane == 31) s_wsum[warp] = v;
+    __syncthreads();
+    int64_t woff = 0;
+    for (int w2 = 0; w2 < warp; ++w2) woff += s_wsum[w2];
+    if (tid < NP) {
+      s_vstart[tid] = woff + v - len;
+      s_pstart[tid] = pst;
+      s_slot[tid] = tid;
+    }
+    if (tid == NP - 1) s_vstart[NP] = woff + v;
+    if (tid == 0) s_np = NP;
+  } else {
+    if (tid == 0) {
+      s_np = 1;
+      s_vstart[0] = 0;
+      s_vstart[1] = (MODE == HM_ROOT) ? a.n : dbg.m;
+      s_pstart[0] = 0;
+      s_slot[0] = 0;
+    }
+  }
+  __syncthreads();
+  const int np = s_np;
+  const int64_t S = s_vstart[np];
+  const int64_t v0 = S * blockIdx.x / gridDim.x, v1 = S * (blockIdx.x + 1) / gridDim.x;
+  if (v0 >= v1) return;
+  if (tid == 0 && MODE != HM_DEBUG && a.units) atomicAdd(&a.units[MODE == HM_ROOT ? KC_HIST_ROOT : KC_HIST], (unsigned long long)(v1 - v0));
+
+  // quantisation scales for ROOT (tree t): q = rint(v * 2^(K-e))
+  double scale_g = 0.0, scale_h = 0.0;
+  if (MODE == HM_ROOT) {
+    scale_g = exp2i(a.K - exp_of(__uint_as_float(a.maxg[t])));
+    scale_h = exp2i(a.K - exp_of(__uint_as_float(a.maxh[t])));
+  }
+  int64_t* Hbase = (MODE == HM_DEBUG) ? dbg.out : a.H[d & 1];
+  const uint2* st_in = (MODE == HM_LEVEL) ? a.st[d & 1] : nullptr;
+  const int F = (MODE == HM_DEBUG) ? kMaxF : a.F;
+
+  // first piece overlapping [v0, v1)
+  int pc = 0;
+  while (pc + 1 < np && s_vstart[pc + 1] <= v0) ++pc;
+  for (; pc < np && s_vstart[pc] < v1; ++pc) {
+    int64_t s0 = max(v0, s_vstart[pc]), s1 = min(v1, s_vstart[pc + 1]);
+    if (s0 >= s1) continue;
+    int64_t* Hg = Hbase + (size_t)s_slot[pc] * SLOT;
+    int64_t* Hh = Hg + kHistBins;
+    for (int64_t c0 = s0; c0 < s1; c0 += HIST_CHUNK) {
+      const int64_t c1 = min(s1, c0 + HIST_CHUNK);
+      const int64_t clen = c1 - c0;
+      // contiguous sub-range per warp
+      const int64_t w0 = c0 + clen * warp / HIST_WARPS, w1 = c0 + clen * (warp + 1) / HIST_WARPS;
+      int prev = -1;
+      int32_t ag = 0;
+      uint32_t ah = 0;
+      for (int64_t base = w0; base < w1; base += 32) {
+        const int64_t vi = base + lane;   // virtual row
+        const int cnt = (int)min((int64_t)32, w1 - base);
+        uint32_t gp = 0;
+        if (vi < w1) {
+          const int64_t pi = s_pstart[pc] + (vi - s_vstart[pc]);  // physical position
+          int64_t ridx;
+          if (MODE == HM_ROOT) {
+            ridx = pi;
+            float yv = a.y[ridx], wv = a.w[ridx], pv = a.p[ridx];
+            float g = __fmul_rn(wv, __fsub_rn(pv, yv));
+            float h = wv;
+            if (row_sampled_out(a.seed, a.target, t, a.row_offset + ridx, a.subsample)) {
+              g = 0.f;
+              h = 0.f;
+            }
+            gp = pack_gp(quantize(g, scale_g), quantize(h, scale_h));
+            a.gp_root[ridx] = gp;
+          } else if (MODE == HM_LEVEL) {
+            uint2 s = st_in[pi];
+            ridx = s.x;
+            gp = s.y;
+          } else {
+            ridx = dbg.idx ? dbg.idx[pi] : pi;
+            gp = pack_gp(dbg.qg[ridx], dbg.qh[ridx]);
+          }
+          const uint4* crow = reinterpret_cast<const uint4*>(a.codes +
+                                                             (size_t)ridx * kMaxF);
+          uint4 c0v = __ldg(crow), c1v = __ldg(crow + 1);
+          *reinterpret_cast<uint4*>(rowbuf + lane * ROWBUF_STRIDE) = c0v;
+          *reinterpret_cast<uint4*>(rowbuf + lane * ROWBUF_STRIDE + 16) = c1v;
+        }
+        __syncwarp();
+        for (int r = 0; r < cnt; ++r) {
+          const uint32_t g2 = __shfl_sync(0xffffffffu, gp, r);
+          if (lane < F) {
+            const int c = rowbuf[r * ROWBUF_STRIDE + lane];
+            if (c != prev) {
+              if (prev >= 0) {
+                atomicAdd(&sg[prev * 32 + lane], ag);
+                atomicAdd(&sh[prev * 32 + lane], ah);
+              }
+              prev = c;
+              ag = 0;
+              ah = 0;
+            }
+            ag += gp_g(g2);
+            ah += (uint32_t)gp_h(g2);
+          }
+        }
+        __syncwarp();
+      }
+      if (prev >= 0 && lane < F) {
+        atomicAdd(&sg[prev * 32 + lane], ag);
+        atomicAdd(&sh[prev * 32 + lane], ah);
+      }
+      __syncthreads();
+      // flush: zero-skipping int64 atomics into the node histogram ([f][b] layout)
+      for (int i = tid; i < kHistBins; i += HIST_THREADS) {
+        const int32_t g = sg[i];
+        const uint32_t h = sh[i];
+        if (g != 0 || h != 0) {
+          const int b = i >> 5, f = i & 31;
+          atomicAdd(reinterpret_cast<unsigned long long*>(&Hg[f * kBins + b]), (unsigned long long)(long long)g);
+          atomicAdd(reinterpret_cast<unsigned long long*>(&Hh[f * kBins + b]), (unsigned long long)h);
+          sg[i] = 0;
+          sh[i] = 0;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// stable partition of the split parents' rows (level d-1) into their children (level d):
+// single pass, decoupled look-back over 2048-row tiles taken in ticket order; left children
+// go to region A = [0, n), right children to region B = [n, 2n) of the output state buffer, so
+// a child's segment is contiguous and keeps the parent's row order.
+__global__ void __launch_bounds__(PART_THREADS) k_partition(const FitArgs a, const int d, const int grid) {
+  const int NP = 1 << (d - 1);
+  const LevelView& P = a.lv[d - 1];
+  const LevelView& C = a.lv[d];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ int s_tile_pref[MAX_PIECES + 1];
+  __shared__ int64_t s_seq_pref[MAX_PIECES + 1];
+  __shared__ uint2 s_state[TILE];
+  __shared__ int s_wsum[PART_THREADS / 32];
+  __shared__ int64_t s_wsum64[PART_THREADS / 32];
+  __shared__ int s_ticket;
+  __shared__ int64_t s_excl;
+
+  // ---- prologue: per-parent tile and row prefixes (two parents per thread)
+  {
+    int tl[2] = {0, 0};
+    int64_t rl[2] = {0, 0};
+    for (int q = 0; q < 2; ++q) {
+      int j = tid * 2 + q;
+      if (j < NP && P.split_f[j] >= 0) {
+        int64_t c = (d == 1) ? a.n : P.cnt[j];
+        rl[q] = c;
+        tl[q] = (int)((c + TILE - 1) / TILE);
+      }
+    }
+    int tv = tl[0] + tl[1];
+    int64_t rv = rl[0] + rl[1];
+    int tinc = tv;
+    int64_t rinc = rv;
+    for (int o = 1; o < 32; o <<= 1) {
+      int u = __shfl_up_sync(0xffffffffu, tinc, o);
+      int64_t u64 = __shfl_up_sync(0xffffffffu, rinc, o);
+      if (lane >= o) {
+        tinc += u;
+        rinc += u64;
+      }
+    }
+    if (lane == 31) {
+      s_wsum[warp] = tinc;
+      s_wsum64[warp] = rinc;
+    }
+    __syncthreads();
+    int toff = 0;
+    int64_t roff = 0;
+    for (int w2 = 0; w2 < warp; ++w2) {
+      toff += s_wsum[w2];
+      roff += s_wsum64[w2];
+    }
+    int te = toff + tinc - tv;
+    int64_t re = roff + rinc - rv;
+    for (int q = 0; q < 2; ++q) {
+      int j = tid * 2 + q;
+      if (j < NP) {
+        s_tile_pref[j] = te;
+        s_seq_pref[j] = re;
+      }
+      te += tl[q];
+      re += rl[q];
+    }
+    if (tid == PART_THREADS - 1) {
+      s_tile_pref[NP] = te;   // grand totals (threads past NP add zeros)
+      s_seq_pref[NP] = re;
+    }
+  }
+  __syncthreads();
+  // ---- zero the built-child histogram slots [0, NP) of this level for split parents
+  {
+    int4* Hz = reinterpret_cast<int4*>(a.H[d & 1]);
+    const size_t per_slot = SLOT / 2;  // int4 per slot
+    const size_t total = (size_t)NP * per_slot;
+    for (size_t e = (size_t)blockIdx.x * PART_THREADS + tid; e < total; e += (size_t)grid * PART_THREADS) {
+      int j = (int)(e / per_slot);
+      if (P.split_f[j] >= 0) Hz[e] = make_int4(0, 0, 0, 0);
+    }
+  }
+  __syncthreads();
+  const int total_tiles = s_tile_pref[NP];
+  const uint2* st_in = (d >= 2) ? a.st[(d - 1) & 1] : nullptr;
+  uint2* st_out = a.st[d & 1];
+
+  while (true) {
+    if (tid == 0) s_ticket = atomicAdd(C.ticket, 1);
+    __syncthreads();
+    const int tk = s_ticket;
+    if (tk >= total_tiles) break;
+    // parent j: largest j with tile_pref[j] <= tk
+    int lo = 0, hi = NP - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (s_tile_pref[mid] <= tk) lo = mid;
+      else hi = mid - 1;
+    }
+    const int j = lo;
+    const int64_t cnt_j = (d == 1) ? a.n : P.cnt[j];
+    const int64_t start_j = (d == 1) ? 0 : P.start[j];
+    const int64_t o = (int64_t)(tk - s_tile_pref[j]) * TILE;
+    const int len = (int)min((int64_t)TILE, cnt_j - o);
+    const int f = P.split_f[j], b = P.split_b[j];
+    if (tid == 0 && a.units) atomicAdd(&a.units[KC_PARTITION], (unsigned long long)len);
+    // stage the tile's (ridx, gpair) state
+    for (int k = tid; k < len; k += PART_THREADS) {
+      if (d == 1) {
+        int64_t r = o + k;
+        s_state[k] = make_uint2((uint32_t)r, a.gp_root[r]);
+      } else {
+        s_state[k] = st_in[start_j + o + k];
+      }
+    }
+    __syncthreads();
+    const uint8_t* col = a.codesT + (size_t)f * a.n;
+    uint32_t lbits = 0;
+    int myl = 0;
+#pragma unroll
+    for (int q = 0; q < PART_ITEMS; ++q) {
+      int k = tid * PART_ITEMS + q;
+      if (k < len) {
+        int left = col[s_state[k].x] <= b;
+        lbits |= (uint32_t)left << q;
+        myl += left;
+      }
+    }
+    // block exclusive scan of left counts
+    int inc = myl;
+    for (int off = 1; off < 32; off <<= 1) {
+      int u = __shfl_up_sync(0xffffffffu, inc, off);
+      if (lane >= off) inc += u;
+    }
+    if (lane == 31) s_wsum[warp] = inc;
+    __syncthreads();
+    int woff = 0, L = 0;
+    for (int w2 = 0; w2 < PART_THREADS / 32; ++w2) {
+      if (w2 < warp) woff += s_wsum[w2];
+      L += s_wsum[w2];
+    }
+    const int my_excl = woff + inc - myl;
+    // decoupled look-back (one thread; predecessors are in flight or done: tickets are ordered)
+    if (tid == 0) {
+      volatile unsigned long long* fl = reinterpret_cast<volatile unsigned long long*>(C.flags);
+      int64_t excl = 0;
+      if (tk == 0) {
+        fl[0] = FLAG_INCL | (uint64_t)L;
+      } else {
+        fl[tk] = FLAG_AGG | (uint64_t)L;
+        int pr = tk - 1;
+        while (true) {
+          unsigned long long v = fl[pr];
+          unsigned long long stt = v & ~FLAG_MASK;
+          if (stt == 0) continue;
+          excl += (int64_t)(v & FLAG_MASK);
+          if (stt == FLAG_INCL) break;
+          --pr;
+        }
+        fl[tk] = FLAG_INCL | (uint64_t)(excl + L);
+      }
+      s_excl = excl;
+      if (o == 0) {
+        C.start[2 * j] = excl;
+        C.start[2 * j + 1] = a.n + (s_seq_pref[j] - excl);
+      }
+      atomicAdd(reinterpret_cast<unsigned long long*>(&C.cnt[2 * j]), (unsigned long long)L);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&C.cnt[2 * j + 1]), (unsigned long long)(len - L));
+    }
+    __syncthreads();
+    const int64_t excl = s_excl;
+    const int64_t rbase = a.n + (s_seq_pref[j] + o - excl);
+    int lpos = my_excl, rpos = tid * PART_ITEMS - my_excl;
+#pragma unroll
+    for (int q = 0; q < PART_ITEMS; ++q) {
+      int k = tid * PART_ITEMS + q;
+      if (k < len) {
+        uint2 s = s_state[k];
+        if ((lbits >> q) & 1u) st_out[excl + lpos++] = s;
+        else st_out[rbase + rpos++] = s;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// split evaluation: one CTA per node of level d
+struct Best {
+  double loss;
+  int f, b;
+};
+__device__ __forceinline__ bool better(const Best& x, const Best& y) {
+  if (x.loss != y.loss) return x.loss > y.loss;
+  if (x.f != y.f) return x.f < y.f;
+  return x.b < y.b;
+}
+
+__global__ void __launch_bounds__(SPLIT_THREADS) k_split(const FitArgs a, const int d, const int t) {
+  const int k = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const LevelView& V = a.lv[d];
+  int64_t* Hself;
+  if (d == 0) {
+    Hself = a.H[0];
+  } else {
+    const int j = k >> 1;
+    if (a.lv[d - 1].split_f[j] < 0) {
+      if (tid == 0) V.split_f[k] = -1;
+      return;
+    }
+    const int side = V.built[j];
+    const bool is_built = (k & 1) == side;
+    Hself = a.H[d & 1] + (size_t)(is_built ? j : (1 << (d - 1)) + j) * SLOT;
+    if (!is_built) {
+      // sibling = parent - built (exact integers)
+      const longlong2* Hp = reinterpret_cast<const longlong2*>(a.H[(d - 1) & 1] + (size_t)node_slot(a, d - 1, j) * SLOT);
+      const longlong2* Hb = reinterpret_cast<const longlong2*>(a.H[d & 1] + (size_t)j * SLOT);
+      longlong2* Hs = reinterpret_cast<longlong2*>(Hself);
+      for (int e = tid; e < SLOT / 2; e += SPLIT_THREADS) {
+        longlong2 p = Hp[e], q = Hb[e];
+        Hs[e] = make_longlong2(p.x - q.x, p.y - q.y);
+      }
+      __syncthreads();
+    }
+  }
+  __shared__ int64_t s_G, s_H;
+  __shared__ uint8_t s_fmask[kMaxF];
+  __shared__ Best s_best[SPLIT_THREADS / 32];
+  const int64_t* Hg = Hself;
+  const int64_t* Hh = Hself + kHistBins;
+  if (warp == 0) {
+    int64_t gs = 0, hs = 0;
+    for (int b = lane; b < kBins; b += 32) {
+      gs += Hg[b];
+      hs += Hh[b];
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      gs += __shfl_xor_sync(0xffffffffu, gs, o);
+      hs += __shfl_xor_sync(0xffffffffu, hs, o);
+    }
+    if (lane == 0) {
+      s_G = gs;
+      s_H = hs;
+    }
+  } else if (warp == 1) {
+    // column sample of tree t: keep ceil(colsample*F) features with the smallest keys
+    int F = a.F;
+    int nkeep = F;
+    if (a.colsample < 1.0f) {
+      nkeep = (int)ceil((double)a.colsample * (double)F);
+      if (nkeep < 1) nkeep = 1;
+    }
+    uint64_t key = (lane < F) ? rng4(a.seed, (uint64_t)(2 * a.target + 1), (uint64_t)t, (uint64_t)lane) : ~0ull;
+    int rank = 0;
+    for (int f2 = 0; f2 < F; ++f2) {
+      uint64_t k2 = __shfl_sync(0xffffffffu, key, f2);
+      if (k2 < key || (k2 == key && f2 < lane)) ++rank;
+    }
+    s_fmask[lane] = (lane < F && rank < nkeep) ? 1 : 0;
+  }
+  __syncthreads();
+  const int64_t Gq = s_G, Hq = s_H;
+  const int eg = exp_of(__uint_as_float(a.maxg[t])), eh = exp_of(__uint_as_float(a.maxh[t]));
+  const double sgi = exp2i(eg - a.K), shi = exp2i(eh - a.K);
+  const double lo = (d == 0) ? -INFINITY : V.lo[k], hi = (d == 0) ? INFINITY : V.hi[k];
+  const double lambda = a.lambda, mcw = a.mcw;
+  const double G = dequant(Gq, sgi), H = dequant(Hq, shi);
+  const double wP = calc_weight(G, H, lo, hi, lambda, mcw);
+  const double gainP = calc_gain(G, H, wP, lambda);
+
+  Best best{-INFINITY, 0x7fffffff, 0x7fffffff};
+  for (int fi = 0; fi < 4; ++fi) {
+    const int f = warp + 8 * fi;
+    if (f >= a.F || !s_fmask[f]) continue;
+    const int nb = a.ncuts[f] + 1;
+    if (nb < 2) continue;
+    int64_t pg[8], ph[8];
+    const longlong2* g2 = reinterpret_cast<const longlong2*>(Hg + f * kBins + lane * 8);
+    const longlong2* h2 = reinterpret_cast<const longlong2*>(Hh + f * kBins + lane * 8);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      longlong2 gv = g2[q], hv = h2[q];
+      pg[2 * q] = gv.x;
+      pg[2 * q + 1] = gv.y;
+      ph[2 * q] = hv.x;
+      ph[2 * q + 1] = hv.y;
+    }
+#pragma unroll
+    for (int q = 1; q < 8; ++q) {
+      pg[q] += pg[q - 1];
+      ph[q] += ph[q - 1];
+    }
+    int64_t ig = pg[7], ih = ph[7];
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t ug = __shfl_up_sync(0xffffffffu, ig, o), uh = __shfl_up_sync(0xffffffffu, ih, o);
+      if (lane >= o) {
+        ig += ug;
+        ih += uh;
+      }
+    }
+    const int64_t bg = ig - pg[7], bh = ih - ph[7];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int b = lane * 8 + q;
+      if (b > nb - 2) break;
+      const int64_t GLq = bg + pg[q], HLq = bh + ph[q];
+      const int64_t GRq = Gq - GLq, HRq = Hq - HLq;
+      const double GL = dequant(GLq, sgi), HL = dequant(HLq, shi);
+      const double GR = dequant(GRq, sgi), HR = dequant(HRq, shi);
+      if (!(HL >= mcw && HR >= mcw)) continue;
+      const double wl = calc_weight(GL, HL, lo, hi, lambda, mcw);
+      const double wr = calc_weight(GR, HR, lo, hi, lambda, mcw);
+      if (a.monotone && f == a.users_col && wl > wr) continue;
+      const double loss = __dsub_rn(__dadd_rn(calc_gain(GL, HL, wl, lambda), calc_gain(GR, HR, wr, lambda)), gainP);
+      Best c{loss, f, b};
+      if (better(c, best)) best = c;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    Best other;
+    other.loss = __shfl_down_sync(0xffffffffu, best.loss, o);
+    other.f = __shfl_down_sync(0xffffffffu, best.f, o);
+    other.b = __shfl_down_sync(0xffffffffu, best.b, o);
+    if (better(other, best)) best = other;
+  }
+  if (lane == 0) s_best[warp] = best;
+  __syncthreads();
+  if (tid != 0) return;
+  best = s_best[0];
+  for (int w2 = 1; w2 < SPLIT_THREADS / 32; ++w2)
+    if (better(s_best[w2], best)) best = s_best[w2];
+  const int gk = (1 << d) - 1 + k;
+  if (best.f != 0x7fffffff && best.loss > 1e-6) {
+    const int f = best.f, b = best.b;
+    int64_t GLq = 0, HLq = 0;
+    for (int bb = 0; bb <= b; ++bb) {
+      GLq += Hg[f * kBins + bb];
+      HLq += Hh[f * kBins + bb];
+    }
+    const double GL = dequant(GLq, sgi), HL = dequant(HLq, shi);
+    const double GR = dequant(Gq - GLq, sgi), HR = dequant(Hq - HLq, shi);
+    const double wl = calc_weight(GL, HL, lo, hi, lambda, mcw);
+    const double wr = calc_weight(GR, HR, lo, hi, lambda, mcw);
+    double loL = lo, hiL = hi, loR = lo, hiR = hi;
+    if (a.monotone && f == a.users_col) {
+      const double mid = __dmul_rn(__dadd_rn(wl, wr), 0.5);
+      hiL = mid;
+      loR = mid;
+    }
+    V.split_f[k] = f;
+    V.split_b[k] = b;
+    a.tfeat[gk] = f;
+    a.tbin[gk] = b;
+    a.tthr[gk] = a.cuts[f * (kBins - 1) + b];
+    a.tval[gk] = 0.0f;
+    if (d + 1 < a.D) {
+      const LevelView& N = a.lv[d + 1];
+      N.lo[2 * k] = loL;
+      N.hi[2 * k] = hiL;
+      N.lo[2 * k + 1] = loR;
+      N.hi[2 * k + 1] = hiR;
+    } else {
+      // children at max depth are leaves: v = (float)(eta * W(G, H, lo, hi))
+      a.tfeat[2 * gk + 1] = -1;
+      a.tval[2 * gk + 1] = (float)__dmul_rn(a.eta, calc_weight(GL, HL, loL, hiL, lambda, mcw));
+      a.tfeat[2 * gk + 2] = -1;
+      a.tval[2 * gk + 2] = (float)__dmul_rn(a.eta, calc_weight(GR, HR, loR, hiR, lambda, mcw));
+    }
+  } else {
+    V.split_f[k] = -1;
+    a.tfeat[gk] = -1;
+    a.tval[gk] = (float)__dmul_rn(a.eta, wP);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// leaf routing + prediction update + next tree's gradient maxima
+constexpr int UPD_THREADS = 256;
+constexpr int MAX_NODES = (1 << (kMaxDepth + 1)) - 1;
+
+__device__ __forceinline__ void block_max2(float& a, float& b, float* s_a, float* s_b) {
+  for (int o = 16; o > 0; o >>= 1) {
+    a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, o));
+    b = fmaxf(b, __shfl_xor_sync(0xffffffffu, b, o));
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    s_a[warp] = a;
+    s_b[warp] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w2 = 1; w2 < (int)(blockDim.x >> 5); ++w2) {
+      a = fmaxf(a, s_a[w2]);
+      b = fmaxf(b, s_b[w2]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(UPD_THREADS) k_update(const FitArgs a, const int t) {
+  __shared__ int8_t s_feat[MAX_NODES];
+  __shared__ uint8_t s_bin[MAX_NODES];
+  __shared__ float s_val[MAX_NODES];
+  __shared__ __align__(16) uint8_t s_row[UPD_THREADS * ROWBUF_STRIDE];
+  __shared__ float s_ma[UPD_THREADS / 32], s_mb[UPD_THREADS / 32];
+  const int tid = threadIdx.x;
+  const int32_t* tf = a.tfeat;  // a.tfeat/tbin/tval already point at tree t
+  for (int i = tid; i < a.nn; i += UPD_THREADS) {
+    int f = tf[i];
+    s_feat[i] = (int8_t)(f < 0 ? -1 : f);
+    s_bin[i] = (uint8_t)a.tbin[i];
+    s_val[i] = a.tval[i];
+  }
+  __syncthreads();
+  const bool has_next = t + 1 < a.T;
+  float mg = 0.f, mh = 0.f;
+  uint8_t* myrow = s_row + tid * ROWBUF_STRIDE;
+  for (int64_t i = (int64_t)blockIdx.x * UPD_THREADS + tid; i < a.n; i += (int64_t)gridDim.x * UPD_THREADS) {
+    const uint4* crow = reinterpret_cast<const uint4*>(a.codes + (size_t)i * kMaxF);
+    *reinterpret_cast<uint4*>(myrow) = __ldg(crow);
+    *reinterpret_cast<uint4*>(myrow + 16) = __ldg(crow + 1);
+    int k = 0;
+    int f = s_feat[0];
+    while (f >= 0) {
+      k = 2 * k + 1 + (myrow[f] > s_bin[k] ? 1 : 0);
+      f = s_feat[k];
+    }
+    const float pn = __fadd_rn(a.p[i], s_val[k]);  // O9: one fp32 rounding
+    a.p[i] = pn;
+    if (has_next) {
+      const float wv = a.w[i];
+      float g = __fmul_rn(wv, __fsub_rn(pn, a.y[i]));
+      float h = wv;
+      if (row_sampled_out(a.seed, a.target, t + 1, a.row_offset + i, a.subsample)) {
+        g = 0.f;
+        h = 0.f;
+      }
+      mg = fmaxf(mg, fabsf(g));
+      mh = fmaxf(mh, h);
+    }
+  }
+  if (!has_next) return;
+  block_max2(mg, mh, s_ma, s_mb);
+  if (tid == 0) {
+    atomicMax(&a.maxg[t + 1], __float_as_uint(mg));
+    atomicMax(&a.maxh[t + 1], __float_as_uint(mh));
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// base score (O3): quantise g = w*(0 - y), h = w over all rows; base = -G/H (lambda = 0)
+constexpr int BASE_THREADS = 256;
+
+__global__ void __launch_bounds__(BASE_THREADS) k_base_max(const FitArgs a) {
+  __shared__ float s_a[BASE_THREADS / 32], s_b[BASE_THREADS / 32];
+  float mg = 0.f, mh = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * BASE_THREADS + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * BASE_THREADS) {
+    const float wv = a.w[i];
+    const float g = __fmul_rn(wv, __fsub_rn(0.0f, a.y[i]));
+    mg = fmaxf(mg, fabsf(g));
+    mh = fmaxf(mh, wv);
+  }
+  block_max2(mg, mh, s_a, s_b);
+  if (threadIdx.x == 0) {
+    atomicMax(&a.maxg[a.T], __float_as_uint(mg));
+    atomicMax(&a.maxh[a.T], __float_as_uint(mh));
+  }
+}
+
+__global__ void __launch_bounds__(BASE_THREADS) k_base_sum(const FitArgs a, int64_t* sums) {
+  const double sg = exp2i(a.K - exp_of(__uint_as_float(a.maxg[a.T])));
+  const double sh = exp2i(a.K - exp_of(__uint_as_float(a.maxh[a.T])));
+  int64_t gs = 0, hs = 0;
+  for (int64_t i = (int64_t)blockIdx.x * BASE_THREADS + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * BASE_THREADS) {
+    const float wv = a.w[i];
+    gs += quantize(__fmul_rn(wv, __fsub_rn(0.0f, a.y[i])), sg);
+    hs += quantize(wv, sh);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    gs += __shfl_xor_sync(0xffffffffu, gs, o);
+    hs += __shfl_xor_sync(0xffffffffu, hs, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(&sums[0]), (unsigned long long)gs);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&sums[1]), (unsigned long long)hs);
+  }
+}
+
+// p = base for all rows; tree 0's gradient maxima
+__global__ void __launch_bounds__(BASE_THREADS) k_base_init(const FitArgs a, const int64_t* sums, float* base_out) {
+  __shared__ float s_a[BASE_THREADS / 32], s_b[BASE_THREADS / 32];
+  const double G = dequant(sums[0], exp2i(exp_of(__uint_as_float(a.maxg[a.T])) - a.K));
+  const double H = dequant(sums[1], exp2i(exp_of(__uint_as_float(a.maxh[a.T])) - a.K));
+  const float base = H > 0.0 ? (float)__ddiv_rn(-G, H) : 0.0f;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *base_out = base;
+  float mg = 0.f, mh = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * BASE_THREADS + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * BASE_THREADS) {
+    a.p[i] = base;
+    if (a.T > 0) {
+      const float wv = a.w[i];
+      float g = __fmul_rn(wv, __fsub_rn(base, a.y[i]));
+      float h = wv;
+      if (row_sampled_out(a.seed, a.target, 0, a.row_offset + i, a.subsample)) {
+        g = 0.f;
+        h = 0.f;
+      }
+      mg = fmaxf(mg, fabsf(g));
+      mh = fmaxf(mh, h);
+    }
+  }
+  block_max2(mg, mh, s_a, s_b);
+  if (threadIdx.x == 0 && a.T > 0) {
+    atomicMax(&a.maxg[0], __float_as_uint(mg));
+    atomicMax(&a.maxh[0], __float_as_uint(mh));
+  }
+}
+
+__global__ void k_fill_trees(int32_t* feat, int32_t* bin, float* thr, float* val, size_t count) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    feat[i] = -2;
+    bin[i] = 0;
+    thr[i] = 0.f;
+    val[i] = 0.f;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Eq. (4) weights and input validation
+__global__ void k_validate(const float* X, const float* y, const int32_t* llm, const int32_t* prof, int64_t n, int F,
+                           int n_llm, int n_prof, int* flag) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    bool bad = !isfinite(y[2 * i]) || !isfinite(y[2 * i + 1]);
+    for (int f = 0; f < F; ++f) bad |= !isfinite(X[i * F + f]);
+    if (llm && (llm[i] < 0 || llm[i] >= n_llm)) bad = true;
+    if (prof && (prof[i] < 0 || prof[i] >= n_prof)) bad = true;
+    if (bad) atomicOr(flag, 1);
+  }
+}
+
+__global__ void k_weights_max(const float* y, const int32_t* llm, const int32_t* prof, int64_t n, int n_prof, double L1,
+                              double L2, unsigned long long* Dmax) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = (int64_t)llm[i] * n_prof + prof[i];
+    const double d1 = fabs(__dsub_rn((double)y[2 * i], L1));
+    const double d2 = fabs(__dsub_rn((double)y[2 * i + 1], L2));
+    atomicMax(&Dmax[2 * g], (unsigned long long)__double_as_longlong(d1));      // d >= 0: bit order = value order
+    atomicMax(&Dmax[2 * g + 1], (unsigned long long)__double_as_longlong(d2));
+  }
+}
+
+__global__ void k_weights_apply(const float* y, const int32_t* llm, const int32_t* prof, int64_t n, int n_prof,
+                                double L1, double L2, const unsigned long long* Dmax, float* w, float* y0, float* y1) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = (int64_t)llm[i] * n_prof + prof[i];
+    const float ya = y[2 * i], yb = y[2 * i + 1];
+    const double d1 = fabs(__dsub_rn((double)ya, L1)), d2 = fabs(__dsub_rn((double)yb, L2));
+    const double D1 = __longlong_as_double((long long)Dmax[2 * g]), D2 = __longlong_as_double((long long)Dmax[2 * g + 1]);
+    const double w1 = D1 > 0.0 ? __dsub_rn(1.0, __ddiv_rn(d1, D1)) : 1.0;
+    const double w2 = D2 > 0.0 ? __dsub_rn(1.0, __ddiv_rn(d2, D2)) : 1.0;
+    w[i] = (float)__dmul_rn(__dadd_rn(w1, w2), 0.5);
+    y0[i] = ya;
+    y1[i] = yb;
+  }
+}
+
+__global__ void k_weights_given(const float* y, const float* win, int64_t n, float* w, float* y0, float* y1) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    w[i] = win ? win[i] : 1.0f;
+    y0[i] = y[2 * i];
+    y1[i] = y[2 * i + 1];
+  }
+}
+
+// Eq. (4) weights of a whole dataset (used by the CV's weighted MAPE)
+void compute_weights(Ctx* ctx, const DatasetDev& ds, float L1, float L2, float* w) {
+  const int64_t n = ds.n;
+  DevBuf d_y0(n * 4), d_y1(n * 4);
+  const size_t ng = (size_t)ds.n_llm * ds.n_prof;
+  DevBuf d_D(ng * 2 * 8);
+  LLMP_CUDA(cudaMemsetAsync(d_D.p, 0, d_D.bytes, ctx->stream));
+  int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->sms * 8);
+  LLMP_LAUNCH(ctx, KC_WEIGHTS, n, k_weights_max, grid, 256, 0, ds.y, ds.llm, ds.prof, n, ds.n_prof, (double)L1,
+              (double)L2, d_D.as<unsigned long long>());
+  allreduce_max_u64(ctx, d_D.as<uint64_t>(), ng * 2);
+  LLMP_LAUNCH(ctx, KC_WEIGHTS, n, k_weights_apply, grid, 256, 0, ds.y, ds.llm, ds.prof, n, ds.n_prof, (double)L1,
+              (double)L2, d_D.as<unsigned long long>(), w, d_y0.as<float>(), d_y1.as<float>());
+}
+
+// ---------------------------------------------------------------------------------------------
+void validate_hparams(const llmpilot_hparams& hp) {
+  LLMP_REQUIRE(hp.n_trees >= 0, "n_trees must be >= 0");
+  LLMP_REQUIRE(hp.max_depth >= 1 && hp.max_depth <= kMaxDepth, "max_depth must be in [1, 10]");
+  LLMP_REQUIRE(hp.max_bin >= 2 && hp.max_bin <= kBins, "max_bin must be in [2, 256]");
+  LLMP_REQUIRE(hp.grad_bits >= 2 && hp.grad_bits <= kMaxGradBits, "grad_bits must be in [2, 14]");
+  LLMP_REQUIRE(hp.subsample > 0.0f && hp.subsample <= 1.0f, "subsample must be in (0, 1]");
+  LLMP_REQUIRE(hp.colsample_bytree > 0.0f && hp.colsample_bytree <= 1.0f, "colsample_bytree must be in (0, 1]");
+  LLMP_REQUIRE(hp.lambda >= 0.0f && isfinite(hp.lambda), "lambda must be >= 0");
+  LLMP_REQUIRE(hp.min_child_weight >= 0.0f && isfinite(hp.min_child_weight), "min_child_weight must be >= 0");
+  LLMP_REQUIRE(isfinite(hp.eta), "eta must be finite");
+}
+
+static int grid_for(Ctx* ctx, int64_t n, int threads, int per_sm) {
+  int64_t g = (n + threads - 1) / threads;
+  int64_t cap = (int64_t)ctx->sms * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float L1, float L2, ModelData& out,
+              bool keep_train_pred) {
+  validate_hparams(hp);
+  const int64_t n = ds.n;
+  const int F = ds.F, D = hp.max_depth, T = hp.n_trees;
+  LLMP_REQUIRE(n >= 1 && n < (int64_t(1) << 30), "n_rows must be in [1, 2^30)");
+  LLMP_REQUIRE(F >= 1 && F <= kMaxF, "n_features must be in [1, 32]");
+  LLMP_REQUIRE(ds.users_col >= 0 && ds.users_col < F, "users_col out of range");
+  LLMP_REQUIRE(isfinite(L1) && isfinite(L2), "L1, L2 must be finite");
+  const bool eq4 = hp.use_eq4_weights != 0;
+  LLMP_REQUIRE(!eq4 || (ds.llm && ds.prof && ds.n_llm >= 1 && ds.n_prof >= 1),
+               "Eq. (4) weights need llm_id/profile_id and n_llm, n_prof >= 1");
+  cudaStream_t s = ctx->stream;
+
+  // ---- validation (NaN/Inf, id ranges) — one host sync per fit
+  DevBuf& d_flag = ctx->workspace("flag", sizeof(int));
+  LLMP_CUDA(cudaMemsetAsync(d_flag.p, 0, sizeof(int), s));
+  LLMP_LAUNCH(ctx, KC_VALIDATE, n, k_validate, grid_for(ctx, n, 256, 8), 256, 0, ds.X, ds.y, eq4 ? ds.llm : nullptr,
+              eq4 ? ds.prof : nullptr, n, F, ds.n_llm, ds.n_prof, d_flag.as<int>());
+  int h_flag = 0;
+  LLMP_CUDA(cudaMemcpyAsync(&h_flag, d_flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  LLMP_CUDA(cudaStreamSynchronize(s));
+  LLMP_REQUIRE(h_flag == 0, "dataset holds a non-finite X or y value or an id out of range");
+
+  // ---- weights (Eq. 4) + de-interleaved targets
+  DevBuf& d_w = ctx->workspace("w", n * 4);
+  DevBuf& d_y0 = ctx->workspace("y0", n * 4);
+  DevBuf& d_y1 = ctx->workspace("y1", n * 4);
+  if (eq4) {
+    const size_t ng = (size_t)ds.n_llm * ds.n_prof;
+    DevBuf& d_D = ctx->workspace("groupmax", ng * 2 * 8);
+    LLMP_CUDA(cudaMemsetAsync(d_D.p, 0, ng * 2 * 8, s));
+    LLMP_LAUNCH(ctx, KC_WEIGHTS, n, k_weights_max, grid_for(ctx, n, 256, 8), 256, 0, ds.y, ds.llm, ds.prof, n,
+                ds.n_prof, (double)L1, (double)L2, d_D.as<unsigned long long>());
+    allreduce_max_u64(ctx, d_D.as<uint64_t>(), ng * 2);
+    LLMP_LAUNCH(ctx, KC_WEIGHTS, n, k_weights_apply, grid_for(ctx, n, 256, 8), 256, 0, ds.y, ds.llm, ds.prof, n,
+                ds.n_prof, (double)L1, (double)L2, d_D.as<unsigned long long>(), d_w.as<float>(), d_y0.as<float>(),
+                d_y1.as<float>());
+  } else {
+    LLMP_LAUNCH(ctx, KC_WEIGHTS, n, k_weights_given, grid_for(ctx, n, 256, 8), 256, 0, ds.y, ds.w, n, d_w.as<float>(),
+                d_y0.as<float>(), d_y1.as<float>());
+  }
+
+  // ---- cuts + codes (row-major for histograms/routing, column-major for partitions)
+  compute_cuts(ctx, ds.X, n, F, ds.row_offset, ds.n_global, hp.max_bin, out.cuts);
+  DevBuf& d_codes = ctx->workspace("codes", (size_t)n * kMaxF);
+  DevBuf& d_codesT = ctx->workspace("codesT", (size_t)n * kMaxF);
+  compute_codes(ctx, ds.X, n, F, out.cuts, d_codes.as<uint8_t>(), d_codesT.as<uint8_t>(), nullptr);
+
+  // ---- training state
+  const int nn = (1 << (D + 1)) - 1;
+  const int half_max = 1 << (D - 1);        // slots per histogram parity buffer
+  // p of both targets: kept by the model (llmpilot_model_train_pred) or a reused workspace
+  if (keep_train_pred) out.d_train_pred.ensure((size_t)n * 4 * 2);
+  DevBuf& d_p = keep_train_pred ? out.d_train_pred : ctx->workspace("p", (size_t)n * 4 * 2);
+  out.device = ctx->device;
+  DevBuf& d_gp = ctx->workspace("gp_root", (size_t)n * 4);
+  DevBuf& d_st0 = ctx->workspace("state0", (size_t)n * 2 * 8);
+  DevBuf& d_st1 = ctx->workspace("state1", (size_t)n * 2 * 8);
+  DevBuf& d_H0 = ctx->workspace("hist0", (size_t)half_max * SLOT * 8);
+  DevBuf& d_H1 = ctx->workspace("hist1", (size_t)half_max * SLOT * 8);
+  DevBuf& d_trees = ctx->workspace("trees", (size_t)2 * std::max(T, 1) * nn * 16);
+  DevBuf& d_max = ctx->workspace("gradmax", (size_t)2 * 2 * (T + 1) * 4);
+  DevBuf& d_sums = ctx->workspace("basesums", 2 * 2 * 8);
+  DevBuf& d_base = ctx->workspace("base", 2 * 4);
+  // level tables: doubles/ints per level, plus the per-tree zeroed control block
+  size_t lvl_nodes = 0;
+  for (int d = 0; d <= D; ++d) lvl_nodes += (size_t)1 << d;
+  int64_t max_tiles_total = 0;
+  std::vector<int64_t> tiles_off(D + 1, 0);
+  for (int d = 1; d <= D; ++d) {
+    tiles_off[d] = max_tiles_total;
+    max_tiles_total += (n + TILE - 1) / TILE + (1 << (d - 1)) + 1;
+  }
+  const size_t ctl_bytes = 64 * 4 /*tickets*/ + lvl_nodes * 8 * 2 /*cnt,gcnt*/ + (size_t)max_tiles_total * 8;
+  DevBuf& d_ctl = ctx->workspace("ctl", ctl_bytes);
+  const size_t tab_bytes = lvl_nodes * (8 /*start*/ + 8 + 8 /*lo,hi*/ + 4 + 4 /*split*/ + 4 /*built*/);
+  DevBuf& d_tab = ctx->workspace("tab", tab_bytes);
+
+  FitArgs a{};
+  a.n = n;
+  a.row_offset = ds.row_offset;
+  a.F = F;
+  a.users_col = ds.users_col;
+  a.D = D;
+  a.K = hp.grad_bits;
+  a.T = T;
+  a.codes = d_codes.as<uint8_t>();
+  a.codesT = d_codesT.as<uint8_t>();
+  a.w = d_w.as<float>();
+  a.gp_root = d_gp.as<uint32_t>();
+  a.st[0] = d_st0.as<uint2>();
+  a.st[1] = d_st1.as<uint2>();
+  a.H[0] = d_H0.as<int64_t>();
+  a.H[1] = d_H1.as<int64_t>();
+  a.cuts = out.cuts.d_cuts.as<float>();
+  a.ncuts = out.cuts.d_ncuts.as<int32_t>();
+  a.eta = (double)hp.eta;
+  a.lambda = (double)hp.lambda;
+  a.mcw = (double)hp.min_child_weight;
+  a.subsample = hp.subsample;
+  a.colsample = hp.colsample_bytree;
+  a.seed = hp.seed;
+  a.monotone = hp.monotone_users;
+  a.nn = nn;
+  a.units = ctx->d_units;
+  {
+    uint8_t* c = d_ctl.as<uint8_t>();
+    int32_t* tickets = reinterpret_cast<int32_t*>(c);
+    int64_t* cnt = reinterpret_cast<int64_t*>(c + 64 * 4);
+    int64_t* gcnt = cnt + lvl_nodes;
+    uint64_t* flags = reinterpret_cast<uint64_t*>(gcnt + lvl_nodes);
+    uint8_t* tb = d_tab.as<uint8_t>();
+    int64_t* start = reinterpret_cast<int64_t*>(tb);
+    double* lo = reinterpret_cast<double*>(start + lvl_nodes);
+    double* hi = lo + lvl_nodes;
+    int32_t* sf = reinterpret_cast<int32_t*>(hi + lvl_nodes);
+    int32_t* sb = sf + lvl_nodes;
+    int32_t* bu = sb + lvl_nodes;
+    size_t off = 0;
+    for (int d = 0; d <= D; ++d) {
+      LevelView& L = a.lv[d];
+      L.start = start + off;
+      L.cnt = cnt + off;
+      L.gcnt = (ctx->nranks > 1) ? gcnt + off : cnt + off;
+      L.lo = lo + off;
+      L.hi = hi + off;
+      L.split_f = sf + off;
+      L.split_b = sb + off;
+      L.built = bu + off;
+      L.flags = flags + tiles_off[d];
+      L.ticket = tickets + d;
+      off += (size_t)1 << d;
+    }
+    LLMP_CUDA(cudaMemsetAsync(d_tab.p, 0, d_tab.bytes, s));
+  }
+  // model arrays (per target views into d_trees)
+  int32_t* feat_all = d_trees.as<int32_t>();
+  int32_t* bin_all = feat_all + (size_t)2 * T * nn;
+  float* thr_all = reinterpret_cast<float*>(bin_all + (size_t)2 * T * nn);
+  float* val_all = thr_all + (size_t)2 * T * nn;
+  if (T > 0)
+    LLMP_LAUNCH(ctx, KC_MISC, 0, k_fill_trees, 256, 256, 0, feat_all, bin_all, thr_all, val_all, (size_t)2 * T * nn);
+  LLMP_CUDA(cudaMemsetAsync(d_max.p, 0, d_max.bytes, s));
+  LLMP_CUDA(cudaMemsetAsync(d_sums.p, 0, d_sums.bytes, s));
+
+  const int hist_grid = 2 * ctx->sms;
+  const int part_grid = 4 * ctx->sms;
+  const int upd_grid = grid_for(ctx, n, UPD_THREADS, 8);
+  const int base_grid = grid_for(ctx, n, BASE_THREADS, 8);
+  static bool attr_set = false;
+  if (!attr_set) {
+    LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_ROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
+    LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_LEVEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
+    LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
+    attr_set = true;
+  }
+  const DbgArgs nodbg{};
+  const size_t ctl_zero = 64 * 4 + lvl_nodes * 8 * 2 + (size_t)max_tiles_total * 8;
+
+  for (int target = 0; target < 2; ++target) {
+    a.target = target;
+    a.y = (target == 0) ? d_y0.as<float>() : d_y1.as<float>();
+    a.p = d_p.as<float>() + (size_t)target * n;
+    a.maxg = d_max.as<uint32_t>() + (size_t)target * 2 * (T + 1);
+    a.maxh = a.maxg + (T + 1);
+    a.tfeat = feat_all + (size_t)target * T * nn;
+    a.tbin = bin_all + (size_t)target * T * nn;
+    a.tthr = thr_all + (size_t)target * T * nn;
+    a.tval = val_all + (size_t)target * T * nn;
+    int64_t* sums = d_sums.as<int64_t>() + 2 * target;
+
+    LLMP_LAUNCH(ctx, KC_BASE, n, k_base_max, base_grid, BASE_THREADS, 0, a);
+    allreduce_max_u32(ctx, a.maxg + T, 1);
+    allreduce_max_u32(ctx, a.maxh + T, 1);
+    LLMP_LAUNCH(ctx, KC_BASE, n, k_base_sum, base_grid, BASE_THREADS, 0, a, sums);
+    allreduce_sum_i64(ctx, sums, 2);
+    LLMP_LAUNCH(ctx, KC_BASE, n, k_base_init, base_grid, BASE_THREADS, 0, a, sums, d_base.as<float>() + target);
+    if (T > 0) {
+      allreduce_max_u32(ctx, a.maxg, 1);
+      allreduce_max_u32(ctx, a.maxh, 1);
+    }
+    for (int t = 0; t < T; ++t) {
+      a.tfeat = feat_all + ((size_t)target * T + t) * nn;
+      a.tbin = bin_all + ((size_t)target * T + t) * nn;
+      a.tthr = thr_all + ((size_t)target * T + t) * nn;
+      a.tval = val_all + ((size_t)target * T + t) * nn;
+      LLMP_CUDA(cudaMemsetAsync(d_ctl.p, 0, ctl_zero, s));
+      LLMP_CUDA(cudaMemsetAsync(a.H[0], 0, (size_t)SLOT * 8, s));
+      LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist<HM_ROOT>, hist_grid, HIST_THREADS, HIST_SMEM, a, 0, t, nodbg);
+      allreduce_sum_i64(ctx, a.H[0], SLOT);
+      LLMP_LAUNCH(ctx, KC_SPLIT, 1, k_split, 1, SPLIT_THREADS, 0, a, 0, t);
+      for (int d = 1; d < D; ++d) {
+        LLMP_LAUNCH(ctx, KC_PARTITION, n, k_partition, part_grid, PART_THREADS, 0, a, d, part_grid);
+        if (ctx->nranks > 1) {
+          LLMP_CUDA(cudaMemcpyAsync(a.lv[d].gcnt, a.lv[d].cnt, ((size_t)1 << d) * 8, cudaMemcpyDeviceToDevice, s));
+          allreduce_sum_i64(ctx, a.lv[d].gcnt, (size_t)1 << d);
+        }
+        LLMP_LAUNCH(ctx, KC_HIST, n / 2, k_hist<HM_LEVEL>, hist_grid, HIST_THREADS, HIST_SMEM, a, d, t, nodbg);
+        allreduce_sum_i64(ctx, a.H[d & 1], (size_t)SLOT << (d - 1));
+        LLMP_LAUNCH(ctx, KC_SPLIT, (1 << d), k_split, (1 << d), SPLIT_THREADS, 0, a, d, t);
+      }
+      LLMP_LAUNCH(ctx, KC_UPDATE, n, k_update, upd_grid, UPD_THREADS, 0, a, t);
+      if (t + 1 < T) {
+        allreduce_max_u32(ctx, a.maxg + t + 1, 1);
+        allreduce_max_u32(ctx, a.maxh + t + 1, 1);
+      }
+    }
+  }
+
+  // ---- model to host
+  out.F = F;
+  out.users_col = ds.users_col;
+  out.T = T;
+  out.D = D;
+  out.nn = nn;
+  out.n_train = n;
+  const size_t tot = (size_t)2 * T * nn;
+  out.feat.resize(tot);
+  out.bin.resize(tot);
+  out.thr.resize(tot);
+  out.val.resize(tot);
+  if (tot) {
+    LLMP_CUDA(cudaMemcpyAsync(out.feat.data(), feat_all, tot * 4, cudaMemcpyDeviceToHost, s));
+    LLMP_CUDA(cudaMemcpyAsync(out.bin.data(), bin_all, tot * 4, cudaMemcpyDeviceToHost, s));
+    LLMP_CUDA(cudaMemcpyAsync(out.thr.data(), thr_all, tot * 4, cudaMemcpyDeviceToHost, s));
+    LLMP_CUDA(cudaMemcpyAsync(out.val.data(), val_all, tot * 4, cudaMemcpyDeviceToHost, s));
+  }
+  LLMP_CUDA(cudaMemcpyAsync(out.base, d_base.p, 8, cudaMemcpyDeviceToHost, s));
+  LLMP_CUDA(cudaStreamSynchronize(s));
+  upload_model_nodes(ctx, out);
+}
+
+// ---------------------------------------------------------------------------------------------
+void debug_histogram(Ctx* ctx, const uint8_t* codes, int64_t n, const int32_t* idx, int64_t m, const int32_t* qg,
+                     const int32_t* qh, int64_t* Hg, int64_t* Hh) {
+  LLMP_REQUIRE(n >= 1 && m >= 0, "bad sizes");
+  FitArgs a{};
+  a.codes = codes;
+  a.n = n;
+  a.F = kMaxF;
+  DevBuf d_out((size_t)SLOT * 8);
+  LLMP_CUDA(cudaMemsetAsync(d_out.p, 0, d_out.bytes, ctx->stream));
+  DbgArgs dbg{idx, qg, qh, idx ? m : n, d_out.as<int64_t>()};
+  static bool attr_set = false;
+  if (!attr_set) {
+    LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
+    attr_set = true;
+  }
+  LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist<HM_DEBUG>, 2 * ctx->sms, HIST_THREADS, HIST_SMEM, a, 0, 0, dbg);
+  LLMP_CUDA(cudaMemcpyAsync(Hg, d_out.p, kHistBins * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  LLMP_CUDA(cudaMemcpyAsync(Hh, d_out.as<int64_t>() + kHistBins, kHistBins * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  LLMP_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+}  // namespace llmp

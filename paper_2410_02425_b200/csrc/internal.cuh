@@ -1,0 +1,83 @@
+// internal.cuh — interfaces between the library's translation units.
+#pragma once
+#include "common.cuh"
+
+namespace llmp {
+
+// cuts: device [32][255] floats + [32] int32 counts; host mirror for export / model
+struct CutsData {
+  int F = 0;
+  int max_bin = 256;
+  DevBuf d_cuts;    // float [32][255]
+  DevBuf d_ncuts;   // int32 [32]
+  std::vector<float> h_cuts;     // [32*255]
+  std::vector<int32_t> h_ncuts;  // [32]
+};
+
+// a fitted model (two ensembles, complete-binary trees)
+struct ModelData {
+  int F = 0, users_col = 0, T = 0, D = 0, nn = 0;
+  int64_t n_train = 0;
+  int device = 0;
+  float base[2] = {0.f, 0.f};
+  std::vector<int32_t> feat, bin;  // [2][T][nn]
+  std::vector<float> thr, val;
+  CutsData cuts;
+  DevBuf d_nodes;                  // uint2 [2][T][nn]: x = thr or leaf value bits, y = feat (int)
+  DevBuf d_base;                   // float [2]
+  DevBuf d_train_pred;             // float [2][n_train] (planar) training predictions, on the device
+};
+
+// binning.cu
+void compute_cuts(Ctx* ctx, const float* X, int64_t n, int F, int64_t row_offset, int64_t n_global, int max_bin,
+                  CutsData& out);
+// codes: row-major n x 32 (may be null); codesT: column-major 32 x n (may be null).
+// flag (device int, may be null) is set to 1 when X holds a non-finite value.
+void compute_codes(Ctx* ctx, const float* X, int64_t n, int F, const CutsData& cuts, uint8_t* codes, uint8_t* codesT,
+                   int* flag);
+
+// fit.cu
+struct DatasetDev {  // resolved device pointers
+  int64_t n, row_offset, n_global;
+  int F, users_col, n_llm, n_prof;
+  const float* X;
+  const float* y;
+  const int32_t* llm;
+  const int32_t* prof;
+  const float* w;
+};
+void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float L1, float L2, ModelData& out,
+              bool keep_train_pred);
+void validate_hparams(const llmpilot_hparams& hp);
+void compute_weights(Ctx* ctx, const DatasetDev& ds, float L1, float L2, float* w);
+void debug_histogram(Ctx* ctx, const uint8_t* codes, int64_t n, const int32_t* idx, int64_t m, const int32_t* qg,
+                     const int32_t* qh, int64_t* Hg, int64_t* Hh);
+
+// predict.cu
+void upload_model_nodes(Ctx* ctx, ModelData& m);
+void predict_impl(Ctx* ctx, const ModelData& m, const float* X, int64_t n, float* out);
+struct RecOut {
+  std::vector<int32_t> profile, u_max;
+  std::vector<int64_t> n_pods;
+  std::vector<double> cost;
+};
+// pred: device [n_llm][n_prof][n_levels][2]; argmin on the device (Eq. 1-3)
+void argmin_impl(Ctx* ctx, const float* pred, int n_llm, int n_prof, int n_levels, const int32_t* levels_host,
+                 const double* cost_host, const uint8_t* allowed_host, float L1, float L2, int64_t U, RecOut& out);
+void recommend_impl(Ctx* ctx, const ModelData& m, const float* llm_feats, int n_llm, int F_llm,
+                    const float* prof_feats, int n_prof, int F_prof, const double* cost, const uint8_t* allowed,
+                    const int32_t* levels, int n_levels, float L1, float L2, int64_t U, RecOut& out,
+                    float* pred_out_dev);
+
+// cv.cu
+struct CvFold {
+  int llm, hp_index;
+  llmpilot_rec rec, truth;
+  int success;
+  double overspend;
+  int truth_feasible;
+};
+void cv_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams* grid, int n_grid, float L1, float L2, int64_t U,
+             const double* prof_cost, std::vector<CvFold>& folds, double& S, double& O, double& SO, int& n_scored);
+
+}  // namespace llmp

@@ -1,0 +1,185 @@
+// runtime.cu — context, error plumbing, instrumentation, host/device pointer handling and the
+// NCCL collectives (NCCL is dlopen'ed so a one-GPU process needs no NCCL at all).
+#include <dlfcn.h>
+#include <string.h>
+
+#include <stdexcept>
+
+#include "common.cuh"
+
+namespace llmp {
+
+[[noreturn]] void fail(llmpilot_status st, const std::string& msg) { throw Error{st, msg}; }
+
+void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  if (e == cudaSuccess) return;
+  llmpilot_status st = (e == cudaErrorMemoryAllocation) ? LLMP_ENOMEM : LLMP_ECUDA;
+  cudaGetLastError();  // clear sticky-free errors
+  fail(st, std::string(cudaGetErrorString(e)) + " in " + what + " (" + file + ":" + std::to_string(line) + ")");
+}
+
+void DevBuf::alloc(size_t b) {
+  bytes = b;
+  if (b == 0) { p = nullptr; return; }
+  cudaError_t e = cudaMalloc(&p, b);
+  if (e != cudaSuccess) {
+    p = nullptr;
+    bytes = 0;
+    cudaGetLastError();
+    fail(LLMP_ENOMEM, "cudaMalloc(" + std::to_string(b) + " bytes) failed: " + cudaGetErrorString(e));
+  }
+}
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+
+cudaEvent_t Ctx::get_event() {
+  if (!free_events.empty()) {
+    cudaEvent_t e = free_events.back();
+    free_events.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  LLMP_CUDA(cudaEventCreate(&e));
+  return e;
+}
+void Ctx::before(int cls, cudaEvent_t* ev) {
+  (void)cls;
+  if (!timing) return;
+  *ev = get_event();
+  LLMP_CUDA(cudaEventRecord(*ev, stream));
+}
+void Ctx::after(int cls, cudaEvent_t ev, double nrows) {
+  launches[cls] += 1;
+  rows[cls] += nrows;
+  if (!timing || !ev) return;
+  cudaEvent_t b = get_event();
+  LLMP_CUDA(cudaEventRecord(b, stream));
+  pending.push_back(EventPair{ev, b, cls});
+  if (pending.size() > 200000) collect();
+}
+void Ctx::collect() {
+  if (pending.empty()) return;
+  LLMP_CUDA(cudaStreamSynchronize(stream));
+  for (auto& e : pending) {
+    float ms = 0.f;
+    LLMP_CUDA(cudaEventElapsedTime(&ms, e.a, e.b));
+    ms_done[e.cls] += ms;
+    free_events.push_back(e.a);
+    free_events.push_back(e.b);
+  }
+  pending.clear();
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+const void* to_device(Ctx* ctx, const void* p, size_t bytes, DevBuf& tmp) {
+  if (!p || is_device_ptr(p)) return p;
+  tmp.ensure(bytes);
+  LLMP_CUDA(cudaMemcpyAsync(tmp.p, p, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return tmp.p;
+}
+
+// ---------------------------------------------------------------------------------------------
+// NCCL through dlopen (the torch-bundled libnccl.so.2 is already loaded in a torch process)
+namespace {
+typedef int ncclResult_t;
+typedef void* ncclComm_t;
+struct NcclUniqueId { char internal[128]; };
+enum { ncclInt8 = 0, ncclUint8 = 1, ncclInt32 = 2, ncclUint32 = 3, ncclInt64 = 4, ncclUint64 = 5 };
+enum { ncclSum = 0, ncclProd = 1, ncclMax = 2, ncclMin = 3 };
+struct NcclApi {
+  bool loaded = false;
+  ncclResult_t (*getUniqueId)(NcclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, NcclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+void load_nccl() {
+  if (g_nccl.loaded) return;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) fail(LLMP_ENCCL, std::string("cannot dlopen libnccl.so.2: ") + dlerror());
+  g_nccl.getUniqueId = (decltype(g_nccl.getUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.commInitRank = (decltype(g_nccl.commInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.allGather = (decltype(g_nccl.allGather))dlsym(h, "ncclAllGather");
+  g_nccl.getErrorString = (decltype(g_nccl.getErrorString))dlsym(h, "ncclGetErrorString");
+  if (!g_nccl.commInitRank || !g_nccl.allReduce || !g_nccl.allGather || !g_nccl.commDestroy)
+    fail(LLMP_ENCCL, "libnccl.so.2 lacks the needed symbols");
+  g_nccl.loaded = true;
+}
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r == 0) return;
+  fail(LLMP_ENCCL, std::string(what) + ": " + (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "nccl error"));
+}
+}  // namespace
+
+void nccl_init(Ctx* ctx, const void* unique_id) {
+  load_nccl();
+  NcclUniqueId id;
+  memcpy(&id, unique_id, sizeof(id));
+  ncclComm_t comm = nullptr;
+  nccl_check(g_nccl.commInitRank(&comm, ctx->nranks, id, ctx->rank), "ncclCommInitRank");
+  ctx->nccl = comm;
+}
+void nccl_unique_id(void* out) {
+  load_nccl();
+  LLMP_REQUIRE(g_nccl.getUniqueId != nullptr, "ncclGetUniqueId missing");
+  NcclUniqueId id;
+  nccl_check(g_nccl.getUniqueId(&id), "ncclGetUniqueId");
+  memcpy(out, &id, sizeof(id));
+}
+void nccl_destroy(Ctx* ctx) {
+  if (ctx->nccl && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)ctx->nccl);
+  ctx->nccl = nullptr;
+}
+static void coll_before(Ctx* ctx, cudaEvent_t* ev) { ctx->before(KC_NCCL, ev); }
+void allreduce_sum_i64(Ctx* ctx, int64_t* buf, size_t count) {
+  if (!ctx->nccl || count == 0) return;
+  cudaEvent_t ev = nullptr;
+  coll_before(ctx, &ev);
+  nccl_check(g_nccl.allReduce(buf, buf, count, ncclInt64, ncclSum, (ncclComm_t)ctx->nccl, ctx->stream), "ncclAllReduce");
+  ctx->after(KC_NCCL, ev, (double)count * 8);
+}
+void allreduce_max_u32(Ctx* ctx, uint32_t* buf, size_t count) {
+  if (!ctx->nccl || count == 0) return;
+  cudaEvent_t ev = nullptr;
+  coll_before(ctx, &ev);
+  nccl_check(g_nccl.allReduce(buf, buf, count, ncclUint32, ncclMax, (ncclComm_t)ctx->nccl, ctx->stream), "ncclAllReduce");
+  ctx->after(KC_NCCL, ev, (double)count * 4);
+}
+void allreduce_max_u64(Ctx* ctx, uint64_t* buf, size_t count) {
+  if (!ctx->nccl || count == 0) return;
+  cudaEvent_t ev = nullptr;
+  coll_before(ctx, &ev);
+  nccl_check(g_nccl.allReduce(buf, buf, count, ncclUint64, ncclMax, (ncclComm_t)ctx->nccl, ctx->stream), "ncclAllReduce");
+  ctx->after(KC_NCCL, ev, (double)count * 8);
+}
+void allgather_bytes(Ctx* ctx, const void* send, void* recv, size_t bytes_per_rank) {
+  if (!ctx->nccl) {
+    if (send != recv) LLMP_CUDA(cudaMemcpyAsync(recv, send, bytes_per_rank, cudaMemcpyDeviceToDevice, ctx->stream));
+    return;
+  }
+  cudaEvent_t ev = nullptr;
+  coll_before(ctx, &ev);
+  nccl_check(g_nccl.allGather(send, recv, bytes_per_rank, ncclUint8, (ncclComm_t)ctx->nccl, ctx->stream), "ncclAllGather");
+  ctx->after(KC_NCCL, ev, (double)bytes_per_rank * ctx->nranks);
+}
+
+}  // namespace llmp

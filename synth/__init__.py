@@ -234,6 +234,22 @@ def make(config: str, seed: int = 0, shard: int = 0, n_shards: int = 1) -> Datas
                    user_levels=np.asarray(levels, np.int32), name=c)
 
 
+def make_scaled(n_llm_total: int, shard: int = 0, n_shards: int = 1, seed: int = 0) -> Dataset:
+    """C3/C4 family: n_llm_total LLMs x the 8 C3 profiles x 16 levels, rows in (LLM, profile, u)
+    order, contiguous LLM-block shards (shard boundaries are multiples of 128 rows, so every
+    Eq. (4) group stays on one rank).  C3 = make_scaled(78125); C4 = make_scaled(781250, r, p)."""
+    lo = shard * n_llm_total // n_shards
+    hi = (shard + 1) * n_llm_total // n_shards
+    X, y, li, pi, fl, fp = _assemble(seed, np.arange(lo, hi), PROFILES_C3, LEVELS_16, 1.0, 16.0, LLM_FIELDS,
+                                     PROFILE_FIELDS, False, local_ids=False)
+    ds = Dataset(X=X, y=y, llm_id=li, prof_id=pi, users_col=X.shape[1] - 1, n_llm=n_llm_total,
+                 n_prof=len(PROFILES_C3), f_llm=fl, f_prof=fp, profiles=list(PROFILES_C3),
+                 cost=profile_cost(PROFILES_C3), user_levels=np.asarray(LEVELS_16, np.int32), name="scaled")
+    ds.row_offset = lo * len(PROFILES_C3) * len(LEVELS_16)
+    ds.n_global = n_llm_total * len(PROFILES_C3) * len(LEVELS_16)
+    return ds
+
+
 def make_s1(n: int, seed: int = 0, F: int = 32, row_offset: int = 0) -> Dataset:
     """S1 control (best case for atomics): uniform random features, SURVEY §8(d)."""
     rows = np.arange(row_offset, row_offset + n, dtype=np.int64)
