@@ -18,9 +18,13 @@
 #include <float.h>
 #include <math.h>
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 
 #include "internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace llmp {
 
@@ -39,9 +43,6 @@ constexpr int TILE = PART_THREADS * PART_ITEMS;  // 2048 rows per look-back tile
 constexpr int SPLIT_THREADS = 256;
 constexpr int SLOT = 2 * kHistBins;        // int64 per histogram slot (g then h)
 
-constexpr uint64_t FLAG_AGG = 1ull << 62;
-constexpr uint64_t FLAG_INCL = 2ull << 62;
-constexpr uint64_t FLAG_MASK = (1ull << 62) - 1;
 
 __device__ __forceinline__ double exp2i(int e) {  // exact 2^e for e in [-1022, 1023]
   return __longlong_as_double((long long)(e + 1023) << 52);
@@ -56,9 +57,12 @@ struct LevelView {
   int32_t* split_f;  // [2^d] -1 = leaf / absent
   int32_t* split_b;
   int32_t* built;    // [2^(d-1)] which child of parent j was histogrammed (0 left, 1 right)
+  int32_t* done;     // [2^d] per-node count of finished split CTAs (self-resetting)
   uint64_t* flags;   // look-back tile flags
   int32_t* ticket;
 };
+
+struct FeatBest;
 
 struct FitArgs {
   int64_t n, row_offset;
@@ -85,6 +89,7 @@ struct FitArgs {
   uint64_t seed;
   int monotone;
   int nn;
+  FeatBest* fbest;            // [2^(D-1)][32] per-(node, feature) best split of the current level
   unsigned long long* units;  // device counters of rows processed per kernel class (instrumentation)
 };
 
@@ -196,7 +201,6 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
   }
   int64_t* Hbase = (MODE == HM_DEBUG) ? dbg.out : a.H[d & 1];
   const uint2* st_in = (MODE == HM_LEVEL) ? a.st[d & 1] : nullptr;
-  const int F = (MODE == HM_DEBUG) ? kMaxF : a.F;
 
   // first piece overlapping [v0, v1)
   int pc = 0;
@@ -209,64 +213,80 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
     for (int64_t c0 = s0; c0 < s1; c0 += HIST_CHUNK) {
       const int64_t c1 = min(s1, c0 + HIST_CHUNK);
       const int64_t clen = c1 - c0;
-      // contiguous sub-range per warp
+      // contiguous sub-range per warp; rows staged 32 at a time in the warp's smem buffer
+      // (bytes 0..31 = the row's codes, bytes 32..35 = its packed gradient pair)
       const int64_t w0 = c0 + clen * warp / HIST_WARPS, w1 = c0 + clen * (warp + 1) / HIST_WARPS;
-      int prev = -1;
-      int32_t ag = 0;
+
+      const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sg) + (uint32_t)lane * 4u;
+      int prev = -1;              // code of the current run of this lane's feature
+      int32_t ag = 0;             // run sums
       uint32_t ah = 0;
-      for (int64_t base = w0; base < w1; base += 32) {
-        const int64_t vi = base + lane;   // virtual row
-        const int cnt = (int)min((int64_t)32, w1 - base);
-        uint32_t gp = 0;
+      // register prefetch of the first batch
+      uint4 nc0 = make_uint4(0, 0, 0, 0), nc1 = nc0;
+      uint32_t ngp = 0;
+      float ny = 0.f, nw = 0.f, np_ = 0.f;
+      auto load_batch = [&](int64_t base) {
+        const int64_t vi = base + lane;
         if (vi < w1) {
           const int64_t pi = s_pstart[pc] + (vi - s_vstart[pc]);  // physical position
           int64_t ridx;
           if (MODE == HM_ROOT) {
             ridx = pi;
-            float yv = a.y[ridx], wv = a.w[ridx], pv = a.p[ridx];
-            float g = __fmul_rn(wv, __fsub_rn(pv, yv));
-            float h = wv;
-            if (row_sampled_out(a.seed, a.target, t, a.row_offset + ridx, a.subsample)) {
-              g = 0.f;
-              h = 0.f;
-            }
-            gp = pack_gp(quantize(g, scale_g), quantize(h, scale_h));
-            a.gp_root[ridx] = gp;
+            ny = a.y[ridx];
+            nw = a.w[ridx];
+            np_ = a.p[ridx];
           } else if (MODE == HM_LEVEL) {
-            uint2 s = st_in[pi];
+            const uint2 s = st_in[pi];
             ridx = s.x;
-            gp = s.y;
+            ngp = s.y;
           } else {
             ridx = dbg.idx ? dbg.idx[pi] : pi;
-            gp = pack_gp(dbg.qg[ridx], dbg.qh[ridx]);
+            ngp = pack_gp(dbg.qg[ridx], dbg.qh[ridx]);
           }
-          const uint4* crow = reinterpret_cast<const uint4*>(a.codes +
-                                                             (size_t)ridx * kMaxF);
-          uint4 c0v = __ldg(crow), c1v = __ldg(crow + 1);
-          *reinterpret_cast<uint4*>(rowbuf + lane * ROWBUF_STRIDE) = c0v;
-          *reinterpret_cast<uint4*>(rowbuf + lane * ROWBUF_STRIDE + 16) = c1v;
+          const uint4* crow = reinterpret_cast<const uint4*>(a.codes + (size_t)ridx * kMaxF);
+          nc0 = __ldg(crow);
+          nc1 = __ldg(crow + 1);
         }
+      };
+      if (w0 < w1) load_batch(w0);
+      for (int64_t base = w0; base < w1; base += 32) {
+        const int cnt = (int)min((int64_t)32, w1 - base);
+        uint32_t gp = ngp;
+        if (MODE == HM_ROOT && lane < cnt) {
+          const int64_t ridx = base + lane + (s_pstart[pc] - s_vstart[pc]);
+          float g = __fmul_rn(nw, __fsub_rn(np_, ny));
+          float h = nw;
+          if (row_sampled_out(a.seed, a.target, t, a.row_offset + ridx, a.subsample)) {
+            g = 0.f;
+            h = 0.f;
+          }
+          gp = pack_gp(quantize(g, scale_g), quantize(h, scale_h));
+          a.gp_root[ridx] = gp;
+        }
+        __syncwarp();   // previous batch fully consumed
+        *reinterpret_cast<uint4*>(rowbuf + lane * ROWBUF_STRIDE) = nc0;
+        *reinterpret_cast<uint4*>(rowbuf + lane * ROWBUF_STRIDE + 16) = nc1;
+        *reinterpret_cast<uint32_t*>(rowbuf + lane * ROWBUF_STRIDE + 32) = gp;
         __syncwarp();
+        if (base + 32 < w1) load_batch(base + 32);   // prefetch the next batch
+        if (prev < 0) prev = rowbuf[lane];
+#pragma unroll 4
         for (int r = 0; r < cnt; ++r) {
-          const uint32_t g2 = __shfl_sync(0xffffffffu, gp, r);
-          if (lane < F) {
-            const int c = rowbuf[r * ROWBUF_STRIDE + lane];
-            if (c != prev) {
-              if (prev >= 0) {
-                atomicAdd(&sg[prev * 32 + lane], ag);
-                atomicAdd(&sh[prev * 32 + lane], ah);
-              }
-              prev = c;
-              ag = 0;
-              ah = 0;
-            }
-            ag += gp_g(g2);
-            ah += (uint32_t)gp_h(g2);
+          const int c = rowbuf[r * ROWBUF_STRIDE + lane];
+          const uint32_t g2 = *reinterpret_cast<const uint32_t*>(rowbuf + r * ROWBUF_STRIDE + 32);
+          const int ch = c != prev;
+          // on a code change flush the finished run (two 32-bit shared reductions, one branch)
+          if (ch) {
+            const uint32_t ad = sbase + (uint32_t)prev * 128u;
+            asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(ad), "r"(ag) : "memory");
+            asm volatile("red.shared.add.u32 [%0+32768], %1;" ::"r"(ad), "r"(ah) : "memory");
           }
+          ag = (ch ? 0 : ag) + gp_g(g2);
+          ah = (ch ? 0u : ah) + (uint32_t)gp_h(g2);
+          prev = c;
         }
-        __syncwarp();
       }
-      if (prev >= 0 && lane < F) {
+      if (prev >= 0) {
         atomicAdd(&sg[prev * 32 + lane], ag);
         atomicAdd(&sh[prev * 32 + lane], ah);
       }
@@ -289,358 +309,355 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
 }
 
 // ---------------------------------------------------------------------------------------------
-// stable partition of the split parents' rows (level d-1) into their children (level d):
-// single pass, decoupled look-back over 2048-row tiles taken in ticket order; left children
-// go to region A = [0, n), right children to region B = [n, 2n) of the output state buffer, so
-// a child's segment is contiguous and keeps the parent's row order.
-__global__ void __launch_bounds__(PART_THREADS) k_partition(const FitArgs a, const int d, const int grid) {
+// stable partition of the split parents' rows (level d-1) into their children (level d).
+// Cooperative single pass (all CTAs co-resident, launched with cudaLaunchCooperativeKernel):
+//   phase 1: each CTA counts the rows going left in its contiguous chunk of the level's row
+//            sequence (split parents concatenated in node order) -> agg[c]
+//   grid.sync()
+//   phase 2: exclusive prefix of agg over CTAs (warp-parallel); the chunk is re-read (mostly L2
+//            hits) in 2048-row sub-tiles, block-scanned, and scattered: left rows to region
+//            A = [0, n) at the global left prefix, right rows to region B = [n, 2n) at the global
+//            right prefix.  Each child segment is contiguous and keeps its parent's row order.
+__global__ void __launch_bounds__(PART_THREADS) k_partition(const FitArgs a, const int d, int64_t* agg) {
+  cg::grid_group grid = cg::this_grid();
   const int NP = 1 << (d - 1);
   const LevelView& P = a.lv[d - 1];
   const LevelView& C = a.lv[d];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  __shared__ int s_tile_pref[MAX_PIECES + 1];
-  __shared__ int64_t s_seq_pref[MAX_PIECES + 1];
-  __shared__ uint2 s_state[TILE];
-  __shared__ int s_wsum[PART_THREADS / 32];
+  const int G = gridDim.x;
+  __shared__ int64_t s_seq_pref[MAX_PIECES + 1];   // virtual start of each parent's rows
   __shared__ int64_t s_wsum64[PART_THREADS / 32];
-  __shared__ int s_ticket;
-  __shared__ int64_t s_excl;
+  __shared__ int s_wsum[PART_THREADS / 32];
+  __shared__ uint2 s_state[TILE];
+  __shared__ int64_t s_prefix;
 
-  // ---- prologue: per-parent tile and row prefixes (two parents per thread)
+  // ---- per-parent row prefix (two parents per thread)
   {
-    int tl[2] = {0, 0};
     int64_t rl[2] = {0, 0};
     for (int q = 0; q < 2; ++q) {
-      int j = tid * 2 + q;
-      if (j < NP && P.split_f[j] >= 0) {
-        int64_t c = (d == 1) ? a.n : P.cnt[j];
-        rl[q] = c;
-        tl[q] = (int)((c + TILE - 1) / TILE);
-      }
+      const int j = tid * 2 + q;
+      if (j < NP && P.split_f[j] >= 0) rl[q] = (d == 1) ? a.n : P.cnt[j];
     }
-    int tv = tl[0] + tl[1];
-    int64_t rv = rl[0] + rl[1];
-    int tinc = tv;
+    const int64_t rv = rl[0] + rl[1];
     int64_t rinc = rv;
     for (int o = 1; o < 32; o <<= 1) {
-      int u = __shfl_up_sync(0xffffffffu, tinc, o);
-      int64_t u64 = __shfl_up_sync(0xffffffffu, rinc, o);
-      if (lane >= o) {
-        tinc += u;
-        rinc += u64;
-      }
+      const int64_t u = __shfl_up_sync(0xffffffffu, rinc, o);
+      if (lane >= o) rinc += u;
     }
-    if (lane == 31) {
-      s_wsum[warp] = tinc;
-      s_wsum64[warp] = rinc;
-    }
+    if (lane == 31) s_wsum64[warp] = rinc;
     __syncthreads();
-    int toff = 0;
     int64_t roff = 0;
-    for (int w2 = 0; w2 < warp; ++w2) {
-      toff += s_wsum[w2];
-      roff += s_wsum64[w2];
-    }
-    int te = toff + tinc - tv;
+    for (int w2 = 0; w2 < warp; ++w2) roff += s_wsum64[w2];
     int64_t re = roff + rinc - rv;
     for (int q = 0; q < 2; ++q) {
-      int j = tid * 2 + q;
-      if (j < NP) {
-        s_tile_pref[j] = te;
-        s_seq_pref[j] = re;
-      }
-      te += tl[q];
+      const int j = tid * 2 + q;
+      if (j < NP) s_seq_pref[j] = re;
       re += rl[q];
     }
-    if (tid == PART_THREADS - 1) {
-      s_tile_pref[NP] = te;   // grand totals (threads past NP add zeros)
-      s_seq_pref[NP] = re;
-    }
+    if (tid == PART_THREADS - 1) s_seq_pref[NP] = re;
   }
-  __syncthreads();
   // ---- zero the built-child histogram slots [0, NP) of this level for split parents
   {
     int4* Hz = reinterpret_cast<int4*>(a.H[d & 1]);
     const size_t per_slot = SLOT / 2;  // int4 per slot
     const size_t total = (size_t)NP * per_slot;
-    for (size_t e = (size_t)blockIdx.x * PART_THREADS + tid; e < total; e += (size_t)grid * PART_THREADS) {
-      int j = (int)(e / per_slot);
+    for (size_t e = (size_t)blockIdx.x * PART_THREADS + tid; e < total; e += (size_t)G * PART_THREADS) {
+      const int j = (int)(e / per_slot);
       if (P.split_f[j] >= 0) Hz[e] = make_int4(0, 0, 0, 0);
     }
   }
   __syncthreads();
-  const int total_tiles = s_tile_pref[NP];
+  const int64_t S = s_seq_pref[NP];
+  const int64_t v0 = S * blockIdx.x / G, v1 = S * (blockIdx.x + 1) / G;
+  if (tid == 0 && a.units) atomicAdd(&a.units[KC_PARTITION], (unsigned long long)(v1 - v0));
   const uint2* st_in = (d >= 2) ? a.st[(d - 1) & 1] : nullptr;
   uint2* st_out = a.st[d & 1];
+  int jfirst = 0;   // first parent overlapping [v0, v1)
+  while (jfirst + 1 < NP && s_seq_pref[jfirst + 1] <= v0) ++jfirst;
 
-  while (true) {
-    if (tid == 0) s_ticket = atomicAdd(C.ticket, 1);
-    __syncthreads();
-    const int tk = s_ticket;
-    if (tk >= total_tiles) break;
-    // parent j: largest j with tile_pref[j] <= tk
-    int lo = 0, hi = NP - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (s_tile_pref[mid] <= tk) lo = mid;
-      else hi = mid - 1;
-    }
-    const int j = lo;
-    const int64_t cnt_j = (d == 1) ? a.n : P.cnt[j];
-    const int64_t start_j = (d == 1) ? 0 : P.start[j];
-    const int64_t o = (int64_t)(tk - s_tile_pref[j]) * TILE;
-    const int len = (int)min((int64_t)TILE, cnt_j - o);
+  // ---- phase 1: count left rows of the chunk
+  int64_t myl = 0;
+  for (int j = jfirst; j < NP && s_seq_pref[j] < v1; ++j) {
+    const int64_t p0 = max(v0, s_seq_pref[j]), p1 = min(v1, s_seq_pref[j + 1]);
+    if (p0 >= p1) continue;
     const int f = P.split_f[j], b = P.split_b[j];
-    if (tid == 0 && a.units) atomicAdd(&a.units[KC_PARTITION], (unsigned long long)len);
-    // stage the tile's (ridx, gpair) state
-    for (int k = tid; k < len; k += PART_THREADS) {
-      if (d == 1) {
-        int64_t r = o + k;
-        s_state[k] = make_uint2((uint32_t)r, a.gp_root[r]);
-      } else {
-        s_state[k] = st_in[start_j + o + k];
-      }
-    }
-    __syncthreads();
     const uint8_t* col = a.codesT + (size_t)f * a.n;
-    uint32_t lbits = 0;
-    int myl = 0;
-#pragma unroll
-    for (int q = 0; q < PART_ITEMS; ++q) {
-      int k = tid * PART_ITEMS + q;
-      if (k < len) {
-        int left = col[s_state[k].x] <= b;
-        lbits |= (uint32_t)left << q;
-        myl += left;
+    const int64_t base = (d == 1) ? 0 : P.start[j] - s_seq_pref[j];   // physical = base + virtual
+    for (int64_t v = p0 + tid; v < p1; v += PART_THREADS) {
+      const uint32_t ridx = (d == 1) ? (uint32_t)v : st_in[base + v].x;
+      myl += col[ridx] <= b;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) myl += __shfl_xor_sync(0xffffffffu, myl, o);
+  if (lane == 0) s_wsum64[warp] = myl;
+  __syncthreads();
+  if (tid == 0) {
+    int64_t t = 0;
+    for (int w2 = 0; w2 < PART_THREADS / 32; ++w2) t += s_wsum64[w2];
+    agg[blockIdx.x] = t;
+  }
+  grid.sync();
+  // ---- exclusive prefix over CTAs
+  if (warp == 0) {
+    int64_t sum = 0;
+    for (int c = lane; c < (int)blockIdx.x; c += 32) sum += agg[c];
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) s_prefix = sum;
+  }
+  __syncthreads();
+  int64_t lrun = s_prefix;   // global left prefix at the current position
+  // ---- phase 2: scatter in 2048-row sub-tiles (blocked: 8 consecutive rows per thread)
+  for (int j = jfirst; j < NP && s_seq_pref[j] < v1; ++j) {
+    const int64_t p0 = max(v0, s_seq_pref[j]), p1 = min(v1, s_seq_pref[j + 1]);
+    if (p0 >= p1) continue;
+    const int f = P.split_f[j], b = P.split_b[j];
+    const uint8_t* col = a.codesT + (size_t)f * a.n;
+    const int64_t base = (d == 1) ? 0 : P.start[j] - s_seq_pref[j];
+    if (p0 == s_seq_pref[j] && tid == 0) {   // this CTA holds the parent's first row
+      C.start[2 * j] = lrun;
+      C.start[2 * j + 1] = a.n + (p0 - lrun);
+    }
+    int64_t piece_left = 0;
+    for (int64_t t0 = p0; t0 < p1; t0 += TILE) {
+      const int len = (int)min((int64_t)TILE, p1 - t0);
+      for (int k = tid; k < len; k += PART_THREADS) {
+        const int64_t v = t0 + k;
+        s_state[k] = (d == 1) ? make_uint2((uint32_t)v, a.gp_root[v]) : st_in[base + v];
       }
-    }
-    // block exclusive scan of left counts
-    int inc = myl;
-    for (int off = 1; off < 32; off <<= 1) {
-      int u = __shfl_up_sync(0xffffffffu, inc, off);
-      if (lane >= off) inc += u;
-    }
-    if (lane == 31) s_wsum[warp] = inc;
-    __syncthreads();
-    int woff = 0, L = 0;
-    for (int w2 = 0; w2 < PART_THREADS / 32; ++w2) {
-      if (w2 < warp) woff += s_wsum[w2];
-      L += s_wsum[w2];
-    }
-    const int my_excl = woff + inc - myl;
-    // decoupled look-back (one thread; predecessors are in flight or done: tickets are ordered)
-    if (tid == 0) {
-      volatile unsigned long long* fl = reinterpret_cast<volatile unsigned long long*>(C.flags);
-      int64_t excl = 0;
-      if (tk == 0) {
-        fl[0] = FLAG_INCL | (uint64_t)L;
-      } else {
-        fl[tk] = FLAG_AGG | (uint64_t)L;
-        int pr = tk - 1;
-        while (true) {
-          unsigned long long v = fl[pr];
-          unsigned long long stt = v & ~FLAG_MASK;
-          if (stt == 0) continue;
-          excl += (int64_t)(v & FLAG_MASK);
-          if (stt == FLAG_INCL) break;
-          --pr;
+      __syncthreads();
+      uint32_t lbits = 0;
+      int cnt = 0;
+#pragma unroll
+      for (int q = 0; q < PART_ITEMS; ++q) {
+        const int k = tid * PART_ITEMS + q;
+        if (k < len) {
+          const int left = col[s_state[k].x] <= b;
+          lbits |= (uint32_t)left << q;
+          cnt += left;
         }
-        fl[tk] = FLAG_INCL | (uint64_t)(excl + L);
       }
-      s_excl = excl;
-      if (o == 0) {
-        C.start[2 * j] = excl;
-        C.start[2 * j + 1] = a.n + (s_seq_pref[j] - excl);
+      int inc = cnt;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
       }
-      atomicAdd(reinterpret_cast<unsigned long long*>(&C.cnt[2 * j]), (unsigned long long)L);
-      atomicAdd(reinterpret_cast<unsigned long long*>(&C.cnt[2 * j + 1]), (unsigned long long)(len - L));
-    }
-    __syncthreads();
-    const int64_t excl = s_excl;
-    const int64_t rbase = a.n + (s_seq_pref[j] + o - excl);
-    int lpos = my_excl, rpos = tid * PART_ITEMS - my_excl;
+      if (lane == 31) s_wsum[warp] = inc;
+      __syncthreads();
+      int woff = 0, L = 0;
+      for (int w2 = 0; w2 < PART_THREADS / 32; ++w2) {
+        if (w2 < warp) woff += s_wsum[w2];
+        L += s_wsum[w2];
+      }
+      const int my_excl = woff + inc - cnt;
+      const int64_t rbase = a.n + (t0 - lrun);     // global right prefix at t0 = t0 - lefts before t0
+      int lpos = my_excl, rpos = tid * PART_ITEMS - my_excl;
 #pragma unroll
-    for (int q = 0; q < PART_ITEMS; ++q) {
-      int k = tid * PART_ITEMS + q;
-      if (k < len) {
-        uint2 s = s_state[k];
-        if ((lbits >> q) & 1u) st_out[excl + lpos++] = s;
-        else st_out[rbase + rpos++] = s;
+      for (int q = 0; q < PART_ITEMS; ++q) {
+        const int k = tid * PART_ITEMS + q;
+        if (k < len) {
+          const uint2 s = s_state[k];
+          if ((lbits >> q) & 1u) st_out[lrun + lpos++] = s;
+          else st_out[rbase + rpos++] = s;
+        }
       }
+      lrun += L;
+      piece_left += L;
+      __syncthreads();
     }
-    __syncthreads();
+    if (tid == 0) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&C.cnt[2 * j]), (unsigned long long)piece_left);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&C.cnt[2 * j + 1]), (unsigned long long)(p1 - p0 - piece_left));
+    }
   }
 }
-
 // ---------------------------------------------------------------------------------------------
-// split evaluation: one CTA per node of level d
-struct Best {
+// split evaluation: one CTA per (node of level d, feature), one bin per thread.  Each CTA forms
+// its feature's histogram (sibling = parent - built, exact int64, written back for the next
+// level), block-scans it, evaluates every threshold in fp64 (monotone veto on users) and
+// publishes its best (loss, b, GL, HL); the last CTA of the node (ticket counter) picks the
+// node's best over features with the (loss desc, f asc, b asc) total order and writes the tree.
+struct FeatBest {
   double loss;
-  int f, b;
+  int32_t b, valid;
+  int64_t GLq, HLq, Gq, Hq;
 };
-__device__ __forceinline__ bool better(const Best& x, const Best& y) {
-  if (x.loss != y.loss) return x.loss > y.loss;
-  if (x.f != y.f) return x.f < y.f;
-  return x.b < y.b;
+
+__device__ __forceinline__ bool better_fb(double la, int fa, int ba, double lb, int fb, int bb) {
+  if (la != lb) return la > lb;
+  if (fa != fb) return fa < fb;
+  return ba < bb;
 }
 
 __global__ void __launch_bounds__(SPLIT_THREADS) k_split(const FitArgs a, const int d, const int t) {
-  const int k = blockIdx.x;
+  const int k = blockIdx.x >> 5, f = blockIdx.x & 31;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const LevelView& V = a.lv[d];
   int64_t* Hself;
+  int64_t g, h;
   if (d == 0) {
     Hself = a.H[0];
+    g = Hself[f * kBins + tid];
+    h = Hself[kHistBins + f * kBins + tid];
   } else {
     const int j = k >> 1;
     if (a.lv[d - 1].split_f[j] < 0) {
-      if (tid == 0) V.split_f[k] = -1;
+      if (f == 0 && tid == 0) V.split_f[k] = -1;
       return;
     }
     const int side = V.built[j];
     const bool is_built = (k & 1) == side;
     Hself = a.H[d & 1] + (size_t)(is_built ? j : (1 << (d - 1)) + j) * SLOT;
-    if (!is_built) {
-      // sibling = parent - built (exact integers)
-      const longlong2* Hp = reinterpret_cast<const longlong2*>(a.H[(d - 1) & 1] + (size_t)node_slot(a, d - 1, j) * SLOT);
-      const longlong2* Hb = reinterpret_cast<const longlong2*>(a.H[d & 1] + (size_t)j * SLOT);
-      longlong2* Hs = reinterpret_cast<longlong2*>(Hself);
-      for (int e = tid; e < SLOT / 2; e += SPLIT_THREADS) {
-        longlong2 p = Hp[e], q = Hb[e];
-        Hs[e] = make_longlong2(p.x - q.x, p.y - q.y);
-      }
-      __syncthreads();
+    if (is_built) {
+      g = Hself[f * kBins + tid];
+      h = Hself[kHistBins + f * kBins + tid];
+    } else {
+      const int64_t* Hp = a.H[(d - 1) & 1] + (size_t)node_slot(a, d - 1, j) * SLOT;
+      const int64_t* Hb = a.H[d & 1] + (size_t)j * SLOT;
+      g = Hp[f * kBins + tid] - Hb[f * kBins + tid];
+      h = Hp[kHistBins + f * kBins + tid] - Hb[kHistBins + f * kBins + tid];
+      Hself[f * kBins + tid] = g;
+      Hself[kHistBins + f * kBins + tid] = h;
     }
   }
-  __shared__ int64_t s_G, s_H;
-  __shared__ uint8_t s_fmask[kMaxF];
-  __shared__ Best s_best[SPLIT_THREADS / 32];
-  const int64_t* Hg = Hself;
-  const int64_t* Hh = Hself + kHistBins;
-  if (warp == 0) {
-    int64_t gs = 0, hs = 0;
-    for (int b = lane; b < kBins; b += 32) {
-      gs += Hg[b];
-      hs += Hh[b];
+  // block inclusive scan of (g, h) over the 256 bins
+  __shared__ int64_t s_wg[SPLIT_THREADS / 32], s_wh[SPLIT_THREADS / 32];
+  __shared__ double s_bl[SPLIT_THREADS / 32];
+  __shared__ int s_bb[SPLIT_THREADS / 32];
+  __shared__ int s_last;
+  int64_t ig = g, ih = h;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t ug = __shfl_up_sync(0xffffffffu, ig, o), uh = __shfl_up_sync(0xffffffffu, ih, o);
+    if (lane >= o) {
+      ig += ug;
+      ih += uh;
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      gs += __shfl_xor_sync(0xffffffffu, gs, o);
-      hs += __shfl_xor_sync(0xffffffffu, hs, o);
-    }
-    if (lane == 0) {
-      s_G = gs;
-      s_H = hs;
-    }
-  } else if (warp == 1) {
-    // column sample of tree t: keep ceil(colsample*F) features with the smallest keys
-    int F = a.F;
-    int nkeep = F;
-    if (a.colsample < 1.0f) {
-      nkeep = (int)ceil((double)a.colsample * (double)F);
-      if (nkeep < 1) nkeep = 1;
-    }
-    uint64_t key = (lane < F) ? rng4(a.seed, (uint64_t)(2 * a.target + 1), (uint64_t)t, (uint64_t)lane) : ~0ull;
-    int rank = 0;
-    for (int f2 = 0; f2 < F; ++f2) {
-      uint64_t k2 = __shfl_sync(0xffffffffu, key, f2);
-      if (k2 < key || (k2 == key && f2 < lane)) ++rank;
-    }
-    s_fmask[lane] = (lane < F && rank < nkeep) ? 1 : 0;
+  }
+  if (lane == 31) {
+    s_wg[warp] = ig;
+    s_wh[warp] = ih;
   }
   __syncthreads();
-  const int64_t Gq = s_G, Hq = s_H;
+  int64_t og = 0, oh = 0, Gq = 0, Hq = 0;
+  for (int w2 = 0; w2 < SPLIT_THREADS / 32; ++w2) {
+    if (w2 < warp) {
+      og += s_wg[w2];
+      oh += s_wh[w2];
+    }
+    Gq += s_wg[w2];
+    Hq += s_wh[w2];
+  }
+  const int64_t GLq = og + ig, HLq = oh + ih;   // left = bins 0..tid
+  // column sample of tree t (R21): rank of f among the F keys
+  bool fin = f < a.F;
+  if (fin && a.colsample < 1.0f) {
+    const int F = a.F;
+    int nkeep = (int)ceil((double)a.colsample * (double)F);
+    if (nkeep < 1) nkeep = 1;
+    const uint64_t kf = rng4(a.seed, (uint64_t)(2 * a.target + 1), (uint64_t)t, (uint64_t)f);
+    const uint64_t kl = lane < F ? rng4(a.seed, (uint64_t)(2 * a.target + 1), (uint64_t)t, (uint64_t)lane) : ~0ull;
+    const unsigned less = __ballot_sync(0xffffffffu, lane < F && (kl < kf || (kl == kf && lane < f)));
+    fin = __popc(less) < nkeep;
+  }
   const int eg = exp_of(__uint_as_float(a.maxg[t])), eh = exp_of(__uint_as_float(a.maxh[t]));
   const double sgi = exp2i(eg - a.K), shi = exp2i(eh - a.K);
   const double lo = (d == 0) ? -INFINITY : V.lo[k], hi = (d == 0) ? INFINITY : V.hi[k];
   const double lambda = a.lambda, mcw = a.mcw;
-  const double G = dequant(Gq, sgi), H = dequant(Hq, shi);
-  const double wP = calc_weight(G, H, lo, hi, lambda, mcw);
-  const double gainP = calc_gain(G, H, wP, lambda);
-
-  Best best{-INFINITY, 0x7fffffff, 0x7fffffff};
-  for (int fi = 0; fi < 4; ++fi) {
-    const int f = warp + 8 * fi;
-    if (f >= a.F || !s_fmask[f]) continue;
-    const int nb = a.ncuts[f] + 1;
-    if (nb < 2) continue;
-    int64_t pg[8], ph[8];
-    const longlong2* g2 = reinterpret_cast<const longlong2*>(Hg + f * kBins + lane * 8);
-    const longlong2* h2 = reinterpret_cast<const longlong2*>(Hh + f * kBins + lane * 8);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      longlong2 gv = g2[q], hv = h2[q];
-      pg[2 * q] = gv.x;
-      pg[2 * q + 1] = gv.y;
-      ph[2 * q] = hv.x;
-      ph[2 * q + 1] = hv.y;
-    }
-#pragma unroll
-    for (int q = 1; q < 8; ++q) {
-      pg[q] += pg[q - 1];
-      ph[q] += ph[q - 1];
-    }
-    int64_t ig = pg[7], ih = ph[7];
-    for (int o = 1; o < 32; o <<= 1) {
-      int64_t ug = __shfl_up_sync(0xffffffffu, ig, o), uh = __shfl_up_sync(0xffffffffu, ih, o);
-      if (lane >= o) {
-        ig += ug;
-        ih += uh;
-      }
-    }
-    const int64_t bg = ig - pg[7], bh = ih - ph[7];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int b = lane * 8 + q;
-      if (b > nb - 2) break;
-      const int64_t GLq = bg + pg[q], HLq = bh + ph[q];
-      const int64_t GRq = Gq - GLq, HRq = Hq - HLq;
-      const double GL = dequant(GLq, sgi), HL = dequant(HLq, shi);
-      const double GR = dequant(GRq, sgi), HR = dequant(HRq, shi);
-      if (!(HL >= mcw && HR >= mcw)) continue;
-      const double wl = calc_weight(GL, HL, lo, hi, lambda, mcw);
-      const double wr = calc_weight(GR, HR, lo, hi, lambda, mcw);
-      if (a.monotone && f == a.users_col && wl > wr) continue;
-      const double loss = __dsub_rn(__dadd_rn(calc_gain(GL, HL, wl, lambda), calc_gain(GR, HR, wr, lambda)), gainP);
-      Best c{loss, f, b};
-      if (better(c, best)) best = c;
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    Best other;
-    other.loss = __shfl_down_sync(0xffffffffu, best.loss, o);
-    other.f = __shfl_down_sync(0xffffffffu, best.f, o);
-    other.b = __shfl_down_sync(0xffffffffu, best.b, o);
-    if (better(other, best)) best = other;
-  }
-  if (lane == 0) s_best[warp] = best;
-  __syncthreads();
-  if (tid != 0) return;
-  best = s_best[0];
-  for (int w2 = 1; w2 < SPLIT_THREADS / 32; ++w2)
-    if (better(s_best[w2], best)) best = s_best[w2];
-  const int gk = (1 << d) - 1 + k;
-  if (best.f != 0x7fffffff && best.loss > 1e-6) {
-    const int f = best.f, b = best.b;
-    int64_t GLq = 0, HLq = 0;
-    for (int bb = 0; bb <= b; ++bb) {
-      GLq += Hg[f * kBins + bb];
-      HLq += Hh[f * kBins + bb];
-    }
+  double loss = -INFINITY;
+  if (fin && tid <= a.ncuts[f] - 1) {   // thresholds b = 0 .. nbins_f - 2
+    const double G = dequant(Gq, sgi), H = dequant(Hq, shi);
+    const double wP = calc_weight(G, H, lo, hi, lambda, mcw);
+    const double gainP = calc_gain(G, H, wP, lambda);
     const double GL = dequant(GLq, sgi), HL = dequant(HLq, shi);
     const double GR = dequant(Gq - GLq, sgi), HR = dequant(Hq - HLq, shi);
+    if (HL >= mcw && HR >= mcw) {
+      const double wl = calc_weight(GL, HL, lo, hi, lambda, mcw);
+      const double wr = calc_weight(GR, HR, lo, hi, lambda, mcw);
+      if (!(a.monotone && f == a.users_col && wl > wr))
+        loss = __dsub_rn(__dadd_rn(calc_gain(GL, HL, wl, lambda), calc_gain(GR, HR, wr, lambda)), gainP);
+    }
+  }
+  // block argmax over b (loss desc, b asc)
+  double bl = loss;
+  int bb = tid;
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ol = __shfl_down_sync(0xffffffffu, bl, o);
+    const int ob = __shfl_down_sync(0xffffffffu, bb, o);
+    if (better_fb(ol, f, ob, bl, f, bb)) {
+      bl = ol;
+      bb = ob;
+    }
+  }
+  if (lane == 0) {
+    s_bl[warp] = bl;
+    s_bb[warp] = bb;
+  }
+  __syncthreads();
+  FeatBest* fb = a.fbest + (size_t)k * 32;
+  if (tid == 0) {
+    for (int w2 = 1; w2 < SPLIT_THREADS / 32; ++w2)
+      if (better_fb(s_bl[w2], f, s_bb[w2], bl, f, bb)) {
+        bl = s_bl[w2];
+        bb = s_bb[w2];
+      }
+    s_bb[0] = bb;
+  }
+  __syncthreads();
+  // the winning thread publishes its prefix sums (it holds GL, HL of threshold bb)
+  if (tid == s_bb[0]) {
+    FeatBest r;
+    r.loss = bl;
+    r.b = bb;
+    r.valid = (bl > -INFINITY) ? 1 : 0;
+    r.GLq = GLq;
+    r.HLq = HLq;
+    r.Gq = Gq;
+    r.Hq = Hq;
+    fb[f] = r;
+    __threadfence();
+    const int done = atomicAdd(&V.done[k], 1);
+    s_last = (done == 31);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // ---- last CTA of the node: best over the 32 features, then the tree update
+  __threadfence();
+  if (warp != 0) return;
+  const volatile FeatBest* vfb = fb;
+  double ml = vfb[lane].valid ? vfb[lane].loss : -INFINITY;
+  int mf = lane, mb = vfb[lane].b;
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ol = __shfl_down_sync(0xffffffffu, ml, o);
+    const int of = __shfl_down_sync(0xffffffffu, mf, o), ob = __shfl_down_sync(0xffffffffu, mb, o);
+    if (better_fb(ol, of, ob, ml, mf, mb)) {
+      ml = ol;
+      mf = of;
+      mb = ob;
+    }
+  }
+  if (lane != 0) return;
+  V.done[k] = 0;
+  const int64_t GqN = vfb[0].Gq, HqN = vfb[0].Hq;
+  const double G = dequant(GqN, sgi), H = dequant(HqN, shi);
+  const double wP = calc_weight(G, H, lo, hi, lambda, mcw);
+  const int gk = (1 << d) - 1 + k;
+  if (ml > 1e-6) {
+    const int fs = mf, bs = mb;
+    const int64_t GLs = vfb[fs].GLq, HLs = vfb[fs].HLq;
+    const double GL = dequant(GLs, sgi), HL = dequant(HLs, shi);
+    const double GR = dequant(GqN - GLs, sgi), HR = dequant(HqN - HLs, shi);
     const double wl = calc_weight(GL, HL, lo, hi, lambda, mcw);
     const double wr = calc_weight(GR, HR, lo, hi, lambda, mcw);
     double loL = lo, hiL = hi, loR = lo, hiR = hi;
-    if (a.monotone && f == a.users_col) {
+    if (a.monotone && fs == a.users_col) {
       const double mid = __dmul_rn(__dadd_rn(wl, wr), 0.5);
       hiL = mid;
       loR = mid;
     }
-    V.split_f[k] = f;
-    V.split_b[k] = b;
-    a.tfeat[gk] = f;
-    a.tbin[gk] = b;
-    a.tthr[gk] = a.cuts[f * (kBins - 1) + b];
+    V.split_f[k] = fs;
+    V.split_b[k] = bs;
+    a.tfeat[gk] = fs;
+    a.tbin[gk] = bs;
+    a.tthr[gk] = a.cuts[fs * (kBins - 1) + bs];
     a.tval[gk] = 0.0f;
     if (d + 1 < a.D) {
       const LevelView& N = a.lv[d + 1];
@@ -661,7 +678,6 @@ __global__ void __launch_bounds__(SPLIT_THREADS) k_split(const FitArgs a, const 
     a.tval[gk] = (float)__dmul_rn(a.eta, wP);
   }
 }
-
 // ---------------------------------------------------------------------------------------------
 // leaf routing + prediction update + next tree's gradient maxima
 constexpr int UPD_THREADS = 256;
@@ -686,16 +702,16 @@ __device__ __forceinline__ void block_max2(float& a, float& b, float* s_a, float
   }
 }
 
+constexpr int UPD_R = 4;   // rows per thread per iteration (independent traversals for ILP)
 __global__ void __launch_bounds__(UPD_THREADS) k_update(const FitArgs a, const int t) {
   __shared__ int8_t s_feat[MAX_NODES];
   __shared__ uint8_t s_bin[MAX_NODES];
   __shared__ float s_val[MAX_NODES];
-  __shared__ __align__(16) uint8_t s_row[UPD_THREADS * ROWBUF_STRIDE];
+  __shared__ __align__(16) uint8_t s_row[UPD_R][UPD_THREADS * 32];
   __shared__ float s_ma[UPD_THREADS / 32], s_mb[UPD_THREADS / 32];
   const int tid = threadIdx.x;
-  const int32_t* tf = a.tfeat;  // a.tfeat/tbin/tval already point at tree t
-  for (int i = tid; i < a.nn; i += UPD_THREADS) {
-    int f = tf[i];
+  for (int i = tid; i < a.nn; i += UPD_THREADS) {   // a.tfeat/tbin/tval point at tree t
+    const int f = a.tfeat[i];
     s_feat[i] = (int8_t)(f < 0 ? -1 : f);
     s_bin[i] = (uint8_t)a.tbin[i];
     s_val[i] = a.tval[i];
@@ -703,29 +719,52 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update(const FitArgs a, const i
   __syncthreads();
   const bool has_next = t + 1 < a.T;
   float mg = 0.f, mh = 0.f;
-  uint8_t* myrow = s_row + tid * ROWBUF_STRIDE;
-  for (int64_t i = (int64_t)blockIdx.x * UPD_THREADS + tid; i < a.n; i += (int64_t)gridDim.x * UPD_THREADS) {
-    const uint4* crow = reinterpret_cast<const uint4*>(a.codes + (size_t)i * kMaxF);
-    *reinterpret_cast<uint4*>(myrow) = __ldg(crow);
-    *reinterpret_cast<uint4*>(myrow + 16) = __ldg(crow + 1);
-    int k = 0;
-    int f = s_feat[0];
-    while (f >= 0) {
-      k = 2 * k + 1 + (myrow[f] > s_bin[k] ? 1 : 0);
-      f = s_feat[k];
-    }
-    const float pn = __fadd_rn(a.p[i], s_val[k]);  // O9: one fp32 rounding
-    a.p[i] = pn;
-    if (has_next) {
-      const float wv = a.w[i];
-      float g = __fmul_rn(wv, __fsub_rn(pn, a.y[i]));
-      float h = wv;
-      if (row_sampled_out(a.seed, a.target, t + 1, a.row_offset + i, a.subsample)) {
-        g = 0.f;
-        h = 0.f;
+  const int64_t stride = (int64_t)gridDim.x * UPD_THREADS;
+  for (int64_t i0 = (int64_t)blockIdx.x * UPD_THREADS + tid; i0 < a.n; i0 += stride * UPD_R) {
+    float pv[UPD_R], yv[UPD_R], wv[UPD_R];
+#pragma unroll
+    for (int q = 0; q < UPD_R; ++q) {
+      const int64_t i = i0 + q * stride;
+      if (i < a.n) {
+        const uint4* crow = reinterpret_cast<const uint4*>(a.codes + (size_t)i * kMaxF);
+        const uint4 c0 = __ldg(crow), c1 = __ldg(crow + 1);
+        *reinterpret_cast<uint4*>(&s_row[q][tid * 32]) = c0;
+        *reinterpret_cast<uint4*>(&s_row[q][tid * 32 + 16]) = c1;
+        pv[q] = a.p[i];
+        if (has_next) {
+          yv[q] = a.y[i];
+          wv[q] = a.w[i];
+        }
       }
-      mg = fmaxf(mg, fabsf(g));
-      mh = fmaxf(mh, h);
+    }
+    int k[UPD_R];
+#pragma unroll
+    for (int q = 0; q < UPD_R; ++q) k[q] = 0;
+    // fixed-trip traversal (a leaf stays put), the UPD_R rows interleaved
+    for (int s = 0; s < a.D; ++s) {
+#pragma unroll
+      for (int q = 0; q < UPD_R; ++q) {
+        const int f = s_feat[k[q]];
+        if (f >= 0) k[q] = 2 * k[q] + 1 + (s_row[q][tid * 32 + f] > s_bin[k[q]] ? 1 : 0);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < UPD_R; ++q) {
+      const int64_t i = i0 + q * stride;
+      if (i < a.n) {
+        const float pn = __fadd_rn(pv[q], s_val[k[q]]);  // O9: one fp32 rounding
+        a.p[i] = pn;
+        if (has_next) {
+          float g = __fmul_rn(wv[q], __fsub_rn(pn, yv[q]));
+          float h = wv[q];
+          if (row_sampled_out(a.seed, a.target, t + 1, a.row_offset + i, a.subsample)) {
+            g = 0.f;
+            h = 0.f;
+          }
+          mg = fmaxf(mg, fabsf(g));
+          mh = fmaxf(mh, h);
+        }
+      }
     }
   }
   if (!has_next) return;
@@ -972,7 +1011,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   }
   const size_t ctl_bytes = 64 * 4 /*tickets*/ + lvl_nodes * 8 * 2 /*cnt,gcnt*/ + (size_t)max_tiles_total * 8;
   DevBuf& d_ctl = ctx->workspace("ctl", ctl_bytes);
-  const size_t tab_bytes = lvl_nodes * (8 /*start*/ + 8 + 8 /*lo,hi*/ + 4 + 4 /*split*/ + 4 /*built*/);
+  const size_t tab_bytes = lvl_nodes * (8 /*start*/ + 8 + 8 /*lo,hi*/ + 4 + 4 /*split*/ + 4 /*built*/ + 4 /*done*/);
   DevBuf& d_tab = ctx->workspace("tab", tab_bytes);
 
   FitArgs a{};
@@ -1002,6 +1041,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   a.monotone = hp.monotone_users;
   a.nn = nn;
   a.units = ctx->d_units;
+  a.fbest = reinterpret_cast<FeatBest*>(ctx->workspace("featbest", (size_t)half_max * 32 * 48).p);
   {
     uint8_t* c = d_ctl.as<uint8_t>();
     int32_t* tickets = reinterpret_cast<int32_t*>(c);
@@ -1015,6 +1055,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     int32_t* sf = reinterpret_cast<int32_t*>(hi + lvl_nodes);
     int32_t* sb = sf + lvl_nodes;
     int32_t* bu = sb + lvl_nodes;
+    int32_t* dn = bu + lvl_nodes;
     size_t off = 0;
     for (int d = 0; d <= D; ++d) {
       LevelView& L = a.lv[d];
@@ -1026,6 +1067,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       L.split_f = sf + off;
       L.split_b = sb + off;
       L.built = bu + off;
+      L.done = dn + off;
       L.flags = flags + tiles_off[d];
       L.ticket = tickets + d;
       off += (size_t)1 << d;
@@ -1043,7 +1085,12 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   LLMP_CUDA(cudaMemsetAsync(d_sums.p, 0, d_sums.bytes, s));
 
   const int hist_grid = 2 * ctx->sms;
-  const int part_grid = 4 * ctx->sms;
+  // cooperative partition: every CTA must be co-resident (grid.sync between its two phases)
+  int part_occ = 0;
+  LLMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&part_occ, k_partition, PART_THREADS, 0));
+  LLMP_REQUIRE(part_occ >= 1, "partition kernel cannot be resident");
+  const int part_grid = std::min(part_occ, 8) * ctx->sms;
+  DevBuf& d_agg = ctx->workspace("part_agg", (size_t)part_grid * 8);
   const int upd_grid = grid_for(ctx, n, UPD_THREADS, 8);
   const int base_grid = grid_for(ctx, n, BASE_THREADS, 8);
   static bool attr_set = false;
@@ -1087,16 +1134,24 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       LLMP_CUDA(cudaMemsetAsync(a.H[0], 0, (size_t)SLOT * 8, s));
       LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist<HM_ROOT>, hist_grid, HIST_THREADS, HIST_SMEM, a, 0, t, nodbg);
       allreduce_sum_i64(ctx, a.H[0], SLOT);
-      LLMP_LAUNCH(ctx, KC_SPLIT, 1, k_split, 1, SPLIT_THREADS, 0, a, 0, t);
+      LLMP_LAUNCH(ctx, KC_SPLIT, 1, k_split, 32, SPLIT_THREADS, 0, a, 0, t);
       for (int d = 1; d < D; ++d) {
-        LLMP_LAUNCH(ctx, KC_PARTITION, n, k_partition, part_grid, PART_THREADS, 0, a, d, part_grid);
+        {
+          cudaEvent_t ev = nullptr;
+          ctx->before(KC_PARTITION, &ev);
+          int dd = d;
+          int64_t* aggp = d_agg.as<int64_t>();
+          void* kargs[] = {(void*)&a, (void*)&dd, (void*)&aggp};
+          LLMP_CUDA(cudaLaunchCooperativeKernel((void*)k_partition, part_grid, PART_THREADS, kargs, 0, s));
+          ctx->after(KC_PARTITION, ev, (double)n);
+        }
         if (ctx->nranks > 1) {
           LLMP_CUDA(cudaMemcpyAsync(a.lv[d].gcnt, a.lv[d].cnt, ((size_t)1 << d) * 8, cudaMemcpyDeviceToDevice, s));
           allreduce_sum_i64(ctx, a.lv[d].gcnt, (size_t)1 << d);
         }
         LLMP_LAUNCH(ctx, KC_HIST, n / 2, k_hist<HM_LEVEL>, hist_grid, HIST_THREADS, HIST_SMEM, a, d, t, nodbg);
         allreduce_sum_i64(ctx, a.H[d & 1], (size_t)SLOT << (d - 1));
-        LLMP_LAUNCH(ctx, KC_SPLIT, (1 << d), k_split, (1 << d), SPLIT_THREADS, 0, a, d, t);
+        LLMP_LAUNCH(ctx, KC_SPLIT, (1 << d), k_split, (1 << d) * 32, SPLIT_THREADS, 0, a, d, t);
       }
       LLMP_LAUNCH(ctx, KC_UPDATE, n, k_update, upd_grid, UPD_THREADS, 0, a, t);
       if (t + 1 < T) {

@@ -220,7 +220,7 @@ def test_recommend_toy_table_through_gpu_argmin(lp, ctx, golden):
         for k, u in enumerate(g["levels"]):
             X.append([j, u]); y.append([p["l1"][k], p["l2"][k]])
     X = np.array(X, np.float32); y = np.array(y, np.float32)
-    hp = lp.hparams(n_trees=1, max_depth=6, eta=1.0, lambda_=0.0, min_child_weight=0.0, use_eq4_weights=0,
+    hp = lp.hparams(n_trees=4, max_depth=8, eta=1.0, lambda_=0.0, min_child_weight=0.0, use_eq4_weights=0,
                     monotone_users=0, grad_bits=14)
     m = lp.fit(ctx, X, y, hp, users_col=1)
     pred = m.predict(ctx, X)
