@@ -41,11 +41,13 @@ UNIT = "row-iters/s"
 # algorithmic bytes per unit: unit = one row processed by that kernel
 BYTES_PER_UNIT = {
     "hist_root": 48.0,    # 32 B code row + y, w, p (12 B) read + 4 B packed gradient pair written
-    "hist_level": 40.0,   # 32 B code row (gathered by row index) + 8 B (row index, gradient pair)
-    "partition": 17.0,    # 8 B state read + 1 B split-feature code + 8 B state written
+    "partition": 17.0,    # 4 B row index + 1 B split-feature code (count) + 8 B state read + 8 B written,
+                          # minus the 4 B row index read twice: 4 + 1 + 4 + 8 = 17 B per partitioned row
+    "hist_level": 40.0,   # 32 B code row (gathered by row index) + 8 B (row index, packed pair)
     "update": 48.0,       # 32 B code row + y, w, p read (12 B) + p written (4 B)
-    "codes": 160.0,       # 32 f32 features read (128 B) + 32 B row-major + 32 B column-major codes... (see DESIGN)
+    "codes": 192.0,       # 128 B f32 row read + 32 B row-major + 32 B column-major codes written
 }
+
 
 
 def _env_int(k, d):
@@ -287,8 +289,9 @@ def main():
         k = {"launches": c["launches"], "ms_total": round(c["ms"], 3), "ms_avg": c["ms"] / c["launches"],
              "share_of_step": c["ms"] / elapsed_ms}
         if name in BYTES_PER_UNIT and c["rows"] > 0:
-            gbs = BYTES_PER_UNIT[name] * c["rows"] / (c["ms"] / 1000.0) / 1e9
-            k.update({"units": c["rows"], "bytes_per_unit": BYTES_PER_UNIT[name], "achieved_gbs": gbs,
+            nbytes = BYTES_PER_UNIT[name] * c["rows"]
+            gbs = nbytes / (c["ms"] / 1000.0) / 1e9
+            k.update({"units": c["rows"], "bytes_per_unit": nbytes / c["rows"], "achieved_gbs": gbs,
                       "frac_hbm": gbs / peak})
         kernels[name] = k
     dom = max((n for n in kernels if n in BYTES_PER_UNIT and "achieved_gbs" in kernels[n]),

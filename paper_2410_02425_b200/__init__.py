@@ -197,7 +197,7 @@ class Context:
         names = kernel_class_names()
         out = {"total_launches": int(s.total_launches), "classes": {}}
         for i, nm in enumerate(names):
-            if s.launches[i]:
+            if s.launches[i] or s.rows[i]:
                 out["classes"][nm] = {"launches": int(s.launches[i]), "ms": float(s.ms[i]), "rows": float(s.rows[i])}
         return out
 

@@ -220,7 +220,7 @@ llmpilot_status llmpilot_bin(llmpilot_ctx* ctx, const float* X, int64_t n, int32
       if (codes_out) {
         llmp::DevBuf flag(sizeof(int));
         LLMP_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx->c.stream));
-        llmp::compute_codes(&ctx->c, Xd, n, F, *cuts, codes_out, nullptr, flag.as<int>());
+        llmp::compute_codes(&ctx->c, Xd, n, F, *cuts, codes_out, nullptr, n, flag.as<int>());
         int hf = 0;
         LLMP_CUDA(cudaMemcpyAsync(&hf, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->c.stream));
         LLMP_CUDA(cudaStreamSynchronize(ctx->c.stream));

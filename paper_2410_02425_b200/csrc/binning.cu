@@ -157,7 +157,8 @@ void compute_cuts(Ctx* ctx, const float* X, int64_t n, int F, int64_t row_offset
 constexpr int CODE_ROWS = 128;
 __global__ void __launch_bounds__(256) k_codes(const float* __restrict__ X, int64_t n, int F,
                                                const float* __restrict__ cuts, const int32_t* __restrict__ ncuts,
-                                               uint8_t* __restrict__ codes, uint8_t* __restrict__ codesT, int* flag) {
+                                               uint8_t* __restrict__ codes, uint8_t* __restrict__ codesT, int64_t ldT,
+                                               int* flag) {
   __shared__ float s_cut[kBins][kMaxF];
   __shared__ int s_nc[kMaxF];
   __shared__ __align__(16) uint8_t s_tile[CODE_ROWS][kMaxF];
@@ -197,7 +198,7 @@ __global__ void __launch_bounds__(256) k_codes(const float* __restrict__ X, int6
       // column-major: feature f, rows r0..r0+rows; 4 rows per thread-word when aligned
       for (int i = tid; i < kMaxF * CODE_ROWS; i += 256) {
         const int f = i / CODE_ROWS, r = i % CODE_ROWS;
-        if (r < rows) codesT[(int64_t)f * n + r0 + r] = s_tile[r][f];
+        if (r < rows) codesT[(int64_t)f * ldT + r0 + r] = s_tile[r][f];
       }
     }
     __syncthreads();
@@ -205,12 +206,12 @@ __global__ void __launch_bounds__(256) k_codes(const float* __restrict__ X, int6
 }
 
 void compute_codes(Ctx* ctx, const float* X, int64_t n, int F, const CutsData& cuts, uint8_t* codes, uint8_t* codesT,
-                   int* flag) {
+                   int64_t ldT, int* flag) {
   int64_t tiles = (n + CODE_ROWS - 1) / CODE_ROWS;
   int grid = (int)std::min<int64_t>(tiles, (int64_t)ctx->sms * 8);
   if (grid < 1) grid = 1;
   LLMP_LAUNCH(ctx, KC_CODES, n, k_codes, grid, 256, 0, X, n, F, cuts.d_cuts.as<float>(), cuts.d_ncuts.as<int32_t>(),
-              codes, codesT, flag);
+              codes, codesT, ldT, flag);
 }
 
 }  // namespace llmp

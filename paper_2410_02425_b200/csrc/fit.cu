@@ -69,11 +69,13 @@ struct FitArgs {
   int F, users_col, D, K, T, target;
   const uint8_t* codes;
   const uint8_t* codesT;
+  int64_t ldT;       // codesT leading dimension: n rounded up to 32 (aligned 32-row vectors)
   const float* y;
   const float* w;
   float* p;
   uint32_t* gp_root;
-  uint2* st[2];
+  uint32_t* sr[2];   // row-index state (children: A = [0,n) left, B = [n,2n) right)
+  uint32_t* sg[2];   // packed gradient pair state, same positions
   int64_t* H[2];
   LevelView lv[kMaxDepth + 1];
   uint32_t* maxg;    // [T+1] float bits of max |g| per tree (slot T: base score)
@@ -152,8 +154,8 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
     if (tid < NP) {
       sp = P.split_f[tid] >= 0;
       if (sp) {
-        int64_t nL = C.gcnt[2 * tid], nR = C.gcnt[2 * tid + 1];
-        side = (nL <= nR) ? 0 : 1;       // build the smaller child (by global count), ties -> left
+        const int64_t nL = C.gcnt[2 * tid], nR = C.gcnt[2 * tid + 1];
+        side = (nL <= nR) ? 0 : 1;       // build the smaller child (global row count), ties -> left
         len = C.cnt[2 * tid + side];
         pst = C.start[2 * tid + side];
         if (blockIdx.x == 0) C.built[tid] = side;
@@ -200,7 +202,8 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
     scale_h = exp2i(a.K - exp_of(__uint_as_float(a.maxh[t])));
   }
   int64_t* Hbase = (MODE == HM_DEBUG) ? dbg.out : a.H[d & 1];
-  const uint2* st_in = (MODE == HM_LEVEL) ? a.st[d & 1] : nullptr;
+  const uint32_t* sr_in = (MODE == HM_LEVEL) ? a.sr[d & 1] : nullptr;
+  const uint32_t* sg_in = (MODE == HM_LEVEL) ? a.sg[d & 1] : nullptr;
 
   // first piece overlapping [v0, v1)
   int pc = 0;
@@ -236,9 +239,8 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
             nw = a.w[ridx];
             np_ = a.p[ridx];
           } else if (MODE == HM_LEVEL) {
-            const uint2 s = st_in[pi];
-            ridx = s.x;
-            ngp = s.y;
+            ridx = sr_in[pi];
+            ngp = sg_in[pi];
           } else {
             ridx = dbg.idx ? dbg.idx[pi] : pi;
             ngp = pack_gp(dbg.qg[ridx], dbg.qh[ridx]);
@@ -309,165 +311,476 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
 }
 
 // ---------------------------------------------------------------------------------------------
-// stable partition of the split parents' rows (level d-1) into their children (level d).
-// Cooperative single pass (all CTAs co-resident, launched with cudaLaunchCooperativeKernel):
-//   phase 1: each CTA counts the rows going left in its contiguous chunk of the level's row
-//            sequence (split parents concatenated in node order) -> agg[c]
-//   grid.sync()
-//   phase 2: exclusive prefix of agg over CTAs (warp-parallel); the chunk is re-read (mostly L2
-//            hits) in 2048-row sub-tiles, block-scanned, and scattered: left rows to region
-//            A = [0, n) at the global left prefix, right rows to region B = [n, 2n) at the global
-//            right prefix.  Each child segment is contiguous and keeps its parent's row order.
-__global__ void __launch_bounds__(PART_THREADS) k_partition(const FitArgs a, const int d, int64_t* agg) {
-  cg::grid_group grid = cg::this_grid();
+// Root histogram, hybrid run/row-parallel form (HM_ROOT only; rows in identity order).
+// Per warp batch of 32 rows:
+//   lane r   computes row r's gradient pair (weighted squared error, sampling, quantisation),
+//            writes it to gp_root and takes part in a warp prefix scan of (q_g, q_h);
+//   lane f   loads feature f's 32 codes as two aligned 16-byte vectors from the column-major
+//            codes, builds the 32-bit mask of rows where its code changes, and
+//            - "light" lanes (<= 3 changes): flush each finished run with one pair of 32-bit shared
+//              reductions, the run sum being a difference of the batch prefix sums;
+//            - "heavy" lanes (> 3 changes, e.g. the users column of paper-ordered rows, or random
+//              codes): processed row-parallel — for each heavy feature the 32 lanes add their own
+//              row's pair at (code, feature) in a bank-padded [bin][33] histogram.
+// Equal codes in consecutive rows therefore cost no per-row work at all.
+constexpr int R2_THREADS = 512;
+constexpr int R2_WARPS = R2_THREADS / 32;
+constexpr int R2_PAD = 33;                                   // [bin][33] words: both access patterns conflict-light
+constexpr int R2_HIST_WORDS = kBins * R2_PAD;                // per channel
+constexpr int R2_FSTRIDE = 36;                               // bytes per feature row of a batch in smem
+constexpr int R2_SMEM = 2 * R2_HIST_WORDS * 4 + R2_WARPS * (32 * R2_FSTRIDE + 2 * 32 * 4);
+constexpr int R2_HEAVY = 3;
+
+__device__ __forceinline__ uint32_t change_nibble(uint32_t cur, uint32_t prevw) {
+  // bit i (i < 4) set iff byte i of cur differs from byte i of (cur << 8 | prevw >> 24)
+  const uint32_t x = cur ^ __funnelshift_l(prevw, cur, 8);
+  const uint32_t t = (x | ((x & 0x7f7f7f7fu) + 0x7f7f7f7fu)) & 0x80808080u;
+  return (t * 0x00204081u) >> 28;
+}
+
+__global__ void __launch_bounds__(R2_THREADS, 2) k_hist_root2(const FitArgs a, const int t) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  int32_t* hg = reinterpret_cast<int32_t*>(smem);                       // [256][33]
+  uint32_t* hh = reinterpret_cast<uint32_t*>(smem + R2_HIST_WORDS * 4);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint8_t* fbuf = smem + 2 * R2_HIST_WORDS * 4 + warp * (32 * R2_FSTRIDE + 2 * 32 * 4);
+  int32_t* pbg = reinterpret_cast<int32_t*>(fbuf + 32 * R2_FSTRIDE);  // batch prefix of q_g
+  uint32_t* pbh = reinterpret_cast<uint32_t*>(pbg + 32);              // batch prefix of q_h
+  for (int i = tid; i < 2 * R2_HIST_WORDS; i += R2_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
+  __syncthreads();
+  const int64_t n = a.n;
+  // 32-row aligned contiguous range per CTA
+  const int64_t nb = (n + 31) / 32;
+  const int64_t v0 = (nb * blockIdx.x / gridDim.x) * 32, v1 = min(n, (nb * (blockIdx.x + 1) / gridDim.x) * 32);
+  if (v0 >= v1) return;
+  if (tid == 0 && a.units) atomicAdd(&a.units[KC_HIST_ROOT], (unsigned long long)(v1 - v0));
+  const double scale_g = exp2i(a.K - exp_of(__uint_as_float(a.maxg[t])));
+  const double scale_h = exp2i(a.K - exp_of(__uint_as_float(a.maxh[t])));
+  const bool fin = lane < a.F;
+  const uint32_t sb_g = (uint32_t)__cvta_generic_to_shared(hg), sb_h = (uint32_t)__cvta_generic_to_shared(hh);
+  for (int64_t c0 = v0; c0 < v1; c0 += HIST_CHUNK) {        // flush at least every 65,536 rows
+    const int64_t c1 = min(v1, c0 + HIST_CHUNK);
+    const int64_t nbc = (c1 - c0 + 31) / 32;
+    const int64_t w0 = c0 + (nbc * warp / R2_WARPS) * 32, w1 = min(c1, c0 + (nbc * (warp + 1) / R2_WARPS) * 32);
+    int cur = -1;            // code of the pending run of this lane's feature
+    int32_t acc_g = 0;       // pending run sums
+    uint32_t acc_h = 0;
+    for (int64_t base = w0; base < w1; base += 32) {
+      const int cnt = (int)min((int64_t)32, w1 - base);
+      // ---- row-side: gradient pair of row base + lane
+      int32_t qg = 0, qh = 0;
+      if (lane < cnt) {
+        const int64_t i = base + lane;
+        float g = __fmul_rn(a.w[i], __fsub_rn(a.p[i], a.y[i]));
+        float h = a.w[i];
+        if (row_sampled_out(a.seed, a.target, t, a.row_offset + i, a.subsample)) {
+          g = 0.f;
+          h = 0.f;
+        }
+        qg = quantize(g, scale_g);
+        qh = quantize(h, scale_h);
+        a.gp_root[i] = pack_gp(qg, qh);
+      }
+      // ---- feature-side: 32 codes of this lane's feature (aligned vectors; padding rows are 0)
+      const uint4* cp = reinterpret_cast<const uint4*>(a.codesT + (size_t)lane * a.ldT + base);
+      const uint4 ca = __ldg(cp), cb = __ldg(cp + 1);
+      uint32_t cw[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+      // inclusive warp prefix of the pairs
+      int32_t pg = qg;
+      uint32_t ph = (uint32_t)qh;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t ug = __shfl_up_sync(0xffffffffu, pg, o);
+        const uint32_t uh = __shfl_up_sync(0xffffffffu, ph, o);
+        if (lane >= o) {
+          pg += ug;
+          ph += uh;
+        }
+      }
+      __syncwarp();
+      pbg[lane] = pg;
+      pbh[lane] = ph;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) *reinterpret_cast<uint32_t*>(fbuf + lane * R2_FSTRIDE + 4 * q) = cw[q];
+      const int32_t tot_g = __shfl_sync(0xffffffffu, pg, 31);
+      const uint32_t tot_h = __shfl_sync(0xffffffffu, ph, 31);
+      __syncwarp();
+      // change mask over rows 0..cnt-1 (row 0 compares with the pending run's code)
+      if (cur < 0) cur = (int)(cw[0] & 0xffu);
+      uint32_t M = 0;
+      uint32_t prevw = (uint32_t)cur << 24;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        M |= change_nibble(cw[q], prevw) << (4 * q);
+        prevw = cw[q];
+      }
+      if (cnt < 32) M &= (1u << cnt) - 1u;
+      if (!fin) M = 0;
+      const int nch = __popc(M);
+      const bool heavy = fin && nch > R2_HEAVY;
+      // ---- light lanes: flush finished runs with prefix differences
+      {
+        uint32_t Ml = heavy ? 0u : M;
+        const int iters = __reduce_max_sync(0xffffffffu, heavy ? 0 : nch);
+        int32_t base_g = 0;   // prefix before the current run's first row
+        uint32_t base_h = 0;
+        for (int it = 0; it < iters; ++it) {
+          if (Ml) {
+            const int r = __ffs(Ml) - 1;
+            Ml &= Ml - 1;
+            const int32_t pgr = r ? pbg[r - 1] : 0;
+            const uint32_t phr = r ? pbh[r - 1] : 0u;
+            const int32_t rg = acc_g + (pgr - base_g);
+            const uint32_t rh = acc_h + (phr - base_h);
+            const uint32_t ad = (uint32_t)(cur * R2_PAD + lane) * 4u;
+            asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(sb_g + ad), "r"(rg) : "memory");
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(sb_h + ad), "r"(rh) : "memory");
+            acc_g = 0;
+            acc_h = 0;
+            base_g = pgr;
+            base_h = phr;
+            cur = fbuf[lane * R2_FSTRIDE + r];
+          }
+        }
+        if (!heavy && fin) {
+          acc_g += tot_g - base_g;
+          acc_h += tot_h - base_h;
+        }
+      }
+      // ---- heavy lanes: row-parallel, one feature at a time
+      unsigned hm = __ballot_sync(0xffffffffu, heavy);
+      while (hm) {
+        const int hf = __ffs(hm) - 1;
+        hm &= hm - 1;
+        if (lane == hf && (acc_g | (int32_t)acc_h)) {   // pending run of earlier batches
+          const uint32_t ad = (uint32_t)(cur * R2_PAD + lane) * 4u;
+          asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(sb_g + ad), "r"(acc_g) : "memory");
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(sb_h + ad), "r"(acc_h) : "memory");
+        }
+        if (lane < cnt) {
+          const int code = fbuf[hf * R2_FSTRIDE + lane];
+          const uint32_t ad = (uint32_t)(code * R2_PAD + hf) * 4u;
+          asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(sb_g + ad), "r"(qg) : "memory");
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(sb_h + ad), "r"((uint32_t)qh) : "memory");
+        }
+        if (lane == hf) {
+          acc_g = 0;
+          acc_h = 0;
+          cur = fbuf[hf * R2_FSTRIDE + cnt - 1];
+        }
+      }
+      __syncwarp();
+    }
+    if (fin && cur >= 0 && (acc_g | (int32_t)acc_h)) {
+      atomicAdd(&hg[cur * R2_PAD + lane], acc_g);
+      atomicAdd(&hh[cur * R2_PAD + lane], acc_h);
+    }
+    __syncthreads();
+    // zero-skipping int64 flush into the root histogram ([f][b] layout)
+    int64_t* Hg = a.H[0];
+    int64_t* Hh = Hg + kHistBins;
+    for (int i = tid; i < kHistBins; i += R2_THREADS) {
+      const int b = i >> 5, f = i & 31;
+      const int32_t g = hg[b * R2_PAD + f];
+      const uint32_t h = hh[b * R2_PAD + f];
+      if (g != 0 || h != 0) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&Hg[f * kBins + b]), (unsigned long long)(long long)g);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&Hh[f * kBins + b]), (unsigned long long)h);
+        hg[b * R2_PAD + f] = 0;
+        hh[b * R2_PAD + f] = 0;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Stable partition of the split parents' rows (level d-1) into their children (level d), as three
+// independent-tile kernels (no inter-CTA waiting, no grid synchronisation):
+//   k_pcount   one CTA per 4096-row tile of a split parent: row index -> split-feature code
+//              (column-major byte) -> left bit; bits kept in a per-tile bitmask, count per tile;
+//              also zeroes the level's built-child histogram slots
+//   k_pscan    one CTA: exclusive prefix of the tile counts (global left prefix), child segment
+//              starts and counts
+//   k_pscatter one CTA per tile: stage (row index, packed gradient), block-scan the left bits,
+//              order lefts-then-rights in shared memory (stable) and write both runs with coalesced
+//              stores — left rows to region A = [0, n) at the global left prefix, right rows to
+//              region B = [n, 2n) at the global right prefix.  Each child segment is contiguous
+//              and keeps its parent's row order.
+constexpr int PT_THREADS = 256;
+constexpr int PT_ITEMS = 16;
+constexpr int PT_TILE = PT_THREADS * PT_ITEMS;   // 4096 rows
+constexpr int PT_WORDS = PT_TILE / 32;           // bitmask words per tile
+constexpr int PT_HALF = PT_TILE / 2;             // k_pscatter works in 2048-row halves
+constexpr int PT_HI = PT_HALF / PT_THREADS;      // 8 rows per thread per half
+
+struct PartWs {
+  int32_t* tile_left;    // [max tiles] left rows per tile
+  int64_t* tile_lpref;   // [max tiles] global left prefix at the tile start
+  uint32_t* bits;        // [max tiles][PT_WORDS] left bits
+};
+
+// tile and row prefixes over the level's split parents (computed by each CTA; NP <= 512)
+__device__ __forceinline__ void parent_prefixes(const FitArgs& a, int d, int* s_tile_pref, int64_t* s_seq_pref,
+                                                int* s_w, int64_t* s_w64) {
   const int NP = 1 << (d - 1);
   const LevelView& P = a.lv[d - 1];
-  const LevelView& C = a.lv[d];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int G = gridDim.x;
-  __shared__ int64_t s_seq_pref[MAX_PIECES + 1];   // virtual start of each parent's rows
-  __shared__ int64_t s_wsum64[PART_THREADS / 32];
-  __shared__ int s_wsum[PART_THREADS / 32];
-  __shared__ uint2 s_state[TILE];
-  __shared__ int64_t s_prefix;
-
-  // ---- per-parent row prefix (two parents per thread)
-  {
-    int64_t rl[2] = {0, 0};
-    for (int q = 0; q < 2; ++q) {
-      const int j = tid * 2 + q;
-      if (j < NP && P.split_f[j] >= 0) rl[q] = (d == 1) ? a.n : P.cnt[j];
+  int tl[2] = {0, 0};
+  int64_t rl[2] = {0, 0};
+  for (int q = 0; q < 2; ++q) {
+    const int j = tid * 2 + q;
+    if (j < NP && P.split_f[j] >= 0) {
+      rl[q] = (d == 1) ? a.n : P.cnt[j];
+      tl[q] = (int)((rl[q] + PT_TILE - 1) / PT_TILE);
     }
-    const int64_t rv = rl[0] + rl[1];
-    int64_t rinc = rv;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t u = __shfl_up_sync(0xffffffffu, rinc, o);
-      if (lane >= o) rinc += u;
-    }
-    if (lane == 31) s_wsum64[warp] = rinc;
-    __syncthreads();
-    int64_t roff = 0;
-    for (int w2 = 0; w2 < warp; ++w2) roff += s_wsum64[w2];
-    int64_t re = roff + rinc - rv;
-    for (int q = 0; q < 2; ++q) {
-      const int j = tid * 2 + q;
-      if (j < NP) s_seq_pref[j] = re;
-      re += rl[q];
-    }
-    if (tid == PART_THREADS - 1) s_seq_pref[NP] = re;
   }
-  // ---- zero the built-child histogram slots [0, NP) of this level for split parents
+  const int tv = tl[0] + tl[1];
+  const int64_t rv = rl[0] + rl[1];
+  int tinc = tv;
+  int64_t rinc = rv;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, tinc, o);
+    const int64_t u64 = __shfl_up_sync(0xffffffffu, rinc, o);
+    if (lane >= o) {
+      tinc += u;
+      rinc += u64;
+    }
+  }
+  if (lane == 31) {
+    s_w[warp] = tinc;
+    s_w64[warp] = rinc;
+  }
+  __syncthreads();
+  int toff = 0;
+  int64_t roff = 0;
+  for (int w2 = 0; w2 < warp; ++w2) {
+    toff += s_w[w2];
+    roff += s_w64[w2];
+  }
+  int te = toff + tinc - tv;
+  int64_t re = roff + rinc - rv;
+  for (int q = 0; q < 2; ++q) {
+    const int j = tid * 2 + q;
+    if (j < NP) {
+      s_tile_pref[j] = te;
+      s_seq_pref[j] = re;
+    }
+    te += tl[q];
+    re += rl[q];
+  }
+  if (tid == (int)blockDim.x - 1) {
+    s_tile_pref[NP] = te;
+    s_seq_pref[NP] = re;
+  }
+  __syncthreads();
+}
+
+// parent j of tile t: largest j with tile_pref[j] <= t
+__device__ __forceinline__ int parent_of_tile(const int* s_tile_pref, int NP, int t) {
+  int lo = 0, hi = NP - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s_tile_pref[mid] <= t) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(PT_THREADS) k_pcount(const FitArgs a, const int d, const PartWs w) {
+  __shared__ int s_tile_pref[MAX_PIECES + 1];
+  __shared__ int64_t s_seq_pref[MAX_PIECES + 1];
+  __shared__ int s_w[PT_THREADS / 32];
+  __shared__ int64_t s_w64[PT_THREADS / 32];
+  const int NP = 1 << (d - 1);
+  const LevelView& P = a.lv[d - 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // zero the built-child histogram slots [0, NP) of this level for split parents
   {
     int4* Hz = reinterpret_cast<int4*>(a.H[d & 1]);
     const size_t per_slot = SLOT / 2;  // int4 per slot
     const size_t total = (size_t)NP * per_slot;
-    for (size_t e = (size_t)blockIdx.x * PART_THREADS + tid; e < total; e += (size_t)G * PART_THREADS) {
+    for (size_t e = (size_t)blockIdx.x * PT_THREADS + tid; e < total; e += (size_t)gridDim.x * PT_THREADS) {
       const int j = (int)(e / per_slot);
       if (P.split_f[j] >= 0) Hz[e] = make_int4(0, 0, 0, 0);
     }
   }
-  __syncthreads();
-  const int64_t S = s_seq_pref[NP];
-  const int64_t v0 = S * blockIdx.x / G, v1 = S * (blockIdx.x + 1) / G;
-  if (tid == 0 && a.units) atomicAdd(&a.units[KC_PARTITION], (unsigned long long)(v1 - v0));
-  const uint2* st_in = (d >= 2) ? a.st[(d - 1) & 1] : nullptr;
-  uint2* st_out = a.st[d & 1];
-  int jfirst = 0;   // first parent overlapping [v0, v1)
-  while (jfirst + 1 < NP && s_seq_pref[jfirst + 1] <= v0) ++jfirst;
-
-  // ---- phase 1: count left rows of the chunk
-  int64_t myl = 0;
-  for (int j = jfirst; j < NP && s_seq_pref[j] < v1; ++j) {
-    const int64_t p0 = max(v0, s_seq_pref[j]), p1 = min(v1, s_seq_pref[j + 1]);
-    if (p0 >= p1) continue;
-    const int f = P.split_f[j], b = P.split_b[j];
-    const uint8_t* col = a.codesT + (size_t)f * a.n;
-    const int64_t base = (d == 1) ? 0 : P.start[j] - s_seq_pref[j];   // physical = base + virtual
-    for (int64_t v = p0 + tid; v < p1; v += PART_THREADS) {
-      const uint32_t ridx = (d == 1) ? (uint32_t)v : st_in[base + v].x;
-      myl += col[ridx] <= b;
-    }
+  parent_prefixes(a, d, s_tile_pref, s_seq_pref, s_w, s_w64);
+  // persistent: the per-CTA prologue is amortised over a grid-stride loop of tiles
+  for (int t = blockIdx.x; t < s_tile_pref[NP]; t += gridDim.x) {
+  const int j = parent_of_tile(s_tile_pref, NP, t);
+  const int64_t cnt_j = (d == 1) ? a.n : P.cnt[j];
+  const int64_t start_j = (d == 1) ? 0 : P.start[j];
+  const int64_t o = (int64_t)(t - s_tile_pref[j]) * PT_TILE;
+  const int len = (int)min((int64_t)PT_TILE, cnt_j - o);
+  const int f = P.split_f[j], b = P.split_b[j];
+  const uint8_t* col = a.codesT + (size_t)f * a.ldT;
+  const uint32_t* rin = (d >= 2) ? a.sr[(d - 1) & 1] + start_j + o : nullptr;
+  uint32_t ridx[PT_ITEMS];
+#pragma unroll
+  for (int q = 0; q < PT_ITEMS; ++q) {
+    const int k = q * PT_THREADS + tid;
+    ridx[q] = k < len ? ((d == 1) ? (uint32_t)(o + k) : rin[k]) : 0u;
   }
-  for (int o = 16; o > 0; o >>= 1) myl += __shfl_xor_sync(0xffffffffu, myl, o);
-  if (lane == 0) s_wsum64[warp] = myl;
+  // all 16 code gathers in flight before any store (a global store between them would stop the
+  // compiler from hoisting the next load)
+  uint32_t code[PT_ITEMS];
+#pragma unroll
+  for (int q = 0; q < PT_ITEMS; ++q) code[q] = __ldg(col + ridx[q]);
+  int myl = 0;
+  unsigned mw[PT_ITEMS];
+#pragma unroll
+  for (int q = 0; q < PT_ITEMS; ++q) {
+    const int k = q * PT_THREADS + tid;
+    const bool left = k < len && code[q] <= (uint32_t)b;
+    myl += left;
+    mw[q] = __ballot_sync(0xffffffffu, left);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < PT_ITEMS; ++q) w.bits[(size_t)t * PT_WORDS + q * (PT_THREADS / 32) + warp] = mw[q];
+  }
+  for (int off = 16; off > 0; off >>= 1) myl += __shfl_xor_sync(0xffffffffu, myl, off);
+  if (lane == 0) s_w[warp] = myl;
   __syncthreads();
   if (tid == 0) {
-    int64_t t = 0;
-    for (int w2 = 0; w2 < PART_THREADS / 32; ++w2) t += s_wsum64[w2];
-    agg[blockIdx.x] = t;
-  }
-  grid.sync();
-  // ---- exclusive prefix over CTAs
-  if (warp == 0) {
-    int64_t sum = 0;
-    for (int c = lane; c < (int)blockIdx.x; c += 32) sum += agg[c];
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    if (lane == 0) s_prefix = sum;
+    int L = 0;
+    for (int w2 = 0; w2 < PT_THREADS / 32; ++w2) L += s_w[w2];
+    w.tile_left[t] = L;
+    if (a.units) atomicAdd(&a.units[KC_PARTITION], (unsigned long long)len);
   }
   __syncthreads();
-  int64_t lrun = s_prefix;   // global left prefix at the current position
-  // ---- phase 2: scatter in 2048-row sub-tiles (blocked: 8 consecutive rows per thread)
-  for (int j = jfirst; j < NP && s_seq_pref[j] < v1; ++j) {
-    const int64_t p0 = max(v0, s_seq_pref[j]), p1 = min(v1, s_seq_pref[j + 1]);
-    if (p0 >= p1) continue;
-    const int f = P.split_f[j], b = P.split_b[j];
-    const uint8_t* col = a.codesT + (size_t)f * a.n;
-    const int64_t base = (d == 1) ? 0 : P.start[j] - s_seq_pref[j];
-    if (p0 == s_seq_pref[j] && tid == 0) {   // this CTA holds the parent's first row
-      C.start[2 * j] = lrun;
-      C.start[2 * j + 1] = a.n + (p0 - lrun);
-    }
-    int64_t piece_left = 0;
-    for (int64_t t0 = p0; t0 < p1; t0 += TILE) {
-      const int len = (int)min((int64_t)TILE, p1 - t0);
-      for (int k = tid; k < len; k += PART_THREADS) {
-        const int64_t v = t0 + k;
-        s_state[k] = (d == 1) ? make_uint2((uint32_t)v, a.gp_root[v]) : st_in[base + v];
-      }
-      __syncthreads();
-      uint32_t lbits = 0;
-      int cnt = 0;
+  }
+}
+
+constexpr int PS_THREADS = 1024;
+__global__ void __launch_bounds__(PS_THREADS) k_pscan(const FitArgs a, const int d, const PartWs w) {
+  __shared__ int s_tile_pref[MAX_PIECES + 1];
+  __shared__ int64_t s_seq_pref[MAX_PIECES + 1];
+  __shared__ int s_w[PS_THREADS / 32];
+  __shared__ int64_t s_w64[PS_THREADS / 32];
+  const int NP = 1 << (d - 1);
+  const LevelView& P = a.lv[d - 1];
+  const LevelView& C = a.lv[d];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  parent_prefixes(a, d, s_tile_pref, s_seq_pref, s_w, s_w64);
+  const int T = s_tile_pref[NP];
+  // exclusive scan of the tile counts: contiguous block of tiles per thread
+  const int t0 = (int)((int64_t)T * tid / PS_THREADS), t1 = (int)((int64_t)T * (tid + 1) / PS_THREADS);
+  int64_t local = 0;
+  for (int t = t0; t < t1; ++t) local += w.tile_left[t];
+  int64_t inc = local;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) s_w64[warp] = inc;
+  __syncthreads();
+  int64_t run = 0;
+  for (int w2 = 0; w2 < warp; ++w2) run += s_w64[w2];
+  run += inc - local;
+  for (int t = t0; t < t1; ++t) {
+    w.tile_lpref[t] = run;
+    run += w.tile_left[t];
+  }
+  __syncthreads();   // global writes of this block are visible to the block after the barrier
+  for (int j = tid; j < NP; j += PS_THREADS) {
+    if (P.split_f[j] < 0) continue;
+    const int ta = s_tile_pref[j], tb = s_tile_pref[j + 1] - 1;
+    const int64_t cnt_j = (d == 1) ? a.n : P.cnt[j];
+    const int64_t lstart = w.tile_lpref[ta];
+    const int64_t nl = w.tile_lpref[tb] + w.tile_left[tb] - lstart;
+    C.start[2 * j] = lstart;
+    C.start[2 * j + 1] = a.n + (s_seq_pref[j] - lstart);
+    C.cnt[2 * j] = nl;
+    C.cnt[2 * j + 1] = cnt_j - nl;
+  }
+}
+
+__global__ void __launch_bounds__(PT_THREADS) k_pscatter(const FitArgs a, const int d, const PartWs w) {
+  __shared__ int s_tile_pref[MAX_PIECES + 1];
+  __shared__ int64_t s_seq_pref[MAX_PIECES + 1];
+  __shared__ int s_w[PT_THREADS / 32];
+  __shared__ int64_t s_w64[PT_THREADS / 32];
+  __shared__ uint32_t s_r[PT_HALF], s_g[PT_HALF];
+  const int NP = 1 << (d - 1);
+  const LevelView& P = a.lv[d - 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  parent_prefixes(a, d, s_tile_pref, s_seq_pref, s_w, s_w64);
+  for (int t = blockIdx.x; t < s_tile_pref[NP]; t += gridDim.x) {
+  const int j = parent_of_tile(s_tile_pref, NP, t);
+  const int64_t cnt_j = (d == 1) ? a.n : P.cnt[j];
+  const int64_t start_j = (d == 1) ? 0 : P.start[j];
+  const int64_t o = (int64_t)(t - s_tile_pref[j]) * PT_TILE;
+  const int len = (int)min((int64_t)PT_TILE, cnt_j - o);
+  const uint32_t* rin = (d >= 2) ? a.sr[(d - 1) & 1] + start_j + o : nullptr;
+  const uint32_t* gin = (d >= 2) ? a.sg[(d - 1) & 1] + start_j + o : a.gp_root + o;
+  int64_t lp = w.tile_lpref[t];
+  int64_t rbase = a.n + (s_seq_pref[j] + o - lp);   // global right prefix at the tile start
+  uint32_t* rout = a.sr[d & 1];
+  uint32_t* gout = a.sg[d & 1];
+  // the 4096-row tile in two 2048-row halves (8 rows per thread: low register pressure)
+  for (int hb = 0; hb < len; hb += PT_HALF) {
+  const int hlen = min(PT_HALF, len - hb);
+  // stage the half (coalesced)
 #pragma unroll
-      for (int q = 0; q < PART_ITEMS; ++q) {
-        const int k = tid * PART_ITEMS + q;
-        if (k < len) {
-          const int left = col[s_state[k].x] <= b;
-          lbits |= (uint32_t)left << q;
-          cnt += left;
-        }
-      }
-      int inc = cnt;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += u;
-      }
-      if (lane == 31) s_wsum[warp] = inc;
-      __syncthreads();
-      int woff = 0, L = 0;
-      for (int w2 = 0; w2 < PART_THREADS / 32; ++w2) {
-        if (w2 < warp) woff += s_wsum[w2];
-        L += s_wsum[w2];
-      }
-      const int my_excl = woff + inc - cnt;
-      const int64_t rbase = a.n + (t0 - lrun);     // global right prefix at t0 = t0 - lefts before t0
-      int lpos = my_excl, rpos = tid * PART_ITEMS - my_excl;
+  for (int q = 0; q < PT_HALF / PT_THREADS; ++q) {
+    const int k = q * PT_THREADS + tid;
+    if (k < hlen) {
+      s_r[k] = (d == 1) ? (uint32_t)(o + hb + k) : rin[hb + k];
+      s_g[k] = gin[hb + k];
+    }
+  }
+  // blocked: thread tid owns rows hb + tid*8 .. +7 = byte (tid & 3) of bitmask word hb/32 + tid/4
+  const uint32_t word = w.bits[(size_t)t * PT_WORDS + (hb >> 5) + (tid >> 2)];
+  uint32_t lbits = (word >> ((tid & 3) * 8)) & 0xffu;
+  const int first = tid * PT_HI;
+  if (first + PT_HI > hlen) lbits &= first >= hlen ? 0u : ((1u << (hlen - first)) - 1u);
+  const int cnt = __popc(lbits);
+  int inc = cnt;
+  for (int off = 1; off < 32; off <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc += u;
+  }
+  if (lane == 31) s_w[warp] = inc;
+  __syncthreads();
+  int woff = 0, L = 0;
+  for (int w2 = 0; w2 < PT_THREADS / 32; ++w2) {
+    if (w2 < warp) woff += s_w[w2];
+    L += s_w[w2];
+  }
+  const int my_excl = woff + inc - cnt;
+  uint32_t rr[PT_HI], gg[PT_HI];
 #pragma unroll
-      for (int q = 0; q < PART_ITEMS; ++q) {
-        const int k = tid * PART_ITEMS + q;
-        if (k < len) {
-          const uint2 s = s_state[k];
-          if ((lbits >> q) & 1u) st_out[lrun + lpos++] = s;
-          else st_out[rbase + rpos++] = s;
-        }
-      }
-      lrun += L;
-      piece_left += L;
-      __syncthreads();
+  for (int q = 0; q < PT_HI; ++q) {
+    const int k = first + q;
+    rr[q] = k < hlen ? s_r[k] : 0u;
+    gg[q] = k < hlen ? s_g[k] : 0u;
+  }
+  __syncthreads();
+  int lpos = my_excl, rpos = L + first - my_excl;
+#pragma unroll
+  for (int q = 0; q < PT_HI; ++q) {
+    if (first + q < hlen) {
+      const int dst = ((lbits >> q) & 1u) ? lpos++ : rpos++;
+      s_r[dst] = rr[q];
+      s_g[dst] = gg[q];
     }
-    if (tid == 0) {
-      atomicAdd(reinterpret_cast<unsigned long long*>(&C.cnt[2 * j]), (unsigned long long)piece_left);
-      atomicAdd(reinterpret_cast<unsigned long long*>(&C.cnt[2 * j + 1]), (unsigned long long)(p1 - p0 - piece_left));
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < PT_HALF / PT_THREADS; ++q) {
+    const int k = q * PT_THREADS + tid;
+    if (k < hlen) {
+      const int64_t dst = k < L ? lp + k : rbase + (k - L);
+      rout[dst] = s_r[k];
+      gout[dst] = s_g[k];
     }
+  }
+  lp += L;
+  rbase += hlen - L;
+  __syncthreads();
+  }
   }
 }
 // ---------------------------------------------------------------------------------------------
@@ -722,20 +1035,22 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update(const FitArgs a, const i
   const int64_t stride = (int64_t)gridDim.x * UPD_THREADS;
   for (int64_t i0 = (int64_t)blockIdx.x * UPD_THREADS + tid; i0 < a.n; i0 += stride * UPD_R) {
     float pv[UPD_R], yv[UPD_R], wv[UPD_R];
+    uint4 cv0[UPD_R], cv1[UPD_R];
+    // all loads first (clamped index, no branches), then the shared-memory stores
 #pragma unroll
     for (int q = 0; q < UPD_R; ++q) {
-      const int64_t i = i0 + q * stride;
-      if (i < a.n) {
-        const uint4* crow = reinterpret_cast<const uint4*>(a.codes + (size_t)i * kMaxF);
-        const uint4 c0 = __ldg(crow), c1 = __ldg(crow + 1);
-        *reinterpret_cast<uint4*>(&s_row[q][tid * 32]) = c0;
-        *reinterpret_cast<uint4*>(&s_row[q][tid * 32 + 16]) = c1;
-        pv[q] = a.p[i];
-        if (has_next) {
-          yv[q] = a.y[i];
-          wv[q] = a.w[i];
-        }
-      }
+      const int64_t i = min(i0 + q * stride, a.n - 1);
+      const uint4* crow = reinterpret_cast<const uint4*>(a.codes + (size_t)i * kMaxF);
+      cv0[q] = __ldg(crow);
+      cv1[q] = __ldg(crow + 1);
+      pv[q] = a.p[i];
+      yv[q] = a.y[i];
+      wv[q] = a.w[i];
+    }
+#pragma unroll
+    for (int q = 0; q < UPD_R; ++q) {
+      *reinterpret_cast<uint4*>(&s_row[q][tid * 32]) = cv0[q];
+      *reinterpret_cast<uint4*>(&s_row[q][tid * 32 + 16]) = cv1[q];
     }
     int k[UPD_R];
 #pragma unroll
@@ -981,8 +1296,10 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   // ---- cuts + codes (row-major for histograms/routing, column-major for partitions)
   compute_cuts(ctx, ds.X, n, F, ds.row_offset, ds.n_global, hp.max_bin, out.cuts);
   DevBuf& d_codes = ctx->workspace("codes", (size_t)n * kMaxF);
-  DevBuf& d_codesT = ctx->workspace("codesT", (size_t)n * kMaxF);
-  compute_codes(ctx, ds.X, n, F, out.cuts, d_codes.as<uint8_t>(), d_codesT.as<uint8_t>(), nullptr);
+  const int64_t ldT = (n + 31) / 32 * 32;
+  DevBuf& d_codesT = ctx->workspace("codesT", (size_t)ldT * kMaxF);
+  LLMP_CUDA(cudaMemsetAsync(d_codesT.p, 0, (size_t)ldT * kMaxF, s));   // zero the padding rows
+  compute_codes(ctx, ds.X, n, F, out.cuts, d_codes.as<uint8_t>(), d_codesT.as<uint8_t>(), ldT, nullptr);
 
   // ---- training state
   const int nn = (1 << (D + 1)) - 1;
@@ -992,8 +1309,10 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   DevBuf& d_p = keep_train_pred ? out.d_train_pred : ctx->workspace("p", (size_t)n * 4 * 2);
   out.device = ctx->device;
   DevBuf& d_gp = ctx->workspace("gp_root", (size_t)n * 4);
-  DevBuf& d_st0 = ctx->workspace("state0", (size_t)n * 2 * 8);
-  DevBuf& d_st1 = ctx->workspace("state1", (size_t)n * 2 * 8);
+  DevBuf& d_sr0 = ctx->workspace("ridx0", (size_t)n * 2 * 4);
+  DevBuf& d_sr1 = ctx->workspace("ridx1", (size_t)n * 2 * 4);
+  DevBuf& d_sg0 = ctx->workspace("gp0", (size_t)n * 2 * 4);
+  DevBuf& d_sg1 = ctx->workspace("gp1", (size_t)n * 2 * 4);
   DevBuf& d_H0 = ctx->workspace("hist0", (size_t)half_max * SLOT * 8);
   DevBuf& d_H1 = ctx->workspace("hist1", (size_t)half_max * SLOT * 8);
   DevBuf& d_trees = ctx->workspace("trees", (size_t)2 * std::max(T, 1) * nn * 16);
@@ -1024,10 +1343,13 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   a.T = T;
   a.codes = d_codes.as<uint8_t>();
   a.codesT = d_codesT.as<uint8_t>();
+  a.ldT = ldT;
   a.w = d_w.as<float>();
   a.gp_root = d_gp.as<uint32_t>();
-  a.st[0] = d_st0.as<uint2>();
-  a.st[1] = d_st1.as<uint2>();
+  a.sr[0] = d_sr0.as<uint32_t>();
+  a.sr[1] = d_sr1.as<uint32_t>();
+  a.sg[0] = d_sg0.as<uint32_t>();
+  a.sg[1] = d_sg1.as<uint32_t>();
   a.H[0] = d_H0.as<int64_t>();
   a.H[1] = d_H1.as<int64_t>();
   a.cuts = out.cuts.d_cuts.as<float>();
@@ -1085,17 +1407,18 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   LLMP_CUDA(cudaMemsetAsync(d_sums.p, 0, d_sums.bytes, s));
 
   const int hist_grid = 2 * ctx->sms;
-  // cooperative partition: every CTA must be co-resident (grid.sync between its two phases)
-  int part_occ = 0;
-  LLMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&part_occ, k_partition, PART_THREADS, 0));
-  LLMP_REQUIRE(part_occ >= 1, "partition kernel cannot be resident");
-  const int part_grid = std::min(part_occ, 8) * ctx->sms;
-  DevBuf& d_agg = ctx->workspace("part_agg", (size_t)part_grid * 8);
+  // partition workspaces: per-tile counts, prefixes and left bits (max tiles over the levels)
+  const int64_t max_tiles = (n + PT_TILE - 1) / PT_TILE + half_max + 1;
+  PartWs pw;
+  pw.tile_left = ctx->workspace("tile_left", (size_t)max_tiles * 4).as<int32_t>();
+  pw.tile_lpref = ctx->workspace("tile_lpref", (size_t)max_tiles * 8).as<int64_t>();
+  pw.bits = ctx->workspace("tile_bits", (size_t)max_tiles * PT_WORDS * 4).as<uint32_t>();
   const int upd_grid = grid_for(ctx, n, UPD_THREADS, 8);
   const int base_grid = grid_for(ctx, n, BASE_THREADS, 8);
   static bool attr_set = false;
   if (!attr_set) {
     LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_ROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
+    LLMP_CUDA(cudaFuncSetAttribute(k_hist_root2, cudaFuncAttributeMaxDynamicSharedMemorySize, R2_SMEM));
     LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_LEVEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
     LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
     attr_set = true;
@@ -1132,24 +1455,19 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       a.tval = val_all + ((size_t)target * T + t) * nn;
       LLMP_CUDA(cudaMemsetAsync(d_ctl.p, 0, ctl_zero, s));
       LLMP_CUDA(cudaMemsetAsync(a.H[0], 0, (size_t)SLOT * 8, s));
-      LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist<HM_ROOT>, hist_grid, HIST_THREADS, HIST_SMEM, a, 0, t, nodbg);
+      LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist_root2, hist_grid, R2_THREADS, R2_SMEM, a, t);
       allreduce_sum_i64(ctx, a.H[0], SLOT);
       LLMP_LAUNCH(ctx, KC_SPLIT, 1, k_split, 32, SPLIT_THREADS, 0, a, 0, t);
       for (int d = 1; d < D; ++d) {
-        {
-          cudaEvent_t ev = nullptr;
-          ctx->before(KC_PARTITION, &ev);
-          int dd = d;
-          int64_t* aggp = d_agg.as<int64_t>();
-          void* kargs[] = {(void*)&a, (void*)&dd, (void*)&aggp};
-          LLMP_CUDA(cudaLaunchCooperativeKernel((void*)k_partition, part_grid, PART_THREADS, kargs, 0, s));
-          ctx->after(KC_PARTITION, ev, (double)n);
-        }
-        if (ctx->nranks > 1) {
+        const int tiles_d = (int)((n + PT_TILE - 1) / PT_TILE) + (1 << (d - 1));
+        LLMP_LAUNCH(ctx, KC_PARTITION, n, k_pcount, std::min(tiles_d, 5 * ctx->sms), PT_THREADS, 0, a, d, pw);
+        LLMP_LAUNCH(ctx, KC_PARTITION, 0, k_pscan, 1, PS_THREADS, 0, a, d, pw);
+        LLMP_LAUNCH(ctx, KC_PARTITION, 0, k_pscatter, std::min(tiles_d, 4 * ctx->sms), PT_THREADS, 0, a, d, pw);
+        if (ctx->nranks > 1) {   // every rank must histogram the same (globally smaller) child
           LLMP_CUDA(cudaMemcpyAsync(a.lv[d].gcnt, a.lv[d].cnt, ((size_t)1 << d) * 8, cudaMemcpyDeviceToDevice, s));
           allreduce_sum_i64(ctx, a.lv[d].gcnt, (size_t)1 << d);
         }
-        LLMP_LAUNCH(ctx, KC_HIST, n / 2, k_hist<HM_LEVEL>, hist_grid, HIST_THREADS, HIST_SMEM, a, d, t, nodbg);
+        LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hist_grid, HIST_THREADS, HIST_SMEM, a, d, t, nodbg);
         allreduce_sum_i64(ctx, a.H[d & 1], (size_t)SLOT << (d - 1));
         LLMP_LAUNCH(ctx, KC_SPLIT, (1 << d), k_split, (1 << d) * 32, SPLIT_THREADS, 0, a, d, t);
       }

@@ -33,8 +33,9 @@ void compute_cuts(Ctx* ctx, const float* X, int64_t n, int F, int64_t row_offset
                   CutsData& out);
 // codes: row-major n x 32 (may be null); codesT: column-major 32 x n (may be null).
 // flag (device int, may be null) is set to 1 when X holds a non-finite value.
+// codesT leading dimension ldT >= n (bytes between features; the fit pads it to a multiple of 32)
 void compute_codes(Ctx* ctx, const float* X, int64_t n, int F, const CutsData& cuts, uint8_t* codes, uint8_t* codesT,
-                   int* flag);
+                   int64_t ldT, int* flag);
 
 // fit.cu
 struct DatasetDev {  // resolved device pointers

@@ -41,6 +41,6 @@ for r in range(a.repeat):
 torch.cuda.synchronize()
 out = {"rows": d.n, "trees": a.trees, "depth": a.depth, "data": "S1" if a.s1 else "S2/C3"}
 for k, v in st["classes"].items():
-    out[k] = {"launches": v["launches"], "ms": round(v["ms"], 3), "us_per_launch": round(1000 * v["ms"] / v["launches"], 2),
+    out[k] = {"launches": v["launches"], "ms": round(v["ms"], 3), "us_per_launch": round(1000 * v["ms"] / max(1, v["launches"]), 2),
               "units": v["rows"]}
 print(json.dumps(out, indent=1))
