@@ -254,7 +254,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     ctx.reset_stats()
-    ctx.set_timing(True)
+    ctx.set_timing(0)            # production mode: each tree replays from a CUDA graph
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
@@ -266,7 +266,6 @@ def main():
         dist.barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
     stats = ctx.stats()
-    ctx.set_timing(False)
     clk = clocks.stop()
     fit_ms = sum(a.elapsed_time(b) for a, b, c in ev)
     pred_ms = sum(b.elapsed_time(c) for a, b, c in ev)
@@ -279,15 +278,29 @@ def main():
     value = row_iters / (elapsed_ms / 1000.0)
     predict_rows = float(sweep_rows) * world * args.steps
 
+    # ---- per-kernel durations: one more step, instrumented (plain launches, every 8th launch of
+    # each kernel class bracketed by CUDA events on the context stream)
+    ctx.reset_stats()
+    ctx.set_timing(8)
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    step(Xd, yd, ld, pd, lfd, pfd)
+    p1.record(stream)
+    torch.cuda.synchronize()
+    prof_step_ms = p0.elapsed_time(p1)
+    pstats = ctx.stats()
+    ctx.set_timing(0)
+
     # ---- per-kernel roofline from the live event timings
     peak, peak_src = measured_peaks()
     traffic = ncu_traffic()
     kernels = {}
-    for name, c in stats["classes"].items():
+    for name, c in pstats["classes"].items():
         if c["ms"] <= 0:
             continue
-        k = {"launches": c["launches"], "ms_total": round(c["ms"], 3), "ms_avg": c["ms"] / c["launches"],
-             "share_of_step": c["ms"] / elapsed_ms}
+        k = {"launches": c["launches"], "timed_launches": c["timed"], "ms_total": round(c["ms"], 3),
+             "ms_avg": c["ms_avg"], "share_of_step": c["ms"] / prof_step_ms}
         if name in BYTES_PER_UNIT and c["rows"] > 0:
             nbytes = BYTES_PER_UNIT[name] * c["rows"]
             gbs = nbytes / (c["ms"] / 1000.0) / 1e9
@@ -370,7 +383,11 @@ def main():
             "fit": {"value": row_iters / (fit_ms / 1000.0), "unit": UNIT, "ms_per_step": fit_ms / args.steps},
             "roofline": roofline,
             "kernels": kernels,
+            "kernels_note": "per-kernel durations from one extra instrumented step (plain launches, every 8th "
+                            "launch of each class CUDA-event-timed on the context stream, %.1f ms); the timed "
+                            "steps replay each tree from a CUDA graph" % prof_step_ms,
             "gpu_launches": stats["total_launches"],
+            "gpu_launches_per_step": stats["total_launches"] / args.steps,
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,

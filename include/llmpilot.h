@@ -65,18 +65,21 @@ void llmpilot_ctx_destroy(llmpilot_ctx* ctx);
  * the other ranks, e.g. over a torch.distributed process group).  LLMP_ENCCL if NCCL is absent. */
 llmpilot_status llmpilot_nccl_unique_id(void* out);
 
-/* Instrumentation (used by bench.py).  With timing enabled every kernel launch is bracketed by
- * CUDA events on the context stream; stats report, per kernel class, the number of launches
- * and the summed event-measured milliseconds since the last reset.  Class names are listed by
- * llmpilot_kernel_class_name(i) for i < LLMP_N_KERNEL_CLASSES. */
+/* Instrumentation (used by bench.py).  llmpilot_ctx_set_timing(ctx, every): every == 0 turns
+ * timing off (fits then replay each tree from a CUDA graph); every >= 1 brackets every
+ * every-th launch of each kernel class with CUDA events on the context stream (plain launches,
+ * no graphs).  Stats report, per kernel class, the launches, the event-timed launches and their
+ * summed milliseconds, and the rows (units) processed, since the last reset.  Class names are
+ * listed by llmpilot_kernel_class_name(i) for i < LLMP_N_KERNEL_CLASSES. */
 #define LLMP_N_KERNEL_CLASSES 16
 typedef struct {
   uint64_t launches[LLMP_N_KERNEL_CLASSES];
-  double ms[LLMP_N_KERNEL_CLASSES];       /* valid only when timing was enabled */
-  double rows[LLMP_N_KERNEL_CLASSES];     /* rows (units) each class processed */
+  uint64_t timed[LLMP_N_KERNEL_CLASSES];  /* launches that were event-timed */
+  double ms[LLMP_N_KERNEL_CLASSES];       /* summed duration of the timed launches */
+  double rows[LLMP_N_KERNEL_CLASSES];     /* rows (units) each class processed (all launches) */
   uint64_t total_launches;
 } llmpilot_stats;
-llmpilot_status llmpilot_ctx_set_timing(llmpilot_ctx* ctx, int enable);
+llmpilot_status llmpilot_ctx_set_timing(llmpilot_ctx* ctx, int every);
 llmpilot_status llmpilot_ctx_stats(llmpilot_ctx* ctx, llmpilot_stats* out); /* synchronises the stream */
 llmpilot_status llmpilot_ctx_reset_stats(llmpilot_ctx* ctx);
 const char* llmpilot_kernel_class_name(int i);

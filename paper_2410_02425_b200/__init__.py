@@ -45,8 +45,9 @@ class DatasetC(C.Structure):
 
 
 class Stats(C.Structure):
-    _fields_ = [("launches", C.c_uint64 * N_KERNEL_CLASSES), ("ms", C.c_double * N_KERNEL_CLASSES),
-                ("rows", C.c_double * N_KERNEL_CLASSES), ("total_launches", C.c_uint64)]
+    _fields_ = [("launches", C.c_uint64 * N_KERNEL_CLASSES), ("timed", C.c_uint64 * N_KERNEL_CLASSES),
+                ("ms", C.c_double * N_KERNEL_CLASSES), ("rows", C.c_double * N_KERNEL_CLASSES),
+                ("total_launches", C.c_uint64)]
 
 
 class Rec(C.Structure):
@@ -185,8 +186,10 @@ class Context:
         except Exception:
             pass
 
-    def set_timing(self, enable: bool):
-        _check(lib().llmpilot_ctx_set_timing(self._h, int(enable)))
+    def set_timing(self, every: int):
+        """0: off (trees replay from CUDA graphs); k >= 1: CUDA-event-time every k-th launch of each
+        kernel class (plain launches)."""
+        _check(lib().llmpilot_ctx_set_timing(self._h, int(every)))
 
     def reset_stats(self):
         _check(lib().llmpilot_ctx_reset_stats(self._h))
@@ -198,7 +201,10 @@ class Context:
         out = {"total_launches": int(s.total_launches), "classes": {}}
         for i, nm in enumerate(names):
             if s.launches[i] or s.rows[i]:
-                out["classes"][nm] = {"launches": int(s.launches[i]), "ms": float(s.ms[i]), "rows": float(s.rows[i])}
+                timed = int(s.timed[i])
+                avg = float(s.ms[i]) / timed if timed else 0.0
+                out["classes"][nm] = {"launches": int(s.launches[i]), "timed": timed, "ms_timed": float(s.ms[i]),
+                                      "ms_avg": avg, "ms": avg * int(s.launches[i]), "rows": float(s.rows[i])}
         return out
 
 

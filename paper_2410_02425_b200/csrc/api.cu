@@ -129,14 +129,17 @@ void llmpilot_ctx_destroy(llmpilot_ctx* ctx) {
   for (auto e : ctx->c.free_events) cudaEventDestroy(e);
   llmp::nccl_destroy(&ctx->c);
   if (ctx->c.d_units) cudaFree(ctx->c.d_units);
+  if (ctx->c.cap_stream) cudaStreamDestroy(ctx->c.cap_stream);
   delete ctx;
 }
 
-llmpilot_status llmpilot_ctx_set_timing(llmpilot_ctx* ctx, int enable) {
+llmpilot_status llmpilot_ctx_set_timing(llmpilot_ctx* ctx, int every) {
   return guarded([&] {
     LLMP_REQUIRE(ctx, "ctx is NULL");
+    LLMP_REQUIRE(every >= 0, "every must be >= 0");
     ctx->c.collect();
-    ctx->c.timing = enable != 0;
+    ctx->c.timing = every != 0;
+    ctx->c.timing_every = every > 0 ? every : 1;
   });
 }
 
@@ -151,6 +154,7 @@ llmpilot_status llmpilot_ctx_stats(llmpilot_ctx* ctx, llmpilot_stats* out) {
     LLMP_CUDA(cudaMemcpy(units, ctx->c.d_units, sizeof(units), cudaMemcpyDeviceToHost));
     for (int i = 0; i < LLMP_N_KERNEL_CLASSES; ++i) {
       out->launches[i] = ctx->c.launches[i];
+      out->timed[i] = ctx->c.timed[i];
       out->ms[i] = ctx->c.ms_done[i];
       const bool dev_counted = i == llmp::KC_HIST_ROOT || i == llmp::KC_HIST || i == llmp::KC_PARTITION;
       out->rows[i] = dev_counted ? (double)units[i] : ctx->c.rows[i];
@@ -165,6 +169,7 @@ llmpilot_status llmpilot_ctx_reset_stats(llmpilot_ctx* ctx) {
     ctx->c.collect();
     for (int i = 0; i < LLMP_N_KERNEL_CLASSES; ++i) {
       ctx->c.launches[i] = 0;
+      ctx->c.timed[i] = 0;
       ctx->c.ms_done[i] = 0;
       ctx->c.rows[i] = 0;
     }
@@ -316,14 +321,10 @@ llmpilot_status llmpilot_predict(llmpilot_ctx* ctx, const llmpilot_model* m, con
     LLMP_REQUIRE(n >= 0, "n must be >= 0");
     if (n == 0) return;
     set_device(&ctx->c);
-    llmp::DevBuf tx, to;
-    const float* Xd = (const float*)llmp::to_device(&ctx->c, X, (size_t)n * m->m.F * 4, tx);
+    const float* Xd = (const float*)llmp::to_device(&ctx->c, X, (size_t)n * m->m.F * 4, ctx->c.ws["pred_X"]);
     const bool out_dev = llmp::is_device_ptr(out);
     float* od = out;
-    if (!out_dev) {
-      to.ensure((size_t)n * 8);
-      od = to.as<float>();
-    }
+    if (!out_dev) od = ctx->c.workspace("pred_out", (size_t)n * 8).as<float>();
     llmp::predict_impl(&ctx->c, m->m, Xd, n, od);
     if (!out_dev) {
       LLMP_CUDA(cudaMemcpyAsync(out, od, (size_t)n * 8, cudaMemcpyDeviceToHost, ctx->c.stream));
@@ -352,9 +353,11 @@ llmpilot_status llmpilot_recommend(llmpilot_ctx* ctx, const llmpilot_model* m, c
     if (n_llm == 0) return;
     LLMP_REQUIRE((F_llm == 0 || llm_feats) && (F_prof == 0 || prof_feats), "feature tables are required");
     set_device(&ctx->c);
-    llmp::DevBuf tl, tp, tpred;
-    const float* lf = (const float*)llmp::to_device(&ctx->c, llm_feats, (size_t)n_llm * F_llm * 4, tl);
-    const float* pf = (const float*)llmp::to_device(&ctx->c, prof_feats, (size_t)n_prof * F_prof * 4, tp);
+    llmp::DevBuf tpred;
+    const float* lf =
+        (const float*)llmp::to_device(&ctx->c, llm_feats, (size_t)n_llm * F_llm * 4, ctx->c.ws["rec_llm"]);
+    const float* pf =
+        (const float*)llmp::to_device(&ctx->c, prof_feats, (size_t)n_prof * F_prof * 4, ctx->c.ws["rec_prof"]);
     const int64_t nrows = (int64_t)n_llm * n_prof * n_levels;
     float* pred_dev = nullptr;
     const bool pred_is_dev = pred_out && llmp::is_device_ptr(pred_out);

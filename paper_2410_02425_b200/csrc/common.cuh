@@ -75,6 +75,15 @@ struct Ctx {
   int sms = 148;
   unsigned long long* d_units = nullptr;  // [LLMP_N_KERNEL_CLASSES] device-side unit counters
   bool timing = false;
+  int timing_every = 1;                    // time every k-th launch of each class
+  uint64_t timed[LLMP_N_KERNEL_CLASSES] = {};
+  bool use_graphs = true;                  // replay each tree from a CUDA graph (off while timing)
+  cudaStream_t cap_stream = nullptr;       // private stream used only for graph capture
+  cudaStream_t capture_stream() {
+    if (!cap_stream) check_cuda(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking), "capture stream",
+                                __FILE__, __LINE__);
+    return cap_stream;
+  }
   uint64_t launches[LLMP_N_KERNEL_CLASSES] = {};
   double rows[LLMP_N_KERNEL_CLASSES] = {};
   double ms_done[LLMP_N_KERNEL_CLASSES] = {};

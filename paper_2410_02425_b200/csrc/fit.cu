@@ -78,6 +78,7 @@ struct FitArgs {
   uint32_t* sg[2];   // packed gradient pair state, same positions
   int64_t* H[2];
   LevelView lv[kMaxDepth + 1];
+  const int* d_tree; // device-side index of the tree being grown (advanced by k_next_tree)
   uint32_t* maxg;    // [T+1] float bits of max |g| per tree (slot T: base score)
   uint32_t* maxh;
   const float* cuts;     // [32][255]
@@ -338,7 +339,8 @@ __device__ __forceinline__ uint32_t change_nibble(uint32_t cur, uint32_t prevw) 
   return (t * 0x00204081u) >> 28;
 }
 
-__global__ void __launch_bounds__(R2_THREADS, 2) k_hist_root2(const FitArgs a, const int t) {
+__global__ void __launch_bounds__(R2_THREADS, 2) k_hist_root2(const FitArgs a) {
+  const int t = *a.d_tree;
   extern __shared__ __align__(16) uint8_t smem[];
   int32_t* hg = reinterpret_cast<int32_t*>(smem);                       // [256][33]
   uint32_t* hh = reinterpret_cast<uint32_t*>(smem + R2_HIST_WORDS * 4);
@@ -801,7 +803,12 @@ __device__ __forceinline__ bool better_fb(double la, int fa, int ba, double lb, 
   return ba < bb;
 }
 
-__global__ void __launch_bounds__(SPLIT_THREADS) k_split(const FitArgs a, const int d, const int t) {
+__global__ void __launch_bounds__(SPLIT_THREADS) k_split(const FitArgs a, const int d) {
+  const int t = *a.d_tree;   // device-side tree index (the tree's kernels are replayed from a CUDA graph)
+  int32_t* const tfeat = a.tfeat + (size_t)t * a.nn;
+  int32_t* const tbin = a.tbin + (size_t)t * a.nn;
+  float* const tthr = a.tthr + (size_t)t * a.nn;
+  float* const tval = a.tval + (size_t)t * a.nn;
   const int k = blockIdx.x >> 5, f = blockIdx.x & 31;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const LevelView& V = a.lv[d];
@@ -968,10 +975,10 @@ __global__ void __launch_bounds__(SPLIT_THREADS) k_split(const FitArgs a, const 
     }
     V.split_f[k] = fs;
     V.split_b[k] = bs;
-    a.tfeat[gk] = fs;
-    a.tbin[gk] = bs;
-    a.tthr[gk] = a.cuts[fs * (kBins - 1) + bs];
-    a.tval[gk] = 0.0f;
+    tfeat[gk] = fs;
+    tbin[gk] = bs;
+    tthr[gk] = a.cuts[fs * (kBins - 1) + bs];
+    tval[gk] = 0.0f;
     if (d + 1 < a.D) {
       const LevelView& N = a.lv[d + 1];
       N.lo[2 * k] = loL;
@@ -980,15 +987,15 @@ __global__ void __launch_bounds__(SPLIT_THREADS) k_split(const FitArgs a, const 
       N.hi[2 * k + 1] = hiR;
     } else {
       // children at max depth are leaves: v = (float)(eta * W(G, H, lo, hi))
-      a.tfeat[2 * gk + 1] = -1;
-      a.tval[2 * gk + 1] = (float)__dmul_rn(a.eta, calc_weight(GL, HL, loL, hiL, lambda, mcw));
-      a.tfeat[2 * gk + 2] = -1;
-      a.tval[2 * gk + 2] = (float)__dmul_rn(a.eta, calc_weight(GR, HR, loR, hiR, lambda, mcw));
+      tfeat[2 * gk + 1] = -1;
+      tval[2 * gk + 1] = (float)__dmul_rn(a.eta, calc_weight(GL, HL, loL, hiL, lambda, mcw));
+      tfeat[2 * gk + 2] = -1;
+      tval[2 * gk + 2] = (float)__dmul_rn(a.eta, calc_weight(GR, HR, loR, hiR, lambda, mcw));
     }
   } else {
     V.split_f[k] = -1;
-    a.tfeat[gk] = -1;
-    a.tval[gk] = (float)__dmul_rn(a.eta, wP);
+    tfeat[gk] = -1;
+    tval[gk] = (float)__dmul_rn(a.eta, wP);
   }
 }
 // ---------------------------------------------------------------------------------------------
@@ -1016,7 +1023,11 @@ __device__ __forceinline__ void block_max2(float& a, float& b, float* s_a, float
 }
 
 constexpr int UPD_R = 4;   // rows per thread per iteration (independent traversals for ILP)
-__global__ void __launch_bounds__(UPD_THREADS) k_update(const FitArgs a, const int t) {
+__global__ void __launch_bounds__(UPD_THREADS) k_update(const FitArgs a) {
+  const int t = *a.d_tree;
+  const int32_t* const tfeat = a.tfeat + (size_t)t * a.nn;
+  const int32_t* const tbin = a.tbin + (size_t)t * a.nn;
+  const float* const tval = a.tval + (size_t)t * a.nn;
   __shared__ int8_t s_feat[MAX_NODES];
   __shared__ uint8_t s_bin[MAX_NODES];
   __shared__ float s_val[MAX_NODES];
@@ -1024,10 +1035,10 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update(const FitArgs a, const i
   __shared__ float s_ma[UPD_THREADS / 32], s_mb[UPD_THREADS / 32];
   const int tid = threadIdx.x;
   for (int i = tid; i < a.nn; i += UPD_THREADS) {   // a.tfeat/tbin/tval point at tree t
-    const int f = a.tfeat[i];
+    const int f = tfeat[i];
     s_feat[i] = (int8_t)(f < 0 ? -1 : f);
-    s_bin[i] = (uint8_t)a.tbin[i];
-    s_val[i] = a.tval[i];
+    s_bin[i] = (uint8_t)tbin[i];
+    s_val[i] = tval[i];
   }
   __syncthreads();
   const bool has_next = t + 1 < a.T;
@@ -1157,6 +1168,8 @@ __global__ void __launch_bounds__(BASE_THREADS) k_base_init(const FitArgs a, con
     atomicMax(&a.maxh[0], __float_as_uint(mh));
   }
 }
+
+__global__ void k_next_tree(int* d_tree) { *d_tree += 1; }
 
 __global__ void k_fill_trees(int32_t* feat, int32_t* bin, float* thr, float* val, size_t count) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
@@ -1424,7 +1437,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     attr_set = true;
   }
   const DbgArgs nodbg{};
-  const size_t ctl_zero = 64 * 4 + lvl_nodes * 8 * 2 + (size_t)max_tiles_total * 8;
+  int* d_tree = ctx->workspace("tree_idx", sizeof(int)).as<int>();
+  a.d_tree = d_tree;
 
   for (int target = 0; target < 2; ++target) {
     a.target = target;
@@ -1448,34 +1462,65 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       allreduce_max_u32(ctx, a.maxg, 1);
       allreduce_max_u32(ctx, a.maxh, 1);
     }
-    for (int t = 0; t < T; ++t) {
-      a.tfeat = feat_all + ((size_t)target * T + t) * nn;
-      a.tbin = bin_all + ((size_t)target * T + t) * nn;
-      a.tthr = thr_all + ((size_t)target * T + t) * nn;
-      a.tval = val_all + ((size_t)target * T + t) * nn;
-      LLMP_CUDA(cudaMemsetAsync(d_ctl.p, 0, ctl_zero, s));
-      LLMP_CUDA(cudaMemsetAsync(a.H[0], 0, (size_t)SLOT * 8, s));
-      LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist_root2, hist_grid, R2_THREADS, R2_SMEM, a, t);
+    // one tree = a fixed sequence of launches that reads the tree index from the device, so it
+    // is captured once into a CUDA graph and replayed T times (no per-kernel launch overhead);
+    // with timing instrumentation on it runs as plain launches instead
+    auto tree = [&]() {
+      const cudaStream_t st = ctx->stream;
+      LLMP_CUDA(cudaMemsetAsync(a.H[0], 0, (size_t)SLOT * 8, st));
+      LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist_root2, hist_grid, R2_THREADS, R2_SMEM, a);
       allreduce_sum_i64(ctx, a.H[0], SLOT);
-      LLMP_LAUNCH(ctx, KC_SPLIT, 1, k_split, 32, SPLIT_THREADS, 0, a, 0, t);
+      LLMP_LAUNCH(ctx, KC_SPLIT, 1, k_split, 32, SPLIT_THREADS, 0, a, 0);
       for (int d = 1; d < D; ++d) {
         const int tiles_d = (int)((n + PT_TILE - 1) / PT_TILE) + (1 << (d - 1));
         LLMP_LAUNCH(ctx, KC_PARTITION, n, k_pcount, std::min(tiles_d, 5 * ctx->sms), PT_THREADS, 0, a, d, pw);
         LLMP_LAUNCH(ctx, KC_PARTITION, 0, k_pscan, 1, PS_THREADS, 0, a, d, pw);
         LLMP_LAUNCH(ctx, KC_PARTITION, 0, k_pscatter, std::min(tiles_d, 4 * ctx->sms), PT_THREADS, 0, a, d, pw);
         if (ctx->nranks > 1) {   // every rank must histogram the same (globally smaller) child
-          LLMP_CUDA(cudaMemcpyAsync(a.lv[d].gcnt, a.lv[d].cnt, ((size_t)1 << d) * 8, cudaMemcpyDeviceToDevice, s));
+          LLMP_CUDA(cudaMemcpyAsync(a.lv[d].gcnt, a.lv[d].cnt, ((size_t)1 << d) * 8, cudaMemcpyDeviceToDevice, st));
           allreduce_sum_i64(ctx, a.lv[d].gcnt, (size_t)1 << d);
         }
-        LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hist_grid, HIST_THREADS, HIST_SMEM, a, d, t, nodbg);
+        LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hist_grid, HIST_THREADS, HIST_SMEM, a, d, 0, nodbg);
         allreduce_sum_i64(ctx, a.H[d & 1], (size_t)SLOT << (d - 1));
-        LLMP_LAUNCH(ctx, KC_SPLIT, (1 << d), k_split, (1 << d) * 32, SPLIT_THREADS, 0, a, d, t);
+        LLMP_LAUNCH(ctx, KC_SPLIT, (1 << d), k_split, (1 << d) * 32, SPLIT_THREADS, 0, a, d);
       }
-      LLMP_LAUNCH(ctx, KC_UPDATE, n, k_update, upd_grid, UPD_THREADS, 0, a, t);
-      if (t + 1 < T) {
-        allreduce_max_u32(ctx, a.maxg + t + 1, 1);
-        allreduce_max_u32(ctx, a.maxh + t + 1, 1);
+      LLMP_LAUNCH(ctx, KC_UPDATE, n, k_update, upd_grid, UPD_THREADS, 0, a);
+      // next tree's gradient maxima (past slots are already equal on every rank, future ones 0)
+      allreduce_max_u32(ctx, a.maxg, (size_t)2 * (T + 1));
+      LLMP_LAUNCH(ctx, KC_MISC, 0, k_next_tree, 1, 1, 0, d_tree);
+    };
+    LLMP_CUDA(cudaMemsetAsync(d_tree, 0, sizeof(int), s));
+    if (T > 0 && !ctx->timing && ctx->use_graphs) {
+      cudaGraph_t g = nullptr;
+      cudaGraphExec_t ge = nullptr;
+      const cudaStream_t user = ctx->stream;
+      ctx->stream = ctx->capture_stream();
+      LLMP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+      uint64_t l0[LLMP_N_KERNEL_CLASSES];
+      double r0[LLMP_N_KERNEL_CLASSES];
+      memcpy(l0, ctx->launches, sizeof(l0));
+      memcpy(r0, ctx->rows, sizeof(r0));
+      try {
+        tree();
+        // launch counters: the captured tree replays T times
+        for (int c = 0; c < LLMP_N_KERNEL_CLASSES; ++c) {
+          ctx->launches[c] += (ctx->launches[c] - l0[c]) * (uint64_t)(T - 1);
+          ctx->rows[c] += (ctx->rows[c] - r0[c]) * (double)(T - 1);
+        }
+      } catch (...) {
+        cudaStreamEndCapture(ctx->stream, &g);
+        if (g) cudaGraphDestroy(g);
+        ctx->stream = user;
+        throw;
       }
+      LLMP_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+      ctx->stream = user;
+      LLMP_CUDA(cudaGraphInstantiate(&ge, g, 0));
+      for (int t = 0; t < T; ++t) LLMP_CUDA(cudaGraphLaunch(ge, s));
+      LLMP_CUDA(cudaGraphExecDestroy(ge));
+      LLMP_CUDA(cudaGraphDestroy(g));
+    } else {
+      for (int t = 0; t < T; ++t) tree();
     }
   }
 

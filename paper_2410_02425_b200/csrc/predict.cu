@@ -184,12 +184,14 @@ __global__ void k_argmin(const float* pred, int n_llm, int n_prof, int n_levels,
 void argmin_impl(Ctx* ctx, const float* pred, int n_llm, int n_prof, int n_levels, const int32_t* levels_host,
                  const double* cost_host, const uint8_t* allowed_host, float L1, float L2, int64_t U, RecOut& out) {
   cudaStream_t s = ctx->stream;
-  DevBuf d_lv((size_t)n_levels * 4), d_cost((size_t)n_prof * 8), d_al(allowed_host ? (size_t)n_llm * n_prof : 0);
+  DevBuf& d_lv = ctx->workspace("am_levels", (size_t)n_levels * 4);
+  DevBuf& d_cost = ctx->workspace("am_cost", (size_t)n_prof * 8);
+  DevBuf& d_al = ctx->workspace("am_allowed", allowed_host ? (size_t)n_llm * n_prof : 1);
   LLMP_CUDA(cudaMemcpyAsync(d_lv.p, levels_host, (size_t)n_levels * 4, cudaMemcpyHostToDevice, s));
   LLMP_CUDA(cudaMemcpyAsync(d_cost.p, cost_host, (size_t)n_prof * 8, cudaMemcpyHostToDevice, s));
   if (allowed_host)
     LLMP_CUDA(cudaMemcpyAsync(d_al.p, allowed_host, (size_t)n_llm * n_prof, cudaMemcpyHostToDevice, s));
-  DevBuf d_o((size_t)n_llm * (4 + 8 + 8 + 4));
+  DevBuf& d_o = ctx->workspace("am_out", (size_t)n_llm * (4 + 8 + 8 + 4));
   int32_t* o_prof = d_o.as<int32_t>();
   int32_t* o_umax = o_prof + n_llm;
   int64_t* o_npods = reinterpret_cast<int64_t*>(d_o.as<uint8_t>() + (size_t)n_llm * 8);
@@ -213,9 +215,9 @@ void recommend_impl(Ctx* ctx, const ModelData& m, const float* llm_feats, int n_
                     const int32_t* levels, int n_levels, float L1, float L2, int64_t U, RecOut& out,
                     float* pred_out_dev) {
   const int64_t n = (int64_t)n_llm * n_prof * n_levels;
-  DevBuf d_pred(pred_out_dev ? 0 : (size_t)std::max<int64_t>(n, 1) * 8);
-  float* pred = pred_out_dev ? pred_out_dev : d_pred.as<float>();
-  DevBuf d_lv((size_t)n_levels * 4);
+  float* pred = pred_out_dev ? pred_out_dev
+                             : ctx->workspace("rec_pred", (size_t)std::max<int64_t>(n, 1) * 8).as<float>();
+  DevBuf& d_lv = ctx->workspace("rec_levels", (size_t)n_levels * 4);
   LLMP_CUDA(cudaMemcpyAsync(d_lv.p, levels, (size_t)n_levels * 4, cudaMemcpyHostToDevice, ctx->stream));
   PredArgs a{};
   a.nodes = m.d_nodes.as<uint2>();

@@ -46,8 +46,8 @@ cudaEvent_t Ctx::get_event() {
   return e;
 }
 void Ctx::before(int cls, cudaEvent_t* ev) {
-  (void)cls;
-  if (!timing) return;
+  if (!timing || (launches[cls] % (uint64_t)timing_every) != 0) return;
+  timed[cls] += 1;
   *ev = get_event();
   LLMP_CUDA(cudaEventRecord(*ev, stream));
 }
