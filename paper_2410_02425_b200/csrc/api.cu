@@ -129,7 +129,10 @@ void llmpilot_ctx_destroy(llmpilot_ctx* ctx) {
   for (auto e : ctx->c.free_events) cudaEventDestroy(e);
   llmp::nccl_destroy(&ctx->c);
   if (ctx->c.d_units) cudaFree(ctx->c.d_units);
-  if (ctx->c.cap_stream) cudaStreamDestroy(ctx->c.cap_stream);
+  for (auto st : ctx->c.cap_stream)
+    if (st) cudaStreamDestroy(st);
+  if (ctx->c.fork_event) cudaEventDestroy(ctx->c.fork_event);
+  if (ctx->c.join_event) cudaEventDestroy(ctx->c.join_event);
   delete ctx;
 }
 

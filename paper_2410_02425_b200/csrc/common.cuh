@@ -78,11 +78,18 @@ struct Ctx {
   int timing_every = 1;                    // time every k-th launch of each class
   uint64_t timed[LLMP_N_KERNEL_CLASSES] = {};
   bool use_graphs = true;                  // replay each tree from a CUDA graph (off while timing)
-  cudaStream_t cap_stream = nullptr;       // private stream used only for graph capture
-  cudaStream_t capture_stream() {
-    if (!cap_stream) check_cuda(cudaStreamCreateWithFlags(&cap_stream, cudaStreamNonBlocking), "capture stream",
-                                __FILE__, __LINE__);
-    return cap_stream;
+  cudaStream_t cap_stream[2] = {nullptr, nullptr};   // private streams used only for graph capture
+  cudaEvent_t fork_event = nullptr, join_event = nullptr;
+  cudaStream_t capture_stream(int i) {
+    if (!cap_stream[i]) {
+      check_cuda(cudaStreamCreateWithFlags(&cap_stream[i], cudaStreamNonBlocking), "capture stream", __FILE__,
+                 __LINE__);
+      if (!fork_event) {
+        check_cuda(cudaEventCreateWithFlags(&fork_event, cudaEventDisableTiming), "event", __FILE__, __LINE__);
+        check_cuda(cudaEventCreateWithFlags(&join_event, cudaEventDisableTiming), "event", __FILE__, __LINE__);
+      }
+    }
+    return cap_stream[i];
   }
   uint64_t launches[LLMP_N_KERNEL_CLASSES] = {};
   double rows[LLMP_N_KERNEL_CLASSES] = {};

@@ -367,14 +367,31 @@ __global__ void __launch_bounds__(R2_THREADS, 2) k_hist_root2(const FitArgs a) {
     int cur = -1;            // code of the pending run of this lane's feature
     int32_t acc_g = 0;       // pending run sums
     uint32_t acc_h = 0;
+    // register prefetch of the next batch (y, w, p of lane r's row; lane f's 32 codes)
+    float ny = 0.f, nw = 0.f, np_ = 0.f;
+    uint4 na = make_uint4(0, 0, 0, 0), nb2 = na;
+    auto load_batch = [&](int64_t b) {
+      if (b + lane < w1) {
+        ny = a.y[b + lane];
+        nw = a.w[b + lane];
+        np_ = a.p[b + lane];
+      }
+      const uint4* cp = reinterpret_cast<const uint4*>(a.codesT + (size_t)lane * a.ldT + b);
+      na = __ldg(cp);
+      nb2 = __ldg(cp + 1);
+    };
+    if (w0 < w1) load_batch(w0);
     for (int64_t base = w0; base < w1; base += 32) {
       const int cnt = (int)min((int64_t)32, w1 - base);
+      const float yv = ny, wv = nw, pv = np_;
+      const uint4 ca = na, cb = nb2;
+      if (base + 32 < w1) load_batch(base + 32);
       // ---- row-side: gradient pair of row base + lane
       int32_t qg = 0, qh = 0;
       if (lane < cnt) {
         const int64_t i = base + lane;
-        float g = __fmul_rn(a.w[i], __fsub_rn(a.p[i], a.y[i]));
-        float h = a.w[i];
+        float g = __fmul_rn(wv, __fsub_rn(pv, yv));
+        float h = wv;
         if (row_sampled_out(a.seed, a.target, t, a.row_offset + i, a.subsample)) {
           g = 0.f;
           h = 0.f;
@@ -384,8 +401,6 @@ __global__ void __launch_bounds__(R2_THREADS, 2) k_hist_root2(const FitArgs a) {
         a.gp_root[i] = pack_gp(qg, qh);
       }
       // ---- feature-side: 32 codes of this lane's feature (aligned vectors; padding rows are 0)
-      const uint4* cp = reinterpret_cast<const uint4*>(a.codesT + (size_t)lane * a.ldT + base);
-      const uint4 ca = __ldg(cp), cb = __ldg(cp + 1);
       uint32_t cw[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
       // inclusive warp prefix of the pairs
       int32_t pg = qg;
@@ -785,6 +800,283 @@ __global__ void __launch_bounds__(PT_THREADS) k_pscatter(const FitArgs a, const 
   }
   }
 }
+// ---------------------------------------------------------------------------------------------
+// Warp-aggregated stable scatter (replaces a shared-memory reorder): in a tile, rows are ordered
+// (q, warp, lane) with row = q*256 + warp*32 + lane, and k_pcount stored exactly the ballot of each
+// (q, warp) group.  Each warp derives every group's exclusive left prefix from those 128 words
+// (popc + warp scan, no block barrier), then each lane writes its row straight to global memory:
+// lefts at lp + prefix + popc(ballot & lanes_below), rights likewise — each group's lefts and
+// rights land in two contiguous runs, so the stores stay coalesced.
+__global__ void __launch_bounds__(PT_THREADS) k_pscatter2(const FitArgs a, const int d, const PartWs w) {
+  __shared__ int s_tile_pref[MAX_PIECES + 1];
+  __shared__ int64_t s_seq_pref[MAX_PIECES + 1];
+  __shared__ int s_w[PT_THREADS / 32];
+  __shared__ int64_t s_w64[PT_THREADS / 32];
+  const int NP = 1 << (d - 1);
+  const LevelView& P = a.lv[d - 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  parent_prefixes(a, d, s_tile_pref, s_seq_pref, s_w, s_w64);
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t* rout = a.sr[d & 1];
+  uint32_t* gout = a.sg[d & 1];
+  for (int t = blockIdx.x; t < s_tile_pref[NP]; t += gridDim.x) {
+    const int j = parent_of_tile(s_tile_pref, NP, t);
+    const int64_t cnt_j = (d == 1) ? a.n : P.cnt[j];
+    const int64_t start_j = (d == 1) ? 0 : P.start[j];
+    const int64_t o = (int64_t)(t - s_tile_pref[j]) * PT_TILE;
+    const int len = (int)min((int64_t)PT_TILE, cnt_j - o);
+    const uint32_t* rin = (d >= 2) ? a.sr[(d - 1) & 1] + start_j + o : nullptr;
+    const uint32_t* gin = (d >= 2) ? a.sg[(d - 1) & 1] + start_j + o : a.gp_root + o;
+    const uint32_t* bw = w.bits + (size_t)t * PT_WORDS;
+    // exclusive left prefix of every (q, warp) group: lane L holds words 4L .. 4L+3
+    const uint4 mw = *reinterpret_cast<const uint4*>(bw + 4 * lane);
+    const int c0 = __popc(mw.x), c1 = __popc(mw.y), c2 = __popc(mw.z), c3 = __popc(mw.w);
+    const int lsum = c0 + c1 + c2 + c3;
+    int inc = lsum;
+    for (int off = 1; off < 32; off <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, inc, off);
+      if (lane >= off) inc += u;
+    }
+    const int ex = inc - lsum;                       // prefix before word 4*lane
+    const int64_t lp = w.tile_lpref[t];
+    const int64_t rbase = a.n + (s_seq_pref[j] + o - lp);   // global right prefix at the tile start
+    // loads of 8 rows first (independent), then their stores; two rounds per tile
+#pragma unroll 1
+    for (int q0 = 0; q0 < PT_ITEMS; q0 += 8) {
+    uint32_t rv[8], gv[8];
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) {
+      const int k = (q0 + qq) * PT_THREADS + warp * 32 + lane;
+      rv[qq] = (k < len) ? ((d == 1) ? (uint32_t)(o + k) : rin[k]) : 0u;
+      gv[qq] = (k < len) ? gin[k] : 0u;
+    }
+#pragma unroll
+    for (int qq = 0; qq < 8; ++qq) {
+      const int q = q0 + qq;
+      const int word = q * (PT_THREADS / 32) + warp;
+      const int owner = word >> 2, sub = word & 3;
+      // prefix before this group = ex(owner) + counts of the owner's earlier words
+      const int exo = __shfl_sync(0xffffffffu, ex, owner);
+      const int a0 = __shfl_sync(0xffffffffu, c0, owner), a1 = __shfl_sync(0xffffffffu, c1, owner);
+      const int a2 = __shfl_sync(0xffffffffu, c2, owner);
+      const int pre = exo + (sub > 0 ? a0 : 0) + (sub > 1 ? a1 : 0) + (sub > 2 ? a2 : 0);
+      const uint32_t m = bw[word];
+      const int k = q * PT_THREADS + warp * 32 + lane;
+      if (k < len) {
+        const bool left = (m >> lane) & 1u;
+        const int rank = __popc(m & lt);
+        const int64_t dst = left ? lp + pre + rank : rbase + (k - lane - pre) + (lane - rank);
+        rout[dst] = rv[qq];
+        gout[dst] = gv[qq];
+      }
+    }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// split evaluation, one CTA of 1024 threads per node of level d: warp f owns feature f, lane l
+// owns bins 8l .. 8l+7.  The warp forms its feature's histogram (sibling = parent - built, exact
+// int64, written back for the next level), prefix-scans it (8 local + warp shuffle scan), evaluates
+// every threshold in fp64 (monotone veto on users) and reduces (loss desc, b asc); warp 0 then
+// picks the node's best over features (loss desc, f asc, b asc) and writes the tree.  Node totals
+// come from each warp's own feature (every feature's histogram sums to them).
+constexpr int SP2_THREADS = 1024;
+__global__ void __launch_bounds__(SP2_THREADS) k_split2(const FitArgs a, const int d) {
+  const int t = *a.d_tree;
+  int32_t* const tfeat = a.tfeat + (size_t)t * a.nn;
+  int32_t* const tbin = a.tbin + (size_t)t * a.nn;
+  float* const tthr = a.tthr + (size_t)t * a.nn;
+  float* const tval = a.tval + (size_t)t * a.nn;
+  const int k = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, f = tid >> 5;
+  const LevelView& V = a.lv[d];
+  __shared__ double s_loss[32];
+  __shared__ int s_b[32];
+  __shared__ int64_t s_GL[32], s_HL[32];
+  __shared__ int64_t s_G, s_H;
+  int64_t* Hself;
+  int64_t g8[8], h8[8];
+  if (d == 0) {
+    Hself = a.H[0];
+  } else {
+    const int j = k >> 1;
+    if (a.lv[d - 1].split_f[j] < 0) {
+      if (tid == 0) V.split_f[k] = -1;
+      return;
+    }
+    const int side = V.built[j];
+    const bool is_built = (k & 1) == side;
+    Hself = a.H[d & 1] + (size_t)(is_built ? j : (1 << (d - 1)) + j) * SLOT;
+    if (!is_built) {
+      const longlong2* Hp = reinterpret_cast<const longlong2*>(a.H[(d - 1) & 1] + (size_t)node_slot(a, d - 1, j) * SLOT);
+      const longlong2* Hb = reinterpret_cast<const longlong2*>(a.H[d & 1] + (size_t)j * SLOT);
+      longlong2* Hs = reinterpret_cast<longlong2*>(Hself);
+      const int eg0 = (f * kBins + lane * 8) / 2, eh0 = (kHistBins + f * kBins + lane * 8) / 2;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const longlong2 pg = Hp[eg0 + q], bg = Hb[eg0 + q], ph = Hp[eh0 + q], bh = Hb[eh0 + q];
+        g8[2 * q] = pg.x - bg.x;
+        g8[2 * q + 1] = pg.y - bg.y;
+        h8[2 * q] = ph.x - bh.x;
+        h8[2 * q + 1] = ph.y - bh.y;
+        Hs[eg0 + q] = make_longlong2(g8[2 * q], g8[2 * q + 1]);
+        Hs[eh0 + q] = make_longlong2(h8[2 * q], h8[2 * q + 1]);
+      }
+    }
+  }
+  if (d == 0 || (k & 1) == a.lv[d].built[k >> 1]) {
+    const longlong2* G2 = reinterpret_cast<const longlong2*>(Hself + f * kBins + lane * 8);
+    const longlong2* H2 = reinterpret_cast<const longlong2*>(Hself + kHistBins + f * kBins + lane * 8);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const longlong2 gv = G2[q], hv = H2[q];
+      g8[2 * q] = gv.x;
+      g8[2 * q + 1] = gv.y;
+      h8[2 * q] = hv.x;
+      h8[2 * q + 1] = hv.y;
+    }
+  }
+  // local inclusive prefix over the lane's 8 bins, then warp exclusive scan of lane totals
+#pragma unroll
+  for (int q = 1; q < 8; ++q) {
+    g8[q] += g8[q - 1];
+    h8[q] += h8[q - 1];
+  }
+  int64_t ig = g8[7], ih = h8[7];
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t ug = __shfl_up_sync(0xffffffffu, ig, o), uh = __shfl_up_sync(0xffffffffu, ih, o);
+    if (lane >= o) {
+      ig += ug;
+      ih += uh;
+    }
+  }
+  const int64_t bg = ig - g8[7], bh = ih - h8[7];
+  const int64_t Gq = __shfl_sync(0xffffffffu, ig, 31), Hq = __shfl_sync(0xffffffffu, ih, 31);
+  // column sample of tree t (R21)
+  bool fin = f < a.F;
+  if (fin && a.colsample < 1.0f) {
+    const int F = a.F;
+    int nkeep = (int)ceil((double)a.colsample * (double)F);
+    if (nkeep < 1) nkeep = 1;
+    const uint64_t kf = rng4(a.seed, (uint64_t)(2 * a.target + 1), (uint64_t)t, (uint64_t)f);
+    const uint64_t kl = lane < F ? rng4(a.seed, (uint64_t)(2 * a.target + 1), (uint64_t)t, (uint64_t)lane) : ~0ull;
+    const unsigned less = __ballot_sync(0xffffffffu, lane < F && (kl < kf || (kl == kf && lane < f)));
+    fin = __popc(less) < nkeep;
+  }
+  const int eg = exp_of(__uint_as_float(a.maxg[t])), eh = exp_of(__uint_as_float(a.maxh[t]));
+  const double sgi = exp2i(eg - a.K), shi = exp2i(eh - a.K);
+  const double lo = (d == 0) ? -INFINITY : V.lo[k], hi = (d == 0) ? INFINITY : V.hi[k];
+  const double lambda = a.lambda, mcw = a.mcw;
+  const double G = dequant(Gq, sgi), H = dequant(Hq, shi);
+  const double wP = calc_weight(G, H, lo, hi, lambda, mcw);
+  const double gainP = calc_gain(G, H, wP, lambda);
+  double bl = -INFINITY;
+  int bb = 0x7fffffff;
+  int64_t bGL = 0, bHL = 0;
+  if (fin) {
+    const int nthr = a.ncuts[f];   // thresholds b = 0 .. nbins_f - 2
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int b = lane * 8 + q;
+      if (b < nthr) {
+        const int64_t GLq = bg + g8[q], HLq = bh + h8[q];
+        const double GL = dequant(GLq, sgi), HL = dequant(HLq, shi);
+        const double GR = dequant(Gq - GLq, sgi), HR = dequant(Hq - HLq, shi);
+        if (HL >= mcw && HR >= mcw) {
+          const double wl = calc_weight(GL, HL, lo, hi, lambda, mcw);
+          const double wr = calc_weight(GR, HR, lo, hi, lambda, mcw);
+          if (!(a.monotone && f == a.users_col && wl > wr)) {
+            const double loss =
+                __dsub_rn(__dadd_rn(calc_gain(GL, HL, wl, lambda), calc_gain(GR, HR, wr, lambda)), gainP);
+            if (loss > bl) {   // b ascending within the lane: strict keeps the smaller b
+              bl = loss;
+              bb = b;
+              bGL = GLq;
+              bHL = HLq;
+            }
+          }
+        }
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ol = __shfl_down_sync(0xffffffffu, bl, o);
+    const int ob = __shfl_down_sync(0xffffffffu, bb, o);
+    const int64_t oG = __shfl_down_sync(0xffffffffu, bGL, o), oH = __shfl_down_sync(0xffffffffu, bHL, o);
+    if (ol > bl || (ol == bl && ob < bb)) {
+      bl = ol;
+      bb = ob;
+      bGL = oG;
+      bHL = oH;
+    }
+  }
+  if (lane == 0) {
+    s_loss[f] = bl;
+    s_b[f] = bb;
+    s_GL[f] = bGL;
+    s_HL[f] = bHL;
+    if (f == 0) {
+      s_G = Gq;
+      s_H = Hq;
+    }
+  }
+  __syncthreads();
+  if (f != 0) return;
+  double ml = s_loss[lane];
+  int mf = lane, mb = s_b[lane];
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ol = __shfl_down_sync(0xffffffffu, ml, o);
+    const int of = __shfl_down_sync(0xffffffffu, mf, o), ob = __shfl_down_sync(0xffffffffu, mb, o);
+    // total order: loss desc, then f asc, then b asc
+    if (ol > ml || (ol == ml && (of < mf || (of == mf && ob < mb)))) {
+      ml = ol;
+      mf = of;
+      mb = ob;
+    }
+  }
+  if (lane != 0) return;
+  const int64_t GqN = s_G, HqN = s_H;
+  const int gk = (1 << d) - 1 + k;
+  if (ml > 1e-6) {
+    const int fs = mf, bs = mb;
+    const int64_t GLs = s_GL[fs], HLs = s_HL[fs];
+    const double GL = dequant(GLs, sgi), HL = dequant(HLs, shi);
+    const double GR = dequant(GqN - GLs, sgi), HR = dequant(HqN - HLs, shi);
+    const double wl = calc_weight(GL, HL, lo, hi, lambda, mcw);
+    const double wr = calc_weight(GR, HR, lo, hi, lambda, mcw);
+    double loL = lo, hiL = hi, loR = lo, hiR = hi;
+    if (a.monotone && fs == a.users_col) {
+      const double mid = __dmul_rn(__dadd_rn(wl, wr), 0.5);
+      hiL = mid;
+      loR = mid;
+    }
+    V.split_f[k] = fs;
+    V.split_b[k] = bs;
+    tfeat[gk] = fs;
+    tbin[gk] = bs;
+    tthr[gk] = a.cuts[fs * (kBins - 1) + bs];
+    tval[gk] = 0.0f;
+    if (d + 1 < a.D) {
+      const LevelView& N = a.lv[d + 1];
+      N.lo[2 * k] = loL;
+      N.hi[2 * k] = hiL;
+      N.lo[2 * k + 1] = loR;
+      N.hi[2 * k + 1] = hiR;
+    } else {
+      // children at max depth are leaves: v = (float)(eta * W(G, H, lo, hi))
+      tfeat[2 * gk + 1] = -1;
+      tval[2 * gk + 1] = (float)__dmul_rn(a.eta, calc_weight(GL, HL, loL, hiL, lambda, mcw));
+      tfeat[2 * gk + 2] = -1;
+      tval[2 * gk + 2] = (float)__dmul_rn(a.eta, calc_weight(GR, HR, loR, hiR, lambda, mcw));
+    }
+  } else {
+    V.split_f[k] = -1;
+    tfeat[gk] = -1;
+    tval[gk] = (float)__dmul_rn(a.eta, wP);
+  }
+}
+
 // ---------------------------------------------------------------------------------------------
 // split evaluation: one CTA per (node of level d, feature), one bin per thread.  Each CTA forms
 // its feature's histogram (sibling = parent - built, exact int64, written back for the next
@@ -1321,71 +1613,82 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   if (keep_train_pred) out.d_train_pred.ensure((size_t)n * 4 * 2);
   DevBuf& d_p = keep_train_pred ? out.d_train_pred : ctx->workspace("p", (size_t)n * 4 * 2);
   out.device = ctx->device;
-  DevBuf& d_gp = ctx->workspace("gp_root", (size_t)n * 4);
-  DevBuf& d_sr0 = ctx->workspace("ridx0", (size_t)n * 2 * 4);
-  DevBuf& d_sr1 = ctx->workspace("ridx1", (size_t)n * 2 * 4);
-  DevBuf& d_sg0 = ctx->workspace("gp0", (size_t)n * 2 * 4);
-  DevBuf& d_sg1 = ctx->workspace("gp1", (size_t)n * 2 * 4);
-  DevBuf& d_H0 = ctx->workspace("hist0", (size_t)half_max * SLOT * 8);
-  DevBuf& d_H1 = ctx->workspace("hist1", (size_t)half_max * SLOT * 8);
   DevBuf& d_trees = ctx->workspace("trees", (size_t)2 * std::max(T, 1) * nn * 16);
   DevBuf& d_max = ctx->workspace("gradmax", (size_t)2 * 2 * (T + 1) * 4);
   DevBuf& d_sums = ctx->workspace("basesums", 2 * 2 * 8);
   DevBuf& d_base = ctx->workspace("base", 2 * 4);
-  // level tables: doubles/ints per level, plus the per-tree zeroed control block
+  int32_t* feat_all = d_trees.as<int32_t>();
+  int32_t* bin_all = feat_all + (size_t)2 * T * nn;
+  float* thr_all = reinterpret_cast<float*>(bin_all + (size_t)2 * T * nn);
+  float* val_all = thr_all + (size_t)2 * T * nn;
+  if (T > 0)
+    LLMP_LAUNCH(ctx, KC_MISC, 0, k_fill_trees, 256, 256, 0, feat_all, bin_all, thr_all, val_all, (size_t)2 * T * nn);
+  LLMP_CUDA(cudaMemsetAsync(d_max.p, 0, d_max.bytes, s));
+  LLMP_CUDA(cudaMemsetAsync(d_sums.p, 0, d_sums.bytes, s));
+  int* d_tree = ctx->workspace("tree_idx", sizeof(int)).as<int>();
+
+  // the two ensembles are independent: on one GPU their trees grow concurrently (two branches
+  // of one CUDA graph, each with its own level workspaces); with NCCL (collectives must be
+  // issued in one order on every rank) or timing instrumentation they run one after the other
+  const bool graphs = T > 0 && !ctx->timing && ctx->use_graphs;
+  const bool concurrent = graphs && ctx->nranks == 1;
   size_t lvl_nodes = 0;
   for (int d = 0; d <= D; ++d) lvl_nodes += (size_t)1 << d;
-  int64_t max_tiles_total = 0;
-  std::vector<int64_t> tiles_off(D + 1, 0);
-  for (int d = 1; d <= D; ++d) {
-    tiles_off[d] = max_tiles_total;
-    max_tiles_total += (n + TILE - 1) / TILE + (1 << (d - 1)) + 1;
-  }
-  const size_t ctl_bytes = 64 * 4 /*tickets*/ + lvl_nodes * 8 * 2 /*cnt,gcnt*/ + (size_t)max_tiles_total * 8;
-  DevBuf& d_ctl = ctx->workspace("ctl", ctl_bytes);
-  const size_t tab_bytes = lvl_nodes * (8 /*start*/ + 8 + 8 /*lo,hi*/ + 4 + 4 /*split*/ + 4 /*built*/ + 4 /*done*/);
-  DevBuf& d_tab = ctx->workspace("tab", tab_bytes);
-
-  FitArgs a{};
-  a.n = n;
-  a.row_offset = ds.row_offset;
-  a.F = F;
-  a.users_col = ds.users_col;
-  a.D = D;
-  a.K = hp.grad_bits;
-  a.T = T;
-  a.codes = d_codes.as<uint8_t>();
-  a.codesT = d_codesT.as<uint8_t>();
-  a.ldT = ldT;
-  a.w = d_w.as<float>();
-  a.gp_root = d_gp.as<uint32_t>();
-  a.sr[0] = d_sr0.as<uint32_t>();
-  a.sr[1] = d_sr1.as<uint32_t>();
-  a.sg[0] = d_sg0.as<uint32_t>();
-  a.sg[1] = d_sg1.as<uint32_t>();
-  a.H[0] = d_H0.as<int64_t>();
-  a.H[1] = d_H1.as<int64_t>();
-  a.cuts = out.cuts.d_cuts.as<float>();
-  a.ncuts = out.cuts.d_ncuts.as<int32_t>();
-  a.eta = (double)hp.eta;
-  a.lambda = (double)hp.lambda;
-  a.mcw = (double)hp.min_child_weight;
-  a.subsample = hp.subsample;
-  a.colsample = hp.colsample_bytree;
-  a.seed = hp.seed;
-  a.monotone = hp.monotone_users;
-  a.nn = nn;
-  a.units = ctx->d_units;
-  a.fbest = reinterpret_cast<FeatBest*>(ctx->workspace("featbest", (size_t)half_max * 32 * 48).p);
-  {
-    uint8_t* c = d_ctl.as<uint8_t>();
-    int32_t* tickets = reinterpret_cast<int32_t*>(c);
-    int64_t* cnt = reinterpret_cast<int64_t*>(c + 64 * 4);
-    int64_t* gcnt = cnt + lvl_nodes;
-    uint64_t* flags = reinterpret_cast<uint64_t*>(gcnt + lvl_nodes);
+  const int64_t max_tiles = (n + PT_TILE - 1) / PT_TILE + half_max + 1;
+  const size_t tab_bytes = lvl_nodes * (8 /*start*/ + 8 /*cnt*/ + 8 /*gcnt*/ + 8 + 8 /*lo,hi*/ + 4 + 4 /*split*/ +
+                                        4 /*built*/ + 4 /*done*/);
+  FitArgs A[2];
+  PartWs PW[2];
+  for (int tg = 0; tg < 2; ++tg) {
+    const std::string sx = (concurrent && tg == 1) ? "_1" : "_0";
+    FitArgs& a = A[tg];
+    a = FitArgs{};
+    a.n = n;
+    a.row_offset = ds.row_offset;
+    a.F = F;
+    a.users_col = ds.users_col;
+    a.D = D;
+    a.K = hp.grad_bits;
+    a.T = T;
+    a.target = tg;
+    a.codes = d_codes.as<uint8_t>();
+    a.codesT = d_codesT.as<uint8_t>();
+    a.ldT = ldT;
+    a.w = d_w.as<float>();
+    a.y = (tg == 0) ? d_y0.as<float>() : d_y1.as<float>();
+    a.p = d_p.as<float>() + (size_t)tg * n;
+    a.gp_root = ctx->workspace("gp_root" + sx, (size_t)n * 4).as<uint32_t>();
+    a.sr[0] = ctx->workspace("ridx0" + sx, (size_t)n * 2 * 4).as<uint32_t>();
+    a.sr[1] = ctx->workspace("ridx1" + sx, (size_t)n * 2 * 4).as<uint32_t>();
+    a.sg[0] = ctx->workspace("gp0" + sx, (size_t)n * 2 * 4).as<uint32_t>();
+    a.sg[1] = ctx->workspace("gp1" + sx, (size_t)n * 2 * 4).as<uint32_t>();
+    a.H[0] = ctx->workspace("hist0" + sx, (size_t)half_max * SLOT * 8).as<int64_t>();
+    a.H[1] = ctx->workspace("hist1" + sx, (size_t)half_max * SLOT * 8).as<int64_t>();
+    a.cuts = out.cuts.d_cuts.as<float>();
+    a.ncuts = out.cuts.d_ncuts.as<int32_t>();
+    a.eta = (double)hp.eta;
+    a.lambda = (double)hp.lambda;
+    a.mcw = (double)hp.min_child_weight;
+    a.subsample = hp.subsample;
+    a.colsample = hp.colsample_bytree;
+    a.seed = hp.seed;
+    a.monotone = hp.monotone_users;
+    a.nn = nn;
+    a.units = ctx->d_units;
+    a.fbest = reinterpret_cast<FeatBest*>(ctx->workspace("featbest" + sx, (size_t)half_max * 32 * 48).p);
+    a.d_tree = d_tree;
+    a.maxg = d_max.as<uint32_t>() + (size_t)tg * 2 * (T + 1);
+    a.maxh = a.maxg + (T + 1);
+    a.tfeat = feat_all + (size_t)tg * T * nn;
+    a.tbin = bin_all + (size_t)tg * T * nn;
+    a.tthr = thr_all + (size_t)tg * T * nn;
+    a.tval = val_all + (size_t)tg * T * nn;
+    DevBuf& d_tab = ctx->workspace("tab" + sx, tab_bytes);
     uint8_t* tb = d_tab.as<uint8_t>();
     int64_t* start = reinterpret_cast<int64_t*>(tb);
-    double* lo = reinterpret_cast<double*>(start + lvl_nodes);
+    int64_t* cnt = start + lvl_nodes;
+    int64_t* gcnt = cnt + lvl_nodes;
+    double* lo = reinterpret_cast<double*>(gcnt + lvl_nodes);
     double* hi = lo + lvl_nodes;
     int32_t* sf = reinterpret_cast<int32_t*>(hi + lvl_nodes);
     int32_t* sb = sf + lvl_nodes;
@@ -1403,124 +1706,118 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       L.split_b = sb + off;
       L.built = bu + off;
       L.done = dn + off;
-      L.flags = flags + tiles_off[d];
-      L.ticket = tickets + d;
       off += (size_t)1 << d;
     }
     LLMP_CUDA(cudaMemsetAsync(d_tab.p, 0, d_tab.bytes, s));
+    PW[tg].tile_left = ctx->workspace("tile_left" + sx, (size_t)max_tiles * 4).as<int32_t>();
+    PW[tg].tile_lpref = ctx->workspace("tile_lpref" + sx, (size_t)max_tiles * 8).as<int64_t>();
+    PW[tg].bits = ctx->workspace("tile_bits" + sx, (size_t)max_tiles * PT_WORDS * 4).as<uint32_t>();
   }
-  // model arrays (per target views into d_trees)
-  int32_t* feat_all = d_trees.as<int32_t>();
-  int32_t* bin_all = feat_all + (size_t)2 * T * nn;
-  float* thr_all = reinterpret_cast<float*>(bin_all + (size_t)2 * T * nn);
-  float* val_all = thr_all + (size_t)2 * T * nn;
-  if (T > 0)
-    LLMP_LAUNCH(ctx, KC_MISC, 0, k_fill_trees, 256, 256, 0, feat_all, bin_all, thr_all, val_all, (size_t)2 * T * nn);
-  LLMP_CUDA(cudaMemsetAsync(d_max.p, 0, d_max.bytes, s));
-  LLMP_CUDA(cudaMemsetAsync(d_sums.p, 0, d_sums.bytes, s));
 
   const int hist_grid = 2 * ctx->sms;
-  // partition workspaces: per-tile counts, prefixes and left bits (max tiles over the levels)
-  const int64_t max_tiles = (n + PT_TILE - 1) / PT_TILE + half_max + 1;
-  PartWs pw;
-  pw.tile_left = ctx->workspace("tile_left", (size_t)max_tiles * 4).as<int32_t>();
-  pw.tile_lpref = ctx->workspace("tile_lpref", (size_t)max_tiles * 8).as<int64_t>();
-  pw.bits = ctx->workspace("tile_bits", (size_t)max_tiles * PT_WORDS * 4).as<uint32_t>();
   const int upd_grid = grid_for(ctx, n, UPD_THREADS, 8);
   const int base_grid = grid_for(ctx, n, BASE_THREADS, 8);
   static bool attr_set = false;
   if (!attr_set) {
-    LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_ROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
     LLMP_CUDA(cudaFuncSetAttribute(k_hist_root2, cudaFuncAttributeMaxDynamicSharedMemorySize, R2_SMEM));
     LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_LEVEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
     LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
     attr_set = true;
   }
   const DbgArgs nodbg{};
-  int* d_tree = ctx->workspace("tree_idx", sizeof(int)).as<int>();
-  a.d_tree = d_tree;
 
-  for (int target = 0; target < 2; ++target) {
-    a.target = target;
-    a.y = (target == 0) ? d_y0.as<float>() : d_y1.as<float>();
-    a.p = d_p.as<float>() + (size_t)target * n;
-    a.maxg = d_max.as<uint32_t>() + (size_t)target * 2 * (T + 1);
-    a.maxh = a.maxg + (T + 1);
-    a.tfeat = feat_all + (size_t)target * T * nn;
-    a.tbin = bin_all + (size_t)target * T * nn;
-    a.tthr = thr_all + (size_t)target * T * nn;
-    a.tval = val_all + (size_t)target * T * nn;
-    int64_t* sums = d_sums.as<int64_t>() + 2 * target;
-
+  // ---- base scores (O3) and tree 0's gradient maxima
+  for (int tg = 0; tg < 2; ++tg) {
+    const FitArgs& a = A[tg];
+    int64_t* sums = d_sums.as<int64_t>() + 2 * tg;
     LLMP_LAUNCH(ctx, KC_BASE, n, k_base_max, base_grid, BASE_THREADS, 0, a);
     allreduce_max_u32(ctx, a.maxg + T, 1);
     allreduce_max_u32(ctx, a.maxh + T, 1);
     LLMP_LAUNCH(ctx, KC_BASE, n, k_base_sum, base_grid, BASE_THREADS, 0, a, sums);
     allreduce_sum_i64(ctx, sums, 2);
-    LLMP_LAUNCH(ctx, KC_BASE, n, k_base_init, base_grid, BASE_THREADS, 0, a, sums, d_base.as<float>() + target);
+    LLMP_LAUNCH(ctx, KC_BASE, n, k_base_init, base_grid, BASE_THREADS, 0, a, sums, d_base.as<float>() + tg);
     if (T > 0) {
       allreduce_max_u32(ctx, a.maxg, 1);
       allreduce_max_u32(ctx, a.maxh, 1);
     }
-    // one tree = a fixed sequence of launches that reads the tree index from the device, so it
-    // is captured once into a CUDA graph and replayed T times (no per-kernel launch overhead);
-    // with timing instrumentation on it runs as plain launches instead
-    auto tree = [&]() {
-      const cudaStream_t st = ctx->stream;
-      LLMP_CUDA(cudaMemsetAsync(a.H[0], 0, (size_t)SLOT * 8, st));
-      LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist_root2, hist_grid, R2_THREADS, R2_SMEM, a);
-      allreduce_sum_i64(ctx, a.H[0], SLOT);
-      LLMP_LAUNCH(ctx, KC_SPLIT, 1, k_split, 32, SPLIT_THREADS, 0, a, 0);
-      for (int d = 1; d < D; ++d) {
-        const int tiles_d = (int)((n + PT_TILE - 1) / PT_TILE) + (1 << (d - 1));
-        LLMP_LAUNCH(ctx, KC_PARTITION, n, k_pcount, std::min(tiles_d, 5 * ctx->sms), PT_THREADS, 0, a, d, pw);
-        LLMP_LAUNCH(ctx, KC_PARTITION, 0, k_pscan, 1, PS_THREADS, 0, a, d, pw);
-        LLMP_LAUNCH(ctx, KC_PARTITION, 0, k_pscatter, std::min(tiles_d, 4 * ctx->sms), PT_THREADS, 0, a, d, pw);
-        if (ctx->nranks > 1) {   // every rank must histogram the same (globally smaller) child
-          LLMP_CUDA(cudaMemcpyAsync(a.lv[d].gcnt, a.lv[d].cnt, ((size_t)1 << d) * 8, cudaMemcpyDeviceToDevice, st));
-          allreduce_sum_i64(ctx, a.lv[d].gcnt, (size_t)1 << d);
-        }
-        LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hist_grid, HIST_THREADS, HIST_SMEM, a, d, 0, nodbg);
-        allreduce_sum_i64(ctx, a.H[d & 1], (size_t)SLOT << (d - 1));
-        LLMP_LAUNCH(ctx, KC_SPLIT, (1 << d), k_split, (1 << d) * 32, SPLIT_THREADS, 0, a, d);
+  }
+
+  // one tree of one target = a fixed sequence of launches that reads the tree index from the
+  // device; both targets' trees + the index advance form one "round", captured once into a CUDA
+  // graph and replayed T times (plain launches when timing instrumentation is on)
+  auto tree = [&](const FitArgs& a, const PartWs& pw) {
+    const cudaStream_t st = ctx->stream;
+    LLMP_CUDA(cudaMemsetAsync(a.H[0], 0, (size_t)SLOT * 8, st));
+    LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist_root2, hist_grid, R2_THREADS, R2_SMEM, a);
+    allreduce_sum_i64(ctx, a.H[0], SLOT);
+    LLMP_LAUNCH(ctx, KC_SPLIT, 1, k_split2, 1, SP2_THREADS, 0, a, 0);
+    for (int d = 1; d < D; ++d) {
+      const int tiles_d = (int)((n + PT_TILE - 1) / PT_TILE) + (1 << (d - 1));
+      LLMP_LAUNCH(ctx, KC_PARTITION, n, k_pcount, std::min(tiles_d, 5 * ctx->sms), PT_THREADS, 0, a, d, pw);
+      LLMP_LAUNCH(ctx, KC_PARTITION, 0, k_pscan, 1, PS_THREADS, 0, a, d, pw);
+      LLMP_LAUNCH(ctx, KC_PARTITION, 0, k_pscatter2, std::min(tiles_d, 5 * ctx->sms), PT_THREADS, 0, a, d, pw);
+      if (ctx->nranks > 1) {   // every rank must histogram the same (globally smaller) child
+        LLMP_CUDA(cudaMemcpyAsync(a.lv[d].gcnt, a.lv[d].cnt, ((size_t)1 << d) * 8, cudaMemcpyDeviceToDevice, st));
+        allreduce_sum_i64(ctx, a.lv[d].gcnt, (size_t)1 << d);
       }
-      LLMP_LAUNCH(ctx, KC_UPDATE, n, k_update, upd_grid, UPD_THREADS, 0, a);
-      // next tree's gradient maxima (past slots are already equal on every rank, future ones 0)
-      allreduce_max_u32(ctx, a.maxg, (size_t)2 * (T + 1));
+      LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hist_grid, HIST_THREADS, HIST_SMEM, a, d, 0, nodbg);
+      allreduce_sum_i64(ctx, a.H[d & 1], (size_t)SLOT << (d - 1));
+      LLMP_LAUNCH(ctx, KC_SPLIT, (1 << d), k_split2, (1 << d), SP2_THREADS, 0, a, d);
+    }
+    LLMP_LAUNCH(ctx, KC_UPDATE, n, k_update, upd_grid, UPD_THREADS, 0, a);
+    // next tree's gradient maxima (past slots are already equal on every rank, future ones 0)
+    allreduce_max_u32(ctx, a.maxg, (size_t)2 * (T + 1));
+  };
+  LLMP_CUDA(cudaMemsetAsync(d_tree, 0, sizeof(int), s));
+  if (graphs) {
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    const cudaStream_t user = ctx->stream;
+    const cudaStream_t sa = ctx->capture_stream(0), sb = ctx->capture_stream(1);
+    uint64_t l0[LLMP_N_KERNEL_CLASSES];
+    double r0[LLMP_N_KERNEL_CLASSES];
+    memcpy(l0, ctx->launches, sizeof(l0));
+    memcpy(r0, ctx->rows, sizeof(r0));
+    ctx->stream = sa;
+    LLMP_CUDA(cudaStreamBeginCapture(sa, cudaStreamCaptureModeThreadLocal));
+    try {
+      if (concurrent) {
+        LLMP_CUDA(cudaEventRecord(ctx->fork_event, sa));
+        LLMP_CUDA(cudaStreamWaitEvent(sb, ctx->fork_event, 0));
+        tree(A[0], PW[0]);
+        ctx->stream = sb;
+        tree(A[1], PW[1]);
+        LLMP_CUDA(cudaEventRecord(ctx->join_event, sb));
+        ctx->stream = sa;
+        LLMP_CUDA(cudaStreamWaitEvent(sa, ctx->join_event, 0));
+      } else {
+        tree(A[0], PW[0]);
+        tree(A[1], PW[1]);
+      }
       LLMP_LAUNCH(ctx, KC_MISC, 0, k_next_tree, 1, 1, 0, d_tree);
-    };
-    LLMP_CUDA(cudaMemsetAsync(d_tree, 0, sizeof(int), s));
-    if (T > 0 && !ctx->timing && ctx->use_graphs) {
-      cudaGraph_t g = nullptr;
-      cudaGraphExec_t ge = nullptr;
-      const cudaStream_t user = ctx->stream;
-      ctx->stream = ctx->capture_stream();
-      LLMP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-      uint64_t l0[LLMP_N_KERNEL_CLASSES];
-      double r0[LLMP_N_KERNEL_CLASSES];
-      memcpy(l0, ctx->launches, sizeof(l0));
-      memcpy(r0, ctx->rows, sizeof(r0));
-      try {
-        tree();
-        // launch counters: the captured tree replays T times
-        for (int c = 0; c < LLMP_N_KERNEL_CLASSES; ++c) {
-          ctx->launches[c] += (ctx->launches[c] - l0[c]) * (uint64_t)(T - 1);
-          ctx->rows[c] += (ctx->rows[c] - r0[c]) * (double)(T - 1);
-        }
-      } catch (...) {
-        cudaStreamEndCapture(ctx->stream, &g);
-        if (g) cudaGraphDestroy(g);
-        ctx->stream = user;
-        throw;
+      // launch counters: the captured round replays T times
+      for (int c = 0; c < LLMP_N_KERNEL_CLASSES; ++c) {
+        ctx->launches[c] += (ctx->launches[c] - l0[c]) * (uint64_t)(T - 1);
+        ctx->rows[c] += (ctx->rows[c] - r0[c]) * (double)(T - 1);
       }
-      LLMP_CUDA(cudaStreamEndCapture(ctx->stream, &g));
+    } catch (...) {
+      ctx->stream = sa;
+      cudaStreamEndCapture(sa, &g);
+      if (g) cudaGraphDestroy(g);
       ctx->stream = user;
-      LLMP_CUDA(cudaGraphInstantiate(&ge, g, 0));
-      for (int t = 0; t < T; ++t) LLMP_CUDA(cudaGraphLaunch(ge, s));
-      LLMP_CUDA(cudaGraphExecDestroy(ge));
-      LLMP_CUDA(cudaGraphDestroy(g));
-    } else {
-      for (int t = 0; t < T; ++t) tree();
+      throw;
+    }
+    LLMP_CUDA(cudaStreamEndCapture(sa, &g));
+    ctx->stream = user;
+    LLMP_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    for (int t = 0; t < T; ++t) LLMP_CUDA(cudaGraphLaunch(ge, s));
+    LLMP_CUDA(cudaGraphExecDestroy(ge));
+    LLMP_CUDA(cudaGraphDestroy(g));
+  } else {
+    for (int t = 0; t < T; ++t) {
+      tree(A[0], PW[0]);
+      tree(A[1], PW[1]);
+      LLMP_LAUNCH(ctx, KC_MISC, 0, k_next_tree, 1, 1, 0, d_tree);
     }
   }
 
