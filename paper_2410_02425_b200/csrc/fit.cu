@@ -62,7 +62,12 @@ struct LevelView {
   int32_t* ticket;
 };
 
-struct FeatBest;
+// best split of one (node, feature), published by the split kernel for the node's final reduction
+struct FeatBest {
+  double loss;
+  int32_t b, valid;
+  int64_t GLq, HLq, Gq, Hq;
+};
 
 struct FitArgs {
   int64_t n, row_offset;
@@ -127,7 +132,8 @@ __device__ __forceinline__ int node_slot(const FitArgs& a, int d, int k) {
 enum { HM_ROOT = 0, HM_LEVEL = 1, HM_DEBUG = 2 };
 
 template <int MODE>
-__global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const int d, const int t, const DbgArgs dbg) {
+__global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const int d, const int t_in, const DbgArgs dbg) {
+  const int t = (MODE == HM_ROOT) ? *a.d_tree : t_in;   // graph replays: tree index from the device
   extern __shared__ __align__(16) uint8_t smem[];
   int32_t* sg = reinterpret_cast<int32_t*>(smem);                 // [256 bins][32 features]
   uint32_t* sh = reinterpret_cast<uint32_t*>(smem + kHistBins * 4);
@@ -875,6 +881,227 @@ __global__ void __launch_bounds__(PT_THREADS) k_pscatter2(const FitArgs a, const
 }
 
 // ---------------------------------------------------------------------------------------------
+// split evaluation, one WARP per (node of level d, feature f) — 4 warps per CTA, no block barriers:
+// lane l owns bins 8l .. 8l+7; the warp forms the feature's histogram (sibling = parent - built,
+// exact int64, written back for the next level), prefix-scans it, evaluates every threshold in
+// fp64 (monotone veto on users) and reduces (loss desc, b asc).  Its lane 0 publishes the result
+// and takes a ticket; the node's last-arriving warp reduces the 32 features (loss desc, f asc,
+// b asc) and writes the tree.
+constexpr int SP3_WARPS = 4;
+__global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitArgs a, const int d) {
+  const int t = *a.d_tree;
+  const int lane = threadIdx.x & 31;
+  const int wg = blockIdx.x * SP3_WARPS + (threadIdx.x >> 5);
+  const int k = wg >> 5, f = wg & 31;
+  const LevelView& V = a.lv[d];
+  int64_t* Hself;
+  int64_t g8[8], h8[8];
+  if (d == 0) {
+    Hself = a.H[0];
+  } else {
+    const int j = k >> 1;
+    if (a.lv[d - 1].split_f[j] < 0) {
+      if (f == 0 && lane == 0) V.split_f[k] = -1;
+      return;
+    }
+    const int side = V.built[j];
+    const bool is_built = (k & 1) == side;
+    Hself = a.H[d & 1] + (size_t)(is_built ? j : (1 << (d - 1)) + j) * SLOT;
+    if (!is_built) {
+      const longlong2* Hp = reinterpret_cast<const longlong2*>(a.H[(d - 1) & 1] + (size_t)node_slot(a, d - 1, j) * SLOT);
+      const longlong2* Hb = reinterpret_cast<const longlong2*>(a.H[d & 1] + (size_t)j * SLOT);
+      longlong2* Hs = reinterpret_cast<longlong2*>(Hself);
+      const int eg0 = (f * kBins + lane * 8) / 2, eh0 = (kHistBins + f * kBins + lane * 8) / 2;
+      longlong2 pg[4], bg2[4], ph[4], bh2[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        pg[q] = Hp[eg0 + q];
+        bg2[q] = Hb[eg0 + q];
+        ph[q] = Hp[eh0 + q];
+        bh2[q] = Hb[eh0 + q];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        g8[2 * q] = pg[q].x - bg2[q].x;
+        g8[2 * q + 1] = pg[q].y - bg2[q].y;
+        h8[2 * q] = ph[q].x - bh2[q].x;
+        h8[2 * q + 1] = ph[q].y - bh2[q].y;
+        Hs[eg0 + q] = make_longlong2(g8[2 * q], g8[2 * q + 1]);
+        Hs[eh0 + q] = make_longlong2(h8[2 * q], h8[2 * q + 1]);
+      }
+    }
+  }
+  if (d == 0 || (k & 1) == a.lv[d].built[k >> 1]) {
+    const longlong2* G2 = reinterpret_cast<const longlong2*>(Hself + f * kBins + lane * 8);
+    const longlong2* H2 = reinterpret_cast<const longlong2*>(Hself + kHistBins + f * kBins + lane * 8);
+    longlong2 gv[4], hv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      gv[q] = G2[q];
+      hv[q] = H2[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      g8[2 * q] = gv[q].x;
+      g8[2 * q + 1] = gv[q].y;
+      h8[2 * q] = hv[q].x;
+      h8[2 * q + 1] = hv[q].y;
+    }
+  }
+#pragma unroll
+  for (int q = 1; q < 8; ++q) {
+    g8[q] += g8[q - 1];
+    h8[q] += h8[q - 1];
+  }
+  int64_t ig = g8[7], ih = h8[7];
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t ug = __shfl_up_sync(0xffffffffu, ig, o), uh = __shfl_up_sync(0xffffffffu, ih, o);
+    if (lane >= o) {
+      ig += ug;
+      ih += uh;
+    }
+  }
+  const int64_t bgp = ig - g8[7], bhp = ih - h8[7];
+  const int64_t Gq = __shfl_sync(0xffffffffu, ig, 31), Hq = __shfl_sync(0xffffffffu, ih, 31);
+  bool fin = f < a.F;
+  if (fin && a.colsample < 1.0f) {
+    const int F = a.F;
+    int nkeep = (int)ceil((double)a.colsample * (double)F);
+    if (nkeep < 1) nkeep = 1;
+    const uint64_t kf = rng4(a.seed, (uint64_t)(2 * a.target + 1), (uint64_t)t, (uint64_t)f);
+    const uint64_t kl = lane < F ? rng4(a.seed, (uint64_t)(2 * a.target + 1), (uint64_t)t, (uint64_t)lane) : ~0ull;
+    const unsigned less = __ballot_sync(0xffffffffu, lane < F && (kl < kf || (kl == kf && lane < f)));
+    fin = __popc(less) < nkeep;
+  }
+  const int eg = exp_of(__uint_as_float(a.maxg[t])), eh = exp_of(__uint_as_float(a.maxh[t]));
+  const double sgi = exp2i(eg - a.K), shi = exp2i(eh - a.K);
+  const double lo = (d == 0) ? -INFINITY : V.lo[k], hi = (d == 0) ? INFINITY : V.hi[k];
+  const double lambda = a.lambda, mcw = a.mcw;
+  double bl = -INFINITY;
+  int bb = 0x7fffffff;
+  int64_t bGL = 0, bHL = 0;
+  if (fin) {
+    const int nthr = a.ncuts[f];   // thresholds b = 0 .. nbins_f - 2
+    if (lane * 8 < nthr) {
+      const double G = dequant(Gq, sgi), H = dequant(Hq, shi);
+      const double gainP = calc_gain(G, H, calc_weight(G, H, lo, hi, lambda, mcw), lambda);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int b = lane * 8 + q;
+        if (b < nthr) {
+          const int64_t GLq = bgp + g8[q], HLq = bhp + h8[q];
+          const double GL = dequant(GLq, sgi), HL = dequant(HLq, shi);
+          const double GR = dequant(Gq - GLq, sgi), HR = dequant(Hq - HLq, shi);
+          if (HL >= mcw && HR >= mcw) {
+            const double wl = calc_weight(GL, HL, lo, hi, lambda, mcw);
+            const double wr = calc_weight(GR, HR, lo, hi, lambda, mcw);
+            if (!(a.monotone && f == a.users_col && wl > wr)) {
+              const double loss =
+                  __dsub_rn(__dadd_rn(calc_gain(GL, HL, wl, lambda), calc_gain(GR, HR, wr, lambda)), gainP);
+              if (loss > bl) {   // b ascending within the lane: strict keeps the smaller b
+                bl = loss;
+                bb = b;
+                bGL = GLq;
+                bHL = HLq;
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ol = __shfl_down_sync(0xffffffffu, bl, o);
+    const int ob = __shfl_down_sync(0xffffffffu, bb, o);
+    const int64_t oG = __shfl_down_sync(0xffffffffu, bGL, o), oH = __shfl_down_sync(0xffffffffu, bHL, o);
+    if (ol > bl || (ol == bl && ob < bb)) {
+      bl = ol;
+      bb = ob;
+      bGL = oG;
+      bHL = oH;
+    }
+  }
+  FeatBest* fb = a.fbest + (size_t)k * 32;
+  int last = 0;
+  if (lane == 0) {
+    FeatBest r;
+    r.loss = bl;
+    r.b = bb;
+    r.valid = (bl > -INFINITY) ? 1 : 0;
+    r.GLq = bGL;
+    r.HLq = bHL;
+    r.Gq = Gq;
+    r.Hq = Hq;
+    fb[f] = r;
+    __threadfence();
+    last = atomicAdd(&V.done[k], 1) == 31;
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  // ---- the node's last warp: best over the 32 features, then the tree update
+  __threadfence();
+  const volatile FeatBest* vfb = fb;
+  double ml = vfb[lane].valid ? vfb[lane].loss : -INFINITY;
+  int mf = lane, mb = vfb[lane].b;
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ol = __shfl_down_sync(0xffffffffu, ml, o);
+    const int of = __shfl_down_sync(0xffffffffu, mf, o), ob = __shfl_down_sync(0xffffffffu, mb, o);
+    if (ol > ml || (ol == ml && (of < mf || (of == mf && ob < mb)))) {
+      ml = ol;
+      mf = of;
+      mb = ob;
+    }
+  }
+  if (lane != 0) return;
+  V.done[k] = 0;
+  int32_t* const tfeat = a.tfeat + (size_t)t * a.nn;
+  int32_t* const tbin = a.tbin + (size_t)t * a.nn;
+  float* const tthr = a.tthr + (size_t)t * a.nn;
+  float* const tval = a.tval + (size_t)t * a.nn;
+  const int64_t GqN = vfb[0].Gq, HqN = vfb[0].Hq;
+  const double G = dequant(GqN, sgi), H = dequant(HqN, shi);
+  const double wP = calc_weight(G, H, lo, hi, lambda, mcw);
+  const int gk = (1 << d) - 1 + k;
+  if (ml > 1e-6) {
+    const int fs = mf, bs = mb;
+    const int64_t GLs = vfb[fs].GLq, HLs = vfb[fs].HLq;
+    const double GL = dequant(GLs, sgi), HL = dequant(HLs, shi);
+    const double GR = dequant(GqN - GLs, sgi), HR = dequant(HqN - HLs, shi);
+    const double wl = calc_weight(GL, HL, lo, hi, lambda, mcw);
+    const double wr = calc_weight(GR, HR, lo, hi, lambda, mcw);
+    double loL = lo, hiL = hi, loR = lo, hiR = hi;
+    if (a.monotone && fs == a.users_col) {
+      const double mid = __dmul_rn(__dadd_rn(wl, wr), 0.5);
+      hiL = mid;
+      loR = mid;
+    }
+    V.split_f[k] = fs;
+    V.split_b[k] = bs;
+    tfeat[gk] = fs;
+    tbin[gk] = bs;
+    tthr[gk] = a.cuts[fs * (kBins - 1) + bs];
+    tval[gk] = 0.0f;
+    if (d + 1 < a.D) {
+      const LevelView& N = a.lv[d + 1];
+      N.lo[2 * k] = loL;
+      N.hi[2 * k] = hiL;
+      N.lo[2 * k + 1] = loR;
+      N.hi[2 * k + 1] = hiR;
+    } else {
+      // children at max depth are leaves: v = (float)(eta * W(G, H, lo, hi))
+      tfeat[2 * gk + 1] = -1;
+      tval[2 * gk + 1] = (float)__dmul_rn(a.eta, calc_weight(GL, HL, loL, hiL, lambda, mcw));
+      tfeat[2 * gk + 2] = -1;
+      tval[2 * gk + 2] = (float)__dmul_rn(a.eta, calc_weight(GR, HR, loR, hiR, lambda, mcw));
+    }
+  } else {
+    V.split_f[k] = -1;
+    tfeat[gk] = -1;
+    tval[gk] = (float)__dmul_rn(a.eta, wP);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
 // split evaluation, one CTA of 1024 threads per node of level d: warp f owns feature f, lane l
 // owns bins 8l .. 8l+7.  The warp forms its feature's histogram (sibling = parent - built, exact
 // int64, written back for the next level), prefix-scans it (8 local + warp shuffle scan), evaluates
@@ -1083,12 +1310,6 @@ __global__ void __launch_bounds__(SP2_THREADS) k_split2(const FitArgs a, const i
 // level), block-scans it, evaluates every threshold in fp64 (monotone veto on users) and
 // publishes its best (loss, b, GL, HL); the last CTA of the node (ticket counter) picks the
 // node's best over features with the (loss desc, f asc, b asc) total order and writes the tree.
-struct FeatBest {
-  double loss;
-  int32_t b, valid;
-  int64_t GLq, HLq, Gq, Hq;
-};
-
 __device__ __forceinline__ bool better_fb(double la, int fa, int ba, double lb, int fb, int bb) {
   if (la != lb) return la > lb;
   if (fa != fb) return fa < fb;
@@ -1720,11 +1941,15 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   static bool attr_set = false;
   if (!attr_set) {
     LLMP_CUDA(cudaFuncSetAttribute(k_hist_root2, cudaFuncAttributeMaxDynamicSharedMemorySize, R2_SMEM));
+    LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_ROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
     LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_LEVEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
     LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
     attr_set = true;
   }
   const DbgArgs nodbg{};
+  // root histogram variant: run-length lane-per-feature (default) or the hybrid run/row-parallel
+  // kernel (LLMP_ROOT2=1; faster on random codes, slower on paper-ordered rows)
+  static const bool use_root2 = getenv("LLMP_ROOT2") && atoi(getenv("LLMP_ROOT2")) != 0;
 
   // ---- base scores (O3) and tree 0's gradient maxima
   for (int tg = 0; tg < 2; ++tg) {
@@ -1748,9 +1973,10 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   auto tree = [&](const FitArgs& a, const PartWs& pw) {
     const cudaStream_t st = ctx->stream;
     LLMP_CUDA(cudaMemsetAsync(a.H[0], 0, (size_t)SLOT * 8, st));
-    LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist_root2, hist_grid, R2_THREADS, R2_SMEM, a);
+    if (use_root2) LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist_root2, hist_grid, R2_THREADS, R2_SMEM, a);
+    else LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist<HM_ROOT>, hist_grid, HIST_THREADS, HIST_SMEM, a, 0, 0, nodbg);
     allreduce_sum_i64(ctx, a.H[0], SLOT);
-    LLMP_LAUNCH(ctx, KC_SPLIT, 1, k_split2, 1, SP2_THREADS, 0, a, 0);
+    LLMP_LAUNCH(ctx, KC_SPLIT, 1, k_split3, 32 / SP3_WARPS, SP3_WARPS * 32, 0, a, 0);
     for (int d = 1; d < D; ++d) {
       const int tiles_d = (int)((n + PT_TILE - 1) / PT_TILE) + (1 << (d - 1));
       LLMP_LAUNCH(ctx, KC_PARTITION, n, k_pcount, std::min(tiles_d, 5 * ctx->sms), PT_THREADS, 0, a, d, pw);
@@ -1762,7 +1988,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       }
       LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hist_grid, HIST_THREADS, HIST_SMEM, a, d, 0, nodbg);
       allreduce_sum_i64(ctx, a.H[d & 1], (size_t)SLOT << (d - 1));
-      LLMP_LAUNCH(ctx, KC_SPLIT, (1 << d), k_split2, (1 << d), SP2_THREADS, 0, a, d);
+      LLMP_LAUNCH(ctx, KC_SPLIT, (1 << d), k_split3, (1 << d) * (32 / SP3_WARPS), SP3_WARPS * 32, 0, a, d);
     }
     LLMP_LAUNCH(ctx, KC_UPDATE, n, k_update, upd_grid, UPD_THREADS, 0, a);
     // next tree's gradient maxima (past slots are already equal on every rank, future ones 0)
