@@ -1,0 +1,76 @@
+"""Summarise an `ncu --set full` capture of one tree (tools/profile_fit.py --trees 1) into
+profiles/: a per-launch CSV, a per-kernel-class text summary, and profiles/ncu_traffic.json
+(measured DRAM bytes per launch per kernel class, which bench.py reports as roofline.traffic).
+
+    python tools/ncu_summary.py gpurun_out/prof_r01_tree.ncu-rep profiles/r01
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+
+METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+           "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+           "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed.sum",
+           "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+           "sm__warps_active.avg.pct_of_peak_sustained_active"]
+CLASS = {"k_hist<0>": "hist_root", "k_hist<1>": "hist_level", "k_hist_root2": "hist_root", "k_pcount": "partition",
+         "k_pscan": "partition", "k_pscatter2": "partition", "k_split3": "split", "k_update": "update"}
+
+
+def kclass(name):
+    base = name.split("(")[0].replace("void ", "").replace("llmp::", "").strip()
+    return CLASS.get(base, base), base
+
+
+def main(rep, prefix):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr = rows[0]
+    data = rows[2:]
+    idx = {m: hdr.index(m) for m in METRICS}
+    ik = hdr.index("Kernel Name")
+    recs = []
+    for r in data:
+        cls, base = kclass(r[ik])
+        rec = {"kernel": base, "class": cls}
+        for m in METRICS:
+            try:
+                rec[m] = float(r[idx[m]].replace(",", ""))
+            except ValueError:
+                rec[m] = None
+        recs.append(rec)
+    with open(prefix + "_ncu_launches.csv", "w", newline="") as f:
+        w = csv.DictWriter(f, fieldnames=["kernel", "class"] + METRICS)
+        w.writeheader()
+        w.writerows(recs)
+    agg = {}
+    for r in recs:
+        a = agg.setdefault(r["class"], {"launches": 0, "us": 0.0, "dram": 0.0, "inst": 0.0})
+        a["launches"] += 1
+        a["us"] += r["gpu__time_duration.sum"] or 0.0
+        a["dram"] += ((r["dram__bytes_read.sum"] or 0) + (r["dram__bytes_write.sum"] or 0)) * 1e6  # Mbyte -> B
+        a["inst"] += r["smsp__inst_executed.sum"] or 0.0
+    lines = ["ncu --set full --clock-control none, one tree of both ensembles (tools/profile_fit.py --trees 1, "
+             "C3: 10M rows, depth 8); cold cache, serialised launches", ""]
+    traffic = {}
+    for c, a in sorted(agg.items(), key=lambda x: -x[1]["us"]):
+        per = a["dram"] / a["launches"]
+        lines.append("%-12s launches %3d  total %9.1f us  avg %8.1f us  DRAM %8.1f MB/launch  %6.2f TB/s  %7.1f M inst"
+                     % (c, a["launches"], a["us"], a["us"] / a["launches"], per / 1e6,
+                        a["dram"] / (a["us"] * 1e-6) / 1e12, a["inst"] / 1e6))
+        traffic[c] = {"dram_bytes_per_launch": per, "avg_duration_us": a["us"] / a["launches"],
+                      "launches_profiled": a["launches"],
+                      "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch from %s" % os.path.basename(rep)}
+    with open(prefix + "_ncu_summary.txt", "w") as f:
+        f.write("\n".join(lines) + "\n")
+    with open(os.path.join(os.path.dirname(prefix), "ncu_traffic.json"), "w") as f:
+        json.dump(traffic, f, indent=1)
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1], sys.argv[2])
