@@ -25,6 +25,7 @@ import statistics
 import subprocess
 import sys
 import tempfile
+import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -41,10 +42,11 @@ UNIT = "row-iters/s"
 # algorithmic bytes per unit: unit = one row processed by that kernel
 BYTES_PER_UNIT = {
     "hist_root": 48.0,    # 32 B code row + y, w, p (12 B) read + 4 B packed gradient pair written
-    "partition": 17.0,    # 4 B row index + 1 B split-feature code (count) + 8 B state read + 8 B written,
-                          # minus the 4 B row index read twice: 4 + 1 + 4 + 8 = 17 B per partitioned row
-    "hist_level": 40.0,   # 32 B code row (gathered by row index) + 8 B (row index, packed pair)
-    "update": 48.0,       # 32 B code row + y, w, p read (12 B) + p written (4 B)
+    "partition": 9.0,     # row index read + 1 B split-feature code + row index written (the tile
+                          # design reads the row index twice: 13 B moved, 9 B algorithmic)
+    "hist_level": 40.0,   # 32 B code row + 4 B packed pair (both gathered by row index) + 4 B row index
+    "update": 52.0,       # fused update of tree t + root histogram of tree t+1 (k_hist<UPDROOT>):
+                          # 32 B code row + y, w, p read (12 B) + p and the packed pair written (8 B)
     "codes": 192.0,       # 128 B f32 row read + 32 B row-major + 32 B column-major codes written
 }
 
@@ -94,53 +96,111 @@ def ncu_traffic():
 
 # ------------------------------------------------------------------------------------- clocks
 class ClockSampler:
-    def __init__(self, gpu_index):
-        self.gpu = gpu_index
-        self.proc = None
-        self.path = None
+    """SM clocks and throttle reasons sampled every 100 ms by an in-process NVML thread.  NVML is
+    initialised before the warm-up (no driver initialisation overlaps the timed region) and only
+    the samples taken between begin() and end() — the timed region — are reported.  Falls back to
+    an `nvidia-smi -lms` process started at open() when NVML is unavailable."""
 
-    def start(self):
-        fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
-        os.close(fd)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, cuda_index):
+        self.cuda_index = cuda_index
+        self.samples = []          # (monotonic time, sm MHz, max sm MHz, set of reasons)
+        self.t0 = self.t1 = None
+        self._stop = threading.Event()
+        self.thread = self.proc = self.path = None
+
+    def open(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), "--query-gpu=" + q,
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
-        except OSError:
-            self.proc = None
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            try:
+                uuid = str(torch.cuda.get_device_properties(self.cuda_index).uuid)
+                h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(self.cuda_index)
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
 
-    def stop(self):
+            def loop():
+                while not self._stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((time.monotonic(), float(sm), float(mx),
+                                             {k for k, b in bits.items() if r & b}))
+                    except Exception:
+                        pass
+                    self._stop.wait(0.1)
+
+            self.nvml = pynvml
+            self.thread = threading.Thread(target=loop, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.nvml = None
+            fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+            os.close(fd)
+            q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            try:
+                self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.cuda_index), "--query-gpu=" + q,
+                                              "--format=csv,noheader,nounits", "-lms", "200"],
+                                             stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            except OSError:
+                self.proc = None
+        return self
+
+    def begin(self):
+        self.t0 = time.monotonic()
+
+    def end(self):
+        self.t1 = time.monotonic()
+
+    def close(self):
         out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        if self.proc is None:
-            return out
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
         sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        with open(self.path) as f:
-            for line in f:
-                parts = [p.strip() for p in line.split(",")]
-                if len(parts) < 9:
-                    continue
-                try:
-                    sm.append(float(parts[1]))
-                    mx.append(float(parts[2]))
-                except ValueError:
-                    continue
-                for nm, v in zip(names, parts[5:9]):
-                    if v.lower() == "active":
-                        reasons.add(nm)
-        os.unlink(self.path)
+        if self.thread is not None:
+            self._stop.set()
+            self.thread.join(timeout=2)
+            for t, a, b, r in self.samples:
+                if self.t0 is not None and self.t0 <= t <= (self.t1 or t):
+                    sm.append(a)
+                    mx.append(b)
+                    reasons |= r
+            try:
+                self.nvml.nvmlShutdown()
+            except Exception:
+                pass
+            out["source"] = "nvml (in-process, 100 ms, timed region only)"
+        elif self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            with open(self.path) as f:
+                for line in f:
+                    parts = [p.strip() for p in line.split(",")]
+                    if len(parts) < 9:
+                        continue
+                    try:
+                        sm.append(float(parts[1]))
+                        mx.append(float(parts[2]))
+                    except ValueError:
+                        continue
+                    for nm, v in zip(self.REASONS, parts[5:9]):
+                        if v.lower() == "active":
+                            reasons.add(nm)
+            os.unlink(self.path)
+            out["source"] = "nvidia-smi -lms 200 (warm-up + timed region)"
         if sm:
-            out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                   "samples": len(sm)}
+            out.update({"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                        "samples": len(sm)})
         return out
 
 
@@ -243,13 +303,12 @@ def main():
         m.free()
         return recs
 
+    clocks = ClockSampler(local_rank).open()   # before the warm-up: no NVML init in the timed region
     for _ in range(args.warmup):
         step(Xd, yd, ld, pd, lfd, pfd)
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, device-resident inputs, CUDA events on the context stream
-    clocks = ClockSampler(local_rank)
-    clocks.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -257,16 +316,18 @@ def main():
     ctx.set_timing(0)            # production mode: each tree replays from a CUDA graph
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    clocks.begin()
     t_start.record(stream)
     for _ in range(args.steps):
         step(Xd, yd, ld, pd, lfd, pfd, record=ev)
     t_end.record(stream)
     torch.cuda.synchronize()
+    clocks.end()
     if world > 1:
         dist.barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
     stats = ctx.stats()
-    clk = clocks.stop()
+    clk = clocks.close()
     fit_ms = sum(a.elapsed_time(b) for a, b, c in ev)
     pred_ms = sum(b.elapsed_time(c) for a, b, c in ev)
     agg = torch.tensor([elapsed_ms, fit_ms, pred_ms], dtype=torch.float64, device=dev)

@@ -6,12 +6,14 @@
 //
 //   per tree t:   k_hist<ROOT>   root histogram over all rows (identity order), fused with the
 //                                gradient computation + quantisation (writes gp_root)
-//                 k_split(0)
+//                 k_split3(0)
 //                 for d = 1..D-1:
-//                   k_partition(d)  stable partition of the split parents' rows into children
-//                                   (decoupled look-back over tiles), zeroes the child hists
-//                   k_hist<LEVEL>   histogram of the smaller child of each split parent
-//                   k_split(d)      sibling = parent - built; prefix scan; fp64 gains; argmax
+//                   k_pcount / k_pscatter2(d)
+//                                   stable partition of the split parents' row indices into
+//                                   children (independent 4096-row tiles); zeroes the child hists
+//                   k_hist<LEVEL>   histogram of the smaller child of each split parent (codes
+//                                   and packed gradient pairs gathered by row index)
+//                   k_split3(d)     sibling = parent - built; prefix scan; fp64 gains; argmax
 //                 k_update(t)    route every row to its leaf, p += v, next tree's max|g|
 //
 // No host synchronisation happens inside the tree loop; all decisions live on the device.
@@ -36,11 +38,6 @@ constexpr int ROWBUF_STRIDE = 48;          // bytes per staged code row (conflic
 constexpr int MAX_PIECES = 512;            // built children per level (2^(kMaxDepth-1))
 constexpr int HIST_SMEM = 2 * kHistBins * 4 + HIST_WARPS * 32 * ROWBUF_STRIDE;  // 64 KB + 24 KB
 
-constexpr int PART_THREADS = 256;
-constexpr int PART_ITEMS = 8;
-constexpr int TILE = PART_THREADS * PART_ITEMS;  // 2048 rows per look-back tile
-
-constexpr int SPLIT_THREADS = 256;
 constexpr int SLOT = 2 * kHistBins;        // int64 per histogram slot (g then h)
 
 
@@ -80,7 +77,6 @@ struct FitArgs {
   float* p;
   uint32_t* gp_root;
   uint32_t* sr[2];   // row-index state (children: A = [0,n) left, B = [n,2n) right)
-  uint32_t* sg[2];   // packed gradient pair state, same positions
   int64_t* H[2];
   LevelView lv[kMaxDepth + 1];
   const int* d_tree; // device-side index of the tree being grown (advanced by k_next_tree)
@@ -96,6 +92,7 @@ struct FitArgs {
   float subsample, colsample;
   uint64_t seed;
   int monotone;
+  int fused_root;     // 1: k_hist<UPDROOT> builds the next root speculatively (root_needed)
   int nn;
   FeatBest* fbest;            // [2^(D-1)][32] per-(node, feature) best split of the current level
   unsigned long long* units;  // device counters of rows processed per kernel class (instrumentation)
@@ -129,11 +126,27 @@ __device__ __forceinline__ int node_slot(const FitArgs& a, int d, int k) {
 // ---------------------------------------------------------------------------------------------
 // histogram kernel: lane = feature, one row per warp step, run-length aggregation of equal
 // consecutive codes in registers, 32-bit shared atomics on change, zero-skipping int64 flush
-enum { HM_ROOT = 0, HM_LEVEL = 1, HM_DEBUG = 2 };
+enum { HM_ROOT = 0, HM_LEVEL = 1, HM_DEBUG = 2, HM_UPDROOT = 3 };
+
+// Fused update + next root (HM_UPDROOT): the update pass of tree t also builds tree
+// t+1's root histogram, quantising tree t+1's gradients with tree t's exponents e (O4) — the
+// speculation that max|g| and max h keep their binary exponent from one tree to the next (true for
+// ~99% of trees: the maxima shrink slowly).  Tree t+1's own maxima are computed in the same pass;
+// when an exponent did change, the speculative histogram and packed pairs are discarded: k_root_fix
+// zeroes the root slot and k_hist<ROOT> rebuilds both with the right scale.  Every histogram is
+// therefore exactly the one O4-O6 define, whichever way it was built.
+__device__ __forceinline__ bool root_needed(const FitArgs& a, int t) {
+  if (!a.fused_root || t == 0) return true;
+  return exp_of(__uint_as_float(a.maxg[t])) != exp_of(__uint_as_float(a.maxg[t - 1])) ||
+         exp_of(__uint_as_float(a.maxh[t])) != exp_of(__uint_as_float(a.maxh[t - 1]));
+}
+constexpr int UPDROOT_TREE_SMEM = 512 * 6;   // s_feat (int8), s_bin (u8), s_val (f32) of one tree
 
 template <int MODE>
 __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const int d, const int t_in, const DbgArgs dbg) {
-  const int t = (MODE == HM_ROOT) ? *a.d_tree : t_in;   // graph replays: tree index from the device
+  const int t = (MODE == HM_ROOT || MODE == HM_UPDROOT) ? *a.d_tree : t_in;   // graph replays: tree index from the device
+  if (MODE == HM_ROOT && !root_needed(a, t)) return;   // built speculatively by the previous update pass
+  const bool has_next = (MODE == HM_UPDROOT) ? (t + 1 < a.T) : true;
   extern __shared__ __align__(16) uint8_t smem[];
   int32_t* sg = reinterpret_cast<int32_t*>(smem);                 // [256 bins][32 features]
   uint32_t* sh = reinterpret_cast<uint32_t*>(smem + kHistBins * 4);
@@ -148,6 +161,19 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
   for (int i = tid; i < kHistBins; i += HIST_THREADS) {
     sg[i] = 0;
     sh[i] = 0;
+  }
+  // fused mode: tree t (the one just grown) in shared memory for routing
+  int8_t* s_feat = reinterpret_cast<int8_t*>(smem + HIST_SMEM);
+  uint8_t* s_bin = smem + HIST_SMEM + 512;
+  float* s_val = reinterpret_cast<float*>(smem + HIST_SMEM + 1024);
+  if (MODE == HM_UPDROOT) {
+    const size_t to = (size_t)t * a.nn;
+    for (int i = tid; i < a.nn; i += HIST_THREADS) {
+      const int f = a.tfeat[to + i];
+      s_feat[i] = (int8_t)(f < 0 ? -1 : f);
+      s_bin[i] = (uint8_t)a.tbin[to + i];
+      s_val[i] = a.tval[to + i];
+    }
   }
   // ---- piece list (virtual concatenation of the rows to histogram)
   if (MODE == HM_LEVEL) {
@@ -190,7 +216,7 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
     if (tid == 0) {
       s_np = 1;
       s_vstart[0] = 0;
-      s_vstart[1] = (MODE == HM_ROOT) ? a.n : dbg.m;
+      s_vstart[1] = (MODE == HM_ROOT || MODE == HM_UPDROOT) ? a.n : dbg.m;
       s_pstart[0] = 0;
       s_slot[0] = 0;
     }
@@ -200,17 +226,19 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
   const int64_t S = s_vstart[np];
   const int64_t v0 = S * blockIdx.x / gridDim.x, v1 = S * (blockIdx.x + 1) / gridDim.x;
   if (v0 >= v1) return;
-  if (tid == 0 && MODE != HM_DEBUG && a.units) atomicAdd(&a.units[MODE == HM_ROOT ? KC_HIST_ROOT : KC_HIST], (unsigned long long)(v1 - v0));
+  if (tid == 0 && MODE != HM_DEBUG && a.units)
+    atomicAdd(&a.units[MODE == HM_ROOT ? KC_HIST_ROOT : MODE == HM_UPDROOT ? KC_UPDATE : KC_HIST], (unsigned long long)(v1 - v0));
 
   // quantisation scales for ROOT (tree t): q = rint(v * 2^(K-e))
+  // (HM_UPDROOT: tree t+1's pairs with tree t's exponents — the speculation described above)
   double scale_g = 0.0, scale_h = 0.0;
-  if (MODE == HM_ROOT) {
+  if (MODE == HM_ROOT || MODE == HM_UPDROOT) {
     scale_g = exp2i(a.K - exp_of(__uint_as_float(a.maxg[t])));
     scale_h = exp2i(a.K - exp_of(__uint_as_float(a.maxh[t])));
   }
+  float mg = 0.f, mh = 0.f;   // HM_UPDROOT: tree t+1's max |g|, max h
   int64_t* Hbase = (MODE == HM_DEBUG) ? dbg.out : a.H[d & 1];
   const uint32_t* sr_in = (MODE == HM_LEVEL) ? a.sr[d & 1] : nullptr;
-  const uint32_t* sg_in = (MODE == HM_LEVEL) ? a.sg[d & 1] : nullptr;
 
   // first piece overlapping [v0, v1)
   int pc = 0;
@@ -240,14 +268,14 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
         if (vi < w1) {
           const int64_t pi = s_pstart[pc] + (vi - s_vstart[pc]);  // physical position
           int64_t ridx;
-          if (MODE == HM_ROOT) {
+          if (MODE == HM_ROOT || MODE == HM_UPDROOT) {
             ridx = pi;
             ny = a.y[ridx];
             nw = a.w[ridx];
             np_ = a.p[ridx];
           } else if (MODE == HM_LEVEL) {
             ridx = sr_in[pi];
-            ngp = sg_in[pi];
+            ngp = a.gp_root[ridx];   // gathered by row index (written by this tree's root pass)
           } else {
             ridx = dbg.idx ? dbg.idx[pi] : pi;
             ngp = pack_gp(dbg.qg[ridx], dbg.qh[ridx]);
@@ -275,9 +303,33 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
         __syncwarp();   // previous batch fully consumed
         *reinterpret_cast<uint4*>(rowbuf + lane * ROWBUF_STRIDE) = nc0;
         *reinterpret_cast<uint4*>(rowbuf + lane * ROWBUF_STRIDE + 16) = nc1;
+        if (MODE == HM_UPDROOT && lane < cnt) {
+          // O9 for tree t (route the lane's own staged row, p += v), then O4 for tree t+1
+          const int64_t ridx = base + lane + (s_pstart[pc] - s_vstart[pc]);
+          int k = 0;
+          for (int s2 = 0; s2 < a.D; ++s2) {
+            const int f = s_feat[k];
+            if (f >= 0) k = 2 * k + 1 + (rowbuf[lane * ROWBUF_STRIDE + f] > s_bin[k] ? 1 : 0);
+          }
+          const float pn = __fadd_rn(np_, s_val[k]);   // one fp32 rounding, tree order
+          a.p[ridx] = pn;
+          if (has_next) {
+            float g = __fmul_rn(nw, __fsub_rn(pn, ny));
+            float h = nw;
+            if (row_sampled_out(a.seed, a.target, t + 1, a.row_offset + ridx, a.subsample)) {
+              g = 0.f;
+              h = 0.f;
+            }
+            mg = fmaxf(mg, fabsf(g));
+            mh = fmaxf(mh, h);
+            gp = pack_gp(quantize(g, scale_g), quantize(h, scale_h));
+            a.gp_root[ridx] = gp;
+          }
+        }
         *reinterpret_cast<uint32_t*>(rowbuf + lane * ROWBUF_STRIDE + 32) = gp;
         __syncwarp();
         if (base + 32 < w1) load_batch(base + 32);   // prefetch the next batch
+        if (MODE == HM_UPDROOT && !has_next) continue;   // last tree: update only
         if (prev < 0) prev = rowbuf[lane];
 #pragma unroll 4
         for (int r = 0; r < cnt; ++r) {
@@ -315,6 +367,23 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
       __syncthreads();
     }
   }
+  if (MODE == HM_UPDROOT && has_next) {   // tree t+1's maxima (float bits of non-negatives order as uints)
+    for (int o = 16; o > 0; o >>= 1) {
+      mg = fmaxf(mg, __shfl_xor_sync(0xffffffffu, mg, o));
+      mh = fmaxf(mh, __shfl_xor_sync(0xffffffffu, mh, o));
+    }
+    if (lane == 0) {
+      atomicMax(&a.maxg[t + 1], __float_as_uint(mg));
+      atomicMax(&a.maxh[t + 1], __float_as_uint(mh));
+    }
+  }
+}
+
+// zero the root histogram slot when k_hist<ROOT> is going to (re)build it (see root_needed)
+__global__ void k_root_fix(const FitArgs a) {
+  if (!root_needed(a, *a.d_tree)) return;
+  int64_t* H = a.H[0];
+  for (int i = threadIdx.x; i < SLOT; i += blockDim.x) H[i] = 0;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -523,23 +592,22 @@ __global__ void __launch_bounds__(R2_THREADS, 2) k_hist_root2(const FitArgs a) {
 //   k_pcount   one CTA per 4096-row tile of a split parent: row index -> split-feature code
 //              (column-major byte) -> left bit; bits kept in a per-tile bitmask, count per tile;
 //              also zeroes the level's built-child histogram slots
-//   k_pscan    one CTA: exclusive prefix of the tile counts (global left prefix), child segment
-//              starts and counts
-//   k_pscatter one CTA per tile: stage (row index, packed gradient), block-scan the left bits,
-//              order lefts-then-rights in shared memory (stable) and write both runs with coalesced
-//              stores — left rows to region A = [0, n) at the global left prefix, right rows to
-//              region B = [n, 2n) at the global right prefix.  Each child segment is contiguous
-//              and keeps its parent's row order.
+//   k_pscatter2 every CTA first scans the tile counts itself (global left prefix of its own
+//              tiles; CTA 0 also writes the child segment starts and counts), then, per tile, a
+//              stable warp-aggregated scatter of the row indices — left rows
+//              to region A = [0, n) at the global left prefix, right rows to region B = [n, 2n)
+//              at the global right prefix.  Each child segment is contiguous and keeps its
+//              parent's row order.  Only row indices move: the level histogram gathers codes and
+//              packed gradient pairs by row index.
 constexpr int PT_THREADS = 256;
 constexpr int PT_ITEMS = 16;
 constexpr int PT_TILE = PT_THREADS * PT_ITEMS;   // 4096 rows
 constexpr int PT_WORDS = PT_TILE / 32;           // bitmask words per tile
-constexpr int PT_HALF = PT_TILE / 2;             // k_pscatter works in 2048-row halves
-constexpr int PT_HI = PT_HALF / PT_THREADS;      // 8 rows per thread per half
+
+constexpr int PT_OWN = 64;                       // tiles per scatter CTA at most (host grid sizing)
 
 struct PartWs {
   int32_t* tile_left;    // [max tiles] left rows per tile
-  int64_t* tile_lpref;   // [max tiles] global left prefix at the tile start
   uint32_t* bits;        // [max tiles][PT_WORDS] left bits
 };
 
@@ -676,136 +744,6 @@ __global__ void __launch_bounds__(PT_THREADS) k_pcount(const FitArgs a, const in
   }
 }
 
-constexpr int PS_THREADS = 1024;
-__global__ void __launch_bounds__(PS_THREADS) k_pscan(const FitArgs a, const int d, const PartWs w) {
-  __shared__ int s_tile_pref[MAX_PIECES + 1];
-  __shared__ int64_t s_seq_pref[MAX_PIECES + 1];
-  __shared__ int s_w[PS_THREADS / 32];
-  __shared__ int64_t s_w64[PS_THREADS / 32];
-  const int NP = 1 << (d - 1);
-  const LevelView& P = a.lv[d - 1];
-  const LevelView& C = a.lv[d];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  parent_prefixes(a, d, s_tile_pref, s_seq_pref, s_w, s_w64);
-  const int T = s_tile_pref[NP];
-  // exclusive scan of the tile counts: contiguous block of tiles per thread
-  const int t0 = (int)((int64_t)T * tid / PS_THREADS), t1 = (int)((int64_t)T * (tid + 1) / PS_THREADS);
-  int64_t local = 0;
-  for (int t = t0; t < t1; ++t) local += w.tile_left[t];
-  int64_t inc = local;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int64_t u = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += u;
-  }
-  if (lane == 31) s_w64[warp] = inc;
-  __syncthreads();
-  int64_t run = 0;
-  for (int w2 = 0; w2 < warp; ++w2) run += s_w64[w2];
-  run += inc - local;
-  for (int t = t0; t < t1; ++t) {
-    w.tile_lpref[t] = run;
-    run += w.tile_left[t];
-  }
-  __syncthreads();   // global writes of this block are visible to the block after the barrier
-  for (int j = tid; j < NP; j += PS_THREADS) {
-    if (P.split_f[j] < 0) continue;
-    const int ta = s_tile_pref[j], tb = s_tile_pref[j + 1] - 1;
-    const int64_t cnt_j = (d == 1) ? a.n : P.cnt[j];
-    const int64_t lstart = w.tile_lpref[ta];
-    const int64_t nl = w.tile_lpref[tb] + w.tile_left[tb] - lstart;
-    C.start[2 * j] = lstart;
-    C.start[2 * j + 1] = a.n + (s_seq_pref[j] - lstart);
-    C.cnt[2 * j] = nl;
-    C.cnt[2 * j + 1] = cnt_j - nl;
-  }
-}
-
-__global__ void __launch_bounds__(PT_THREADS) k_pscatter(const FitArgs a, const int d, const PartWs w) {
-  __shared__ int s_tile_pref[MAX_PIECES + 1];
-  __shared__ int64_t s_seq_pref[MAX_PIECES + 1];
-  __shared__ int s_w[PT_THREADS / 32];
-  __shared__ int64_t s_w64[PT_THREADS / 32];
-  __shared__ uint32_t s_r[PT_HALF], s_g[PT_HALF];
-  const int NP = 1 << (d - 1);
-  const LevelView& P = a.lv[d - 1];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  parent_prefixes(a, d, s_tile_pref, s_seq_pref, s_w, s_w64);
-  for (int t = blockIdx.x; t < s_tile_pref[NP]; t += gridDim.x) {
-  const int j = parent_of_tile(s_tile_pref, NP, t);
-  const int64_t cnt_j = (d == 1) ? a.n : P.cnt[j];
-  const int64_t start_j = (d == 1) ? 0 : P.start[j];
-  const int64_t o = (int64_t)(t - s_tile_pref[j]) * PT_TILE;
-  const int len = (int)min((int64_t)PT_TILE, cnt_j - o);
-  const uint32_t* rin = (d >= 2) ? a.sr[(d - 1) & 1] + start_j + o : nullptr;
-  const uint32_t* gin = (d >= 2) ? a.sg[(d - 1) & 1] + start_j + o : a.gp_root + o;
-  int64_t lp = w.tile_lpref[t];
-  int64_t rbase = a.n + (s_seq_pref[j] + o - lp);   // global right prefix at the tile start
-  uint32_t* rout = a.sr[d & 1];
-  uint32_t* gout = a.sg[d & 1];
-  // the 4096-row tile in two 2048-row halves (8 rows per thread: low register pressure)
-  for (int hb = 0; hb < len; hb += PT_HALF) {
-  const int hlen = min(PT_HALF, len - hb);
-  // stage the half (coalesced)
-#pragma unroll
-  for (int q = 0; q < PT_HALF / PT_THREADS; ++q) {
-    const int k = q * PT_THREADS + tid;
-    if (k < hlen) {
-      s_r[k] = (d == 1) ? (uint32_t)(o + hb + k) : rin[hb + k];
-      s_g[k] = gin[hb + k];
-    }
-  }
-  // blocked: thread tid owns rows hb + tid*8 .. +7 = byte (tid & 3) of bitmask word hb/32 + tid/4
-  const uint32_t word = w.bits[(size_t)t * PT_WORDS + (hb >> 5) + (tid >> 2)];
-  uint32_t lbits = (word >> ((tid & 3) * 8)) & 0xffu;
-  const int first = tid * PT_HI;
-  if (first + PT_HI > hlen) lbits &= first >= hlen ? 0u : ((1u << (hlen - first)) - 1u);
-  const int cnt = __popc(lbits);
-  int inc = cnt;
-  for (int off = 1; off < 32; off <<= 1) {
-    const int u = __shfl_up_sync(0xffffffffu, inc, off);
-    if (lane >= off) inc += u;
-  }
-  if (lane == 31) s_w[warp] = inc;
-  __syncthreads();
-  int woff = 0, L = 0;
-  for (int w2 = 0; w2 < PT_THREADS / 32; ++w2) {
-    if (w2 < warp) woff += s_w[w2];
-    L += s_w[w2];
-  }
-  const int my_excl = woff + inc - cnt;
-  uint32_t rr[PT_HI], gg[PT_HI];
-#pragma unroll
-  for (int q = 0; q < PT_HI; ++q) {
-    const int k = first + q;
-    rr[q] = k < hlen ? s_r[k] : 0u;
-    gg[q] = k < hlen ? s_g[k] : 0u;
-  }
-  __syncthreads();
-  int lpos = my_excl, rpos = L + first - my_excl;
-#pragma unroll
-  for (int q = 0; q < PT_HI; ++q) {
-    if (first + q < hlen) {
-      const int dst = ((lbits >> q) & 1u) ? lpos++ : rpos++;
-      s_r[dst] = rr[q];
-      s_g[dst] = gg[q];
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < PT_HALF / PT_THREADS; ++q) {
-    const int k = q * PT_THREADS + tid;
-    if (k < hlen) {
-      const int64_t dst = k < L ? lp + k : rbase + (k - L);
-      rout[dst] = s_r[k];
-      gout[dst] = s_g[k];
-    }
-  }
-  lp += L;
-  rbase += hlen - L;
-  __syncthreads();
-  }
-  }
-}
 // ---------------------------------------------------------------------------------------------
 // Warp-aggregated stable scatter (replaces a shared-memory reorder): in a tile, rows are ordered
 // (q, warp, lane) with row = q*256 + warp*32 + lane, and k_pcount stored exactly the ballot of each
@@ -818,13 +756,71 @@ __global__ void __launch_bounds__(PT_THREADS) k_pscatter2(const FitArgs a, const
   __shared__ int64_t s_seq_pref[MAX_PIECES + 1];
   __shared__ int s_w[PT_THREADS / 32];
   __shared__ int64_t s_w64[PT_THREADS / 32];
+  __shared__ int64_t s_own[PT_OWN];                       // global left prefix of this CTA's tiles
+  __shared__ int64_t s_ls[MAX_PIECES], s_le[MAX_PIECES];  // CTA 0: left prefix at parent start / end
   const int NP = 1 << (d - 1);
   const LevelView& P = a.lv[d - 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   parent_prefixes(a, d, s_tile_pref, s_seq_pref, s_w, s_w64);
+  // ---- exclusive scan of the tile left counts (k_pcount), contiguous chunk per thread; the
+  // common case (<= 16 tiles per thread, <= 4096 tiles) keeps the chunk in registers
+  {
+    const int T = s_tile_pref[NP];
+    const int c0 = (int)((int64_t)T * tid / PT_THREADS), c1 = (int)((int64_t)T * (tid + 1) / PT_THREADS);
+    int v[16];
+    int64_t local = 0;
+    for (int b0 = c0; b0 < c1; b0 += 16) {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = (b0 + q < c1) ? w.tile_left[b0 + q] : 0;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) local += v[q];
+    }
+    int64_t inc = local;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t u = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += u;
+    }
+    __syncthreads();   // s_w64 was used by parent_prefixes
+    if (lane == 31) s_w64[warp] = inc;
+    __syncthreads();
+    int64_t run = inc - local;
+    for (int w2 = 0; w2 < warp; ++w2) run += s_w64[w2];
+    const int G = gridDim.x, bid = blockIdx.x;
+    for (int b0 = c0; b0 < c1; b0 += 16) {
+      if (c1 - c0 > 16) {   // rare: reload this round of the chunk
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = (b0 + q < c1) ? w.tile_left[b0 + q] : 0;
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int t = b0 + q;
+        if (t < c1) {
+          if (t % G == bid) s_own[t / G] = run;
+          if (bid == 0) {
+            const int j = parent_of_tile(s_tile_pref, NP, t);
+            if (t == s_tile_pref[j]) s_ls[j] = run;
+            if (t == s_tile_pref[j + 1] - 1) s_le[j] = run + v[q];
+          }
+          run += v[q];
+        }
+      }
+    }
+    __syncthreads();
+    if (bid == 0) {   // child segments: lefts in region A at the parent's left prefix, rights in B
+      const LevelView& C = a.lv[d];
+      for (int j = tid; j < NP; j += PT_THREADS) {
+        if (P.split_f[j] < 0) continue;
+        const int64_t cnt_j = (d == 1) ? a.n : P.cnt[j];
+        const int64_t nl = s_le[j] - s_ls[j];
+        C.start[2 * j] = s_ls[j];
+        C.start[2 * j + 1] = a.n + (s_seq_pref[j] - s_ls[j]);
+        C.cnt[2 * j] = nl;
+        C.cnt[2 * j + 1] = cnt_j - nl;
+      }
+    }
+  }
   const uint32_t lt = (1u << lane) - 1u;
   uint32_t* rout = a.sr[d & 1];
-  uint32_t* gout = a.sg[d & 1];
   for (int t = blockIdx.x; t < s_tile_pref[NP]; t += gridDim.x) {
     const int j = parent_of_tile(s_tile_pref, NP, t);
     const int64_t cnt_j = (d == 1) ? a.n : P.cnt[j];
@@ -832,7 +828,6 @@ __global__ void __launch_bounds__(PT_THREADS) k_pscatter2(const FitArgs a, const
     const int64_t o = (int64_t)(t - s_tile_pref[j]) * PT_TILE;
     const int len = (int)min((int64_t)PT_TILE, cnt_j - o);
     const uint32_t* rin = (d >= 2) ? a.sr[(d - 1) & 1] + start_j + o : nullptr;
-    const uint32_t* gin = (d >= 2) ? a.sg[(d - 1) & 1] + start_j + o : a.gp_root + o;
     const uint32_t* bw = w.bits + (size_t)t * PT_WORDS;
     // exclusive left prefix of every (q, warp) group: lane L holds words 4L .. 4L+3
     const uint4 mw = *reinterpret_cast<const uint4*>(bw + 4 * lane);
@@ -844,17 +839,16 @@ __global__ void __launch_bounds__(PT_THREADS) k_pscatter2(const FitArgs a, const
       if (lane >= off) inc += u;
     }
     const int ex = inc - lsum;                       // prefix before word 4*lane
-    const int64_t lp = w.tile_lpref[t];
+    const int64_t lp = s_own[t / gridDim.x];
     const int64_t rbase = a.n + (s_seq_pref[j] + o - lp);   // global right prefix at the tile start
     // loads of 8 rows first (independent), then their stores; two rounds per tile
 #pragma unroll 1
     for (int q0 = 0; q0 < PT_ITEMS; q0 += 8) {
-    uint32_t rv[8], gv[8];
+    uint32_t rv[8];
 #pragma unroll
     for (int qq = 0; qq < 8; ++qq) {
       const int k = (q0 + qq) * PT_THREADS + warp * 32 + lane;
       rv[qq] = (k < len) ? ((d == 1) ? (uint32_t)(o + k) : rin[k]) : 0u;
-      gv[qq] = (k < len) ? gin[k] : 0u;
     }
 #pragma unroll
     for (int qq = 0; qq < 8; ++qq) {
@@ -873,7 +867,6 @@ __global__ void __launch_bounds__(PT_THREADS) k_pscatter2(const FitArgs a, const
         const int rank = __popc(m & lt);
         const int64_t dst = left ? lp + pre + rank : rbase + (k - lane - pre) + (lane - rank);
         rout[dst] = rv[qq];
-        gout[dst] = gv[qq];
       }
     }
     }
@@ -1101,416 +1094,6 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitArgs a, cons
   }
 }
 
-// ---------------------------------------------------------------------------------------------
-// split evaluation, one CTA of 1024 threads per node of level d: warp f owns feature f, lane l
-// owns bins 8l .. 8l+7.  The warp forms its feature's histogram (sibling = parent - built, exact
-// int64, written back for the next level), prefix-scans it (8 local + warp shuffle scan), evaluates
-// every threshold in fp64 (monotone veto on users) and reduces (loss desc, b asc); warp 0 then
-// picks the node's best over features (loss desc, f asc, b asc) and writes the tree.  Node totals
-// come from each warp's own feature (every feature's histogram sums to them).
-constexpr int SP2_THREADS = 1024;
-__global__ void __launch_bounds__(SP2_THREADS) k_split2(const FitArgs a, const int d) {
-  const int t = *a.d_tree;
-  int32_t* const tfeat = a.tfeat + (size_t)t * a.nn;
-  int32_t* const tbin = a.tbin + (size_t)t * a.nn;
-  float* const tthr = a.tthr + (size_t)t * a.nn;
-  float* const tval = a.tval + (size_t)t * a.nn;
-  const int k = blockIdx.x;
-  const int tid = threadIdx.x, lane = tid & 31, f = tid >> 5;
-  const LevelView& V = a.lv[d];
-  __shared__ double s_loss[32];
-  __shared__ int s_b[32];
-  __shared__ int64_t s_GL[32], s_HL[32];
-  __shared__ int64_t s_G, s_H;
-  int64_t* Hself;
-  int64_t g8[8], h8[8];
-  if (d == 0) {
-    Hself = a.H[0];
-  } else {
-    const int j = k >> 1;
-    if (a.lv[d - 1].split_f[j] < 0) {
-      if (tid == 0) V.split_f[k] = -1;
-      return;
-    }
-    const int side = V.built[j];
-    const bool is_built = (k & 1) == side;
-    Hself = a.H[d & 1] + (size_t)(is_built ? j : (1 << (d - 1)) + j) * SLOT;
-    if (!is_built) {
-      const longlong2* Hp = reinterpret_cast<const longlong2*>(a.H[(d - 1) & 1] + (size_t)node_slot(a, d - 1, j) * SLOT);
-      const longlong2* Hb = reinterpret_cast<const longlong2*>(a.H[d & 1] + (size_t)j * SLOT);
-      longlong2* Hs = reinterpret_cast<longlong2*>(Hself);
-      const int eg0 = (f * kBins + lane * 8) / 2, eh0 = (kHistBins + f * kBins + lane * 8) / 2;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const longlong2 pg = Hp[eg0 + q], bg = Hb[eg0 + q], ph = Hp[eh0 + q], bh = Hb[eh0 + q];
-        g8[2 * q] = pg.x - bg.x;
-        g8[2 * q + 1] = pg.y - bg.y;
-        h8[2 * q] = ph.x - bh.x;
-        h8[2 * q + 1] = ph.y - bh.y;
-        Hs[eg0 + q] = make_longlong2(g8[2 * q], g8[2 * q + 1]);
-        Hs[eh0 + q] = make_longlong2(h8[2 * q], h8[2 * q + 1]);
-      }
-    }
-  }
-  if (d == 0 || (k & 1) == a.lv[d].built[k >> 1]) {
-    const longlong2* G2 = reinterpret_cast<const longlong2*>(Hself + f * kBins + lane * 8);
-    const longlong2* H2 = reinterpret_cast<const longlong2*>(Hself + kHistBins + f * kBins + lane * 8);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const longlong2 gv = G2[q], hv = H2[q];
-      g8[2 * q] = gv.x;
-      g8[2 * q + 1] = gv.y;
-      h8[2 * q] = hv.x;
-      h8[2 * q + 1] = hv.y;
-    }
-  }
-  // local inclusive prefix over the lane's 8 bins, then warp exclusive scan of lane totals
-#pragma unroll
-  for (int q = 1; q < 8; ++q) {
-    g8[q] += g8[q - 1];
-    h8[q] += h8[q - 1];
-  }
-  int64_t ig = g8[7], ih = h8[7];
-  for (int o = 1; o < 32; o <<= 1) {
-    const int64_t ug = __shfl_up_sync(0xffffffffu, ig, o), uh = __shfl_up_sync(0xffffffffu, ih, o);
-    if (lane >= o) {
-      ig += ug;
-      ih += uh;
-    }
-  }
-  const int64_t bg = ig - g8[7], bh = ih - h8[7];
-  const int64_t Gq = __shfl_sync(0xffffffffu, ig, 31), Hq = __shfl_sync(0xffffffffu, ih, 31);
-  // column sample of tree t (R21)
-  bool fin = f < a.F;
-  if (fin && a.colsample < 1.0f) {
-    const int F = a.F;
-    int nkeep = (int)ceil((double)a.colsample * (double)F);
-    if (nkeep < 1) nkeep = 1;
-    const uint64_t kf = rng4(a.seed, (uint64_t)(2 * a.target + 1), (uint64_t)t, (uint64_t)f);
-    const uint64_t kl = lane < F ? rng4(a.seed, (uint64_t)(2 * a.target + 1), (uint64_t)t, (uint64_t)lane) : ~0ull;
-    const unsigned less = __ballot_sync(0xffffffffu, lane < F && (kl < kf || (kl == kf && lane < f)));
-    fin = __popc(less) < nkeep;
-  }
-  const int eg = exp_of(__uint_as_float(a.maxg[t])), eh = exp_of(__uint_as_float(a.maxh[t]));
-  const double sgi = exp2i(eg - a.K), shi = exp2i(eh - a.K);
-  const double lo = (d == 0) ? -INFINITY : V.lo[k], hi = (d == 0) ? INFINITY : V.hi[k];
-  const double lambda = a.lambda, mcw = a.mcw;
-  const double G = dequant(Gq, sgi), H = dequant(Hq, shi);
-  const double wP = calc_weight(G, H, lo, hi, lambda, mcw);
-  const double gainP = calc_gain(G, H, wP, lambda);
-  double bl = -INFINITY;
-  int bb = 0x7fffffff;
-  int64_t bGL = 0, bHL = 0;
-  if (fin) {
-    const int nthr = a.ncuts[f];   // thresholds b = 0 .. nbins_f - 2
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int b = lane * 8 + q;
-      if (b < nthr) {
-        const int64_t GLq = bg + g8[q], HLq = bh + h8[q];
-        const double GL = dequant(GLq, sgi), HL = dequant(HLq, shi);
-        const double GR = dequant(Gq - GLq, sgi), HR = dequant(Hq - HLq, shi);
-        if (HL >= mcw && HR >= mcw) {
-          const double wl = calc_weight(GL, HL, lo, hi, lambda, mcw);
-          const double wr = calc_weight(GR, HR, lo, hi, lambda, mcw);
-          if (!(a.monotone && f == a.users_col && wl > wr)) {
-            const double loss =
-                __dsub_rn(__dadd_rn(calc_gain(GL, HL, wl, lambda), calc_gain(GR, HR, wr, lambda)), gainP);
-            if (loss > bl) {   // b ascending within the lane: strict keeps the smaller b
-              bl = loss;
-              bb = b;
-              bGL = GLq;
-              bHL = HLq;
-            }
-          }
-        }
-      }
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ol = __shfl_down_sync(0xffffffffu, bl, o);
-    const int ob = __shfl_down_sync(0xffffffffu, bb, o);
-    const int64_t oG = __shfl_down_sync(0xffffffffu, bGL, o), oH = __shfl_down_sync(0xffffffffu, bHL, o);
-    if (ol > bl || (ol == bl && ob < bb)) {
-      bl = ol;
-      bb = ob;
-      bGL = oG;
-      bHL = oH;
-    }
-  }
-  if (lane == 0) {
-    s_loss[f] = bl;
-    s_b[f] = bb;
-    s_GL[f] = bGL;
-    s_HL[f] = bHL;
-    if (f == 0) {
-      s_G = Gq;
-      s_H = Hq;
-    }
-  }
-  __syncthreads();
-  if (f != 0) return;
-  double ml = s_loss[lane];
-  int mf = lane, mb = s_b[lane];
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ol = __shfl_down_sync(0xffffffffu, ml, o);
-    const int of = __shfl_down_sync(0xffffffffu, mf, o), ob = __shfl_down_sync(0xffffffffu, mb, o);
-    // total order: loss desc, then f asc, then b asc
-    if (ol > ml || (ol == ml && (of < mf || (of == mf && ob < mb)))) {
-      ml = ol;
-      mf = of;
-      mb = ob;
-    }
-  }
-  if (lane != 0) return;
-  const int64_t GqN = s_G, HqN = s_H;
-  const int gk = (1 << d) - 1 + k;
-  if (ml > 1e-6) {
-    const int fs = mf, bs = mb;
-    const int64_t GLs = s_GL[fs], HLs = s_HL[fs];
-    const double GL = dequant(GLs, sgi), HL = dequant(HLs, shi);
-    const double GR = dequant(GqN - GLs, sgi), HR = dequant(HqN - HLs, shi);
-    const double wl = calc_weight(GL, HL, lo, hi, lambda, mcw);
-    const double wr = calc_weight(GR, HR, lo, hi, lambda, mcw);
-    double loL = lo, hiL = hi, loR = lo, hiR = hi;
-    if (a.monotone && fs == a.users_col) {
-      const double mid = __dmul_rn(__dadd_rn(wl, wr), 0.5);
-      hiL = mid;
-      loR = mid;
-    }
-    V.split_f[k] = fs;
-    V.split_b[k] = bs;
-    tfeat[gk] = fs;
-    tbin[gk] = bs;
-    tthr[gk] = a.cuts[fs * (kBins - 1) + bs];
-    tval[gk] = 0.0f;
-    if (d + 1 < a.D) {
-      const LevelView& N = a.lv[d + 1];
-      N.lo[2 * k] = loL;
-      N.hi[2 * k] = hiL;
-      N.lo[2 * k + 1] = loR;
-      N.hi[2 * k + 1] = hiR;
-    } else {
-      // children at max depth are leaves: v = (float)(eta * W(G, H, lo, hi))
-      tfeat[2 * gk + 1] = -1;
-      tval[2 * gk + 1] = (float)__dmul_rn(a.eta, calc_weight(GL, HL, loL, hiL, lambda, mcw));
-      tfeat[2 * gk + 2] = -1;
-      tval[2 * gk + 2] = (float)__dmul_rn(a.eta, calc_weight(GR, HR, loR, hiR, lambda, mcw));
-    }
-  } else {
-    V.split_f[k] = -1;
-    tfeat[gk] = -1;
-    tval[gk] = (float)__dmul_rn(a.eta, wP);
-  }
-}
-
-// ---------------------------------------------------------------------------------------------
-// split evaluation: one CTA per (node of level d, feature), one bin per thread.  Each CTA forms
-// its feature's histogram (sibling = parent - built, exact int64, written back for the next
-// level), block-scans it, evaluates every threshold in fp64 (monotone veto on users) and
-// publishes its best (loss, b, GL, HL); the last CTA of the node (ticket counter) picks the
-// node's best over features with the (loss desc, f asc, b asc) total order and writes the tree.
-__device__ __forceinline__ bool better_fb(double la, int fa, int ba, double lb, int fb, int bb) {
-  if (la != lb) return la > lb;
-  if (fa != fb) return fa < fb;
-  return ba < bb;
-}
-
-__global__ void __launch_bounds__(SPLIT_THREADS) k_split(const FitArgs a, const int d) {
-  const int t = *a.d_tree;   // device-side tree index (the tree's kernels are replayed from a CUDA graph)
-  int32_t* const tfeat = a.tfeat + (size_t)t * a.nn;
-  int32_t* const tbin = a.tbin + (size_t)t * a.nn;
-  float* const tthr = a.tthr + (size_t)t * a.nn;
-  float* const tval = a.tval + (size_t)t * a.nn;
-  const int k = blockIdx.x >> 5, f = blockIdx.x & 31;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const LevelView& V = a.lv[d];
-  int64_t* Hself;
-  int64_t g, h;
-  if (d == 0) {
-    Hself = a.H[0];
-    g = Hself[f * kBins + tid];
-    h = Hself[kHistBins + f * kBins + tid];
-  } else {
-    const int j = k >> 1;
-    if (a.lv[d - 1].split_f[j] < 0) {
-      if (f == 0 && tid == 0) V.split_f[k] = -1;
-      return;
-    }
-    const int side = V.built[j];
-    const bool is_built = (k & 1) == side;
-    Hself = a.H[d & 1] + (size_t)(is_built ? j : (1 << (d - 1)) + j) * SLOT;
-    if (is_built) {
-      g = Hself[f * kBins + tid];
-      h = Hself[kHistBins + f * kBins + tid];
-    } else {
-      const int64_t* Hp = a.H[(d - 1) & 1] + (size_t)node_slot(a, d - 1, j) * SLOT;
-      const int64_t* Hb = a.H[d & 1] + (size_t)j * SLOT;
-      g = Hp[f * kBins + tid] - Hb[f * kBins + tid];
-      h = Hp[kHistBins + f * kBins + tid] - Hb[kHistBins + f * kBins + tid];
-      Hself[f * kBins + tid] = g;
-      Hself[kHistBins + f * kBins + tid] = h;
-    }
-  }
-  // block inclusive scan of (g, h) over the 256 bins
-  __shared__ int64_t s_wg[SPLIT_THREADS / 32], s_wh[SPLIT_THREADS / 32];
-  __shared__ double s_bl[SPLIT_THREADS / 32];
-  __shared__ int s_bb[SPLIT_THREADS / 32];
-  __shared__ int s_last;
-  int64_t ig = g, ih = h;
-  for (int o = 1; o < 32; o <<= 1) {
-    const int64_t ug = __shfl_up_sync(0xffffffffu, ig, o), uh = __shfl_up_sync(0xffffffffu, ih, o);
-    if (lane >= o) {
-      ig += ug;
-      ih += uh;
-    }
-  }
-  if (lane == 31) {
-    s_wg[warp] = ig;
-    s_wh[warp] = ih;
-  }
-  __syncthreads();
-  int64_t og = 0, oh = 0, Gq = 0, Hq = 0;
-  for (int w2 = 0; w2 < SPLIT_THREADS / 32; ++w2) {
-    if (w2 < warp) {
-      og += s_wg[w2];
-      oh += s_wh[w2];
-    }
-    Gq += s_wg[w2];
-    Hq += s_wh[w2];
-  }
-  const int64_t GLq = og + ig, HLq = oh + ih;   // left = bins 0..tid
-  // column sample of tree t (R21): rank of f among the F keys
-  bool fin = f < a.F;
-  if (fin && a.colsample < 1.0f) {
-    const int F = a.F;
-    int nkeep = (int)ceil((double)a.colsample * (double)F);
-    if (nkeep < 1) nkeep = 1;
-    const uint64_t kf = rng4(a.seed, (uint64_t)(2 * a.target + 1), (uint64_t)t, (uint64_t)f);
-    const uint64_t kl = lane < F ? rng4(a.seed, (uint64_t)(2 * a.target + 1), (uint64_t)t, (uint64_t)lane) : ~0ull;
-    const unsigned less = __ballot_sync(0xffffffffu, lane < F && (kl < kf || (kl == kf && lane < f)));
-    fin = __popc(less) < nkeep;
-  }
-  const int eg = exp_of(__uint_as_float(a.maxg[t])), eh = exp_of(__uint_as_float(a.maxh[t]));
-  const double sgi = exp2i(eg - a.K), shi = exp2i(eh - a.K);
-  const double lo = (d == 0) ? -INFINITY : V.lo[k], hi = (d == 0) ? INFINITY : V.hi[k];
-  const double lambda = a.lambda, mcw = a.mcw;
-  double loss = -INFINITY;
-  if (fin && tid <= a.ncuts[f] - 1) {   // thresholds b = 0 .. nbins_f - 2
-    const double G = dequant(Gq, sgi), H = dequant(Hq, shi);
-    const double wP = calc_weight(G, H, lo, hi, lambda, mcw);
-    const double gainP = calc_gain(G, H, wP, lambda);
-    const double GL = dequant(GLq, sgi), HL = dequant(HLq, shi);
-    const double GR = dequant(Gq - GLq, sgi), HR = dequant(Hq - HLq, shi);
-    if (HL >= mcw && HR >= mcw) {
-      const double wl = calc_weight(GL, HL, lo, hi, lambda, mcw);
-      const double wr = calc_weight(GR, HR, lo, hi, lambda, mcw);
-      if (!(a.monotone && f == a.users_col && wl > wr))
-        loss = __dsub_rn(__dadd_rn(calc_gain(GL, HL, wl, lambda), calc_gain(GR, HR, wr, lambda)), gainP);
-    }
-  }
-  // block argmax over b (loss desc, b asc)
-  double bl = loss;
-  int bb = tid;
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ol = __shfl_down_sync(0xffffffffu, bl, o);
-    const int ob = __shfl_down_sync(0xffffffffu, bb, o);
-    if (better_fb(ol, f, ob, bl, f, bb)) {
-      bl = ol;
-      bb = ob;
-    }
-  }
-  if (lane == 0) {
-    s_bl[warp] = bl;
-    s_bb[warp] = bb;
-  }
-  __syncthreads();
-  FeatBest* fb = a.fbest + (size_t)k * 32;
-  if (tid == 0) {
-    for (int w2 = 1; w2 < SPLIT_THREADS / 32; ++w2)
-      if (better_fb(s_bl[w2], f, s_bb[w2], bl, f, bb)) {
-        bl = s_bl[w2];
-        bb = s_bb[w2];
-      }
-    s_bb[0] = bb;
-  }
-  __syncthreads();
-  // the winning thread publishes its prefix sums (it holds GL, HL of threshold bb)
-  if (tid == s_bb[0]) {
-    FeatBest r;
-    r.loss = bl;
-    r.b = bb;
-    r.valid = (bl > -INFINITY) ? 1 : 0;
-    r.GLq = GLq;
-    r.HLq = HLq;
-    r.Gq = Gq;
-    r.Hq = Hq;
-    fb[f] = r;
-    __threadfence();
-    const int done = atomicAdd(&V.done[k], 1);
-    s_last = (done == 31);
-  }
-  __syncthreads();
-  if (!s_last) return;
-  // ---- last CTA of the node: best over the 32 features, then the tree update
-  __threadfence();
-  if (warp != 0) return;
-  const volatile FeatBest* vfb = fb;
-  double ml = vfb[lane].valid ? vfb[lane].loss : -INFINITY;
-  int mf = lane, mb = vfb[lane].b;
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ol = __shfl_down_sync(0xffffffffu, ml, o);
-    const int of = __shfl_down_sync(0xffffffffu, mf, o), ob = __shfl_down_sync(0xffffffffu, mb, o);
-    if (better_fb(ol, of, ob, ml, mf, mb)) {
-      ml = ol;
-      mf = of;
-      mb = ob;
-    }
-  }
-  if (lane != 0) return;
-  V.done[k] = 0;
-  const int64_t GqN = vfb[0].Gq, HqN = vfb[0].Hq;
-  const double G = dequant(GqN, sgi), H = dequant(HqN, shi);
-  const double wP = calc_weight(G, H, lo, hi, lambda, mcw);
-  const int gk = (1 << d) - 1 + k;
-  if (ml > 1e-6) {
-    const int fs = mf, bs = mb;
-    const int64_t GLs = vfb[fs].GLq, HLs = vfb[fs].HLq;
-    const double GL = dequant(GLs, sgi), HL = dequant(HLs, shi);
-    const double GR = dequant(GqN - GLs, sgi), HR = dequant(HqN - HLs, shi);
-    const double wl = calc_weight(GL, HL, lo, hi, lambda, mcw);
-    const double wr = calc_weight(GR, HR, lo, hi, lambda, mcw);
-    double loL = lo, hiL = hi, loR = lo, hiR = hi;
-    if (a.monotone && fs == a.users_col) {
-      const double mid = __dmul_rn(__dadd_rn(wl, wr), 0.5);
-      hiL = mid;
-      loR = mid;
-    }
-    V.split_f[k] = fs;
-    V.split_b[k] = bs;
-    tfeat[gk] = fs;
-    tbin[gk] = bs;
-    tthr[gk] = a.cuts[fs * (kBins - 1) + bs];
-    tval[gk] = 0.0f;
-    if (d + 1 < a.D) {
-      const LevelView& N = a.lv[d + 1];
-      N.lo[2 * k] = loL;
-      N.hi[2 * k] = hiL;
-      N.lo[2 * k + 1] = loR;
-      N.hi[2 * k + 1] = hiR;
-    } else {
-      // children at max depth are leaves: v = (float)(eta * W(G, H, lo, hi))
-      tfeat[2 * gk + 1] = -1;
-      tval[2 * gk + 1] = (float)__dmul_rn(a.eta, calc_weight(GL, HL, loL, hiL, lambda, mcw));
-      tfeat[2 * gk + 2] = -1;
-      tval[2 * gk + 2] = (float)__dmul_rn(a.eta, calc_weight(GR, HR, loR, hiR, lambda, mcw));
-    }
-  } else {
-    V.split_f[k] = -1;
-    tfeat[gk] = -1;
-    tval[gk] = (float)__dmul_rn(a.eta, wP);
-  }
-}
 // ---------------------------------------------------------------------------------------------
 // leaf routing + prediction update + next tree's gradient maxima
 constexpr int UPD_THREADS = 256;
@@ -1858,10 +1441,17 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   const int64_t max_tiles = (n + PT_TILE - 1) / PT_TILE + half_max + 1;
   const size_t tab_bytes = lvl_nodes * (8 /*start*/ + 8 /*cnt*/ + 8 /*gcnt*/ + 8 + 8 /*lo,hi*/ + 4 + 4 /*split*/ +
                                         4 /*built*/ + 4 /*done*/);
+  // root histogram variant: run-length lane-per-feature (default) or the hybrid run/row-parallel
+  // kernel (LLMP_ROOT2=1; faster on random codes, slower on paper-ordered rows).  The default
+  // fuses each tree's update with the next tree's root histogram (LLMP_NOFUSE=1 disables).
+  static const bool use_root2 = getenv("LLMP_ROOT2") && atoi(getenv("LLMP_ROOT2")) != 0;
+  static const bool fused = !use_root2 && !(getenv("LLMP_NOFUSE") && atoi(getenv("LLMP_NOFUSE")) != 0);
   FitArgs A[2];
   PartWs PW[2];
   for (int tg = 0; tg < 2; ++tg) {
-    const std::string sx = (concurrent && tg == 1) ? "_1" : "_0";
+    // per-target workspaces: the fused update pass leaves the next tree's root histogram and
+    // packed pairs in them, so the two ensembles never share one (also when they run in sequence)
+    const std::string sx = (tg == 1) ? "_1" : "_0";
     FitArgs& a = A[tg];
     a = FitArgs{};
     a.n = n;
@@ -1881,8 +1471,6 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     a.gp_root = ctx->workspace("gp_root" + sx, (size_t)n * 4).as<uint32_t>();
     a.sr[0] = ctx->workspace("ridx0" + sx, (size_t)n * 2 * 4).as<uint32_t>();
     a.sr[1] = ctx->workspace("ridx1" + sx, (size_t)n * 2 * 4).as<uint32_t>();
-    a.sg[0] = ctx->workspace("gp0" + sx, (size_t)n * 2 * 4).as<uint32_t>();
-    a.sg[1] = ctx->workspace("gp1" + sx, (size_t)n * 2 * 4).as<uint32_t>();
     a.H[0] = ctx->workspace("hist0" + sx, (size_t)half_max * SLOT * 8).as<int64_t>();
     a.H[1] = ctx->workspace("hist1" + sx, (size_t)half_max * SLOT * 8).as<int64_t>();
     a.cuts = out.cuts.d_cuts.as<float>();
@@ -1894,6 +1482,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     a.colsample = hp.colsample_bytree;
     a.seed = hp.seed;
     a.monotone = hp.monotone_users;
+    a.fused_root = fused ? 1 : 0;
     a.nn = nn;
     a.units = ctx->d_units;
     a.fbest = reinterpret_cast<FeatBest*>(ctx->workspace("featbest" + sx, (size_t)half_max * 32 * 48).p);
@@ -1931,7 +1520,6 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     }
     LLMP_CUDA(cudaMemsetAsync(d_tab.p, 0, d_tab.bytes, s));
     PW[tg].tile_left = ctx->workspace("tile_left" + sx, (size_t)max_tiles * 4).as<int32_t>();
-    PW[tg].tile_lpref = ctx->workspace("tile_lpref" + sx, (size_t)max_tiles * 8).as<int64_t>();
     PW[tg].bits = ctx->workspace("tile_bits" + sx, (size_t)max_tiles * PT_WORDS * 4).as<uint32_t>();
   }
 
@@ -1943,13 +1531,12 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     LLMP_CUDA(cudaFuncSetAttribute(k_hist_root2, cudaFuncAttributeMaxDynamicSharedMemorySize, R2_SMEM));
     LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_ROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
     LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_LEVEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
+    LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_UPDROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   HIST_SMEM + UPDROOT_TREE_SMEM));
     LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
     attr_set = true;
   }
   const DbgArgs nodbg{};
-  // root histogram variant: run-length lane-per-feature (default) or the hybrid run/row-parallel
-  // kernel (LLMP_ROOT2=1; faster on random codes, slower on paper-ordered rows)
-  static const bool use_root2 = getenv("LLMP_ROOT2") && atoi(getenv("LLMP_ROOT2")) != 0;
 
   // ---- base scores (O3) and tree 0's gradient maxima
   for (int tg = 0; tg < 2; ++tg) {
@@ -1972,16 +1559,19 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   // graph and replayed T times (plain launches when timing instrumentation is on)
   auto tree = [&](const FitArgs& a, const PartWs& pw) {
     const cudaStream_t st = ctx->stream;
-    LLMP_CUDA(cudaMemsetAsync(a.H[0], 0, (size_t)SLOT * 8, st));
+    // fused: the previous round's update pass built this root already unless root_needed
+    if (fused) LLMP_LAUNCH(ctx, KC_MISC, 0, k_root_fix, 1, 1024, 0, a);
+    else LLMP_CUDA(cudaMemsetAsync(a.H[0], 0, (size_t)SLOT * 8, st));
     if (use_root2) LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist_root2, hist_grid, R2_THREADS, R2_SMEM, a);
     else LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist<HM_ROOT>, hist_grid, HIST_THREADS, HIST_SMEM, a, 0, 0, nodbg);
     allreduce_sum_i64(ctx, a.H[0], SLOT);
     LLMP_LAUNCH(ctx, KC_SPLIT, 1, k_split3, 32 / SP3_WARPS, SP3_WARPS * 32, 0, a, 0);
     for (int d = 1; d < D; ++d) {
       const int tiles_d = (int)((n + PT_TILE - 1) / PT_TILE) + (1 << (d - 1));
-      LLMP_LAUNCH(ctx, KC_PARTITION, n, k_pcount, std::min(tiles_d, 5 * ctx->sms), PT_THREADS, 0, a, d, pw);
-      LLMP_LAUNCH(ctx, KC_PARTITION, 0, k_pscan, 1, PS_THREADS, 0, a, d, pw);
-      LLMP_LAUNCH(ctx, KC_PARTITION, 0, k_pscatter2, std::min(tiles_d, 5 * ctx->sms), PT_THREADS, 0, a, d, pw);
+      // persistent tile loops; a scatter CTA owns at most PT_OWN tiles
+      const int pgrid = std::max(std::min(tiles_d, 5 * ctx->sms), (tiles_d + PT_OWN - 1) / PT_OWN);
+      LLMP_LAUNCH(ctx, KC_PARTITION, n, k_pcount, pgrid, PT_THREADS, 0, a, d, pw);
+      LLMP_LAUNCH(ctx, KC_PARTITION, 0, k_pscatter2, pgrid, PT_THREADS, 0, a, d, pw);
       if (ctx->nranks > 1) {   // every rank must histogram the same (globally smaller) child
         LLMP_CUDA(cudaMemcpyAsync(a.lv[d].gcnt, a.lv[d].cnt, ((size_t)1 << d) * 8, cudaMemcpyDeviceToDevice, st));
         allreduce_sum_i64(ctx, a.lv[d].gcnt, (size_t)1 << d);
@@ -1990,7 +1580,13 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       allreduce_sum_i64(ctx, a.H[d & 1], (size_t)SLOT << (d - 1));
       LLMP_LAUNCH(ctx, KC_SPLIT, (1 << d), k_split3, (1 << d) * (32 / SP3_WARPS), SP3_WARPS * 32, 0, a, d);
     }
-    LLMP_LAUNCH(ctx, KC_UPDATE, n, k_update, upd_grid, UPD_THREADS, 0, a);
+    if (fused) {   // update tree t + root histogram of tree t+1 (into the now free root slot)
+      LLMP_CUDA(cudaMemsetAsync(a.H[0], 0, (size_t)SLOT * 8, st));
+      LLMP_LAUNCH(ctx, KC_UPDATE, n, k_hist<HM_UPDROOT>, hist_grid, HIST_THREADS, HIST_SMEM + UPDROOT_TREE_SMEM, a, 0,
+                  0, nodbg);
+    } else {
+      LLMP_LAUNCH(ctx, KC_UPDATE, n, k_update, upd_grid, UPD_THREADS, 0, a);
+    }
     // next tree's gradient maxima (past slots are already equal on every rank, future ones 0)
     allreduce_max_u32(ctx, a.maxg, (size_t)2 * (T + 1));
   };

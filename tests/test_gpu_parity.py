@@ -171,6 +171,53 @@ def test_fit_parity_ragged_sizes(lp, ctx, n):
     assert _bits_equal(otp, gm.train_pred(d.n))
 
 
+def test_fit_sequential_mode_and_root_speculation(lp, ctx):
+    """Instrumented mode runs the two ensembles one after the other with plain launches (the
+    NCCL path does too); it must give the oracle's model like the concurrent graph replay.  The
+    fused update pass builds each next root histogram speculatively: the device
+    row counters show both paths taken — speculative roots kept, and rebuilt ones (tree 0 and
+    exponent changes)."""
+    d = synth.make("C2")
+    kw = dict(n_trees=30, max_depth=6)
+    om, otp = oracle.fit(d.X, d.y, _o_hp(**kw), d.users_col, d.llm_id, d.prof_id, d.n_llm, d.n_prof, L1, L2,
+                         return_train_pred=True)
+    for every in (1, 0):
+        ctx.reset_stats()
+        ctx.set_timing(every)
+        try:
+            gm = lp.fit(ctx, d.X, d.y, _g_hp(lp, **kw), d.users_col, d.llm_id, d.prof_id, d.n_llm, d.n_prof, L1, L2)
+            st = ctx.stats()["classes"]
+        finally:
+            ctx.set_timing(0)
+        _assert_same_model(om, gm.export(), "timing every=%d" % every)
+        assert _bits_equal(otp, gm.train_pred(d.n))
+        root_rows = st["hist_root"]["rows"]
+        assert root_rows % d.n == 0
+        # rebuilt roots = tree 0 of each target + every tree whose max|g| exponent differs from the
+        # previous tree's (max h = max w never changes without subsampling)
+        assert root_rows // d.n == 2 + _exponent_changes(om, d), (root_rows // d.n, every)
+
+
+def _exponent_changes(om, d):
+    """Number of trees t >= 1 (both targets) whose gradient-maximum exponent (O4: e with
+    max|g| = m 2^e, m in [0.5, 1)) differs from tree t-1's, from the oracle's model."""
+    w = oracle.weights(d.y, d.llm_id, d.prof_id, d.n_llm, d.n_prof, L1, L2)
+    T = om.feat.shape[1]
+    ch = 0
+    for tg in range(2):
+        p = np.full(d.n, om.base[tg], np.float32)
+        prev = None
+        for t in range(T):
+            g = w * (p - d.y[:, tg])          # float32 throughout, like O4
+            e = int(np.frexp(np.abs(g).max())[1]) if np.abs(g).max() > 0 else 0
+            ch += prev is not None and e != prev
+            prev = e
+            one = oracle.Model(om.F, om.hp, om.cuts, om.ncuts, np.zeros(2, np.float32), om.feat[:, t:t + 1],
+                               om.bin[:, t:t + 1], om.thr[:, t:t + 1], om.val[:, t:t + 1])
+            p = p + oracle.predict(one, d.X)[:, tg]
+    return ch
+
+
 def test_fit_host_and_device_inputs_identical_and_deterministic(lp, ctx):
     d = synth.make("C2")
     hp = lp.hparams(n_trees=10, max_depth=6)
