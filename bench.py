@@ -285,22 +285,30 @@ def main():
     sweep_rows = lf.shape[0] * pf.shape[0] * len(levels)
 
     ev = []
+    host = {"fit": 0.0, "recommend": 0.0, "free": 0.0}   # host wall time per phase (diagnostics)
 
-    def step(X, y, li, pi, lfx, pfx, record=None):
+    def step(X, y, li, pi, lfx, pfx, record=None, hacc=None):
         if record is not None:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e2 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
+        h0 = time.perf_counter()
         m = lp.fit(ctx, X, y, hp, d.users_col, li, pi, d.n_llm, d.n_prof, L1, L2, row_offset=d.row_offset,
                    n_global=n_global)
+        h1 = time.perf_counter()
         if record is not None:
             e1.record(stream)
         recs = lp.recommend(ctx, m, lfx, pfx, cost, levels, L1, L2, U)
+        h2 = time.perf_counter()
         if record is not None:
             e2.record(stream)
             record.append((e0, e1, e2))
         m.free()
+        if hacc is not None:
+            hacc["fit"] += h1 - h0
+            hacc["recommend"] += h2 - h1
+            hacc["free"] += time.perf_counter() - h2
         return recs
 
     clocks = ClockSampler(local_rank).open()   # before the warm-up: no NVML init in the timed region
@@ -319,7 +327,7 @@ def main():
     clocks.begin()
     t_start.record(stream)
     for _ in range(args.steps):
-        step(Xd, yd, ld, pd, lfd, pfd, record=ev)
+        step(Xd, yd, ld, pd, lfd, pfd, record=ev, hacc=host)
     t_end.record(stream)
     torch.cuda.synchronize()
     clocks.end()
@@ -395,9 +403,10 @@ def main():
             dist.barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        host_e2e = {"fit": 0.0, "recommend": 0.0, "free": 0.0}
         e0.record(stream)
         for _ in range(args.steps):
-            step(Xh, yh, lh, ph, lfh, pfh)
+            step(Xh, yh, lh, ph, lfh, pfh, hacc=host_e2e)
         e1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
@@ -407,7 +416,8 @@ def main():
         h2d = d.X.nbytes + d.y.nbytes + d.llm_id.nbytes + d.prof_id.nbytes + lf.nbytes + pf.nbytes
         d2h = 2 * args.trees * nn * 16 + 8 + lf.shape[0] * 24
         e2e = {"value": row_iters / (e2e_ms.item() / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms.item() / args.steps}
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms.item() / args.steps,
+               "host_ms_per_step": {k: 1000.0 * v / args.steps for k, v in host_e2e.items()}}
 
     # ---- CPU baseline: the oracle as it stands, rank 0, N = 1, bounded sample
     cpu = None
@@ -442,6 +452,7 @@ def main():
             "predict": {"value": predict_rows / (pred_ms / 1000.0), "unit": "rows/s", "rows_per_step": sweep_rows * world,
                         "ms_per_step": pred_ms / args.steps},
             "fit": {"value": row_iters / (fit_ms / 1000.0), "unit": UNIT, "ms_per_step": fit_ms / args.steps},
+            "host_ms_per_step": {k: 1000.0 * v / args.steps for k, v in host.items()},
             "roofline": roofline,
             "kernels": kernels,
             "kernels_note": "per-kernel durations from one extra instrumented step (plain launches, every 8th "

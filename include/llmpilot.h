@@ -132,7 +132,7 @@ llmpilot_status llmpilot_bin(llmpilot_ctx* ctx, const float* X, int64_t n, int32
                              const llmpilot_cuts* cuts_in, llmpilot_cuts** cuts_out, uint8_t* codes_out);
 /* Copy cuts to host: cuts (F x 255 floats, row f holds ncuts[f] values), ncuts (F ints). */
 llmpilot_status llmpilot_cuts_export(const llmpilot_cuts* cuts, int32_t* F, float* cuts_out, int32_t* ncuts_out);
-void llmpilot_cuts_free(llmpilot_cuts* cuts);
+void llmpilot_cuts_free(llmpilot_cuts* cuts);   /* stream-ordered release, as llmpilot_model_free */
 
 /* Fit the two ensembles (nTTFT, ITL) on the dataset with constraints L1, L2 used by Eq. (4).
  * In a multi-GPU context every rank calls with its shard; the model is bit-identical on all. */
@@ -148,6 +148,10 @@ llmpilot_status llmpilot_model_info(const llmpilot_model* m, int32_t* F, int32_t
 llmpilot_status llmpilot_model_export(const llmpilot_model* m, float* base, int32_t* feat, int32_t* bin, float* thr,
                                       float* val);
 llmpilot_status llmpilot_model_train_pred(const llmpilot_model* m, float* train_pred /* host, n_rows x 2 */);
+/* Free a model.  Its device buffers are released stream-ordered (cudaFreeAsync into the
+ * device's default memory pool, which keeps the memory cached) on the stream of the context
+ * that fitted it: free a model before destroying that stream, and only after work that reads the
+ * model on other streams has completed.  Never synchronises the device. */
 void llmpilot_model_free(llmpilot_model* m);
 
 /* Predict both targets: out[i] = (nTTFT, ITL) = base + sum over trees in order.

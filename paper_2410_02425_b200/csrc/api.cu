@@ -102,6 +102,14 @@ llmpilot_status llmpilot_ctx_create(int device, void* cuda_stream, const void* n
       LLMP_CUDA(cudaGetDeviceProperties(&prop, device));
       LLMP_REQUIRE(prop.major >= 10, "this library is built for sm_100a (B200); device is older");
       h->c.sms = prop.multiProcessorCount;
+      {  // model/cuts buffers come from the default pool (stream-ordered): keep freed memory cached
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+          uint64_t thr = UINT64_MAX;
+          cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        cudaGetLastError();
+      }
       LLMP_CUDA(cudaMalloc(&h->c.d_units, LLMP_N_KERNEL_CLASSES * 8));
       LLMP_CUDA(cudaMemset(h->c.d_units, 0, LLMP_N_KERNEL_CLASSES * 8));
       if (nccl_unique_id) llmp::nccl_init(&h->c, nccl_unique_id);

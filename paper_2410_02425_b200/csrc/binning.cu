@@ -139,6 +139,8 @@ void compute_cuts(Ctx* ctx, const float* X, int64_t n, int F, int64_t row_offset
   ctx->launches[KC_CUTS] += 1;
   out.F = F;
   out.max_bin = max_bin;
+  out.d_cuts.set_stream(ctx->stream);
+  out.d_ncuts.set_stream(ctx->stream);
   out.d_cuts.ensure((size_t)kMaxF * (kBins - 1) * 4);
   out.d_ncuts.ensure((size_t)kMaxF * 4);
   LLMP_CUDA(cudaMemsetAsync(out.d_cuts.p, 0, out.d_cuts.bytes, s));

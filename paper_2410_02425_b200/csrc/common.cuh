@@ -46,16 +46,24 @@ void check_cuda(cudaError_t e, const char* what, const char* file, int line);
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  // stream-ordered buffers (model and cuts handles returned to the caller): allocated with
+  // cudaMallocAsync and released with cudaFreeAsync on `ord` from the device's default pool, so a
+  // fit/free cycle neither synchronises the device nor returns memory to the driver
+  cudaStream_t ord = nullptr;
+  bool stream_ordered = false;
   DevBuf() = default;
   explicit DevBuf(size_t b) { alloc(b); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes), ord(o.ord), stream_ordered(o.stream_ordered) {
+    o.p = nullptr; o.bytes = 0;
+  }
   DevBuf& operator=(DevBuf&& o) noexcept {
     release();
-    p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0;
+    p = o.p; bytes = o.bytes; ord = o.ord; stream_ordered = o.stream_ordered; o.p = nullptr; o.bytes = 0;
     return *this;
   }
+  void set_stream(cudaStream_t s) { ord = s; stream_ordered = true; }
   ~DevBuf() { release(); }
   void alloc(size_t b);
   void ensure(size_t b) { if (b > bytes) { release(); alloc(b); } }

@@ -36,7 +36,11 @@ constexpr int HIST_WARPS = HIST_THREADS / 32;
 constexpr int HIST_CHUNK = 65536;          // rows per CTA between flushes: |sum q_g| < 2^30 in int32
 constexpr int ROWBUF_STRIDE = 48;          // bytes per staged code row (conflict-free 16B stores)
 constexpr int MAX_PIECES = 512;            // built children per level (2^(kMaxDepth-1))
-constexpr int HIST_SMEM = 2 * kHistBins * 4 + HIST_WARPS * 32 * ROWBUF_STRIDE;  // 64 KB + 24 KB
+// shared histogram: [257 bin rows][32 features] int32 for q_g, then the same for q_h; bin row 256 is
+// a dummy cell row (the users lane's run target, see k_hist)
+constexpr int HH_OFF = (kBins + 1) * kMaxF * 4;   // byte offset of the q_h half (32,896)
+constexpr int U_OFF = 2 * HH_OFF + HIST_WARPS * 32 * ROWBUF_STRIDE;     // users column: [256] q_g, [256] q_h
+constexpr int HIST_SMEM = U_OFF + 2 * kBins * 4;                             // 64.3 KB + 24 KB + 2 KB
 
 constexpr int SLOT = 2 * kHistBins;        // int64 per histogram slot (g then h)
 
@@ -54,9 +58,7 @@ struct LevelView {
   int32_t* split_f;  // [2^d] -1 = leaf / absent
   int32_t* split_b;
   int32_t* built;    // [2^(d-1)] which child of parent j was histogrammed (0 left, 1 right)
-  int32_t* done;     // [2^d] per-node count of finished split CTAs (self-resetting)
-  uint64_t* flags;   // look-back tile flags
-  int32_t* ticket;
+  int32_t* done;     // [2^d] per-node count of finished split warps (self-resetting; plain k_split3)
 };
 
 // best split of one (node, feature), published by the split kernel for the node's final reduction
@@ -93,6 +95,7 @@ struct FitArgs {
   uint64_t seed;
   int monotone;
   int fused_root;     // 1: k_hist<UPDROOT> builds the next root speculatively (root_needed)
+  int urow;           // 1: the histogram kernels take the users column row-parallel
   int nn;
   FeatBest* fbest;            // [2^(D-1)][32] per-(node, feature) best split of the current level
   unsigned long long* units;  // device counters of rows processed per kernel class (instrumentation)
@@ -142,25 +145,52 @@ __device__ __forceinline__ bool root_needed(const FitArgs& a, int t) {
 }
 constexpr int UPDROOT_TREE_SMEM = 512 * 6;   // s_feat (int8), s_bin (u8), s_val (f32) of one tree
 
+// One row of a lane's run-length aggregation: if the row's cell address `ca` differs from the
+// current run's `pa`, flush the run (two 32-bit shared reductions) and start a new one; then add
+// the row's (q_g, q_h), stored unpacked so one 64-bit shared load fetches both.  The common
+// no-change path is compare, branch, two adds.
+constexpr uint32_t kNoRun = 0xffffffffu;
+__device__ __forceinline__ void run_flush(uint32_t pa, int32_t ag, uint32_t ah) {
+  asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(pa), "r"(ag) : "memory");
+  asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(pa), "r"(ah), "n"(HH_OFF) : "memory");
+}
+__device__ __forceinline__ void run_step(uint32_t& pa, int32_t& ag, uint32_t& ah, uint32_t ca, uint2 gh) {
+  if (ca != pa) {
+    run_flush(pa, ag, ah);
+    ag = 0;
+    ah = 0;
+    pa = ca;
+  }
+  ag += (int32_t)gh.x;
+  ah += gh.y;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const int d, const int t_in, const DbgArgs dbg) {
   const int t = (MODE == HM_ROOT || MODE == HM_UPDROOT) ? *a.d_tree : t_in;   // graph replays: tree index from the device
   if (MODE == HM_ROOT && !root_needed(a, t)) return;   // built speculatively by the previous update pass
   const bool has_next = (MODE == HM_UPDROOT) ? (t + 1 < a.T) : true;
+  const int ucol = (a.urow && a.users_col >= 0 && a.users_col < kMaxF) ? a.users_col : -1;   // row-parallel column
   extern __shared__ __align__(16) uint8_t smem[];
   int32_t* sg = reinterpret_cast<int32_t*>(smem);                 // [256 bins][32 features]
-  uint32_t* sh = reinterpret_cast<uint32_t*>(smem + kHistBins * 4);
+  uint32_t* sh = reinterpret_cast<uint32_t*>(smem + HH_OFF);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  uint8_t* rowbuf = smem + 2 * kHistBins * 4 + warp * 32 * ROWBUF_STRIDE;
+  uint8_t* rowbuf = smem + 2 * HH_OFF + warp * 32 * ROWBUF_STRIDE;
 
   __shared__ int64_t s_vstart[MAX_PIECES + 1];
   __shared__ int64_t s_pstart[MAX_PIECES];
   __shared__ int32_t s_slot[MAX_PIECES];
   __shared__ int s_np;
 
+  int32_t* sug = reinterpret_cast<int32_t*>(smem + U_OFF);   // users column (row-parallel), bank = bin
+  uint32_t* suh = reinterpret_cast<uint32_t*>(smem + U_OFF + kBins * 4);
   for (int i = tid; i < kHistBins; i += HIST_THREADS) {
     sg[i] = 0;
     sh[i] = 0;
+  }
+  for (int i = tid; i < kBins; i += HIST_THREADS) {
+    sug[i] = 0;
+    suh[i] = 0;
   }
   // fused mode: tree t (the one just grown) in shared memory for routing
   int8_t* s_feat = reinterpret_cast<int8_t*>(smem + HIST_SMEM);
@@ -255,14 +285,28 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
       // (bytes 0..31 = the row's codes, bytes 32..35 = its packed gradient pair)
       const int64_t w0 = c0 + clen * warp / HIST_WARPS, w1 = c0 + clen * (warp + 1) / HIST_WARPS;
 
-      const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sg) + (uint32_t)lane * 4u;
-      int prev = -1;              // code of the current run of this lane's feature
+      // The users column changes on nearly every row of paper-ordered data, so run-length
+      // aggregation cannot help it and its flushes would make the whole warp take the flush branch
+      // on every row: it is histogrammed row-parallel by the loader lanes instead (two shared
+      // reductions per 32-row batch), and its lane's runs target the dummy bin row (never read).
+      const uint32_t sg0 = (uint32_t)__cvta_generic_to_shared(sg);
+      const uint32_t su0 = (uint32_t)__cvta_generic_to_shared(sug);
+      const bool ulane = lane == ucol;
+      const uint32_t sbase = ulane ? sg0 + (uint32_t)(kBins * 128) + (uint32_t)lane * 4u : sg0 + (uint32_t)lane * 4u;
+      const uint32_t cstride = ulane ? 0u : 128u;
+      uint32_t pa = kNoRun;       // shared address of the current run's (bin, feature) cell
       int32_t ag = 0;             // run sums
       uint32_t ah = 0;
       // register prefetch of the first batch
       uint4 nc0 = make_uint4(0, 0, 0, 0), nc1 = nc0;
       uint32_t ngp = 0;
       float ny = 0.f, nw = 0.f, np_ = 0.f;
+      // HM_LEVEL: row indices run two batches ahead of the gathers (one exposed round trip per batch)
+      uint32_t nri = 0;
+      auto load_ridx = [&](int64_t base) {
+        const int64_t vi = base + lane;
+        if (MODE == HM_LEVEL && vi < w1) nri = sr_in[s_pstart[pc] + (vi - s_vstart[pc])];
+      };
       auto load_batch = [&](int64_t base) {
         const int64_t vi = base + lane;
         if (vi < w1) {
@@ -274,7 +318,7 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
             nw = a.w[ridx];
             np_ = a.p[ridx];
           } else if (MODE == HM_LEVEL) {
-            ridx = sr_in[pi];
+            ridx = nri;              // loaded by load_ridx(base)
             ngp = a.gp_root[ridx];   // gathered by row index (written by this tree's root pass)
           } else {
             ridx = dbg.idx ? dbg.idx[pi] : pi;
@@ -285,7 +329,11 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
           nc1 = __ldg(crow + 1);
         }
       };
-      if (w0 < w1) load_batch(w0);
+      if (w0 < w1) {
+        load_ridx(w0);
+        load_batch(w0);
+        load_ridx(w0 + 32);
+      }
       for (int64_t base = w0; base < w1; base += 32) {
         const int cnt = (int)min((int64_t)32, w1 - base);
         uint32_t gp = ngp;
@@ -326,32 +374,48 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
             a.gp_root[ridx] = gp;
           }
         }
-        *reinterpret_cast<uint32_t*>(rowbuf + lane * ROWBUF_STRIDE + 32) = gp;
+        *reinterpret_cast<uint2*>(rowbuf + lane * ROWBUF_STRIDE + 32) = make_uint2((uint32_t)gp_g(gp), (uint32_t)gp_h(gp));
         __syncwarp();
-        if (base + 32 < w1) load_batch(base + 32);   // prefetch the next batch
-        if (MODE == HM_UPDROOT && !has_next) continue;   // last tree: update only
-        if (prev < 0) prev = rowbuf[lane];
-#pragma unroll 4
-        for (int r = 0; r < cnt; ++r) {
-          const int c = rowbuf[r * ROWBUF_STRIDE + lane];
-          const uint32_t g2 = *reinterpret_cast<const uint32_t*>(rowbuf + r * ROWBUF_STRIDE + 32);
-          const int ch = c != prev;
-          // on a code change flush the finished run (two 32-bit shared reductions, one branch)
-          if (ch) {
-            const uint32_t ad = sbase + (uint32_t)prev * 128u;
-            asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(ad), "r"(ag) : "memory");
-            asm volatile("red.shared.add.u32 [%0+32768], %1;" ::"r"(ad), "r"(ah) : "memory");
-          }
-          ag = (ch ? 0 : ag) + gp_g(g2);
-          ah = (ch ? 0u : ah) + (uint32_t)gp_h(g2);
-          prev = c;
+        if (base + 32 < w1) {   // prefetch the next batch (and the row indices of the one after)
+          load_batch(base + 32);
+          load_ridx(base + 64);
         }
+        if (MODE == HM_UPDROOT && !has_next) continue;   // last tree: update only
+        if (ucol >= 0 && lane < cnt) {   // users column, row-parallel (lane = row)
+          const uint32_t cu = rowbuf[lane * ROWBUF_STRIDE + ucol];
+          const uint2 ghu = *reinterpret_cast<const uint2*>(rowbuf + lane * ROWBUF_STRIDE + 32);
+          const uint32_t ua = su0 + cu * 4u;   // dense per-bin cells: distinct bins, distinct banks
+          asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(ua), "r"((int32_t)ghu.x) : "memory");
+          asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(ua), "r"(ghu.y), "n"(kBins * 4) : "memory");
+        }
+        if (pa == kNoRun) pa = sbase + (uint32_t)rowbuf[lane] * cstride;
+        int r = 0;
+        for (; r + 4 <= cnt; r += 4) {   // the group's shared loads first, then 4 branch-free steps
+          uint32_t ca[4];
+          uint2 gh[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            ca[q] = sbase + (uint32_t)rowbuf[(r + q) * ROWBUF_STRIDE + lane] * cstride;
+            gh[q] = *reinterpret_cast<const uint2*>(rowbuf + (r + q) * ROWBUF_STRIDE + 32);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) run_step(pa, ag, ah, ca[q], gh[q]);
+        }
+        for (; r < cnt; ++r)
+          run_step(pa, ag, ah, sbase + (uint32_t)rowbuf[r * ROWBUF_STRIDE + lane] * cstride,
+                   *reinterpret_cast<const uint2*>(rowbuf + r * ROWBUF_STRIDE + 32));
       }
-      if (prev >= 0) {
-        atomicAdd(&sg[prev * 32 + lane], ag);
-        atomicAdd(&sh[prev * 32 + lane], ah);
-      }
+      if (pa != kNoRun) run_flush(pa, ag, ah);
       __syncthreads();
+      if (ucol >= 0) {   // the users column's cells (left zero by its lane) from the dense histogram
+        for (int b = tid; b < kBins; b += HIST_THREADS) {
+          sg[b * 32 + ucol] = sug[b];
+          sh[b * 32 + ucol] = suh[b];
+          sug[b] = 0;
+          suh[b] = 0;
+        }
+        __syncthreads();
+      }
       // flush: zero-skipping int64 atomics into the node histogram ([f][b] layout)
       for (int i = tid; i < kHistBins; i += HIST_THREADS) {
         const int32_t g = sg[i];
@@ -752,6 +816,8 @@ __global__ void __launch_bounds__(PT_THREADS) k_pcount(const FitArgs a, const in
 // lefts at lp + prefix + popc(ballot & lanes_below), rights likewise — each group's lefts and
 // rights land in two contiguous runs, so the stores stay coalesced.
 __global__ void __launch_bounds__(PT_THREADS) k_pscatter2(const FitArgs a, const int d, const PartWs w) {
+  __shared__ __align__(16) int s_pre[PT_THREADS / 32][PT_WORDS];        // per warp: group prefixes of a tile
+  __shared__ __align__(16) uint32_t s_bits[PT_THREADS / 32][PT_WORDS];  // per warp: the tile's ballot words
   __shared__ int s_tile_pref[MAX_PIECES + 1];
   __shared__ int64_t s_seq_pref[MAX_PIECES + 1];
   __shared__ int s_w[PT_THREADS / 32];
@@ -786,6 +852,7 @@ __global__ void __launch_bounds__(PT_THREADS) k_pscatter2(const FitArgs a, const
     int64_t run = inc - local;
     for (int w2 = 0; w2 < warp; ++w2) run += s_w64[w2];
     const int G = gridDim.x, bid = blockIdx.x;
+    int nxt = c0 + ((bid - c0 % G) + G) % G;   // this CTA's first tile (t = bid mod G) at or after c0
     for (int b0 = c0; b0 < c1; b0 += 16) {
       if (c1 - c0 > 16) {   // rare: reload this round of the chunk
 #pragma unroll
@@ -795,7 +862,10 @@ __global__ void __launch_bounds__(PT_THREADS) k_pscatter2(const FitArgs a, const
       for (int q = 0; q < 16; ++q) {
         const int t = b0 + q;
         if (t < c1) {
-          if (t % G == bid) s_own[t / G] = run;
+          if (t == nxt) {
+            s_own[t / G] = run;
+            nxt += G;
+          }
           if (bid == 0) {
             const int j = parent_of_tile(s_tile_pref, NP, t);
             if (t == s_tile_pref[j]) s_ls[j] = run;
@@ -829,79 +899,89 @@ __global__ void __launch_bounds__(PT_THREADS) k_pscatter2(const FitArgs a, const
     const int len = (int)min((int64_t)PT_TILE, cnt_j - o);
     const uint32_t* rin = (d >= 2) ? a.sr[(d - 1) & 1] + start_j + o : nullptr;
     const uint32_t* bw = w.bits + (size_t)t * PT_WORDS;
-    // exclusive left prefix of every (q, warp) group: lane L holds words 4L .. 4L+3
+    // all of the warp's row indices in flight first (independent of the ballot words)
+    uint32_t rv[PT_ITEMS];
+#pragma unroll
+    for (int q = 0; q < PT_ITEMS; ++q) {
+      const int k = q * PT_THREADS + warp * 32 + lane;
+      rv[q] = (k < len) ? ((d == 1) ? (uint32_t)(o + k) : rin[k]) : 0u;
+    }
+    // exclusive left prefix of every (q, warp) group, in this warp's table: lane L handles words
+    // 4L .. 4L+3 (popc + warp scan, no block barrier)
     const uint4 mw = *reinterpret_cast<const uint4*>(bw + 4 * lane);
-    const int c0 = __popc(mw.x), c1 = __popc(mw.y), c2 = __popc(mw.z), c3 = __popc(mw.w);
-    const int lsum = c0 + c1 + c2 + c3;
+    const int c0 = __popc(mw.x), c1 = __popc(mw.y), c2 = __popc(mw.z);
+    const int lsum = c0 + c1 + c2 + __popc(mw.w);
     int inc = lsum;
     for (int off = 1; off < 32; off <<= 1) {
       const int u = __shfl_up_sync(0xffffffffu, inc, off);
       if (lane >= off) inc += u;
     }
-    const int ex = inc - lsum;                       // prefix before word 4*lane
+    const int ex = inc - lsum;
+    __syncwarp();   // the previous tile's table reads are done
+    reinterpret_cast<int4*>(s_pre[warp])[lane] = make_int4(ex, ex + c0, ex + c0 + c1, ex + c0 + c1 + c2);
+    reinterpret_cast<uint4*>(s_bits[warp])[lane] = mw;
+    __syncwarp();
     const int64_t lp = s_own[t / gridDim.x];
     const int64_t rbase = a.n + (s_seq_pref[j] + o - lp);   // global right prefix at the tile start
-    // loads of 8 rows first (independent), then their stores; two rounds per tile
-#pragma unroll 1
-    for (int q0 = 0; q0 < PT_ITEMS; q0 += 8) {
-    uint32_t rv[8];
 #pragma unroll
-    for (int qq = 0; qq < 8; ++qq) {
-      const int k = (q0 + qq) * PT_THREADS + warp * 32 + lane;
-      rv[qq] = (k < len) ? ((d == 1) ? (uint32_t)(o + k) : rin[k]) : 0u;
-    }
-#pragma unroll
-    for (int qq = 0; qq < 8; ++qq) {
-      const int q = q0 + qq;
+    for (int q = 0; q < PT_ITEMS; ++q) {
       const int word = q * (PT_THREADS / 32) + warp;
-      const int owner = word >> 2, sub = word & 3;
-      // prefix before this group = ex(owner) + counts of the owner's earlier words
-      const int exo = __shfl_sync(0xffffffffu, ex, owner);
-      const int a0 = __shfl_sync(0xffffffffu, c0, owner), a1 = __shfl_sync(0xffffffffu, c1, owner);
-      const int a2 = __shfl_sync(0xffffffffu, c2, owner);
-      const int pre = exo + (sub > 0 ? a0 : 0) + (sub > 1 ? a1 : 0) + (sub > 2 ? a2 : 0);
-      const uint32_t m = bw[word];
+      const int pre = s_pre[warp][word];
+      const uint32_t m = s_bits[warp][word];
       const int k = q * PT_THREADS + warp * 32 + lane;
       if (k < len) {
         const bool left = (m >> lane) & 1u;
         const int rank = __popc(m & lt);
         const int64_t dst = left ? lp + pre + rank : rbase + (k - lane - pre) + (lane - rank);
-        rout[dst] = rv[qq];
+        rout[dst] = rv[q];
       }
-    }
     }
   }
 }
 
 // ---------------------------------------------------------------------------------------------
-// split evaluation, one WARP per (node of level d, feature f) — 4 warps per CTA, no block barriers:
-// lane l owns bins 8l .. 8l+7; the warp forms the feature's histogram (sibling = parent - built,
-// exact int64, written back for the next level), prefix-scans it, evaluates every threshold in
-// fp64 (monotone veto on users) and reduces (loss desc, b asc).  Its lane 0 publishes the result
-// and takes a ticket; the node's last-arriving warp reduces the 32 features (loss desc, f asc,
-// b asc) and writes the tree.
+// split evaluation: one thread-block CLUSTER of 8 CTAs per node of level d, one WARP per
+// (node, feature f) — 4 warps per CTA.  Lane l owns bins 8l .. 8l+7; the warp forms the feature's
+// histogram (sibling = parent - built, exact int64, written back for the next level),
+// prefix-scans it, evaluates every threshold in fp64 (monotone veto on users) and reduces
+// (loss desc, b asc) into its CTA's shared memory.  After a cluster barrier, warp 0 of the
+// cluster's first CTA reads the 32 per-feature results through distributed shared memory,
+// reduces them (loss desc, f asc, b asc) and writes the tree; a second barrier keeps the other
+// CTAs' shared memory alive until then.  Every index and scalar the kernel needs is loaded at
+// entry (one round trip).
 constexpr int SP3_WARPS = 4;
+constexpr int SP3_CLUSTER = 32 / SP3_WARPS;   // 8 CTAs = the node's 32 features
+template <bool CL>
 __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitArgs a, const int d) {
-  const int t = *a.d_tree;
-  const int lane = threadIdx.x & 31;
-  const int wg = blockIdx.x * SP3_WARPS + (threadIdx.x >> 5);
-  const int k = wg >> 5, f = wg & 31;
+  __shared__ FeatBest s_fb[SP3_WARPS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int k = blockIdx.x / SP3_CLUSTER;                  // node of level d
+  const int f = (blockIdx.x % SP3_CLUSTER) * SP3_WARPS + warp;
   const LevelView& V = a.lv[d];
+  const int j = k >> 1;                                     // parent (level d-1)
+  // ---- independent loads, all issued up front
+  const int t = *a.d_tree;
+  const int pf = (d == 0) ? 0 : a.lv[d - 1].split_f[j];
+  const int side = (d == 0) ? 0 : V.built[j];
+  const int pside = (d >= 2) ? a.lv[d - 1].built[j >> 1] : 0;
+  const double lo = (d == 0) ? -INFINITY : V.lo[k], hi = (d == 0) ? INFINITY : V.hi[k];
+  const int nthr = a.ncuts[f];   // thresholds b = 0 .. nbins_f - 2
+  if (d > 0 && pf < 0) {         // node absent (uniform over the cluster)
+    if (f == 0 && lane == 0) V.split_f[k] = -1;
+    return;
+  }
+  const uint32_t mgb = a.maxg[t], mhb = a.maxh[t];
   int64_t* Hself;
   int64_t g8[8], h8[8];
   if (d == 0) {
     Hself = a.H[0];
   } else {
-    const int j = k >> 1;
-    if (a.lv[d - 1].split_f[j] < 0) {
-      if (f == 0 && lane == 0) V.split_f[k] = -1;
-      return;
-    }
-    const int side = V.built[j];
     const bool is_built = (k & 1) == side;
     Hself = a.H[d & 1] + (size_t)(is_built ? j : (1 << (d - 1)) + j) * SLOT;
     if (!is_built) {
-      const longlong2* Hp = reinterpret_cast<const longlong2*>(a.H[(d - 1) & 1] + (size_t)node_slot(a, d - 1, j) * SLOT);
+      // parent's slot at level d-1 (node_slot without the dependent load)
+      const int pslot = (d == 1) ? 0 : (((j & 1) == pside) ? (j >> 1) : (1 << (d - 2)) + (j >> 1));
+      const longlong2* Hp = reinterpret_cast<const longlong2*>(a.H[(d - 1) & 1] + (size_t)pslot * SLOT);
       const longlong2* Hb = reinterpret_cast<const longlong2*>(a.H[d & 1] + (size_t)j * SLOT);
       longlong2* Hs = reinterpret_cast<longlong2*>(Hself);
       const int eg0 = (f * kBins + lane * 8) / 2, eh0 = (kHistBins + f * kBins + lane * 8) / 2;
@@ -924,7 +1004,7 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitArgs a, cons
       }
     }
   }
-  if (d == 0 || (k & 1) == a.lv[d].built[k >> 1]) {
+  if (d == 0 || (k & 1) == side) {
     const longlong2* G2 = reinterpret_cast<const longlong2*>(Hself + f * kBins + lane * 8);
     const longlong2* H2 = reinterpret_cast<const longlong2*>(Hself + kHistBins + f * kBins + lane * 8);
     longlong2 gv[4], hv[4];
@@ -966,15 +1046,13 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitArgs a, cons
     const unsigned less = __ballot_sync(0xffffffffu, lane < F && (kl < kf || (kl == kf && lane < f)));
     fin = __popc(less) < nkeep;
   }
-  const int eg = exp_of(__uint_as_float(a.maxg[t])), eh = exp_of(__uint_as_float(a.maxh[t]));
+  const int eg = exp_of(__uint_as_float(mgb)), eh = exp_of(__uint_as_float(mhb));
   const double sgi = exp2i(eg - a.K), shi = exp2i(eh - a.K);
-  const double lo = (d == 0) ? -INFINITY : V.lo[k], hi = (d == 0) ? INFINITY : V.hi[k];
   const double lambda = a.lambda, mcw = a.mcw;
   double bl = -INFINITY;
   int bb = 0x7fffffff;
   int64_t bGL = 0, bHL = 0;
   if (fin) {
-    const int nthr = a.ncuts[f];   // thresholds b = 0 .. nbins_f - 2
     if (lane * 8 < nthr) {
       const double G = dequant(Gq, sgi), H = dequant(Hq, shi);
       const double gainP = calc_gain(G, H, calc_weight(G, H, lo, hi, lambda, mcw), lambda);
@@ -1014,8 +1092,6 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitArgs a, cons
       bHL = oH;
     }
   }
-  FeatBest* fb = a.fbest + (size_t)k * 32;
-  int last = 0;
   if (lane == 0) {
     FeatBest r;
     r.loss = bl;
@@ -1025,17 +1101,46 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitArgs a, cons
     r.HLq = bHL;
     r.Gq = Gq;
     r.Hq = Hq;
-    fb[f] = r;
-    __threadfence();
-    last = atomicAdd(&V.done[k], 1) == 31;
+    if (CL) s_fb[warp] = r;
+    else a.fbest[(size_t)k * 32 + f] = r;
   }
-  last = __shfl_sync(0xffffffffu, last, 0);
-  if (!last) return;
-  // ---- the node's last warp: best over the 32 features, then the tree update
-  __threadfence();
-  const volatile FeatBest* vfb = fb;
-  double ml = vfb[lane].valid ? vfb[lane].loss : -INFINITY;
-  int mf = lane, mb = vfb[lane].b;
+  // ---- the node's reduction, by one warp: lane l takes feature l's result
+  int rvalid, rb;
+  double rloss;
+  int64_t rGL, rHL;
+  if constexpr (CL) {   // cluster launch: results exchanged through distributed shared memory
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();
+    if (blockIdx.x % SP3_CLUSTER != 0 || warp != 0) {
+      cluster.sync();   // keep this CTA's s_fb readable until the reduction warp has read it
+      return;
+    }
+    const FeatBest* rf = cluster.map_shared_rank(&s_fb[0], lane / SP3_WARPS) + (lane % SP3_WARPS);
+    rvalid = rf->valid;
+    rb = rf->b;
+    rloss = rf->loss;
+    rGL = rf->GLq;
+    rHL = rf->HLq;
+    cluster.sync();
+  } else {              // plain launch: the node's last-arriving warp (global ticket) reduces
+    int last = 0;
+    if (lane == 0) {
+      __threadfence();
+      last = atomicAdd(&V.done[k], 1) == 31;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
+    __threadfence();
+    const volatile FeatBest* rf = a.fbest + (size_t)k * 32 + lane;
+    rvalid = rf->valid;
+    rb = rf->b;
+    rloss = rf->loss;
+    rGL = rf->GLq;
+    rHL = rf->HLq;
+    if (lane == 0) V.done[k] = 0;
+  }
+  double ml = rvalid ? rloss : -INFINITY;
+  int mf = lane, mb = rb;
   for (int o = 16; o > 0; o >>= 1) {
     const double ol = __shfl_down_sync(0xffffffffu, ml, o);
     const int of = __shfl_down_sync(0xffffffffu, mf, o), ob = __shfl_down_sync(0xffffffffu, mb, o);
@@ -1045,19 +1150,21 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitArgs a, cons
       mb = ob;
     }
   }
+  ml = __shfl_sync(0xffffffffu, ml, 0);
+  mf = __shfl_sync(0xffffffffu, mf, 0);
+  mb = __shfl_sync(0xffffffffu, mb, 0);
+  const int64_t GLs = __shfl_sync(0xffffffffu, rGL, mf), HLs = __shfl_sync(0xffffffffu, rHL, mf);
   if (lane != 0) return;
-  V.done[k] = 0;
   int32_t* const tfeat = a.tfeat + (size_t)t * a.nn;
   int32_t* const tbin = a.tbin + (size_t)t * a.nn;
   float* const tthr = a.tthr + (size_t)t * a.nn;
   float* const tval = a.tval + (size_t)t * a.nn;
-  const int64_t GqN = vfb[0].Gq, HqN = vfb[0].Hq;
+  const int64_t GqN = Gq, HqN = Hq;   // node totals (every feature's histogram sums to them; this warp's)
   const double G = dequant(GqN, sgi), H = dequant(HqN, shi);
   const double wP = calc_weight(G, H, lo, hi, lambda, mcw);
   const int gk = (1 << d) - 1 + k;
   if (ml > 1e-6) {
     const int fs = mf, bs = mb;
-    const int64_t GLs = vfb[fs].GLq, HLs = vfb[fs].HLq;
     const double GL = dequant(GLs, sgi), HL = dequant(HLs, shi);
     const double GR = dequant(GqN - GLs, sgi), HR = dequant(HqN - HLs, shi);
     const double wl = calc_weight(GL, HL, lo, hi, lambda, mcw);
@@ -1414,7 +1521,10 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   const int nn = (1 << (D + 1)) - 1;
   const int half_max = 1 << (D - 1);        // slots per histogram parity buffer
   // p of both targets: kept by the model (llmpilot_model_train_pred) or a reused workspace
-  if (keep_train_pred) out.d_train_pred.ensure((size_t)n * 4 * 2);
+  if (keep_train_pred) {
+    out.d_train_pred.set_stream(s);
+    out.d_train_pred.ensure((size_t)n * 4 * 2);
+  }
   DevBuf& d_p = keep_train_pred ? out.d_train_pred : ctx->workspace("p", (size_t)n * 4 * 2);
   out.device = ctx->device;
   DevBuf& d_trees = ctx->workspace("trees", (size_t)2 * std::max(T, 1) * nn * 16);
@@ -1435,7 +1545,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   // of one CUDA graph, each with its own level workspaces); with NCCL (collectives must be
   // issued in one order on every rank) or timing instrumentation they run one after the other
   const bool graphs = T > 0 && !ctx->timing && ctx->use_graphs;
-  const bool concurrent = graphs && ctx->nranks == 1;
+  static const bool serial_env = getenv("LLMP_SERIAL") && atoi(getenv("LLMP_SERIAL")) != 0;   // diagnostics
+  const bool concurrent = graphs && ctx->nranks == 1 && !serial_env;
   size_t lvl_nodes = 0;
   for (int d = 0; d <= D; ++d) lvl_nodes += (size_t)1 << d;
   const int64_t max_tiles = (n + PT_TILE - 1) / PT_TILE + half_max + 1;
@@ -1446,6 +1557,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   // fuses each tree's update with the next tree's root histogram (LLMP_NOFUSE=1 disables).
   static const bool use_root2 = getenv("LLMP_ROOT2") && atoi(getenv("LLMP_ROOT2")) != 0;
   static const bool fused = !use_root2 && !(getenv("LLMP_NOFUSE") && atoi(getenv("LLMP_NOFUSE")) != 0);
+  static const bool urow = !(getenv("LLMP_NO_UROW") && atoi(getenv("LLMP_NO_UROW")) != 0);
   FitArgs A[2];
   PartWs PW[2];
   for (int tg = 0; tg < 2; ++tg) {
@@ -1483,6 +1595,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     a.seed = hp.seed;
     a.monotone = hp.monotone_users;
     a.fused_root = fused ? 1 : 0;
+    a.urow = urow ? 1 : 0;
     a.nn = nn;
     a.units = ctx->d_units;
     a.fbest = reinterpret_cast<FeatBest*>(ctx->workspace("featbest" + sx, (size_t)half_max * 32 * 48).p);
@@ -1557,6 +1670,31 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   // one tree of one target = a fixed sequence of launches that reads the tree index from the
   // device; both targets' trees + the index advance form one "round", captured once into a CUDA
   // graph and replayed T times (plain launches when timing instrumentation is on)
+  // split kernel: plain launch with a global ticket per node (default) or one thread-block cluster
+  // per node exchanging results through distributed shared memory (LLMP_SPLIT_CLUSTER=1)
+  static const bool split_cluster = getenv("LLMP_SPLIT_CLUSTER") && atoi(getenv("LLMP_SPLIT_CLUSTER")) != 0;
+  auto split = [&](const FitArgs& a, int d) {
+    const int grid = (1 << d) * SP3_CLUSTER;
+    if (!split_cluster) {
+      LLMP_LAUNCH(ctx, KC_SPLIT, (1 << d), k_split3<false>, grid, SP3_WARPS * 32, 0, a, d);
+      return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(SP3_WARPS * 32);
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = SP3_CLUSTER;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaEvent_t ev = nullptr;
+    ctx->before(KC_SPLIT, &ev);
+    LLMP_CUDA(cudaLaunchKernelEx(&cfg, k_split3<true>, a, d));
+    ctx->after(KC_SPLIT, ev, (double)(1 << d));
+  };
   auto tree = [&](const FitArgs& a, const PartWs& pw) {
     const cudaStream_t st = ctx->stream;
     // fused: the previous round's update pass built this root already unless root_needed
@@ -1565,7 +1703,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     if (use_root2) LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist_root2, hist_grid, R2_THREADS, R2_SMEM, a);
     else LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist<HM_ROOT>, hist_grid, HIST_THREADS, HIST_SMEM, a, 0, 0, nodbg);
     allreduce_sum_i64(ctx, a.H[0], SLOT);
-    LLMP_LAUNCH(ctx, KC_SPLIT, 1, k_split3, 32 / SP3_WARPS, SP3_WARPS * 32, 0, a, 0);
+    split(a, 0);
     for (int d = 1; d < D; ++d) {
       const int tiles_d = (int)((n + PT_TILE - 1) / PT_TILE) + (1 << (d - 1));
       // persistent tile loops; a scatter CTA owns at most PT_OWN tiles
@@ -1578,7 +1716,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       }
       LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hist_grid, HIST_THREADS, HIST_SMEM, a, d, 0, nodbg);
       allreduce_sum_i64(ctx, a.H[d & 1], (size_t)SLOT << (d - 1));
-      LLMP_LAUNCH(ctx, KC_SPLIT, (1 << d), k_split3, (1 << d) * (32 / SP3_WARPS), SP3_WARPS * 32, 0, a, d);
+      split(a, d);
     }
     if (fused) {   // update tree t + root histogram of tree t+1 (into the now free root slot)
       LLMP_CUDA(cudaMemsetAsync(a.H[0], 0, (size_t)SLOT * 8, st));
@@ -1671,6 +1809,7 @@ void debug_histogram(Ctx* ctx, const uint8_t* codes, int64_t n, const int32_t* i
                      const int32_t* qh, int64_t* Hg, int64_t* Hh) {
   LLMP_REQUIRE(n >= 1 && m >= 0, "bad sizes");
   FitArgs a{};
+  a.urow = 1;   // users_col = 0: lane 0 takes the row-parallel path (both paths covered by the tests)
   a.codes = codes;
   a.n = n;
   a.F = kMaxF;

@@ -109,6 +109,8 @@ void upload_model_nodes(Ctx* ctx, ModelData& m) {
     memcpy(&bits, &v, 4);
     h[i] = make_uint2(bits, (uint32_t)(f >= 0 ? f : -1));
   }
+  m.d_nodes.set_stream(ctx->stream);
+  m.d_base.set_stream(ctx->stream);
   m.d_nodes.ensure(h.size() * 8);
   LLMP_CUDA(cudaMemcpyAsync(m.d_nodes.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
   m.d_base.ensure(8);

@@ -21,7 +21,7 @@ void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
 void DevBuf::alloc(size_t b) {
   bytes = b;
   if (b == 0) { p = nullptr; return; }
-  cudaError_t e = cudaMalloc(&p, b);
+  cudaError_t e = stream_ordered ? cudaMallocAsync(&p, b, ord) : cudaMalloc(&p, b);
   if (e != cudaSuccess) {
     p = nullptr;
     bytes = 0;
@@ -30,7 +30,15 @@ void DevBuf::alloc(size_t b) {
   }
 }
 void DevBuf::release() {
-  if (p) cudaFree(p);
+  if (p && stream_ordered) {
+    if (cudaFreeAsync(p, ord) != cudaSuccess) {   // e.g. the stream is gone: synchronous fallback
+      cudaGetLastError();
+      cudaDeviceSynchronize();
+      cudaFree(p);
+    }
+  } else if (p) {
+    cudaFree(p);
+  }
   p = nullptr;
   bytes = 0;
 }

@@ -218,6 +218,22 @@ def _exponent_changes(om, d):
     return ch
 
 
+@pytest.mark.parametrize("env", ["LLMP_NOFUSE=1", "LLMP_ROOT2=1", "LLMP_SPLIT_CLUSTER=1", "LLMP_NO_UROW=1"])
+def test_kernel_variants(lp, env):
+    """Every selectable kernel variant gives the oracle's models (own process: the switches are
+    read once per process)."""
+    import os
+    import subprocess
+    import sys
+    e = dict(os.environ)
+    for kv in env.split():
+        k, v = kv.split("=")
+        e[k] = v
+    p = subprocess.run([sys.executable, os.path.join(os.path.dirname(__file__), "_variant_fit.py")], env=e,
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0 and "OK" in p.stdout, (env, p.stdout[-2000:], p.stderr[-2000:])
+
+
 def test_fit_host_and_device_inputs_identical_and_deterministic(lp, ctx):
     d = synth.make("C2")
     hp = lp.hparams(n_trees=10, max_depth=6)

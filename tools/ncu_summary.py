@@ -2,7 +2,10 @@
 profiles/: a per-launch CSV, a per-kernel-class text summary, and profiles/ncu_traffic.json
 (measured DRAM bytes per launch per kernel class, which bench.py reports as roofline.traffic).
 
-    python tools/ncu_summary.py gpurun_out/prof_r01_tree.ncu-rep profiles/r01
+    python tools/ncu_summary.py REP.ncu-rep OUT_PREFIX ["what was captured"] [kernel1,kernel2,...]
+
+(the optional kernel list also dumps the SASS source page of each kernel's first launch; run it
+on the GPU box next to the report and ship only the CSVs — reports exceed gpurun's copy limit)
 """
 import csv
 import io
@@ -16,8 +19,9 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "smsp__inst_executed.sum",
            "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
            "sm__warps_active.avg.pct_of_peak_sustained_active"]
-CLASS = {"k_hist<0>": "hist_root", "k_hist<1>": "hist_level", "k_hist_root2": "hist_root", "k_pcount": "partition",
-         "k_pscan": "partition", "k_pscatter2": "partition", "k_split3": "split", "k_update": "update"}
+CLASS = {"k_hist<0>": "hist_root", "k_hist<1>": "hist_level", "k_hist<3>": "update", "k_hist_root2": "hist_root",
+         "k_pcount": "partition", "k_pscan": "partition", "k_pscatter2": "partition", "k_split3": "split",
+         "k_update": "update", "k_root_fix": "misc", "k_next_tree": "misc"}
 
 
 def kclass(name):
@@ -25,7 +29,20 @@ def kclass(name):
     return CLASS.get(base, base), base
 
 
-def main(rep, prefix):
+def dump_sass(rep, prefix, recs, names):
+    """Source (SASS) page of the first launch of each named kernel -> prefix_sass_<name>.csv"""
+    for nm in names:
+        idx = next((i for i, r in enumerate(recs) if r["kernel"] == nm), None)
+        if idx is None:
+            continue
+        out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
+                              "--launch-skip", str(idx), "--launch-count", "1"], capture_output=True, text=True).stdout
+        safe = nm.replace("<", "_").replace(">", "")
+        with open("%s_sass_%s.csv" % (prefix, safe), "w") as f:
+            f.write(out)
+
+
+def main(rep, prefix, sass=()):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(METRICS)],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
@@ -54,8 +71,8 @@ def main(rep, prefix):
         a["us"] += r["gpu__time_duration.sum"] or 0.0
         a["dram"] += ((r["dram__bytes_read.sum"] or 0) + (r["dram__bytes_write.sum"] or 0)) * 1e6  # Mbyte -> B
         a["inst"] += r["smsp__inst_executed.sum"] or 0.0
-    lines = ["ncu --set full --clock-control none, one tree of both ensembles (tools/profile_fit.py --trees 1, "
-             "C3: 10M rows, depth 8); cold cache, serialised launches", ""]
+    lines = ["ncu --set full --clock-control none, %s (C3: 10M rows, depth 8); cold cache, serialised launches"
+             % (sys.argv[3] if len(sys.argv) > 3 else "one tree of both ensembles"), ""]
     traffic = {}
     for c, a in sorted(agg.items(), key=lambda x: -x[1]["us"]):
         per = a["dram"] / a["launches"]
@@ -70,7 +87,9 @@ def main(rep, prefix):
     with open(os.path.join(os.path.dirname(prefix), "ncu_traffic.json"), "w") as f:
         json.dump(traffic, f, indent=1)
     print("\n".join(lines))
+    if sass:
+        dump_sass(rep, prefix, recs, sass)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], sys.argv[4].split(",") if len(sys.argv) > 4 else ())
