@@ -161,6 +161,14 @@ class ClockSampler:
     def end(self):
         self.t1 = time.monotonic()
 
+    def window(self, t0, t1):
+        """(median SM MHz, reasons, samples) of the NVML samples taken in [t0, t1]"""
+        sel = [(a, r) for t, a, b, r in self.samples if t0 <= t <= t1]
+        if not sel:
+            return None
+        return {"sm_mhz": statistics.median(a for a, r in sel), "reasons": sorted(set().union(*[r for a, r in sel])),
+                "samples": len(sel)}
+
     def close(self):
         out = {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         sm, mx, reasons = [], [], set()
@@ -335,7 +343,6 @@ def main():
         dist.barrier()
     elapsed_ms = t_start.elapsed_time(t_end)
     stats = ctx.stats()
-    clk = clocks.close()
     fit_ms = sum(a.elapsed_time(b) for a, b, c in ev)
     pred_ms = sum(b.elapsed_time(c) for a, b, c in ev)
     agg = torch.tensor([elapsed_ms, fit_ms, pred_ms], dtype=torch.float64, device=dev)
@@ -404,11 +411,13 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         host_e2e = {"fit": 0.0, "recommend": 0.0, "free": 0.0}
+        te0 = time.monotonic()
         e0.record(stream)
         for _ in range(args.steps):
             step(Xh, yh, lh, ph, lfh, pfh, hacc=host_e2e)
         e1.record(stream)
         torch.cuda.synchronize()
+        te1 = time.monotonic()
         e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
@@ -417,7 +426,10 @@ def main():
         d2h = 2 * args.trees * nn * 16 + 8 + lf.shape[0] * 24
         e2e = {"value": row_iters / (e2e_ms.item() / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_ms.item() / args.steps,
-               "host_ms_per_step": {k: 1000.0 * v / args.steps for k, v in host_e2e.items()}}
+               "host_ms_per_step": {k: 1000.0 * v / args.steps for k, v in host_e2e.items()},
+               "clocks": clocks.window(te0, te1)}
+
+    clk = clocks.close()   # SM clocks of the timed region (the e2e leg's are in e2e["clocks"])
 
     # ---- CPU baseline: the oracle as it stands, rank 0, N = 1, bounded sample
     cpu = None
