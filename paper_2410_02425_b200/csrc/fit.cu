@@ -443,6 +443,380 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// k_hist2: change-mask histogram.  Same modes, piece list, chunking and flush as
+// k_hist; a different inner loop, built so that equal codes in consecutive rows cost no per-row
+// work.  Per warp batch of 32 staged rows:
+//   lane r (row side)  XORs its row's 32 code bytes with the previous row's (8 words, SWAR) into a
+//                      32-bit mask of the features whose code changes at row r; the warp transposes
+//                      the 32 masks (5 shuffle stages), after which lane L holds, for feature
+//                      f = h2_feat(L), the rows of the batch where its code changes; the warp's
+//                      inclusive prefix sums of (q_g, q_h) give every run's sums as differences;
+//   lane L (feature side) flushes each finished run of its feature with one pair of 32-bit shared
+//                      reductions ("light" features, <= H2_HEAVY changes in the batch); "heavy"
+//                      features (random codes, deep levels) go row-parallel instead (lane = row, a
+//                      pair of reductions per row at (code, f)); the bank-padded [bin][33] layout
+//                      keeps both access patterns conflict-light.
+// The users column (a change on every row of paper-ordered data) stays row-parallel into the dense
+// per-bin histogram (bank = bin).
+constexpr int H2_THREADS = 512;
+constexpr int H2_WARPS = H2_THREADS / 32;
+constexpr int H2_PAD = 33;
+constexpr int H2_CELLS = kBins * H2_PAD;                 // words per channel
+constexpr int H2_HH = H2_CELLS * 4;                      // byte offset of the q_h channel
+constexpr int H2_ROWB = 48;                              // bytes per staged row (conflict-free 16-B stores)
+constexpr int H2_WBUF = 33 * H2_ROWB;                    // per warp: slots 1..32 = the batch's rows
+constexpr int H2_U_OFF = 2 * H2_HH + H2_WARPS * H2_WBUF;
+constexpr int H2_SMEM = H2_U_OFF + 2 * kBins * 4;        // 66 KB + 24.8 KB + 2 KB
+constexpr int H2_HEAVY = 3;
+
+// bit 8j+7-q of a row's change mask is feature 4q+j, so after the transpose lane L holds feature
+__device__ __forceinline__ int h2_feat(int L) { return 4 * (7 - (L & 7)) + (L >> 3); }
+// bit 8j+7 set iff byte j of x is non-zero
+__device__ __forceinline__ uint32_t byte_ne_hi(uint32_t x) {
+  return (x | ((x & 0x7f7f7f7fu) + 0x7f7f7f7fu)) & 0x80808080u;
+}
+// 32x32 bit transpose across the warp: afterwards bit r of lane L = bit L of lane r's input
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const uint32_t m = s == 16 ? 0x0000ffffu : s == 8 ? 0x00ff00ffu : s == 4 ? 0x0f0f0f0fu : s == 2 ? 0x33333333u : 0x55555555u;
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
+    x = (lane & s) ? ((x & ~m) | ((y >> s) & m)) : ((x & m) | ((y << s) & ~m));
+  }
+  return x;
+}
+__device__ __forceinline__ void red2(uint32_t addr, int32_t g, uint32_t h) {
+  asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(addr), "r"(g) : "memory");
+  asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(addr), "r"(h), "n"(H2_HH) : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitArgs a, const int d, const int t_in, const DbgArgs dbg) {
+  const int t = (MODE == HM_ROOT || MODE == HM_UPDROOT) ? *a.d_tree : t_in;   // graph replays: tree index from the device
+  if (MODE == HM_ROOT && !root_needed(a, t)) return;   // built speculatively by the previous update pass
+  const bool has_next = (MODE == HM_UPDROOT) ? (t + 1 < a.T) : true;
+  const int ucol = (a.users_col >= 0 && a.users_col < kMaxF) ? a.users_col : -1;   // row-parallel column
+  extern __shared__ __align__(16) uint8_t smem[];
+  int32_t* sg = reinterpret_cast<int32_t*>(smem);                 // [256 bins][33] (column 32 unused)
+  uint32_t* sh = reinterpret_cast<uint32_t*>(smem + H2_HH);
+  int32_t* sug = reinterpret_cast<int32_t*>(smem + H2_U_OFF);     // users column (row-parallel), bank = bin
+  uint32_t* suh = reinterpret_cast<uint32_t*>(smem + H2_U_OFF + kBins * 4);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  uint8_t* wb = smem + 2 * H2_HH + warp * H2_WBUF;                // staged row r at wb + (r+1)*48
+
+  __shared__ int64_t s_vstart[MAX_PIECES + 1];
+  __shared__ int64_t s_pstart[MAX_PIECES];
+  __shared__ int32_t s_slot[MAX_PIECES];
+  __shared__ int s_np;
+
+  for (int i = tid; i < 2 * H2_CELLS; i += H2_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
+  for (int i = tid; i < 2 * kBins; i += H2_THREADS) reinterpret_cast<uint32_t*>(sug)[i] = 0u;
+  // fused mode: tree t (the one just grown) in shared memory for routing
+  int8_t* s_feat = reinterpret_cast<int8_t*>(smem + H2_SMEM);
+  uint8_t* s_bin = smem + H2_SMEM + 512;
+  float* s_val = reinterpret_cast<float*>(smem + H2_SMEM + 1024);
+  if (MODE == HM_UPDROOT) {
+    const size_t to = (size_t)t * a.nn;
+    for (int i = tid; i < a.nn; i += H2_THREADS) {
+      const int f = a.tfeat[to + i];
+      s_feat[i] = (int8_t)(f < 0 ? -1 : f);
+      s_bin[i] = (uint8_t)a.tbin[to + i];
+      s_val[i] = a.tval[to + i];
+    }
+  }
+  // ---- piece list (virtual concatenation of the rows to histogram)
+  if (MODE == HM_LEVEL) {
+    const int NP = 1 << (d - 1);
+    const LevelView& P = a.lv[d - 1];
+    const LevelView& C = a.lv[d];
+    int64_t len = 0, pst = 0;
+    int side = 0;
+    if (tid < NP && P.split_f[tid] >= 0) {
+      const int64_t nL = C.gcnt[2 * tid], nR = C.gcnt[2 * tid + 1];
+      side = (nL <= nR) ? 0 : 1;       // build the smaller child (global row count), ties -> left
+      len = C.cnt[2 * tid + side];
+      pst = C.start[2 * tid + side];
+      if (blockIdx.x == 0) C.built[tid] = side;
+    }
+    __shared__ int64_t s_wsum[H2_WARPS];
+    int64_t v = len;
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    if (lane == 31) s_wsum[warp] = v;
+    __syncthreads();
+    int64_t woff = 0;
+    for (int w2 = 0; w2 < warp; ++w2) woff += s_wsum[w2];
+    if (tid < NP) {
+      s_vstart[tid] = woff + v - len;
+      s_pstart[tid] = pst;
+      s_slot[tid] = tid;
+    }
+    if (tid == NP - 1) s_vstart[NP] = woff + v;
+    if (tid == 0) s_np = NP;
+  } else if (tid == 0) {
+    s_np = 1;
+    s_vstart[0] = 0;
+    s_vstart[1] = (MODE == HM_ROOT || MODE == HM_UPDROOT) ? a.n : dbg.m;
+    s_pstart[0] = 0;
+    s_slot[0] = 0;
+  }
+  __syncthreads();
+  const int np = s_np;
+  const int64_t S = s_vstart[np];
+  const int64_t v0 = S * blockIdx.x / gridDim.x, v1 = S * (blockIdx.x + 1) / gridDim.x;
+  if (v0 >= v1) return;
+  if (tid == 0 && MODE != HM_DEBUG && a.units)
+    atomicAdd(&a.units[MODE == HM_ROOT ? KC_HIST_ROOT : MODE == HM_UPDROOT ? KC_UPDATE : KC_HIST], (unsigned long long)(v1 - v0));
+
+  // quantisation scales for ROOT (tree t): q = rint(v * 2^(K-e))
+  // (HM_UPDROOT: tree t+1's pairs with tree t's exponents — the speculation described at k_hist)
+  double scale_g = 0.0, scale_h = 0.0;
+  if (MODE == HM_ROOT || MODE == HM_UPDROOT) {
+    scale_g = exp2i(a.K - exp_of(__uint_as_float(a.maxg[t])));
+    scale_h = exp2i(a.K - exp_of(__uint_as_float(a.maxh[t])));
+  }
+  float mg = 0.f, mh = 0.f;   // HM_UPDROOT: tree t+1's max |g|, max h
+  int64_t* Hbase = (MODE == HM_DEBUG) ? dbg.out : a.H[d & 1];
+  const uint32_t* sr_in = (MODE == HM_LEVEL) ? a.sr[d & 1] : nullptr;
+  const uint32_t sgb = (uint32_t)__cvta_generic_to_shared(sg);
+  const uint32_t sub = (uint32_t)__cvta_generic_to_shared(sug);
+  const int myf = h2_feat(lane);
+  const bool active = myf < a.F && myf != ucol;
+  const bool hist_on = !(MODE == HM_UPDROOT && !has_next);   // last tree: update only
+
+  int pc = 0;
+  while (pc + 1 < np && s_vstart[pc + 1] <= v0) ++pc;
+  for (; pc < np && s_vstart[pc] < v1; ++pc) {
+    int64_t s0 = max(v0, s_vstart[pc]), s1 = min(v1, s_vstart[pc + 1]);
+    if (s0 >= s1) continue;
+    int64_t* Hg = Hbase + (size_t)s_slot[pc] * SLOT;
+    int64_t* Hh = Hg + kHistBins;
+    const int64_t poff = s_pstart[pc] - s_vstart[pc];   // physical position = virtual + poff
+    for (int64_t c0 = s0; c0 < s1; c0 += HIST_CHUNK) {
+      const int64_t c1 = min(s1, c0 + HIST_CHUNK);
+      const int64_t clen = c1 - c0;
+      const int64_t w0 = c0 + clen * warp / H2_WARPS, w1 = c0 + clen * (warp + 1) / H2_WARPS;
+      uint32_t cur = 0;           // pending run of feature myf: byte offset of its (bin, f) cell
+      int32_t acc_g = 0;          // its sums from earlier batches
+      uint32_t acc_h = 0;
+      bool fresh = true;          // no previous row yet
+      uint4 nc0 = make_uint4(0, 0, 0, 0), nc1 = nc0;
+      uint32_t ngp = 0, nri = 0;
+      float ny = 0.f, nw = 0.f, np_ = 0.f;
+      auto load_ridx = [&](int64_t vb) {
+        const int64_t vi = vb + lane;
+        if (MODE == HM_LEVEL && vi < w1) nri = sr_in[vi + poff];
+      };
+      auto load_batch = [&](int64_t vb) {
+        const int64_t vi = vb + lane;
+        if (vi < w1) {
+          const int64_t pi = vi + poff;
+          int64_t ridx;
+          if (MODE == HM_ROOT || MODE == HM_UPDROOT) {
+            ridx = pi;
+            ny = a.y[ridx];
+            nw = a.w[ridx];
+            np_ = a.p[ridx];
+          } else if (MODE == HM_LEVEL) {
+            ridx = nri;
+            ngp = a.gp_root[ridx];
+          } else {
+            ridx = dbg.idx ? dbg.idx[pi] : pi;
+            ngp = pack_gp(dbg.qg[ridx], dbg.qh[ridx]);
+          }
+          const uint4* crow = reinterpret_cast<const uint4*>(a.codes + (size_t)ridx * kMaxF);
+          nc0 = __ldg(crow);
+          nc1 = __ldg(crow + 1);
+        }
+      };
+      if (w0 < w1) {
+        load_ridx(w0);
+        load_batch(w0);
+        load_ridx(w0 + 32);
+      }
+      for (int64_t base = w0; base < w1; base += 32) {
+        const int cnt = (int)min((int64_t)32, w1 - base);
+        const bool valid = lane < cnt;
+        uint32_t gp = ngp;
+        if (MODE == HM_ROOT && valid) {
+          const int64_t ridx = base + lane + poff;
+          float g = __fmul_rn(nw, __fsub_rn(np_, ny));
+          float h = nw;
+          if (row_sampled_out(a.seed, a.target, t, a.row_offset + ridx, a.subsample)) {
+            g = 0.f;
+            h = 0.f;
+          }
+          gp = pack_gp(quantize(g, scale_g), quantize(h, scale_h));
+          a.gp_root[ridx] = gp;
+        }
+        // previous row of lane 0: the last staged row of the previous batch (read before it is overwritten)
+        uint4 pv0 = nc0, pv1 = nc1;
+        if (lane == 0 && !fresh) {
+          pv0 = *reinterpret_cast<const uint4*>(wb + 32 * H2_ROWB);
+          pv1 = *reinterpret_cast<const uint4*>(wb + 32 * H2_ROWB + 16);
+        }
+        __syncwarp();   // previous batch fully consumed
+        uint8_t* myrow = wb + (lane + 1) * H2_ROWB;
+        *reinterpret_cast<uint4*>(myrow) = nc0;
+        *reinterpret_cast<uint4*>(myrow + 16) = nc1;
+        if (MODE == HM_UPDROOT && valid) {
+          // O9 for tree t (route the lane's own staged row, p += v), then O4 for tree t+1
+          const int64_t ridx = base + lane + poff;
+          int k = 0;
+          for (int s2 = 0; s2 < a.D; ++s2) {
+            const int f = s_feat[k];
+            const int nk = 2 * k + 1 + (myrow[f & 31] > s_bin[k] ? 1 : 0);
+            k = f >= 0 ? nk : k;
+          }
+          const float pn = __fadd_rn(np_, s_val[k]);   // one fp32 rounding, tree order
+          a.p[ridx] = pn;
+          if (has_next) {
+            float g = __fmul_rn(nw, __fsub_rn(pn, ny));
+            float h = nw;
+            if (row_sampled_out(a.seed, a.target, t + 1, a.row_offset + ridx, a.subsample)) {
+              g = 0.f;
+              h = 0.f;
+            }
+            mg = fmaxf(mg, fabsf(g));
+            mh = fmaxf(mh, h);
+            gp = pack_gp(quantize(g, scale_g), quantize(h, scale_h));
+            a.gp_root[ridx] = gp;
+          }
+        }
+        __syncwarp();
+        const uint4 cc0 = nc0, cc1 = nc1;   // this batch's row (the prefetch below overwrites nc*)
+        if (lane > 0) {
+          pv0 = *reinterpret_cast<const uint4*>(myrow - H2_ROWB);
+          pv1 = *reinterpret_cast<const uint4*>(myrow - H2_ROWB + 16);
+        }
+        if (base + 32 < w1) {   // prefetch the next batch (and the row indices of the one after)
+          load_batch(base + 32);
+          load_ridx(base + 64);
+        }
+        if (!hist_on) continue;
+        // ---- row side: change mask of this lane's row (bit 8j+7-q = feature 4q+j)
+        uint32_t m = 0;
+        if (valid) {
+          m = byte_ne_hi(cc0.x ^ pv0.x) | (byte_ne_hi(cc0.y ^ pv0.y) >> 1) | (byte_ne_hi(cc0.z ^ pv0.z) >> 2) |
+              (byte_ne_hi(cc0.w ^ pv0.w) >> 3) | (byte_ne_hi(cc1.x ^ pv1.x) >> 4) | (byte_ne_hi(cc1.y ^ pv1.y) >> 5) |
+              (byte_ne_hi(cc1.z ^ pv1.z) >> 6) | (byte_ne_hi(cc1.w ^ pv1.w) >> 7);
+        }
+        const int32_t qg = valid ? gp_g(gp) : 0;
+        const uint32_t qh = valid ? (uint32_t)gp_h(gp) : 0u;
+        if (ucol >= 0 && valid) {   // users column, row-parallel into the dense per-bin histogram
+          const uint32_t ua = sub + (uint32_t)myrow[ucol] * 4u;
+          asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(ua), "r"(qg) : "memory");
+          asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(ua), "r"(qh), "n"(kBins * 4) : "memory");
+        }
+        // inclusive prefix sums of the pairs over the batch's rows
+        int32_t pg = qg;
+        uint32_t ph = qh;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t ug = __shfl_up_sync(0xffffffffu, pg, o);
+          const uint32_t uh = __shfl_up_sync(0xffffffffu, ph, o);
+          if (lane >= o) {
+            pg += ug;
+            ph += uh;
+          }
+        }
+        const int32_t tot_g = __shfl_sync(0xffffffffu, pg, 31);
+        const uint32_t tot_h = __shfl_sync(0xffffffffu, ph, 31);
+        // ---- feature side
+        uint32_t M = warp_transpose32(m, lane);
+        if (fresh) {
+          if (active) cur = (uint32_t)(wb[H2_ROWB + myf] * H2_PAD + myf) * 4u;   // run starts at row 0
+          fresh = false;
+        }
+        if (!active) M = 0;
+        const bool heavy = __popc(M) > H2_HEAVY;
+        uint32_t Ml = heavy ? 0u : M;
+        int32_t bg = 0;      // prefix before the current run's first row in this batch
+        uint32_t bh = 0;
+        while (__any_sync(0xffffffffu, Ml != 0u)) {
+          const int r = __ffs(Ml) - 1;
+          const int32_t pgr = __shfl_sync(0xffffffffu, pg, (r - 1) & 31);
+          const uint32_t phr = __shfl_sync(0xffffffffu, ph, (r - 1) & 31);
+          if (Ml) {
+            const int32_t vg = r ? pgr : 0;
+            const uint32_t vh = r ? phr : 0u;
+            red2(sgb + cur, acc_g + (vg - bg), acc_h + (vh - bh));
+            acc_g = 0;
+            acc_h = 0;
+            bg = vg;
+            bh = vh;
+            cur = (uint32_t)(wb[(r + 1) * H2_ROWB + myf] * H2_PAD + myf) * 4u;
+            Ml &= Ml - 1u;
+          }
+        }
+        if (!heavy) {
+          acc_g += tot_g - bg;
+          acc_h += tot_h - bh;
+        }
+        // heavy features: row-parallel, one feature at a time
+        unsigned hm = __ballot_sync(0xffffffffu, heavy);
+        while (hm) {
+          const int hl = __ffs(hm) - 1;
+          hm &= hm - 1u;
+          const int hf = h2_feat(hl);
+          if (lane == hl && (acc_g | (int32_t)acc_h)) red2(sgb + cur, acc_g, acc_h);   // pending run of earlier batches
+          if (valid) red2(sgb + (uint32_t)(myrow[hf] * H2_PAD + hf) * 4u, qg, qh);
+          if (lane == hl) {
+            acc_g = 0;
+            acc_h = 0;
+            cur = (uint32_t)(wb[cnt * H2_ROWB + hf] * H2_PAD + hf) * 4u;   // the batch's last row
+          }
+        }
+      }
+      if (active && !fresh && (acc_g | (int32_t)acc_h)) red2(sgb + cur, acc_g, acc_h);
+      __syncthreads();
+      if (ucol >= 0) {   // the users column's cells (untouched by its lane) from the dense histogram
+        for (int b = tid; b < kBins; b += H2_THREADS) {
+          sg[b * H2_PAD + ucol] = sug[b];
+          sh[b * H2_PAD + ucol] = suh[b];
+          sug[b] = 0;
+          suh[b] = 0;
+        }
+        __syncthreads();
+      }
+      // flush: zero-skipping int64 atomics into the node histogram ([f][b] layout)
+      for (int i = tid; i < kHistBins; i += H2_THREADS) {
+        const int b = i >> 5, f = i & 31;
+        const int32_t g = sg[b * H2_PAD + f];
+        const uint32_t h = sh[b * H2_PAD + f];
+        if (g != 0 || h != 0) {
+          atomicAdd(reinterpret_cast<unsigned long long*>(&Hg[f * kBins + b]), (unsigned long long)(long long)g);
+          atomicAdd(reinterpret_cast<unsigned long long*>(&Hh[f * kBins + b]), (unsigned long long)h);
+          sg[b * H2_PAD + f] = 0;
+          sh[b * H2_PAD + f] = 0;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (MODE == HM_UPDROOT && has_next) {   // tree t+1's maxima (float bits of non-negatives order as uints)
+    for (int o = 16; o > 0; o >>= 1) {
+      mg = fmaxf(mg, __shfl_xor_sync(0xffffffffu, mg, o));
+      mh = fmaxf(mh, __shfl_xor_sync(0xffffffffu, mh, o));
+    }
+    if (lane == 0) {
+      atomicMax(&a.maxg[t + 1], __float_as_uint(mg));
+      atomicMax(&a.maxh[t + 1], __float_as_uint(mh));
+    }
+  }
+}
+
+// histogram inner loop: run-length k_hist (default) or change-mask k_hist2 (LLMP_HIST2=1; a bit
+// mask selects k_hist2 per mode: 1 root, 2 level, 4 fused update + root)
+static int hist1_mask() {
+  static const int v = getenv("LLMP_HIST2") ? 7 & ~(atoi(getenv("LLMP_HIST2")) == 1 ? 7 : atoi(getenv("LLMP_HIST2"))) : 7;
+  return v;
+}
+static bool use_hist1() { return hist1_mask() == 7; }
+
 // zero the root histogram slot when k_hist<ROOT> is going to (re)build it (see root_needed)
 __global__ void k_root_fix(const FitArgs a) {
   if (!root_needed(a, *a.d_tree)) return;
@@ -673,6 +1047,7 @@ constexpr int PT_OWN = 64;                       // tiles per scatter CTA at mos
 struct PartWs {
   int32_t* tile_left;    // [max tiles] left rows per tile
   uint32_t* bits;        // [max tiles][PT_WORDS] left bits
+  int* ticket;           // k_part's arrival counter (self-resetting)
 };
 
 // tile and row prefixes over the level's split parents (computed by each CTA; NP <= 512)
@@ -940,6 +1315,121 @@ __global__ void __launch_bounds__(PT_THREADS) k_pscatter2(const FitArgs a, const
 }
 
 // ---------------------------------------------------------------------------------------------
+// Single-pass partition (default; the two-kernel stable form above is LLMP_PART2=1).  Every
+// histogram is an integer sum, so the order of the rows inside a child segment cannot change any
+// result — only which CTA processes which rows.  Each 4096-row tile of a split parent j therefore
+// reserves its block of each child with one global atomic per child instead of waiting for a
+// prefix over all tiles: the left child fills the parent's own range [s_j, s_j + n_j) of the other
+// ping-pong buffer from the bottom (cursor C.cnt[2j]), the right child from the top (cursor
+// C.cnt[2j+1]); inside a block the rows keep their order (ballot + per-warp prefix table), so the
+// children are contiguous runs of the parent's order, permuted block-wise.  Row indices are read
+// once; there is no tile-count array, no scan, no second launch.  The cursors start at 0 (zeroed
+// by the split kernel of level d-1); the last CTA (ticket) writes both children's starts.
+__global__ void __launch_bounds__(PT_THREADS) k_part(const FitArgs a, const int d, int* ticket) {
+  __shared__ int s_tile_pref[MAX_PIECES + 1];
+  __shared__ int64_t s_seq_pref[MAX_PIECES + 1];
+  __shared__ int s_w[PT_THREADS / 32];
+  __shared__ int64_t s_w64[PT_THREADS / 32];
+  __shared__ __align__(16) uint32_t s_bits[PT_WORDS];   // the tile's ballot words, group = (q, warp)
+  __shared__ __align__(16) int s_pre[PT_WORDS];         // exclusive left prefix of each group
+  __shared__ int64_t s_lb, s_rb;                        // the tile's block offsets (left from the bottom, right from the top)
+  __shared__ int s_last;
+  const int NP = 1 << (d - 1);
+  const LevelView& P = a.lv[d - 1];
+  const LevelView& C = a.lv[d];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  {   // zero the built-child histogram slots [0, NP) of this level for split parents
+    int4* Hz = reinterpret_cast<int4*>(a.H[d & 1]);
+    const size_t per_slot = SLOT / 2;  // int4 per slot
+    const size_t total = (size_t)NP * per_slot;
+    for (size_t e = (size_t)blockIdx.x * PT_THREADS + tid; e < total; e += (size_t)gridDim.x * PT_THREADS) {
+      const int j = (int)(e / per_slot);
+      if (P.split_f[j] >= 0) Hz[e] = make_int4(0, 0, 0, 0);
+    }
+  }
+  parent_prefixes(a, d, s_tile_pref, s_seq_pref, s_w, s_w64);
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t* const rin_all = a.sr[(d - 1) & 1];
+  uint32_t* const rout = a.sr[d & 1];
+  for (int t = blockIdx.x; t < s_tile_pref[NP]; t += gridDim.x) {
+    const int j = parent_of_tile(s_tile_pref, NP, t);
+    const int64_t cnt_j = (d == 1) ? a.n : P.cnt[j];
+    const int64_t start_j = (d == 1) ? 0 : P.start[j];
+    const int64_t o = (int64_t)(t - s_tile_pref[j]) * PT_TILE;
+    const int len = (int)min((int64_t)PT_TILE, cnt_j - o);
+    const int f = P.split_f[j], b = P.split_b[j];
+    const uint8_t* col = a.codesT + (size_t)f * a.ldT;
+    const uint32_t* rin = rin_all + start_j + o;
+    uint32_t ridx[PT_ITEMS];
+#pragma unroll
+    for (int q = 0; q < PT_ITEMS; ++q) {
+      const int k = q * PT_THREADS + tid;
+      ridx[q] = k < len ? ((d == 1) ? (uint32_t)(o + k) : rin[k]) : 0u;
+    }
+    uint32_t code[PT_ITEMS];
+#pragma unroll
+    for (int q = 0; q < PT_ITEMS; ++q) code[q] = __ldg(col + ridx[q]);
+    unsigned mw[PT_ITEMS];
+#pragma unroll
+    for (int q = 0; q < PT_ITEMS; ++q) {
+      const int k = q * PT_THREADS + tid;
+      mw[q] = __ballot_sync(0xffffffffu, k < len && code[q] <= (uint32_t)b);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int q = 0; q < PT_ITEMS; ++q) s_bits[q * (PT_THREADS / 32) + warp] = mw[q];
+    }
+    __syncthreads();
+    if (warp == 0) {   // group prefixes: lane L takes words 4L .. 4L+3; one atomic per child
+      const uint4 m4 = reinterpret_cast<const uint4*>(s_bits)[lane];
+      const int c0 = __popc(m4.x), c1 = __popc(m4.y), c2 = __popc(m4.z);
+      const int lsum = c0 + c1 + c2 + __popc(m4.w);
+      int inc = lsum;
+      for (int off = 1; off < 32; off <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += u;
+      }
+      const int ex = inc - lsum;
+      reinterpret_cast<int4*>(s_pre)[lane] = make_int4(ex, ex + c0, ex + c0 + c1, ex + c0 + c1 + c2);
+      if (lane == 31) {
+        const int L = inc, R = len - inc;
+        s_lb = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(&C.cnt[2 * j]), (unsigned long long)L);
+        s_rb = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(&C.cnt[2 * j + 1]), (unsigned long long)R) + R;
+        if (a.units) atomicAdd(&a.units[KC_PARTITION], (unsigned long long)len);
+      }
+    }
+    __syncthreads();
+    const int64_t lbase = start_j + s_lb;                // left rows: lbase + (lefts before the row)
+    const int64_t rtop = start_j + cnt_j - s_rb;         // right rows: rtop + (rights before the row)
+#pragma unroll
+    for (int q = 0; q < PT_ITEMS; ++q) {
+      const int word = q * (PT_THREADS / 32) + warp;
+      const int k = q * PT_THREADS + tid;
+      if (k < len) {
+        const int pre = s_pre[word] + __popc(mw[q] & lt);   // lefts before row k in the tile
+        const bool left = (mw[q] >> lane) & 1u;
+        rout[left ? lbase + pre : rtop + (k - pre)] = ridx[q];
+      }
+    }
+    __syncthreads();   // s_bits / s_pre / s_lb / s_rb are reused by the next tile
+  }
+  // the last CTA writes the children's starts (counts are final once every CTA has arrived)
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int jj = tid; jj < NP; jj += PT_THREADS) {
+    if (P.split_f[jj] < 0) continue;
+    const int64_t sj = (d == 1) ? 0 : P.start[jj];
+    C.start[2 * jj] = sj;
+    C.start[2 * jj + 1] = sj + *reinterpret_cast<volatile int64_t*>(&C.cnt[2 * jj]);
+  }
+  if (tid == 0) *ticket = 0;
+}
+
+// ---------------------------------------------------------------------------------------------
 // split evaluation: one thread-block CLUSTER of 8 CTAs per node of level d, one WARP per
 // (node, feature f) — 4 warps per CTA.  Lane l owns bins 8l .. 8l+7; the warp forms the feature's
 // histogram (sibling = parent - built, exact int64, written back for the next level),
@@ -1107,7 +1597,7 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitArgs a, cons
   // ---- the node's reduction, by one warp: lane l takes feature l's result
   int rvalid, rb;
   double rloss;
-  int64_t rGL, rHL;
+  int64_t rGL, rHL, rG, rH;
   if constexpr (CL) {   // cluster launch: results exchanged through distributed shared memory
     cg::cluster_group cluster = cg::this_cluster();
     cluster.sync();
@@ -1121,6 +1611,8 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitArgs a, cons
     rloss = rf->loss;
     rGL = rf->GLq;
     rHL = rf->HLq;
+    rG = rf->Gq;
+    rH = rf->Hq;
     cluster.sync();
   } else {              // plain launch: the node's last-arriving warp (global ticket) reduces
     int last = 0;
@@ -1137,6 +1629,8 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitArgs a, cons
     rloss = rf->loss;
     rGL = rf->GLq;
     rHL = rf->HLq;
+    rG = rf->Gq;
+    rH = rf->Hq;
     if (lane == 0) V.done[k] = 0;
   }
   double ml = rvalid ? rloss : -INFINITY;
@@ -1154,12 +1648,13 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitArgs a, cons
   mf = __shfl_sync(0xffffffffu, mf, 0);
   mb = __shfl_sync(0xffffffffu, mb, 0);
   const int64_t GLs = __shfl_sync(0xffffffffu, rGL, mf), HLs = __shfl_sync(0xffffffffu, rHL, mf);
+  // node totals from feature 0 (always < F): the histogram kernels leave features >= F empty
+  const int64_t GqN = __shfl_sync(0xffffffffu, rG, 0), HqN = __shfl_sync(0xffffffffu, rH, 0);
   if (lane != 0) return;
   int32_t* const tfeat = a.tfeat + (size_t)t * a.nn;
   int32_t* const tbin = a.tbin + (size_t)t * a.nn;
   float* const tthr = a.tthr + (size_t)t * a.nn;
   float* const tval = a.tval + (size_t)t * a.nn;
-  const int64_t GqN = Gq, HqN = Hq;   // node totals (every feature's histogram sums to them; this warp's)
   const double G = dequant(GqN, sgi), H = dequant(HqN, shi);
   const double wP = calc_weight(G, H, lo, hi, lambda, mcw);
   const int gk = (1 << d) - 1 + k;
@@ -1183,6 +1678,8 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitArgs a, cons
     tval[gk] = 0.0f;
     if (d + 1 < a.D) {
       const LevelView& N = a.lv[d + 1];
+      N.cnt[2 * k] = 0;   // k_part's child cursors
+      N.cnt[2 * k + 1] = 0;
       N.lo[2 * k] = loL;
       N.hi[2 * k] = hiL;
       N.lo[2 * k + 1] = loR;
@@ -1558,6 +2055,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   static const bool use_root2 = getenv("LLMP_ROOT2") && atoi(getenv("LLMP_ROOT2")) != 0;
   static const bool fused = !use_root2 && !(getenv("LLMP_NOFUSE") && atoi(getenv("LLMP_NOFUSE")) != 0);
   static const bool urow = !(getenv("LLMP_NO_UROW") && atoi(getenv("LLMP_NO_UROW")) != 0);
+  static const int hist1 = hist1_mask();
+  static const bool part2 = getenv("LLMP_PART2") && atoi(getenv("LLMP_PART2")) != 0;   // two-kernel stable partition
   FitArgs A[2];
   PartWs PW[2];
   for (int tg = 0; tg < 2; ++tg) {
@@ -1634,6 +2133,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     LLMP_CUDA(cudaMemsetAsync(d_tab.p, 0, d_tab.bytes, s));
     PW[tg].tile_left = ctx->workspace("tile_left" + sx, (size_t)max_tiles * 4).as<int32_t>();
     PW[tg].bits = ctx->workspace("tile_bits" + sx, (size_t)max_tiles * PT_WORDS * 4).as<uint32_t>();
+    PW[tg].ticket = ctx->workspace("part_ticket" + sx, sizeof(int)).as<int>();
+    LLMP_CUDA(cudaMemsetAsync(PW[tg].ticket, 0, sizeof(int), s));
   }
 
   const int hist_grid = 2 * ctx->sms;
@@ -1647,6 +2148,10 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_UPDROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    HIST_SMEM + UPDROOT_TREE_SMEM));
     LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
+    LLMP_CUDA(cudaFuncSetAttribute(k_hist2<HM_ROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, H2_SMEM));
+    LLMP_CUDA(cudaFuncSetAttribute(k_hist2<HM_LEVEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, H2_SMEM));
+    LLMP_CUDA(cudaFuncSetAttribute(k_hist2<HM_UPDROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   H2_SMEM + UPDROOT_TREE_SMEM));
     attr_set = true;
   }
   const DbgArgs nodbg{};
@@ -1701,27 +2206,37 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     if (fused) LLMP_LAUNCH(ctx, KC_MISC, 0, k_root_fix, 1, 1024, 0, a);
     else LLMP_CUDA(cudaMemsetAsync(a.H[0], 0, (size_t)SLOT * 8, st));
     if (use_root2) LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist_root2, hist_grid, R2_THREADS, R2_SMEM, a);
-    else LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist<HM_ROOT>, hist_grid, HIST_THREADS, HIST_SMEM, a, 0, 0, nodbg);
+    else if (hist1 & 1) LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist<HM_ROOT>, hist_grid, HIST_THREADS, HIST_SMEM, a, 0, 0, nodbg);
+    else LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist2<HM_ROOT>, hist_grid, H2_THREADS, H2_SMEM, a, 0, 0, nodbg);
     allreduce_sum_i64(ctx, a.H[0], SLOT);
     split(a, 0);
     for (int d = 1; d < D; ++d) {
       const int tiles_d = (int)((n + PT_TILE - 1) / PT_TILE) + (1 << (d - 1));
       // persistent tile loops; a scatter CTA owns at most PT_OWN tiles
       const int pgrid = std::max(std::min(tiles_d, 5 * ctx->sms), (tiles_d + PT_OWN - 1) / PT_OWN);
-      LLMP_LAUNCH(ctx, KC_PARTITION, n, k_pcount, pgrid, PT_THREADS, 0, a, d, pw);
-      LLMP_LAUNCH(ctx, KC_PARTITION, 0, k_pscatter2, pgrid, PT_THREADS, 0, a, d, pw);
+      if (part2) {
+        LLMP_LAUNCH(ctx, KC_PARTITION, n, k_pcount, pgrid, PT_THREADS, 0, a, d, pw);
+        LLMP_LAUNCH(ctx, KC_PARTITION, 0, k_pscatter2, pgrid, PT_THREADS, 0, a, d, pw);
+      } else {
+        LLMP_LAUNCH(ctx, KC_PARTITION, n, k_part, std::min(tiles_d, 6 * ctx->sms), PT_THREADS, 0, a, d, pw.ticket);
+      }
       if (ctx->nranks > 1) {   // every rank must histogram the same (globally smaller) child
         LLMP_CUDA(cudaMemcpyAsync(a.lv[d].gcnt, a.lv[d].cnt, ((size_t)1 << d) * 8, cudaMemcpyDeviceToDevice, st));
         allreduce_sum_i64(ctx, a.lv[d].gcnt, (size_t)1 << d);
       }
-      LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hist_grid, HIST_THREADS, HIST_SMEM, a, d, 0, nodbg);
+      if (hist1 & 2) LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hist_grid, HIST_THREADS, HIST_SMEM, a, d, 0, nodbg);
+      else LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist2<HM_LEVEL>, hist_grid, H2_THREADS, H2_SMEM, a, d, 0, nodbg);
       allreduce_sum_i64(ctx, a.H[d & 1], (size_t)SLOT << (d - 1));
       split(a, d);
     }
     if (fused) {   // update tree t + root histogram of tree t+1 (into the now free root slot)
       LLMP_CUDA(cudaMemsetAsync(a.H[0], 0, (size_t)SLOT * 8, st));
-      LLMP_LAUNCH(ctx, KC_UPDATE, n, k_hist<HM_UPDROOT>, hist_grid, HIST_THREADS, HIST_SMEM + UPDROOT_TREE_SMEM, a, 0,
-                  0, nodbg);
+      if (hist1 & 4)
+        LLMP_LAUNCH(ctx, KC_UPDATE, n, k_hist<HM_UPDROOT>, hist_grid, HIST_THREADS, HIST_SMEM + UPDROOT_TREE_SMEM, a, 0,
+                    0, nodbg);
+      else
+        LLMP_LAUNCH(ctx, KC_UPDATE, n, k_hist2<HM_UPDROOT>, hist_grid, H2_THREADS, H2_SMEM + UPDROOT_TREE_SMEM, a, 0, 0,
+                    nodbg);
     } else {
       LLMP_LAUNCH(ctx, KC_UPDATE, n, k_update, upd_grid, UPD_THREADS, 0, a);
     }
@@ -1819,9 +2334,13 @@ void debug_histogram(Ctx* ctx, const uint8_t* codes, int64_t n, const int32_t* i
   static bool attr_set = false;
   if (!attr_set) {
     LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
+    LLMP_CUDA(cudaFuncSetAttribute(k_hist2<HM_DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize, H2_SMEM));
     attr_set = true;
   }
-  LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist<HM_DEBUG>, 2 * ctx->sms, HIST_THREADS, HIST_SMEM, a, 0, 0, dbg);
+  if (use_hist1())
+    LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist<HM_DEBUG>, 2 * ctx->sms, HIST_THREADS, HIST_SMEM, a, 0, 0, dbg);
+  else
+    LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist2<HM_DEBUG>, 2 * ctx->sms, H2_THREADS, H2_SMEM, a, 0, 0, dbg);
   LLMP_CUDA(cudaMemcpyAsync(Hg, d_out.p, kHistBins * 8, cudaMemcpyDeviceToHost, ctx->stream));
   LLMP_CUDA(cudaMemcpyAsync(Hh, d_out.as<int64_t>() + kHistBins, kHistBins * 8, cudaMemcpyDeviceToHost, ctx->stream));
   LLMP_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -1,7 +1,8 @@
 """Subprocess helper for test_gpu_parity.test_kernel_variants: the kernel-variant switches
-(LLMP_NOFUSE, LLMP_ROOT2, LLMP_SPLIT_CLUSTER, LLMP_NO_UROW) are read once per process, so each variant is checked in
-its own interpreter.  Fits paper-shaped (C2) and random (S1, ragged) data through the C-ABI in
-both execution modes (graph replay, instrumented plain launches) and compares with the oracle."""
+(LLMP_NOFUSE, LLMP_ROOT2, LLMP_SPLIT_CLUSTER, LLMP_NO_UROW, LLMP_HIST2, LLMP_PART2) are read once per process, so each variant is checked in
+its own interpreter.  Fits paper-shaped (C1 with 12 features, C2) and random (S1, ragged) data through the
+C-ABI in both execution modes (graph replay, instrumented plain launches) and compares with the oracle;
+checks the histogram test hook (the variant's histogram kernel) against brute-force sums."""
 import os
 import sys
 
@@ -29,7 +30,19 @@ def same(om, ge):
 
 def main():
     ctx = lp.Context(0, torch.cuda.current_stream())
-    cases = [(synth.make("C2"), None, dict(n_trees=12, max_depth=7)),
+    rng = np.random.default_rng(3)
+    codes = np.repeat(rng.integers(0, 256, (2000 // 7 + 1, 32)), 7, axis=0)[:2000].astype(np.uint8)
+    codes[:, 5] = rng.integers(0, 16, 2000)
+    qg = rng.integers(-(1 << 14), (1 << 14) + 1, 2000).astype(np.int32)
+    qh = rng.integers(0, (1 << 14) + 1, 2000).astype(np.int32)
+    Og, Oh = oracle.node_hist(codes, np.arange(2000), qg, qh)
+    Gg, Gh = lp.debug_histogram(ctx, torch.from_numpy(codes).cuda(), torch.from_numpy(qg).cuda(),
+                                torch.from_numpy(qh).cuda())
+    if not (np.array_equal(Og, Gg) and np.array_equal(Oh, Gh)):
+        print("MISMATCH histogram hook")
+        return 1
+    cases = [(synth.make("C1"), None, dict(n_trees=20, max_depth=4)),
+             (synth.make("C2"), None, dict(n_trees=12, max_depth=7)),
              (synth.make_s1(70001, seed=5), "w", dict(n_trees=4, max_depth=8, use_eq4_weights=0)),
              (synth.make_s1(4097, seed=6), "w", dict(n_trees=3, max_depth=6, use_eq4_weights=0))]
     for d, wk, kw in cases:
