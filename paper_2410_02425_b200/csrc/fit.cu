@@ -8,13 +8,14 @@
 //                                gradient computation + quantisation (writes gp_root)
 //                 k_split3(0)
 //                 for d = 1..D-1:
-//                   k_pcount / k_pscatter2(d)
-//                                   stable partition of the split parents' row indices into
-//                                   children (independent 4096-row tiles); zeroes the child hists
+//                   k_part(d)       partition of the split parents' row indices into children
+//                                   (4096-row tiles, one atomic reservation per child per tile);
+//                                   zeroes the built-child histograms
 //                   k_hist<LEVEL>   histogram of the smaller child of each split parent (codes
 //                                   and packed gradient pairs gathered by row index)
 //                   k_split3(d)     sibling = parent - built; prefix scan; fp64 gains; argmax
-//                 k_update(t)    route every row to its leaf, p += v, next tree's max|g|
+//                 k_hist<UPDROOT>(t)  route every row to its leaf, p += v, and build tree t+1's
+//                                   root histogram (k_update when unfused)
 //
 // No host synchronisation happens inside the tree loop; all decisions live on the device.
 #include <float.h>
@@ -50,7 +51,7 @@ __device__ __forceinline__ double exp2i(int e) {  // exact 2^e for e in [-1022, 
 }
 
 struct LevelView {
-  int64_t* start;    // [2^d] segment start in the 2n state buffer (A = [0,n), B = [n,2n))
+  int64_t* start;    // [2^d] segment start in the row-index buffer (a child lies inside its parent's range)
   int64_t* cnt;      // [2^d] local rows
   int64_t* gcnt;     // [2^d] global rows (== cnt for one rank)
   double* lo;        // [2^d] monotone bounds
@@ -78,7 +79,7 @@ struct FitArgs {
   const float* w;
   float* p;
   uint32_t* gp_root;
-  uint32_t* sr[2];   // row-index state (children: A = [0,n) left, B = [n,2n) right)
+  uint32_t* sr[2];   // row-index ping-pong buffers, n each (level d's segments in sr[d & 1])
   int64_t* H[2];
   LevelView lv[kMaxDepth + 1];
   const int* d_tree; // device-side index of the tree being grown (advanced by k_next_tree)
@@ -220,8 +221,14 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const
         const int64_t nL = C.gcnt[2 * tid], nR = C.gcnt[2 * tid + 1];
         side = (nL <= nR) ? 0 : 1;       // build the smaller child (global row count), ties -> left
         len = C.cnt[2 * tid + side];
-        pst = C.start[2 * tid + side];
-        if (blockIdx.x == 0) C.built[tid] = side;
+        // k_part: left child at the parent's start, right child after it
+        const int64_t ps = (d == 1) ? 0 : P.start[tid], cl = C.cnt[2 * tid];
+        pst = side ? ps + cl : ps;
+        if (blockIdx.x == 0) {
+          C.built[tid] = side;
+          C.start[2 * tid] = ps;
+          C.start[2 * tid + 1] = ps + cl;
+        }
       }
     }
     // block exclusive scan of len over 512 threads
@@ -536,8 +543,14 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitArgs a, const 
       const int64_t nL = C.gcnt[2 * tid], nR = C.gcnt[2 * tid + 1];
       side = (nL <= nR) ? 0 : 1;       // build the smaller child (global row count), ties -> left
       len = C.cnt[2 * tid + side];
-      pst = C.start[2 * tid + side];
-      if (blockIdx.x == 0) C.built[tid] = side;
+      // k_part: left child at the parent's start, right child after it
+      const int64_t ps = (d == 1) ? 0 : P.start[tid], cl = C.cnt[2 * tid];
+      pst = side ? ps + cl : ps;
+      if (blockIdx.x == 0) {
+        C.built[tid] = side;
+        C.start[2 * tid] = ps;
+        C.start[2 * tid + 1] = ps + cl;
+      }
     }
     __shared__ int64_t s_wsum[H2_WARPS];
     int64_t v = len;
@@ -1025,30 +1038,11 @@ __global__ void __launch_bounds__(R2_THREADS, 2) k_hist_root2(const FitArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// Stable partition of the split parents' rows (level d-1) into their children (level d), as three
-// independent-tile kernels (no inter-CTA waiting, no grid synchronisation):
-//   k_pcount   one CTA per 4096-row tile of a split parent: row index -> split-feature code
-//              (column-major byte) -> left bit; bits kept in a per-tile bitmask, count per tile;
-//              also zeroes the level's built-child histogram slots
-//   k_pscatter2 every CTA first scans the tile counts itself (global left prefix of its own
-//              tiles; CTA 0 also writes the child segment starts and counts), then, per tile, a
-//              stable warp-aggregated scatter of the row indices — left rows
-//              to region A = [0, n) at the global left prefix, right rows to region B = [n, 2n)
-//              at the global right prefix.  Each child segment is contiguous and keeps its
-//              parent's row order.  Only row indices move: the level histogram gathers codes and
-//              packed gradient pairs by row index.
+// Row partition of the split parents (level d-1) into their children (level d): see k_part.
 constexpr int PT_THREADS = 256;
 constexpr int PT_ITEMS = 16;
 constexpr int PT_TILE = PT_THREADS * PT_ITEMS;   // 4096 rows
 constexpr int PT_WORDS = PT_TILE / 32;           // bitmask words per tile
-
-constexpr int PT_OWN = 64;                       // tiles per scatter CTA at most (host grid sizing)
-
-struct PartWs {
-  int32_t* tile_left;    // [max tiles] left rows per tile
-  uint32_t* bits;        // [max tiles][PT_WORDS] left bits
-  int* ticket;           // k_part's arrival counter (self-resetting)
-};
 
 // tile and row prefixes over the level's split parents (computed by each CTA; NP <= 512)
 __device__ __forceinline__ void parent_prefixes(const FitArgs& a, int d, int* s_tile_pref, int64_t* s_seq_pref,
@@ -1117,223 +1111,26 @@ __device__ __forceinline__ int parent_of_tile(const int* s_tile_pref, int NP, in
   return lo;
 }
 
-__global__ void __launch_bounds__(PT_THREADS) k_pcount(const FitArgs a, const int d, const PartWs w) {
-  __shared__ int s_tile_pref[MAX_PIECES + 1];
-  __shared__ int64_t s_seq_pref[MAX_PIECES + 1];
-  __shared__ int s_w[PT_THREADS / 32];
-  __shared__ int64_t s_w64[PT_THREADS / 32];
-  const int NP = 1 << (d - 1);
-  const LevelView& P = a.lv[d - 1];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // zero the built-child histogram slots [0, NP) of this level for split parents
-  {
-    int4* Hz = reinterpret_cast<int4*>(a.H[d & 1]);
-    const size_t per_slot = SLOT / 2;  // int4 per slot
-    const size_t total = (size_t)NP * per_slot;
-    for (size_t e = (size_t)blockIdx.x * PT_THREADS + tid; e < total; e += (size_t)gridDim.x * PT_THREADS) {
-      const int j = (int)(e / per_slot);
-      if (P.split_f[j] >= 0) Hz[e] = make_int4(0, 0, 0, 0);
-    }
-  }
-  parent_prefixes(a, d, s_tile_pref, s_seq_pref, s_w, s_w64);
-  // persistent: the per-CTA prologue is amortised over a grid-stride loop of tiles
-  for (int t = blockIdx.x; t < s_tile_pref[NP]; t += gridDim.x) {
-  const int j = parent_of_tile(s_tile_pref, NP, t);
-  const int64_t cnt_j = (d == 1) ? a.n : P.cnt[j];
-  const int64_t start_j = (d == 1) ? 0 : P.start[j];
-  const int64_t o = (int64_t)(t - s_tile_pref[j]) * PT_TILE;
-  const int len = (int)min((int64_t)PT_TILE, cnt_j - o);
-  const int f = P.split_f[j], b = P.split_b[j];
-  const uint8_t* col = a.codesT + (size_t)f * a.ldT;
-  const uint32_t* rin = (d >= 2) ? a.sr[(d - 1) & 1] + start_j + o : nullptr;
-  uint32_t ridx[PT_ITEMS];
-#pragma unroll
-  for (int q = 0; q < PT_ITEMS; ++q) {
-    const int k = q * PT_THREADS + tid;
-    ridx[q] = k < len ? ((d == 1) ? (uint32_t)(o + k) : rin[k]) : 0u;
-  }
-  // all 16 code gathers in flight before any store (a global store between them would stop the
-  // compiler from hoisting the next load)
-  uint32_t code[PT_ITEMS];
-#pragma unroll
-  for (int q = 0; q < PT_ITEMS; ++q) code[q] = __ldg(col + ridx[q]);
-  int myl = 0;
-  unsigned mw[PT_ITEMS];
-#pragma unroll
-  for (int q = 0; q < PT_ITEMS; ++q) {
-    const int k = q * PT_THREADS + tid;
-    const bool left = k < len && code[q] <= (uint32_t)b;
-    myl += left;
-    mw[q] = __ballot_sync(0xffffffffu, left);
-  }
-  if (lane == 0) {
-#pragma unroll
-    for (int q = 0; q < PT_ITEMS; ++q) w.bits[(size_t)t * PT_WORDS + q * (PT_THREADS / 32) + warp] = mw[q];
-  }
-  for (int off = 16; off > 0; off >>= 1) myl += __shfl_xor_sync(0xffffffffu, myl, off);
-  if (lane == 0) s_w[warp] = myl;
-  __syncthreads();
-  if (tid == 0) {
-    int L = 0;
-    for (int w2 = 0; w2 < PT_THREADS / 32; ++w2) L += s_w[w2];
-    w.tile_left[t] = L;
-    if (a.units) atomicAdd(&a.units[KC_PARTITION], (unsigned long long)len);
-  }
-  __syncthreads();
-  }
-}
-
 // ---------------------------------------------------------------------------------------------
-// Warp-aggregated stable scatter (replaces a shared-memory reorder): in a tile, rows are ordered
-// (q, warp, lane) with row = q*256 + warp*32 + lane, and k_pcount stored exactly the ballot of each
-// (q, warp) group.  Each warp derives every group's exclusive left prefix from those 128 words
-// (popc + warp scan, no block barrier), then each lane writes its row straight to global memory:
-// lefts at lp + prefix + popc(ballot & lanes_below), rights likewise — each group's lefts and
-// rights land in two contiguous runs, so the stores stay coalesced.
-__global__ void __launch_bounds__(PT_THREADS) k_pscatter2(const FitArgs a, const int d, const PartWs w) {
-  __shared__ __align__(16) int s_pre[PT_THREADS / 32][PT_WORDS];        // per warp: group prefixes of a tile
-  __shared__ __align__(16) uint32_t s_bits[PT_THREADS / 32][PT_WORDS];  // per warp: the tile's ballot words
+// Single-pass partition.  Every histogram is an integer sum, so the order of the rows inside a
+// child segment cannot change any result — only which CTA processes which rows.  Each 4096-row
+// tile of a split parent j therefore reserves its block of each child with one global atomic per
+// child instead of waiting for a prefix over all tiles: the left child fills the parent's own range
+// [s_j, s_j + n_j) of the other ping-pong buffer from the bottom (cursor C.cnt[2j]), the right child
+// from the top (cursor C.cnt[2j+1]); inside a block the rows keep their order (ballot + per-group
+// prefix table), so the children are block-wise permutations of runs of the parent's order.  Row
+// indices are read once; the next tile's row indices are loaded while this tile waits for its
+// reservation.  The cursors start at 0 (zeroed by the split kernel of level d-1); the children's
+// starts follow from the counts (s_j and s_j + n_L; written by the level histogram kernel).
+constexpr int PT_CTAS_PER_SM = 4;
+__global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitArgs a, const int d) {
   __shared__ int s_tile_pref[MAX_PIECES + 1];
   __shared__ int64_t s_seq_pref[MAX_PIECES + 1];
   __shared__ int s_w[PT_THREADS / 32];
   __shared__ int64_t s_w64[PT_THREADS / 32];
-  __shared__ int64_t s_own[PT_OWN];                       // global left prefix of this CTA's tiles
-  __shared__ int64_t s_ls[MAX_PIECES], s_le[MAX_PIECES];  // CTA 0: left prefix at parent start / end
-  const int NP = 1 << (d - 1);
-  const LevelView& P = a.lv[d - 1];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  parent_prefixes(a, d, s_tile_pref, s_seq_pref, s_w, s_w64);
-  // ---- exclusive scan of the tile left counts (k_pcount), contiguous chunk per thread; the
-  // common case (<= 16 tiles per thread, <= 4096 tiles) keeps the chunk in registers
-  {
-    const int T = s_tile_pref[NP];
-    const int c0 = (int)((int64_t)T * tid / PT_THREADS), c1 = (int)((int64_t)T * (tid + 1) / PT_THREADS);
-    int v[16];
-    int64_t local = 0;
-    for (int b0 = c0; b0 < c1; b0 += 16) {
-#pragma unroll
-      for (int q = 0; q < 16; ++q) v[q] = (b0 + q < c1) ? w.tile_left[b0 + q] : 0;
-#pragma unroll
-      for (int q = 0; q < 16; ++q) local += v[q];
-    }
-    int64_t inc = local;
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t u = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += u;
-    }
-    __syncthreads();   // s_w64 was used by parent_prefixes
-    if (lane == 31) s_w64[warp] = inc;
-    __syncthreads();
-    int64_t run = inc - local;
-    for (int w2 = 0; w2 < warp; ++w2) run += s_w64[w2];
-    const int G = gridDim.x, bid = blockIdx.x;
-    int nxt = c0 + ((bid - c0 % G) + G) % G;   // this CTA's first tile (t = bid mod G) at or after c0
-    for (int b0 = c0; b0 < c1; b0 += 16) {
-      if (c1 - c0 > 16) {   // rare: reload this round of the chunk
-#pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] = (b0 + q < c1) ? w.tile_left[b0 + q] : 0;
-      }
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const int t = b0 + q;
-        if (t < c1) {
-          if (t == nxt) {
-            s_own[t / G] = run;
-            nxt += G;
-          }
-          if (bid == 0) {
-            const int j = parent_of_tile(s_tile_pref, NP, t);
-            if (t == s_tile_pref[j]) s_ls[j] = run;
-            if (t == s_tile_pref[j + 1] - 1) s_le[j] = run + v[q];
-          }
-          run += v[q];
-        }
-      }
-    }
-    __syncthreads();
-    if (bid == 0) {   // child segments: lefts in region A at the parent's left prefix, rights in B
-      const LevelView& C = a.lv[d];
-      for (int j = tid; j < NP; j += PT_THREADS) {
-        if (P.split_f[j] < 0) continue;
-        const int64_t cnt_j = (d == 1) ? a.n : P.cnt[j];
-        const int64_t nl = s_le[j] - s_ls[j];
-        C.start[2 * j] = s_ls[j];
-        C.start[2 * j + 1] = a.n + (s_seq_pref[j] - s_ls[j]);
-        C.cnt[2 * j] = nl;
-        C.cnt[2 * j + 1] = cnt_j - nl;
-      }
-    }
-  }
-  const uint32_t lt = (1u << lane) - 1u;
-  uint32_t* rout = a.sr[d & 1];
-  for (int t = blockIdx.x; t < s_tile_pref[NP]; t += gridDim.x) {
-    const int j = parent_of_tile(s_tile_pref, NP, t);
-    const int64_t cnt_j = (d == 1) ? a.n : P.cnt[j];
-    const int64_t start_j = (d == 1) ? 0 : P.start[j];
-    const int64_t o = (int64_t)(t - s_tile_pref[j]) * PT_TILE;
-    const int len = (int)min((int64_t)PT_TILE, cnt_j - o);
-    const uint32_t* rin = (d >= 2) ? a.sr[(d - 1) & 1] + start_j + o : nullptr;
-    const uint32_t* bw = w.bits + (size_t)t * PT_WORDS;
-    // all of the warp's row indices in flight first (independent of the ballot words)
-    uint32_t rv[PT_ITEMS];
-#pragma unroll
-    for (int q = 0; q < PT_ITEMS; ++q) {
-      const int k = q * PT_THREADS + warp * 32 + lane;
-      rv[q] = (k < len) ? ((d == 1) ? (uint32_t)(o + k) : rin[k]) : 0u;
-    }
-    // exclusive left prefix of every (q, warp) group, in this warp's table: lane L handles words
-    // 4L .. 4L+3 (popc + warp scan, no block barrier)
-    const uint4 mw = *reinterpret_cast<const uint4*>(bw + 4 * lane);
-    const int c0 = __popc(mw.x), c1 = __popc(mw.y), c2 = __popc(mw.z);
-    const int lsum = c0 + c1 + c2 + __popc(mw.w);
-    int inc = lsum;
-    for (int off = 1; off < 32; off <<= 1) {
-      const int u = __shfl_up_sync(0xffffffffu, inc, off);
-      if (lane >= off) inc += u;
-    }
-    const int ex = inc - lsum;
-    __syncwarp();   // the previous tile's table reads are done
-    reinterpret_cast<int4*>(s_pre[warp])[lane] = make_int4(ex, ex + c0, ex + c0 + c1, ex + c0 + c1 + c2);
-    reinterpret_cast<uint4*>(s_bits[warp])[lane] = mw;
-    __syncwarp();
-    const int64_t lp = s_own[t / gridDim.x];
-    const int64_t rbase = a.n + (s_seq_pref[j] + o - lp);   // global right prefix at the tile start
-#pragma unroll
-    for (int q = 0; q < PT_ITEMS; ++q) {
-      const int word = q * (PT_THREADS / 32) + warp;
-      const int pre = s_pre[warp][word];
-      const uint32_t m = s_bits[warp][word];
-      const int k = q * PT_THREADS + warp * 32 + lane;
-      if (k < len) {
-        const bool left = (m >> lane) & 1u;
-        const int rank = __popc(m & lt);
-        const int64_t dst = left ? lp + pre + rank : rbase + (k - lane - pre) + (lane - rank);
-        rout[dst] = rv[q];
-      }
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------------------------
-// Single-pass partition (default; the two-kernel stable form above is LLMP_PART2=1).  Every
-// histogram is an integer sum, so the order of the rows inside a child segment cannot change any
-// result — only which CTA processes which rows.  Each 4096-row tile of a split parent j therefore
-// reserves its block of each child with one global atomic per child instead of waiting for a
-// prefix over all tiles: the left child fills the parent's own range [s_j, s_j + n_j) of the other
-// ping-pong buffer from the bottom (cursor C.cnt[2j]), the right child from the top (cursor
-// C.cnt[2j+1]); inside a block the rows keep their order (ballot + per-warp prefix table), so the
-// children are contiguous runs of the parent's order, permuted block-wise.  Row indices are read
-// once; there is no tile-count array, no scan, no second launch.  The cursors start at 0 (zeroed
-// by the split kernel of level d-1); the last CTA (ticket) writes both children's starts.
-__global__ void __launch_bounds__(PT_THREADS) k_part(const FitArgs a, const int d, int* ticket) {
-  __shared__ int s_tile_pref[MAX_PIECES + 1];
-  __shared__ int64_t s_seq_pref[MAX_PIECES + 1];
-  __shared__ int s_w[PT_THREADS / 32];
-  __shared__ int64_t s_w64[PT_THREADS / 32];
-  __shared__ __align__(16) uint32_t s_bits[PT_WORDS];   // the tile's ballot words, group = (q, warp)
+  __shared__ __align__(16) uint32_t s_bits[2][PT_WORDS];   // the tile's ballot words, group = (q, warp); by tile parity
   __shared__ __align__(16) int s_pre[PT_WORDS];         // exclusive left prefix of each group
   __shared__ int64_t s_lb, s_rb;                        // the tile's block offsets (left from the bottom, right from the top)
-  __shared__ int s_last;
   const int NP = 1 << (d - 1);
   const LevelView& P = a.lv[d - 1];
   const LevelView& C = a.lv[d];
@@ -1348,10 +1145,29 @@ __global__ void __launch_bounds__(PT_THREADS) k_part(const FitArgs a, const int 
     }
   }
   parent_prefixes(a, d, s_tile_pref, s_seq_pref, s_w, s_w64);
+  const int ntiles = s_tile_pref[NP];
   const uint32_t lt = (1u << lane) - 1u;
   const uint32_t* const rin_all = a.sr[(d - 1) & 1];
   uint32_t* const rout = a.sr[d & 1];
-  for (int t = blockIdx.x; t < s_tile_pref[NP]; t += gridDim.x) {
+  // row indices of tile t (the parent's segment in the input buffer; identity at d = 1)
+  auto load_rows = [&](int t, uint32_t (&r)[PT_ITEMS]) {
+    if (t >= ntiles) return;
+    const int j = parent_of_tile(s_tile_pref, NP, t);
+    const int64_t cnt_j = (d == 1) ? a.n : P.cnt[j];
+    const int64_t o = (int64_t)(t - s_tile_pref[j]) * PT_TILE;
+    const int len = (int)min((int64_t)PT_TILE, cnt_j - o);
+    const uint32_t* rin = rin_all + ((d == 1) ? 0 : P.start[j]) + o;
+#pragma unroll
+    for (int q = 0; q < PT_ITEMS; ++q) {
+      const int k = q * PT_THREADS + tid;
+      r[q] = k < len ? ((d == 1) ? (uint32_t)(o + k) : rin[k]) : 0u;
+    }
+  };
+  uint32_t ridx[PT_ITEMS], nridx[PT_ITEMS];
+  load_rows(blockIdx.x, ridx);
+  int par = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x, par ^= 1) {
+    uint32_t* const bits = s_bits[par];
     const int j = parent_of_tile(s_tile_pref, NP, t);
     const int64_t cnt_j = (d == 1) ? a.n : P.cnt[j];
     const int64_t start_j = (d == 1) ? 0 : P.start[j];
@@ -1359,29 +1175,19 @@ __global__ void __launch_bounds__(PT_THREADS) k_part(const FitArgs a, const int 
     const int len = (int)min((int64_t)PT_TILE, cnt_j - o);
     const int f = P.split_f[j], b = P.split_b[j];
     const uint8_t* col = a.codesT + (size_t)f * a.ldT;
-    const uint32_t* rin = rin_all + start_j + o;
-    uint32_t ridx[PT_ITEMS];
-#pragma unroll
-    for (int q = 0; q < PT_ITEMS; ++q) {
-      const int k = q * PT_THREADS + tid;
-      ridx[q] = k < len ? ((d == 1) ? (uint32_t)(o + k) : rin[k]) : 0u;
-    }
     uint32_t code[PT_ITEMS];
 #pragma unroll
     for (int q = 0; q < PT_ITEMS; ++q) code[q] = __ldg(col + ridx[q]);
-    unsigned mw[PT_ITEMS];
 #pragma unroll
     for (int q = 0; q < PT_ITEMS; ++q) {
       const int k = q * PT_THREADS + tid;
-      mw[q] = __ballot_sync(0xffffffffu, k < len && code[q] <= (uint32_t)b);
+      const unsigned mw = __ballot_sync(0xffffffffu, k < len && code[q] <= (uint32_t)b);
+      if (lane == 0) bits[q * (PT_THREADS / 32) + warp] = mw;
     }
-    if (lane == 0) {
-#pragma unroll
-      for (int q = 0; q < PT_ITEMS; ++q) s_bits[q * (PT_THREADS / 32) + warp] = mw[q];
-    }
+    load_rows(t + gridDim.x, nridx);   // in flight across the reservation below
     __syncthreads();
     if (warp == 0) {   // group prefixes: lane L takes words 4L .. 4L+3; one atomic per child
-      const uint4 m4 = reinterpret_cast<const uint4*>(s_bits)[lane];
+      const uint4 m4 = reinterpret_cast<const uint4*>(bits)[lane];
       const int c0 = __popc(m4.x), c1 = __popc(m4.y), c2 = __popc(m4.z);
       const int lsum = c0 + c1 + c2 + __popc(m4.w);
       int inc = lsum;
@@ -1403,30 +1209,19 @@ __global__ void __launch_bounds__(PT_THREADS) k_part(const FitArgs a, const int 
     const int64_t rtop = start_j + cnt_j - s_rb;         // right rows: rtop + (rights before the row)
 #pragma unroll
     for (int q = 0; q < PT_ITEMS; ++q) {
-      const int word = q * (PT_THREADS / 32) + warp;
       const int k = q * PT_THREADS + tid;
       if (k < len) {
-        const int pre = s_pre[word] + __popc(mw[q] & lt);   // lefts before row k in the tile
-        const bool left = (mw[q] >> lane) & 1u;
+        const uint32_t mw = bits[q * (PT_THREADS / 32) + warp];
+        const int pre = s_pre[q * (PT_THREADS / 32) + warp] + __popc(mw & lt);   // lefts before row k
+        const bool left = (mw >> lane) & 1u;
         rout[left ? lbase + pre : rtop + (k - pre)] = ridx[q];
       }
     }
-    __syncthreads();   // s_bits / s_pre / s_lb / s_rb are reused by the next tile
+#pragma unroll
+    for (int q = 0; q < PT_ITEMS; ++q) ridx[q] = nridx[q];
+    // (no barrier: s_bits is double-buffered; the next writes of s_pre / s_lb follow the next
+    // tile's first barrier)
   }
-  // the last CTA writes the children's starts (counts are final once every CTA has arrived)
-  __threadfence();
-  __syncthreads();
-  if (tid == 0) s_last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  for (int jj = tid; jj < NP; jj += PT_THREADS) {
-    if (P.split_f[jj] < 0) continue;
-    const int64_t sj = (d == 1) ? 0 : P.start[jj];
-    C.start[2 * jj] = sj;
-    C.start[2 * jj + 1] = sj + *reinterpret_cast<volatile int64_t*>(&C.cnt[2 * jj]);
-  }
-  if (tid == 0) *ticket = 0;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -2046,7 +1841,6 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   const bool concurrent = graphs && ctx->nranks == 1 && !serial_env;
   size_t lvl_nodes = 0;
   for (int d = 0; d <= D; ++d) lvl_nodes += (size_t)1 << d;
-  const int64_t max_tiles = (n + PT_TILE - 1) / PT_TILE + half_max + 1;
   const size_t tab_bytes = lvl_nodes * (8 /*start*/ + 8 /*cnt*/ + 8 /*gcnt*/ + 8 + 8 /*lo,hi*/ + 4 + 4 /*split*/ +
                                         4 /*built*/ + 4 /*done*/);
   // root histogram variant: run-length lane-per-feature (default) or the hybrid run/row-parallel
@@ -2056,9 +1850,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   static const bool fused = !use_root2 && !(getenv("LLMP_NOFUSE") && atoi(getenv("LLMP_NOFUSE")) != 0);
   static const bool urow = !(getenv("LLMP_NO_UROW") && atoi(getenv("LLMP_NO_UROW")) != 0);
   static const int hist1 = hist1_mask();
-  static const bool part2 = getenv("LLMP_PART2") && atoi(getenv("LLMP_PART2")) != 0;   // two-kernel stable partition
   FitArgs A[2];
-  PartWs PW[2];
   for (int tg = 0; tg < 2; ++tg) {
     // per-target workspaces: the fused update pass leaves the next tree's root histogram and
     // packed pairs in them, so the two ensembles never share one (also when they run in sequence)
@@ -2080,8 +1872,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     a.y = (tg == 0) ? d_y0.as<float>() : d_y1.as<float>();
     a.p = d_p.as<float>() + (size_t)tg * n;
     a.gp_root = ctx->workspace("gp_root" + sx, (size_t)n * 4).as<uint32_t>();
-    a.sr[0] = ctx->workspace("ridx0" + sx, (size_t)n * 2 * 4).as<uint32_t>();
-    a.sr[1] = ctx->workspace("ridx1" + sx, (size_t)n * 2 * 4).as<uint32_t>();
+    a.sr[0] = ctx->workspace("ridx0" + sx, (size_t)n * 4).as<uint32_t>();
+    a.sr[1] = ctx->workspace("ridx1" + sx, (size_t)n * 4).as<uint32_t>();
     a.H[0] = ctx->workspace("hist0" + sx, (size_t)half_max * SLOT * 8).as<int64_t>();
     a.H[1] = ctx->workspace("hist1" + sx, (size_t)half_max * SLOT * 8).as<int64_t>();
     a.cuts = out.cuts.d_cuts.as<float>();
@@ -2131,10 +1923,6 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       off += (size_t)1 << d;
     }
     LLMP_CUDA(cudaMemsetAsync(d_tab.p, 0, d_tab.bytes, s));
-    PW[tg].tile_left = ctx->workspace("tile_left" + sx, (size_t)max_tiles * 4).as<int32_t>();
-    PW[tg].bits = ctx->workspace("tile_bits" + sx, (size_t)max_tiles * PT_WORDS * 4).as<uint32_t>();
-    PW[tg].ticket = ctx->workspace("part_ticket" + sx, sizeof(int)).as<int>();
-    LLMP_CUDA(cudaMemsetAsync(PW[tg].ticket, 0, sizeof(int), s));
   }
 
   const int hist_grid = 2 * ctx->sms;
@@ -2200,7 +1988,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     LLMP_CUDA(cudaLaunchKernelEx(&cfg, k_split3<true>, a, d));
     ctx->after(KC_SPLIT, ev, (double)(1 << d));
   };
-  auto tree = [&](const FitArgs& a, const PartWs& pw) {
+  auto tree = [&](const FitArgs& a) {
     const cudaStream_t st = ctx->stream;
     // fused: the previous round's update pass built this root already unless root_needed
     if (fused) LLMP_LAUNCH(ctx, KC_MISC, 0, k_root_fix, 1, 1024, 0, a);
@@ -2212,14 +2000,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     split(a, 0);
     for (int d = 1; d < D; ++d) {
       const int tiles_d = (int)((n + PT_TILE - 1) / PT_TILE) + (1 << (d - 1));
-      // persistent tile loops; a scatter CTA owns at most PT_OWN tiles
-      const int pgrid = std::max(std::min(tiles_d, 5 * ctx->sms), (tiles_d + PT_OWN - 1) / PT_OWN);
-      if (part2) {
-        LLMP_LAUNCH(ctx, KC_PARTITION, n, k_pcount, pgrid, PT_THREADS, 0, a, d, pw);
-        LLMP_LAUNCH(ctx, KC_PARTITION, 0, k_pscatter2, pgrid, PT_THREADS, 0, a, d, pw);
-      } else {
-        LLMP_LAUNCH(ctx, KC_PARTITION, n, k_part, std::min(tiles_d, 6 * ctx->sms), PT_THREADS, 0, a, d, pw.ticket);
-      }
+      // persistent tile loop (upper bound of the level's tile count: one partial tile per parent)
+      LLMP_LAUNCH(ctx, KC_PARTITION, n, k_part, std::min(tiles_d, PT_CTAS_PER_SM * ctx->sms), PT_THREADS, 0, a, d);
       if (ctx->nranks > 1) {   // every rank must histogram the same (globally smaller) child
         LLMP_CUDA(cudaMemcpyAsync(a.lv[d].gcnt, a.lv[d].cnt, ((size_t)1 << d) * 8, cudaMemcpyDeviceToDevice, st));
         allreduce_sum_i64(ctx, a.lv[d].gcnt, (size_t)1 << d);
@@ -2259,15 +2041,15 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       if (concurrent) {
         LLMP_CUDA(cudaEventRecord(ctx->fork_event, sa));
         LLMP_CUDA(cudaStreamWaitEvent(sb, ctx->fork_event, 0));
-        tree(A[0], PW[0]);
+        tree(A[0]);
         ctx->stream = sb;
-        tree(A[1], PW[1]);
+        tree(A[1]);
         LLMP_CUDA(cudaEventRecord(ctx->join_event, sb));
         ctx->stream = sa;
         LLMP_CUDA(cudaStreamWaitEvent(sa, ctx->join_event, 0));
       } else {
-        tree(A[0], PW[0]);
-        tree(A[1], PW[1]);
+        tree(A[0]);
+        tree(A[1]);
       }
       LLMP_LAUNCH(ctx, KC_MISC, 0, k_next_tree, 1, 1, 0, d_tree);
       // launch counters: the captured round replays T times
@@ -2290,8 +2072,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     LLMP_CUDA(cudaGraphDestroy(g));
   } else {
     for (int t = 0; t < T; ++t) {
-      tree(A[0], PW[0]);
-      tree(A[1], PW[1]);
+      tree(A[0]);
+      tree(A[1]);
       LLMP_LAUNCH(ctx, KC_MISC, 0, k_next_tree, 1, 1, 0, d_tree);
     }
   }
