@@ -769,18 +769,30 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitArgs a, const 
           acc_g += tot_g - bg;
           acc_h += tot_h - bh;
         }
-        // heavy features: row-parallel, one feature at a time
-        unsigned hm = __ballot_sync(0xffffffffu, heavy);
-        while (hm) {
-          const int hl = __ffs(hm) - 1;
-          hm &= hm - 1u;
-          const int hf = h2_feat(hl);
-          if (lane == hl && (acc_g | (int32_t)acc_h)) red2(sgb + cur, acc_g, acc_h);   // pending run of earlier batches
-          if (valid) red2(sgb + (uint32_t)(myrow[hf] * H2_PAD + hf) * 4u, qg, qh);
-          if (lane == hl) {
-            acc_g = 0;
-            acc_h = 0;
-            cur = (uint32_t)(wb[cnt * H2_ROWB + hf] * H2_PAD + hf) * 4u;   // the batch's last row
+        // heavy features: row-parallel, one feature at a time, unrolled over the lanes so every
+        // feature index is a constant and each row's code byte comes from its own registers
+        const unsigned hm = __ballot_sync(0xffffffffu, heavy);
+        if (hm) {
+          const uint32_t cw[8] = {cc0.x, cc0.y, cc0.z, cc0.w, cc1.x, cc1.y, cc1.z, cc1.w};
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {   // lanes 7-q, 15-q, 23-q, 31-q hold features 4q .. 4q+3
+            if (hm & (0x01010101u << (7 - q))) {
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int hl = 8 * j + 7 - q, hf = 4 * q + j;
+                if (hm & (1u << hl)) {
+                  const uint32_t code = (cw[q] >> (8 * j)) & 0xffu;
+                  if (valid) red2(sgb + (code * H2_PAD + (uint32_t)hf) * 4u, qg, qh);
+                  const uint32_t last = __shfl_sync(0xffffffffu, code, cnt - 1);
+                  if (lane == hl) {
+                    if (acc_g | (int32_t)acc_h) red2(sgb + cur, acc_g, acc_h);   // pending run of earlier batches
+                    acc_g = 0;
+                    acc_h = 0;
+                    cur = (last * H2_PAD + (uint32_t)hf) * 4u;   // the batch's last row
+                  }
+                }
+              }
+            }
           }
         }
       }
@@ -822,13 +834,14 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitArgs a, const 
   }
 }
 
-// histogram inner loop: run-length k_hist (default) or change-mask k_hist2 (LLMP_HIST2=1; a bit
-// mask selects k_hist2 per mode: 1 root, 2 level, 4 fused update + root)
+// histogram inner loop per mode: change-mask k_hist2 or run-length k_hist.  LLMP_HIST2 is a bit mask
+// of the modes that use k_hist2 (1 root, 2 level, 4 fused update + root); default 5 = the measured
+// winners (root and update on k_hist2, level histograms on k_hist)
 static int hist1_mask() {
-  static const int v = getenv("LLMP_HIST2") ? 7 & ~(atoi(getenv("LLMP_HIST2")) == 1 ? 7 : atoi(getenv("LLMP_HIST2"))) : 7;
+  static const int v = 7 & ~(getenv("LLMP_HIST2") ? atoi(getenv("LLMP_HIST2")) : 5);
   return v;
 }
-static bool use_hist1() { return hist1_mask() == 7; }
+static bool use_hist1() { return (hist1_mask() & 2) != 0; }   // the test hook follows the level kernel
 
 // zero the root histogram slot when k_hist<ROOT> is going to (re)build it (see root_needed)
 __global__ void k_root_fix(const FitArgs a) {

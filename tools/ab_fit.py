@@ -77,8 +77,8 @@ def main():
     for v, ms in res.items():
         if ms:
             ms = sorted(ms)
-            print("%-28s min %8.2f  median %8.2f ms per fit (%d trees)  %s" % (repr(v), ms[0], ms[len(ms) // 2], a.trees,
-                                                                       extra.get(v)))
+            print("%-28s min %8.2f  median %8.2f ms per fit (%d trees)  %s  all %s" % (
+                repr(v), ms[0], ms[len(ms) // 2], a.trees, extra.get(v), " ".join("%.1f" % x for x in res[v])))
 
 
 if __name__ == "__main__":
