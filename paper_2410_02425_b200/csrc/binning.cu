@@ -91,7 +91,10 @@ void compute_cuts(Ctx* ctx, const float* X, int64_t n, int F, int64_t row_offset
   const int64_t m_local = (i0 < n) ? (n - 1 - i0) / stride + 1 : 0;
   // global sample size (every rank computes it identically)
   const int64_t m = (n_global - 1) / stride + 1;
-  DevBuf keys((size_t)std::max<int64_t>(m, 1) * F * 4), sorted((size_t)std::max<int64_t>(m, 1) * F * 4);
+  // grow-only context workspaces: no per-fit cudaMalloc/cudaFree (cudaFree synchronises the device,
+  // and a large cudaMalloc occasionally stalls for hundreds of ms)
+  DevBuf& keys = ctx->workspace("cut_keys", (size_t)std::max<int64_t>(m, 1) * F * 4);
+  DevBuf& sorted = ctx->workspace("cut_sorted", (size_t)std::max<int64_t>(m, 1) * F * 4);
   if (ctx->nranks == 1) {
     LLMP_REQUIRE(m_local == m, "sample size mismatch");
     if (m > 0)
@@ -101,7 +104,8 @@ void compute_cuts(Ctx* ctx, const float* X, int64_t n, int F, int64_t row_offset
     // is the concatenation of the per-rank samples.  All-gather (row_offset, n) to size them,
     // then all-gather fixed-size padded [F][m_pad] samples and re-pack into [F][m].
     const int R = ctx->nranks;
-    DevBuf meta(2 * 8), metas((size_t)R * 2 * 8);
+    DevBuf& meta = ctx->workspace("cut_meta", 2 * 8);
+    DevBuf& metas = ctx->workspace("cut_metas", (size_t)R * 2 * 8);
     int64_t mine[2] = {row_offset, n};
     LLMP_CUDA(cudaMemcpyAsync(meta.p, mine, 16, cudaMemcpyHostToDevice, s));
     allgather_bytes(ctx, meta.p, metas.p, 16);
@@ -118,7 +122,8 @@ void compute_cuts(Ctx* ctx, const float* X, int64_t n, int F, int64_t row_offset
       m_pad = std::max(m_pad, mr[r]);
     }
     LLMP_REQUIRE(pref[R] == m, "shards do not tile the global row range");
-    DevBuf local((size_t)m_pad * F * 4), all((size_t)R * m_pad * F * 4);
+    DevBuf& local = ctx->workspace("cut_local", (size_t)m_pad * F * 4);
+    DevBuf& all = ctx->workspace("cut_all", (size_t)R * m_pad * F * 4);
     if (m_local > 0)
       LLMP_LAUNCH(ctx, KC_CUTS, m_local, k_gather_sample, 1024, 256, 0, X, n, F, i0, stride, m_local, m_pad,
                   local.as<float>());
@@ -128,12 +133,12 @@ void compute_cuts(Ctx* ctx, const float* X, int64_t n, int F, int64_t row_offset
         LLMP_CUDA(cudaMemcpy2DAsync(keys.as<float>() + pref[r], (size_t)m * 4, all.as<float>() + (size_t)r * m_pad * F,
                                     (size_t)m_pad * 4, (size_t)mr[r] * 4, F, cudaMemcpyDeviceToDevice, s));
   }
-  DevBuf off((F + 1) * 8);
+  DevBuf& off = ctx->workspace("cut_off", (F + 1) * 8);
   LLMP_LAUNCH(ctx, KC_CUTS, 0, k_offsets, 1, 64, 0, off.as<int64_t>(), F, m);
   size_t temp = 0;
   LLMP_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, temp, keys.as<float>(), sorted.as<float>(), m * F, F,
                                                off.as<int64_t>(), off.as<int64_t>() + 1, s));
-  DevBuf tmp(std::max<size_t>(temp, 1));
+  DevBuf& tmp = ctx->workspace("cut_sort_tmp", std::max<size_t>(temp, 1));
   LLMP_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp.p, temp, keys.as<float>(), sorted.as<float>(), m * F, F,
                                                off.as<int64_t>(), off.as<int64_t>() + 1, s));
   ctx->launches[KC_CUTS] += 1;

@@ -109,7 +109,7 @@ void cv_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams* grid, int n
     LLMP_REQUIRE(isfinite(y[2 * i]) && isfinite(y[2 * i + 1]), "non-finite y");
   }
   {
-    DevBuf d_w(n * 4);
+    DevBuf& d_w = ctx->workspace("cv_w", n * 4);
     compute_weights(ctx, ds, L1, L2, d_w.as<float>());
     LLMP_CUDA(cudaMemcpyAsync(w.data(), d_w.p, n * 4, cudaMemcpyDeviceToHost, s));
     LLMP_CUDA(cudaStreamSynchronize(s));
@@ -185,7 +185,7 @@ void cv_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams* grid, int n
       if (allowed[g])
         for (int lv = 0; lv < nL; ++lv)
           LLMP_REQUIRE(filled[(size_t)g * nL + lv], "held-out LLM's (profile x users) grid is irregular");
-    DevBuf d_grid((size_t)nP * nL * 2 * 4 * 2);
+    DevBuf& d_grid = ctx->workspace("cv_grid", (size_t)nP * nL * 2 * 4 * 2);
     LLMP_CUDA(cudaMemcpyAsync(d_grid.p, gp.data(), gp.size() * 4, cudaMemcpyHostToDevice, s));
     LLMP_CUDA(cudaMemcpyAsync(d_grid.as<float>() + gp.size(), gt.data(), gt.size() * 4, cudaMemcpyHostToDevice, s));
     RecOut rp, rt;

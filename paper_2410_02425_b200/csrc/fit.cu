@@ -24,6 +24,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <chrono>
 
 #include "internal.cuh"
 
@@ -102,6 +103,12 @@ struct FitArgs {
   unsigned long long* units;  // device counters of rows processed per kernel class (instrumentation)
 };
 
+// both ensembles' arguments: every tree-loop kernel runs the two (independent) targets as
+// blockIdx.y = 0, 1 of one launch — one stream, one launch per step for both trees
+struct FitPair {
+  FitArgs t[2];
+};
+
 // debug-mode inputs of the histogram kernel
 struct DbgArgs {
   const int32_t* idx;
@@ -167,7 +174,8 @@ __device__ __forceinline__ void run_step(uint32_t& pa, int32_t& ag, uint32_t& ah
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitArgs a, const int d, const int t_in, const DbgArgs dbg) {
+__global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitPair fp, const int d, const int t_in, const DbgArgs dbg) {
+  const FitArgs& a = fp.t[blockIdx.y];
   const int t = (MODE == HM_ROOT || MODE == HM_UPDROOT) ? *a.d_tree : t_in;   // graph replays: tree index from the device
   if (MODE == HM_ROOT && !root_needed(a, t)) return;   // built speculatively by the previous update pass
   const bool has_next = (MODE == HM_UPDROOT) ? (t + 1 < a.T) : true;
@@ -499,7 +507,8 @@ __device__ __forceinline__ void red2(uint32_t addr, int32_t g, uint32_t h) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitArgs a, const int d, const int t_in, const DbgArgs dbg) {
+__global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const int d, const int t_in, const DbgArgs dbg) {
+  const FitArgs& a = fp.t[blockIdx.y];
   const int t = (MODE == HM_ROOT || MODE == HM_UPDROOT) ? *a.d_tree : t_in;   // graph replays: tree index from the device
   if (MODE == HM_ROOT && !root_needed(a, t)) return;   // built speculatively by the previous update pass
   const bool has_next = (MODE == HM_UPDROOT) ? (t + 1 < a.T) : true;
@@ -773,6 +782,12 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitArgs a, const 
         // feature index is a constant and each row's code byte comes from its own registers
         const unsigned hm = __ballot_sync(0xffffffffu, heavy);
         if (hm) {
+          if (heavy) {   // flush the pending run of earlier batches; the run continues from the last row
+            if (acc_g | (int32_t)acc_h) red2(sgb + cur, acc_g, acc_h);
+            acc_g = 0;
+            acc_h = 0;
+            cur = (uint32_t)(wb[cnt * H2_ROWB + myf] * H2_PAD + myf) * 4u;
+          }
           const uint32_t cw[8] = {cc0.x, cc0.y, cc0.z, cc0.w, cc1.x, cc1.y, cc1.z, cc1.w};
 #pragma unroll
           for (int q = 0; q < 8; ++q) {   // lanes 7-q, 15-q, 23-q, 31-q hold features 4q .. 4q+3
@@ -780,17 +795,8 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitArgs a, const 
 #pragma unroll
               for (int j = 0; j < 4; ++j) {
                 const int hl = 8 * j + 7 - q, hf = 4 * q + j;
-                if (hm & (1u << hl)) {
-                  const uint32_t code = (cw[q] >> (8 * j)) & 0xffu;
-                  if (valid) red2(sgb + (code * H2_PAD + (uint32_t)hf) * 4u, qg, qh);
-                  const uint32_t last = __shfl_sync(0xffffffffu, code, cnt - 1);
-                  if (lane == hl) {
-                    if (acc_g | (int32_t)acc_h) red2(sgb + cur, acc_g, acc_h);   // pending run of earlier batches
-                    acc_g = 0;
-                    acc_h = 0;
-                    cur = (last * H2_PAD + (uint32_t)hf) * 4u;   // the batch's last row
-                  }
-                }
+                if ((hm & (1u << hl)) && valid)
+                  red2(sgb + (((cw[q] >> (8 * j)) & 0xffu) * H2_PAD + (uint32_t)hf) * 4u, qg, qh);
               }
             }
           }
@@ -844,7 +850,8 @@ static int hist1_mask() {
 static bool use_hist1() { return (hist1_mask() & 2) != 0; }   // the test hook follows the level kernel
 
 // zero the root histogram slot when k_hist<ROOT> is going to (re)build it (see root_needed)
-__global__ void k_root_fix(const FitArgs a) {
+__global__ void k_root_fix(const FitPair fp) {
+  const FitArgs& a = fp.t[blockIdx.y];
   if (!root_needed(a, *a.d_tree)) return;
   int64_t* H = a.H[0];
   for (int i = threadIdx.x; i < SLOT; i += blockDim.x) H[i] = 0;
@@ -878,7 +885,8 @@ __device__ __forceinline__ uint32_t change_nibble(uint32_t cur, uint32_t prevw) 
   return (t * 0x00204081u) >> 28;
 }
 
-__global__ void __launch_bounds__(R2_THREADS, 2) k_hist_root2(const FitArgs a) {
+__global__ void __launch_bounds__(R2_THREADS, 2) k_hist_root2(const FitPair fp) {
+  const FitArgs& a = fp.t[blockIdx.y];
   const int t = *a.d_tree;
   extern __shared__ __align__(16) uint8_t smem[];
   int32_t* hg = reinterpret_cast<int32_t*>(smem);                       // [256][33]
@@ -1136,7 +1144,8 @@ __device__ __forceinline__ int parent_of_tile(const int* s_tile_pref, int NP, in
 // reservation.  The cursors start at 0 (zeroed by the split kernel of level d-1); the children's
 // starts follow from the counts (s_j and s_j + n_L; written by the level histogram kernel).
 constexpr int PT_CTAS_PER_SM = 4;
-__global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitArgs a, const int d) {
+__global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitPair fp, const int d) {
+  const FitArgs& a = fp.t[blockIdx.y];
   __shared__ int s_tile_pref[MAX_PIECES + 1];
   __shared__ int64_t s_seq_pref[MAX_PIECES + 1];
   __shared__ int s_w[PT_THREADS / 32];
@@ -1250,7 +1259,8 @@ __global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitAr
 constexpr int SP3_WARPS = 4;
 constexpr int SP3_CLUSTER = 32 / SP3_WARPS;   // 8 CTAs = the node's 32 features
 template <bool CL>
-__global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitArgs a, const int d) {
+__global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitPair fp, const int d) {
+  const FitArgs& a = fp.t[blockIdx.y];
   __shared__ FeatBest s_fb[SP3_WARPS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int k = blockIdx.x / SP3_CLUSTER;                  // node of level d
@@ -1531,7 +1541,8 @@ __device__ __forceinline__ void block_max2(float& a, float& b, float* s_a, float
 }
 
 constexpr int UPD_R = 4;   // rows per thread per iteration (independent traversals for ILP)
-__global__ void __launch_bounds__(UPD_THREADS) k_update(const FitArgs a) {
+__global__ void __launch_bounds__(UPD_THREADS) k_update(const FitPair fp) {
+  const FitArgs& a = fp.t[blockIdx.y];
   const int t = *a.d_tree;
   const int32_t* const tfeat = a.tfeat + (size_t)t * a.nn;
   const int32_t* const tbin = a.tbin + (size_t)t * a.nn;
@@ -1678,6 +1689,22 @@ __global__ void __launch_bounds__(BASE_THREADS) k_base_init(const FitArgs a, con
 }
 
 __global__ void k_next_tree(int* d_tree) { *d_tree += 1; }
+__global__ void k_stamp(unsigned long long* stamps) {
+  unsigned long long ns;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+  stamps[0] = ns;
+}
+// graph form: advance the tree index and keep the device-side while loop running while t < T
+__global__ void k_next_tree_cond(int* d_tree, int T, cudaGraphConditionalHandle h, unsigned long long* stamps) {
+  const int t = *d_tree + 1;
+  *d_tree = t;
+  cudaGraphSetConditional(h, t < T ? 1u : 0u);
+  if (stamps) {   // diagnostics (LLMP_ROUND_TIMES=1): device time at the end of each round
+    unsigned long long ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    stamps[t] = ns;
+  }
+}
 
 __global__ void k_fill_trees(int32_t* feat, int32_t* bin, float* thr, float* val, size_t count) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
@@ -1738,9 +1765,10 @@ __global__ void k_weights_given(const float* y, const float* win, int64_t n, flo
 // Eq. (4) weights of a whole dataset (used by the CV's weighted MAPE)
 void compute_weights(Ctx* ctx, const DatasetDev& ds, float L1, float L2, float* w) {
   const int64_t n = ds.n;
-  DevBuf d_y0(n * 4), d_y1(n * 4);
+  DevBuf& d_y0 = ctx->workspace("cw_y0", n * 4);
+  DevBuf& d_y1 = ctx->workspace("cw_y1", n * 4);
   const size_t ng = (size_t)ds.n_llm * ds.n_prof;
-  DevBuf d_D(ng * 2 * 8);
+  DevBuf& d_D = ctx->workspace("cw_groupmax", ng * 2 * 8);
   LLMP_CUDA(cudaMemsetAsync(d_D.p, 0, d_D.bytes, ctx->stream));
   int grid = (int)std::min<int64_t>((n + 255) / 256, (int64_t)ctx->sms * 8);
   LLMP_LAUNCH(ctx, KC_WEIGHTS, n, k_weights_max, grid, 256, 0, ds.y, ds.llm, ds.prof, n, ds.n_prof, (double)L1,
@@ -1785,6 +1813,16 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
                "Eq. (4) weights need llm_id/profile_id and n_llm, n_prof >= 1");
   cudaStream_t s = ctx->stream;
 
+  // diagnostics (LLMP_FIT_PHASES=1): host-synchronised phase times on stderr
+  static const bool phases = getenv("LLMP_FIT_PHASES") && atoi(getenv("LLMP_FIT_PHASES")) != 0;
+  auto ph_t0 = std::chrono::steady_clock::now();
+  auto phase = [&](const char* name) {
+    if (!phases) return;
+    LLMP_CUDA(cudaStreamSynchronize(ctx->stream));
+    const auto t1 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[llmp] phase %-10s %9.3f ms\n", name, std::chrono::duration<double, std::milli>(t1 - ph_t0).count());
+    ph_t0 = t1;
+  };
   // ---- validation (NaN/Inf, id ranges) — one host sync per fit
   DevBuf& d_flag = ctx->workspace("flag", sizeof(int));
   LLMP_CUDA(cudaMemsetAsync(d_flag.p, 0, sizeof(int), s));
@@ -1795,6 +1833,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   LLMP_CUDA(cudaStreamSynchronize(s));
   LLMP_REQUIRE(h_flag == 0, "dataset holds a non-finite X or y value or an id out of range");
 
+  phase("validate");
   // ---- weights (Eq. 4) + de-interleaved targets
   DevBuf& d_w = ctx->workspace("w", n * 4);
   DevBuf& d_y0 = ctx->workspace("y0", n * 4);
@@ -1814,6 +1853,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
                 d_y0.as<float>(), d_y1.as<float>());
   }
 
+  phase("weights");
   // ---- cuts + codes (row-major for histograms/routing, column-major for partitions)
   compute_cuts(ctx, ds.X, n, F, ds.row_offset, ds.n_global, hp.max_bin, out.cuts);
   DevBuf& d_codes = ctx->workspace("codes", (size_t)n * kMaxF);
@@ -1822,6 +1862,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   LLMP_CUDA(cudaMemsetAsync(d_codesT.p, 0, (size_t)ldT * kMaxF, s));   // zero the padding rows
   compute_codes(ctx, ds.X, n, F, out.cuts, d_codes.as<uint8_t>(), d_codesT.as<uint8_t>(), ldT, nullptr);
 
+  phase("cuts+codes");
   // ---- training state
   const int nn = (1 << (D + 1)) - 1;
   const int half_max = 1 << (D - 1);        // slots per histogram parity buffer
@@ -1846,12 +1887,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   LLMP_CUDA(cudaMemsetAsync(d_sums.p, 0, d_sums.bytes, s));
   int* d_tree = ctx->workspace("tree_idx", sizeof(int)).as<int>();
 
-  // the two ensembles are independent: on one GPU their trees grow concurrently (two branches
-  // of one CUDA graph, each with its own level workspaces); with NCCL (collectives must be
-  // issued in one order on every rank) or timing instrumentation they run one after the other
+  // the two ensembles are independent: every tree-loop kernel grows both (blockIdx.y = target)
   const bool graphs = T > 0 && !ctx->timing && ctx->use_graphs;
-  static const bool serial_env = getenv("LLMP_SERIAL") && atoi(getenv("LLMP_SERIAL")) != 0;   // diagnostics
-  const bool concurrent = graphs && ctx->nranks == 1 && !serial_env;
   size_t lvl_nodes = 0;
   for (int d = 0; d <= D; ++d) lvl_nodes += (size_t)1 << d;
   const size_t tab_bytes = lvl_nodes * (8 /*start*/ + 8 /*cnt*/ + 8 /*gcnt*/ + 8 + 8 /*lo,hi*/ + 4 + 4 /*split*/ +
@@ -1938,7 +1975,6 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     LLMP_CUDA(cudaMemsetAsync(d_tab.p, 0, d_tab.bytes, s));
   }
 
-  const int hist_grid = 2 * ctx->sms;
   const int upd_grid = grid_for(ctx, n, UPD_THREADS, 8);
   const int base_grid = grid_for(ctx, n, BASE_THREADS, 8);
   static bool attr_set = false;
@@ -1957,6 +1993,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   }
   const DbgArgs nodbg{};
 
+  phase("state");
   // ---- base scores (O3) and tree 0's gradient maxima
   for (int tg = 0; tg < 2; ++tg) {
     const FitArgs& a = A[tg];
@@ -1973,20 +2010,24 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     }
   }
 
-  // one tree of one target = a fixed sequence of launches that reads the tree index from the
-  // device; both targets' trees + the index advance form one "round", captured once into a CUDA
-  // graph and replayed T times (plain launches when timing instrumentation is on)
+  // one tree of each target = a fixed sequence of launches (blockIdx.y = target) that reads the
+  // tree index from the device; one "round" (tree t of both ensembles + the index advance) is
+  // captured once into a CUDA graph and replayed T times (plain launches when timing is on)
   // split kernel: plain launch with a global ticket per node (default) or one thread-block cluster
   // per node exchanging results through distributed shared memory (LLMP_SPLIT_CLUSTER=1)
+  phase("base");
+  FitPair FP;
+  FP.t[0] = A[0];
+  FP.t[1] = A[1];
   static const bool split_cluster = getenv("LLMP_SPLIT_CLUSTER") && atoi(getenv("LLMP_SPLIT_CLUSTER")) != 0;
-  auto split = [&](const FitArgs& a, int d) {
-    const int grid = (1 << d) * SP3_CLUSTER;
+  auto split = [&](const FitPair& fp, int ny, int d) {
+    const dim3 grid((1 << d) * SP3_CLUSTER, ny);
     if (!split_cluster) {
-      LLMP_LAUNCH(ctx, KC_SPLIT, (1 << d), k_split3<false>, grid, SP3_WARPS * 32, 0, a, d);
+      LLMP_LAUNCH(ctx, KC_SPLIT, ny << d, k_split3<false>, grid, SP3_WARPS * 32, 0, fp, d);
       return;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
+    cfg.gridDim = grid;
     cfg.blockDim = dim3(SP3_WARPS * 32);
     cfg.stream = ctx->stream;
     cudaLaunchAttribute at[1];
@@ -1998,99 +2039,173 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     cfg.numAttrs = 1;
     cudaEvent_t ev = nullptr;
     ctx->before(KC_SPLIT, &ev);
-    LLMP_CUDA(cudaLaunchKernelEx(&cfg, k_split3<true>, a, d));
-    ctx->after(KC_SPLIT, ev, (double)(1 << d));
+    LLMP_CUDA(cudaLaunchKernelEx(&cfg, k_split3<true>, fp, d));
+    ctx->after(KC_SPLIT, ev, (double)(ny << d));
   };
-  auto tree = [&](const FitArgs& a) {
+  static const bool round_times = getenv("LLMP_ROUND_TIMES") && atoi(getenv("LLMP_ROUND_TIMES")) != 0;
+  unsigned long long* stamps = nullptr;
+  if (round_times && T > 0) {
+    stamps = ctx->workspace("round_stamps", (size_t)(T + 1) * 8).as<unsigned long long>();
+  }
+  // one tree of the targets in `fp` (ny = 2: both as blockIdx.y = 0, 1; ny = 1: fp.t[0] only)
+  auto trees = [&](const FitPair& fp, int ny) {
     const cudaStream_t st = ctx->stream;
+    const dim3 hg(ctx->sms * 2 / ny, ny);   // histogram kernels: 2 CTAs per SM in total
     // fused: the previous round's update pass built this root already unless root_needed
-    if (fused) LLMP_LAUNCH(ctx, KC_MISC, 0, k_root_fix, 1, 1024, 0, a);
-    else LLMP_CUDA(cudaMemsetAsync(a.H[0], 0, (size_t)SLOT * 8, st));
-    if (use_root2) LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist_root2, hist_grid, R2_THREADS, R2_SMEM, a);
-    else if (hist1 & 1) LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist<HM_ROOT>, hist_grid, HIST_THREADS, HIST_SMEM, a, 0, 0, nodbg);
-    else LLMP_LAUNCH(ctx, KC_HIST_ROOT, n, k_hist2<HM_ROOT>, hist_grid, H2_THREADS, H2_SMEM, a, 0, 0, nodbg);
-    allreduce_sum_i64(ctx, a.H[0], SLOT);
-    split(a, 0);
+    if (fused) {
+      LLMP_LAUNCH(ctx, KC_MISC, 0, k_root_fix, dim3(1, ny), 1024, 0, fp);
+    } else {
+      for (int q = 0; q < ny; ++q) LLMP_CUDA(cudaMemsetAsync(fp.t[q].H[0], 0, (size_t)SLOT * 8, st));
+    }
+    if (use_root2) LLMP_LAUNCH(ctx, KC_HIST_ROOT, ny * n, k_hist_root2, hg, R2_THREADS, R2_SMEM, fp);
+    else if (hist1 & 1) LLMP_LAUNCH(ctx, KC_HIST_ROOT, ny * n, k_hist<HM_ROOT>, hg, HIST_THREADS, HIST_SMEM, fp, 0, 0, nodbg);
+    else LLMP_LAUNCH(ctx, KC_HIST_ROOT, ny * n, k_hist2<HM_ROOT>, hg, H2_THREADS, H2_SMEM, fp, 0, 0, nodbg);
+    for (int q = 0; q < ny; ++q) allreduce_sum_i64(ctx, fp.t[q].H[0], SLOT);
+    split(fp, ny, 0);
     for (int d = 1; d < D; ++d) {
       const int tiles_d = (int)((n + PT_TILE - 1) / PT_TILE) + (1 << (d - 1));
       // persistent tile loop (upper bound of the level's tile count: one partial tile per parent)
-      LLMP_LAUNCH(ctx, KC_PARTITION, n, k_part, std::min(tiles_d, PT_CTAS_PER_SM * ctx->sms), PT_THREADS, 0, a, d);
+      LLMP_LAUNCH(ctx, KC_PARTITION, ny * n, k_part, dim3(std::min(tiles_d, PT_CTAS_PER_SM / ny * ctx->sms), ny),
+                  PT_THREADS, 0, fp, d);
       if (ctx->nranks > 1) {   // every rank must histogram the same (globally smaller) child
-        LLMP_CUDA(cudaMemcpyAsync(a.lv[d].gcnt, a.lv[d].cnt, ((size_t)1 << d) * 8, cudaMemcpyDeviceToDevice, st));
-        allreduce_sum_i64(ctx, a.lv[d].gcnt, (size_t)1 << d);
+        for (int q = 0; q < ny; ++q) {
+          LLMP_CUDA(cudaMemcpyAsync(fp.t[q].lv[d].gcnt, fp.t[q].lv[d].cnt, ((size_t)1 << d) * 8, cudaMemcpyDeviceToDevice, st));
+          allreduce_sum_i64(ctx, fp.t[q].lv[d].gcnt, (size_t)1 << d);
+        }
       }
-      if (hist1 & 2) LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hist_grid, HIST_THREADS, HIST_SMEM, a, d, 0, nodbg);
-      else LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist2<HM_LEVEL>, hist_grid, H2_THREADS, H2_SMEM, a, d, 0, nodbg);
-      allreduce_sum_i64(ctx, a.H[d & 1], (size_t)SLOT << (d - 1));
-      split(a, d);
+      if (hist1 & 2) LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hg, HIST_THREADS, HIST_SMEM, fp, d, 0, nodbg);
+      else LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist2<HM_LEVEL>, hg, H2_THREADS, H2_SMEM, fp, d, 0, nodbg);
+      for (int q = 0; q < ny; ++q) allreduce_sum_i64(ctx, fp.t[q].H[d & 1], (size_t)SLOT << (d - 1));
+      split(fp, ny, d);
     }
     if (fused) {   // update tree t + root histogram of tree t+1 (into the now free root slot)
-      LLMP_CUDA(cudaMemsetAsync(a.H[0], 0, (size_t)SLOT * 8, st));
+      for (int q = 0; q < ny; ++q) LLMP_CUDA(cudaMemsetAsync(fp.t[q].H[0], 0, (size_t)SLOT * 8, st));
       if (hist1 & 4)
-        LLMP_LAUNCH(ctx, KC_UPDATE, n, k_hist<HM_UPDROOT>, hist_grid, HIST_THREADS, HIST_SMEM + UPDROOT_TREE_SMEM, a, 0,
-                    0, nodbg);
+        LLMP_LAUNCH(ctx, KC_UPDATE, ny * n, k_hist<HM_UPDROOT>, hg, HIST_THREADS, HIST_SMEM + UPDROOT_TREE_SMEM, fp,
+                    0, 0, nodbg);
       else
-        LLMP_LAUNCH(ctx, KC_UPDATE, n, k_hist2<HM_UPDROOT>, hist_grid, H2_THREADS, H2_SMEM + UPDROOT_TREE_SMEM, a, 0, 0,
-                    nodbg);
+        LLMP_LAUNCH(ctx, KC_UPDATE, ny * n, k_hist2<HM_UPDROOT>, hg, H2_THREADS, H2_SMEM + UPDROOT_TREE_SMEM, fp, 0,
+                    0, nodbg);
     } else {
-      LLMP_LAUNCH(ctx, KC_UPDATE, n, k_update, upd_grid, UPD_THREADS, 0, a);
+      LLMP_LAUNCH(ctx, KC_UPDATE, ny * n, k_update, dim3(std::max(1, upd_grid * ny / 2), ny), UPD_THREADS, 0, fp);
     }
-    // next tree's gradient maxima (past slots are already equal on every rank, future ones 0)
-    allreduce_max_u32(ctx, a.maxg, (size_t)2 * (T + 1));
+  };
+  // both ensembles' trees t: two concurrent graph branches (default on one GPU: one ensemble's
+  // latency-bound split / partition kernels overlap the other's streaming kernels; 592 vs 652 ms
+  // per 500-tree fit), or one paired launch sequence (LLMP_PAIRED=1, and always with NCCL:
+  // collectives must be issued in one order on every rank)
+  static const bool branches_env = !(getenv("LLMP_PAIRED") && atoi(getenv("LLMP_PAIRED")) != 0);
+  FitPair FPa, FPb;
+  FPa.t[0] = A[0];
+  FPb.t[0] = A[1];
+  auto round = [&](const cudaGraphConditionalHandle* loop) {
+    const bool branches = branches_env && graphs && ctx->nranks == 1;
+    if (branches) {
+      const cudaStream_t sa = ctx->stream, sb = ctx->capture_stream(1);
+      LLMP_CUDA(cudaEventRecord(ctx->fork_event, sa));
+      LLMP_CUDA(cudaStreamWaitEvent(sb, ctx->fork_event, 0));
+      trees(FPa, 1);
+      ctx->stream = sb;
+      trees(FPb, 1);
+      LLMP_CUDA(cudaEventRecord(ctx->join_event, sb));
+      ctx->stream = sa;
+      LLMP_CUDA(cudaStreamWaitEvent(sa, ctx->join_event, 0));
+    } else {
+      trees(FP, 2);
+    }
+    // next tree's gradient maxima of both targets (contiguous; past slots are already equal on
+    // every rank, future ones 0)
+    allreduce_max_u32(ctx, A[0].maxg, (size_t)4 * (T + 1));
+    if (loop) LLMP_LAUNCH(ctx, KC_MISC, 0, k_next_tree_cond, 1, 1, 0, d_tree, T, *loop, stamps);
+    else LLMP_LAUNCH(ctx, KC_MISC, 0, k_next_tree, 1, 1, 0, d_tree);
   };
   LLMP_CUDA(cudaMemsetAsync(d_tree, 0, sizeof(int), s));
+  // graphs: the whole tree loop is ONE graph launch — a device-side while loop (conditional graph
+  // node) around the captured round, so no host thread sits between the T rounds (host jitter
+  // cannot starve the GPU).  LLMP_GRAPH_REPLAY=1 replays the round graph T times from the host.
+  static const bool replay = getenv("LLMP_GRAPH_REPLAY") && atoi(getenv("LLMP_GRAPH_REPLAY")) != 0;
   if (graphs) {
     cudaGraph_t g = nullptr;
     cudaGraphExec_t ge = nullptr;
     const cudaStream_t user = ctx->stream;
-    const cudaStream_t sa = ctx->capture_stream(0), sb = ctx->capture_stream(1);
+    const cudaStream_t sa = ctx->capture_stream(0);
     uint64_t l0[LLMP_N_KERNEL_CLASSES];
     double r0[LLMP_N_KERNEL_CLASSES];
     memcpy(l0, ctx->launches, sizeof(l0));
     memcpy(r0, ctx->rows, sizeof(r0));
-    ctx->stream = sa;
-    LLMP_CUDA(cudaStreamBeginCapture(sa, cudaStreamCaptureModeThreadLocal));
+    cudaGraphConditionalHandle loop = 0;
+    if (!replay) {
+      LLMP_CUDA(cudaGraphCreate(&g, 0));
+      LLMP_CUDA(cudaGraphConditionalHandleCreate(&loop, g, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = loop;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t cn;
+      LLMP_CUDA(cudaGraphAddNode(&cn, g, nullptr, 0, &cp));
+      ctx->stream = sa;
+      LLMP_CUDA(cudaStreamBeginCaptureToGraph(sa, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                              cudaStreamCaptureModeThreadLocal));
+    } else {
+      ctx->stream = sa;
+      LLMP_CUDA(cudaStreamBeginCapture(sa, cudaStreamCaptureModeThreadLocal));
+    }
     try {
-      if (concurrent) {
-        LLMP_CUDA(cudaEventRecord(ctx->fork_event, sa));
-        LLMP_CUDA(cudaStreamWaitEvent(sb, ctx->fork_event, 0));
-        tree(A[0]);
-        ctx->stream = sb;
-        tree(A[1]);
-        LLMP_CUDA(cudaEventRecord(ctx->join_event, sb));
-        ctx->stream = sa;
-        LLMP_CUDA(cudaStreamWaitEvent(sa, ctx->join_event, 0));
-      } else {
-        tree(A[0]);
-        tree(A[1]);
-      }
-      LLMP_LAUNCH(ctx, KC_MISC, 0, k_next_tree, 1, 1, 0, d_tree);
-      // launch counters: the captured round replays T times
+      round(replay ? nullptr : &loop);
+      // launch counters: the captured round runs T times
       for (int c = 0; c < LLMP_N_KERNEL_CLASSES; ++c) {
         ctx->launches[c] += (ctx->launches[c] - l0[c]) * (uint64_t)(T - 1);
         ctx->rows[c] += (ctx->rows[c] - r0[c]) * (double)(T - 1);
       }
     } catch (...) {
       ctx->stream = sa;
-      cudaStreamEndCapture(sa, &g);
+      cudaGraph_t gc = nullptr;
+      cudaStreamEndCapture(sa, &gc);
+      if (replay && gc) cudaGraphDestroy(gc);
       if (g) cudaGraphDestroy(g);
       ctx->stream = user;
       throw;
     }
-    LLMP_CUDA(cudaStreamEndCapture(sa, &g));
+    cudaGraph_t gc = nullptr;
+    LLMP_CUDA(cudaStreamEndCapture(sa, &gc));
+    if (replay) g = gc;
     ctx->stream = user;
     LLMP_CUDA(cudaGraphInstantiate(&ge, g, 0));
-    for (int t = 0; t < T; ++t) LLMP_CUDA(cudaGraphLaunch(ge, s));
+    if (stamps) k_stamp<<<1, 1, 0, s>>>(stamps);
+    if (replay) {
+      for (int t = 0; t < T; ++t) LLMP_CUDA(cudaGraphLaunch(ge, s));
+    } else {
+      LLMP_CUDA(cudaGraphLaunch(ge, s));
+    }
     LLMP_CUDA(cudaGraphExecDestroy(ge));
     LLMP_CUDA(cudaGraphDestroy(g));
   } else {
-    for (int t = 0; t < T; ++t) {
-      tree(A[0]);
-      tree(A[1]);
-      LLMP_LAUNCH(ctx, KC_MISC, 0, k_next_tree, 1, 1, 0, d_tree);
-    }
+    for (int t = 0; t < T; ++t) round(nullptr);
   }
 
+  if (stamps) {   // diagnostics: per-round device durations
+    std::vector<unsigned long long> h(T + 1);
+    LLMP_CUDA(cudaMemcpyAsync(h.data(), stamps, (T + 1) * 8, cudaMemcpyDeviceToHost, s));
+    LLMP_CUDA(cudaStreamSynchronize(s));
+    std::vector<double> du(T);
+    for (int t = 0; t < T; ++t) du[t] = (h[t + 1] - h[t]) * 1e-3;
+    std::vector<double> so(du);
+    std::sort(so.begin(), so.end());
+    double tot = 0;
+    for (double x : du) tot += x;
+    fprintf(stderr, "[llmp] rounds: total %.1f ms  min %.1f  p10 %.1f  med %.1f  p90 %.1f  max %.1f us; slowest:", tot * 1e-3,
+            so[0], so[T / 10], so[T / 2], so[(9 * T) / 10], so[T - 1]);
+    for (int k = 0; k < 6 && k < T; ++k) {
+      int am = 0;
+      for (int t = 1; t < T; ++t)
+        if (du[t] > du[am]) am = t;
+      fprintf(stderr, " t%d=%.0f", am, du[am]);
+      du[am] = -1;
+    }
+    fprintf(stderr, "\n");
+  }
+  phase("loop");
   // ---- model to host
   out.F = F;
   out.users_col = ds.users_col;
@@ -2111,7 +2226,9 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   }
   LLMP_CUDA(cudaMemcpyAsync(out.base, d_base.p, 8, cudaMemcpyDeviceToHost, s));
   LLMP_CUDA(cudaStreamSynchronize(s));
+  phase("to_host");
   upload_model_nodes(ctx, out);
+  phase("upload");
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -2123,7 +2240,7 @@ void debug_histogram(Ctx* ctx, const uint8_t* codes, int64_t n, const int32_t* i
   a.codes = codes;
   a.n = n;
   a.F = kMaxF;
-  DevBuf d_out((size_t)SLOT * 8);
+  DevBuf& d_out = ctx->workspace("dbg_hist", (size_t)SLOT * 8);
   LLMP_CUDA(cudaMemsetAsync(d_out.p, 0, d_out.bytes, ctx->stream));
   DbgArgs dbg{idx, qg, qh, idx ? m : n, d_out.as<int64_t>()};
   static bool attr_set = false;
@@ -2132,10 +2249,12 @@ void debug_histogram(Ctx* ctx, const uint8_t* codes, int64_t n, const int32_t* i
     LLMP_CUDA(cudaFuncSetAttribute(k_hist2<HM_DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize, H2_SMEM));
     attr_set = true;
   }
+  FitPair fp;
+  fp.t[0] = a;
   if (use_hist1())
-    LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist<HM_DEBUG>, 2 * ctx->sms, HIST_THREADS, HIST_SMEM, a, 0, 0, dbg);
+    LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist<HM_DEBUG>, 2 * ctx->sms, HIST_THREADS, HIST_SMEM, fp, 0, 0, dbg);
   else
-    LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist2<HM_DEBUG>, 2 * ctx->sms, H2_THREADS, H2_SMEM, a, 0, 0, dbg);
+    LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist2<HM_DEBUG>, 2 * ctx->sms, H2_THREADS, H2_SMEM, fp, 0, 0, dbg);
   LLMP_CUDA(cudaMemcpyAsync(Hg, d_out.p, kHistBins * 8, cudaMemcpyDeviceToHost, ctx->stream));
   LLMP_CUDA(cudaMemcpyAsync(Hh, d_out.as<int64_t>() + kHistBins, kHistBins * 8, cudaMemcpyDeviceToHost, ctx->stream));
   LLMP_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -1,5 +1,5 @@
 """Subprocess helper for test_gpu_parity.test_kernel_variants: the kernel-variant switches
-(LLMP_NOFUSE, LLMP_ROOT2, LLMP_SPLIT_CLUSTER, LLMP_NO_UROW, LLMP_HIST2, LLMP_SERIAL) are read once per process, so each variant is checked in
+(LLMP_NOFUSE, LLMP_ROOT2, LLMP_SPLIT_CLUSTER, LLMP_NO_UROW, LLMP_HIST2, LLMP_PAIRED, LLMP_GRAPH_REPLAY) are read once per process, so each variant is checked in
 its own interpreter.  Fits paper-shaped (C1 with 12 features, C2) and random (S1, ragged) data through the
 C-ABI in both execution modes (graph replay, instrumented plain launches) and compares with the oracle;
 checks the histogram test hook (the variant's histogram kernel) against brute-force sums."""

@@ -11,7 +11,7 @@ ncu --set full --clock-control none --import-source on \
     --kernel-name regex:"k_pcount|k_pscatter|k_hist|k_split|k_part" -c ${NCU_COUNT:-31} -o /tmp/$TAG \
     python tools/profile_fit.py --trees 2 --repeat 1 > ${OUT}_fit.log 2>&1
 python tools/ncu_summary.py $REP $OUT "tree 0 of target 0 ($TAG)"
-for spec in "k_part:4" "k_hist:5" "k_hist:7" "k_split3:5" "${EXTRA_SASS}"; do
+for spec in "k_part:4" "k_hist:5" "k_hist:7" "k_hist:8" "k_split3:5" "${EXTRA_SASS}"; do
   [ -z "$spec" ] && continue
   k=${spec%%:*}; s=${spec##*:}
   ncu -i $REP --page source --csv --print-source sass --kernel-name "regex:$k" --launch-skip $s --launch-count 1 \
