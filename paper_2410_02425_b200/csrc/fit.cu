@@ -1888,7 +1888,9 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   int* d_tree = ctx->workspace("tree_idx", sizeof(int)).as<int>();
 
   // the two ensembles are independent: every tree-loop kernel grows both (blockIdx.y = target)
-  const bool graphs = T > 0 && !ctx->timing && ctx->use_graphs;
+  // multi-rank: plain launches (the NCCL calls are never captured, in particular not into the body of
+  // a conditional graph node; the plain-launch loop is the one the 1-GPU timing mode exercises)
+  const bool graphs = T > 0 && !ctx->timing && ctx->use_graphs && ctx->nranks == 1;
   size_t lvl_nodes = 0;
   for (int d = 0; d <= D; ++d) lvl_nodes += (size_t)1 << d;
   const size_t tab_bytes = lvl_nodes * (8 /*start*/ + 8 /*cnt*/ + 8 /*gcnt*/ + 8 + 8 /*lo,hi*/ + 4 + 4 /*split*/ +

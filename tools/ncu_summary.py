@@ -21,7 +21,8 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "sm__warps_active.avg.pct_of_peak_sustained_active"]
 CLASS = {"k_hist<0>": "hist_root", "k_hist<1>": "hist_level", "k_hist<3>": "update", "k_hist_root2": "hist_root",
          "k_pcount": "partition", "k_pscan": "partition", "k_pscatter2": "partition", "k_split3": "split",
-         "k_update": "update", "k_root_fix": "misc", "k_next_tree": "misc"}
+         "k_update": "update", "k_root_fix": "misc", "k_next_tree": "misc", "k_next_tree_cond": "misc",
+         "k_part": "partition", "k_hist2<0>": "hist_root", "k_hist2<1>": "hist_level", "k_hist2<3>": "update"}
 
 
 def kclass(name):
