@@ -148,6 +148,17 @@ llmpilot_status llmpilot_model_info(const llmpilot_model* m, int32_t* F, int32_t
 llmpilot_status llmpilot_model_export(const llmpilot_model* m, float* base, int32_t* feat, int32_t* bin, float* thr,
                                       float* val);
 llmpilot_status llmpilot_model_train_pred(const llmpilot_model* m, float* train_pred /* host, n_rows x 2 */);
+/* Split losses ((gain(L) + gain(R)) - gain(parent), fp64) of every split node,
+ * [2][n_trees][nodes] host doubles, 0 at leaves and unused slots. */
+llmpilot_status llmpilot_model_gains(const llmpilot_model* m, double* gain);
+/* MDI feature importance (Mean Decrease in Impurity, §III-B P:L120 and §III-D
+ * P:L156-158).  For weighted squared error a split's impurity decrease is its
+ * loss G_L^2/(H_L+lambda) + G_R^2/(H_R+lambda) - G^2/(H+lambda) (the weighted SSE decrease when
+ * lambda = 0).  out (host, 2 x F doubles, target-major): per target, the losses of the splits on
+ * each feature summed over the trees in order and each tree's nodes in index order; if normalize
+ * != 0, divided by the target's total (all zeros when the ensemble has no split).
+ * Errors: LLMP_EINVAL for NULL arguments. */
+llmpilot_status llmpilot_model_importance(const llmpilot_model* m, int32_t normalize, double* out);
 /* Free a model.  Its device buffers are released stream-ordered (cudaFreeAsync into the
  * device's default memory pool, which keeps the memory cached) on the stream of the context
  * that fitted it: free a model before destroying that stream, and only after work that reads the

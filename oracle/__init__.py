@@ -97,6 +97,10 @@ def lib():
         L.orc_fit.argtypes = [P, P, P, P, P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                               C.c_int64, C.c_int64, P, C.c_float, C.c_float, P, P, P, P, P, P, P, P,
                               C.c_int32]
+        L.orc_fit_gain.restype = C.c_int
+        L.orc_fit_gain.argtypes = L.orc_fit.argtypes[:22] + [P] + L.orc_fit.argtypes[22:]
+        L.orc_importance.restype = None
+        L.orc_importance.argtypes = [C.c_int32, C.c_int32, C.c_int32, P, P, C.c_int32, P]
         L.orc_predict.argtypes = [P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, P, P, P, P, P]
         L.orc_recommend.argtypes = [P, C.c_int32, C.c_int32, C.c_int32, P, P, P, C.c_float, C.c_float,
                                     C.c_int64, P]
@@ -191,10 +195,11 @@ def best_split(Hg, Hh, nbins, users_col=-1, monotone_users=0, eg=0, eh=0, K=0, l
 class Model:
     """Oracle ensemble: complete-binary trees [2][T][2^(D+1)-1]."""
 
-    def __init__(self, F, hp, cuts_, ncuts, base, feat, bin_, thr, val):
+    def __init__(self, F, hp, cuts_, ncuts, base, feat, bin_, thr, val, gain=None):
         self.F, self.hp = F, hp
         self.cuts, self.ncuts, self.base = cuts_, ncuts, base
         self.feat, self.bin, self.thr, self.val = feat, bin_, thr, val
+        self.gain = gain   # [2][T][nodes] split losses (fp64), 0 at leaves / unused slots
 
     @property
     def n_trees(self):
@@ -218,16 +223,27 @@ def fit(X, y, hp: Hparams, users_col, llm_id=None, prof_id=None, n_llm=1, n_prof
     bin_ = np.zeros((2, T, nn), np.int32)
     thr = np.zeros((2, T, nn), np.float32)
     val = np.zeros((2, T, nn), np.float32)
+    gain = np.zeros((2, T, nn), np.float64)
     tp = np.zeros((n, 2), np.float32)
-    rc = lib().orc_fit(_p(X), _p(y), None if wv is None else _p(wv), _p(li), _p(pi), n, F, users_col, n_llm,
-                       n_prof, row_offset, n if n_global is None else n_global, C.byref(hp), L1, L2, _p(ct),
-                       _p(nc), _p(base), _p(feat), _p(bin_), _p(thr), _p(val), _p(tp), n_trees_limit)
+    rc = lib().orc_fit_gain(_p(X), _p(y), None if wv is None else _p(wv), _p(li), _p(pi), n, F, users_col, n_llm,
+                            n_prof, row_offset, n if n_global is None else n_global, C.byref(hp), L1, L2, _p(ct),
+                            _p(nc), _p(base), _p(feat), _p(bin_), _p(thr), _p(val), _p(gain), _p(tp), n_trees_limit)
     if rc:
         raise ValueError("orc_fit: invalid input")
     if n_trees_limit and n_trees_limit < T:
-        feat, bin_, thr, val = (a[:, :n_trees_limit].copy() for a in (feat, bin_, thr, val))
-    m = Model(F, hp, ct[:F].copy(), nc[:F].copy(), base, feat, bin_, thr, val)
+        feat, bin_, thr, val, gain = (a[:, :n_trees_limit].copy() for a in (feat, bin_, thr, val, gain))
+    m = Model(F, hp, ct[:F].copy(), nc[:F].copy(), base, feat, bin_, thr, val, gain)
     return (m, tp) if return_train_pred else m
+
+
+def importance(model: Model, normalize=True) -> np.ndarray:
+    """MDI feature importance: 2 x F, fp64."""
+    feat = _c(model.feat, np.int32)
+    T, nn = feat.shape[1], feat.shape[2]
+    D = int(np.log2(nn + 1)) - 1
+    out = np.zeros((2, model.F), np.float64)
+    lib().orc_importance(T, D, model.F, _p(feat), _p(_c(model.gain, np.float64)), 1 if normalize else 0, _p(out))
+    return out
 
 
 def predict(model: Model, X) -> np.ndarray:

@@ -223,7 +223,7 @@ typedef struct {
 static int fit_one_target(const uint8_t* codes, const float* y, const float* w, int64_t n, int32_t F,
                           int32_t users_col, int64_t row_offset, const orc_hparams* hp, const float* cuts,
                           const int32_t* ncuts, int target, float* base_out, int32_t* feat, int32_t* bin,
-                          float* thr, float* val, float* p, int32_t n_trees_fit) {
+                          float* thr, float* val, double* gain, float* p, int32_t n_trees_fit) {
   const int32_t K = hp->grad_bits, D = hp->max_depth;
   const int64_t n_nodes = ((int64_t)1 << (D + 1)) - 1;
   const double lambda = (double)hp->lambda, mcw = (double)hp->min_child_weight, eta = (double)hp->eta;
@@ -264,11 +264,13 @@ static int fit_one_target(const uint8_t* codes, const float* y, const float* w, 
     int32_t* tb = bin + (int64_t)t * n_nodes;
     float* tt = thr + (int64_t)t * n_nodes;
     float* tv = val + (int64_t)t * n_nodes;
+    double* tgn = gain ? gain + (int64_t)t * n_nodes : NULL;
     for (int64_t k = 0; k < n_nodes; ++k) {
       tf[k] = -2;
       tb[k] = 0;
       tt[k] = 0.0f;
       tv[k] = 0.0f;
+      if (tgn) tgn[k] = 0.0;
     }
     /* O4 — gradients of weighted squared error, fp32; row subsampling */
     for (int64_t i = 0; i < n; ++i) {
@@ -341,6 +343,7 @@ static int fit_one_target(const uint8_t* codes, const float* y, const float* w, 
         }
         tf[nd->k] = sp.f;
         tb[nd->k] = sp.b;
+        if (tgn) tgn[nd->k] = sp.loss;   /* the split's loss reduction (O6), kept for MDI */
         tt[nd->k] = cuts[(int64_t)sp.f * (ORC_MAX_BIN - 1) + sp.b];
         /* O7 — children: code <= b goes left; monotone bounds on users splits */
         double lo_l = nd->lo, hi_l = nd->hi, lo_r = nd->lo, hi_r = nd->hi;
@@ -398,6 +401,15 @@ int orc_fit(const float* X, const float* y, const float* w_in, const int32_t* ll
             int64_t n, int32_t F, int32_t users_col, int32_t n_llm, int32_t n_prof, int64_t row_offset,
             int64_t n_global, const orc_hparams* hp, float L1, float L2, float* cuts, int32_t* ncuts, float* base,
             int32_t* feat, int32_t* bin, float* thr, float* val, float* train_pred, int32_t n_trees_limit) {
+  return orc_fit_gain(X, y, w_in, llm_id, prof_id, n, F, users_col, n_llm, n_prof, row_offset, n_global, hp, L1, L2,
+                      cuts, ncuts, base, feat, bin, thr, val, NULL, train_pred, n_trees_limit);
+}
+
+int orc_fit_gain(const float* X, const float* y, const float* w_in, const int32_t* llm_id, const int32_t* prof_id,
+                 int64_t n, int32_t F, int32_t users_col, int32_t n_llm, int32_t n_prof, int64_t row_offset,
+                 int64_t n_global, const orc_hparams* hp, float L1, float L2, float* cuts, int32_t* ncuts,
+                 float* base, int32_t* feat, int32_t* bin, float* thr, float* val, double* gain, float* train_pred,
+                 int32_t n_trees_limit) {
   if (n < 1 || F < 1 || F > ORC_MAX_F || users_col < 0 || users_col >= F) return 1;
   if (hp->max_depth < 1 || hp->max_depth > 12 || hp->n_trees < 0 || hp->grad_bits < 2 || hp->grad_bits > 14) return 1;
   if (hp->max_bin < 2 || hp->max_bin > 256) return 1;
@@ -424,7 +436,7 @@ int orc_fit(const float* X, const float* y, const float* w_in, const int32_t* ll
   for (int target = 0; target < 2; ++target) {
     int64_t off = (int64_t)target * hp->n_trees * n_nodes;
     fit_one_target(codes, y, w, n, F, users_col, row_offset, hp, cuts, ncuts, target, &base[target], feat + off,
-                   bin + off, thr + off, val + off, p, nt);
+                   bin + off, thr + off, val + off, gain ? gain + off : NULL, p, nt);
     if (train_pred)
       for (int64_t i = 0; i < n; ++i) train_pred[i * 2 + target] = p[i];
   }
@@ -432,6 +444,33 @@ int orc_fit(const float* X, const float* y, const float* w_in, const int32_t* ll
   free(codes);
   free(w);
   return 0;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* MDI feature importance (§III-B P:L120 and §III-D P:L156-158 use
+ * the Mean Decrease in Impurity [3]).  For weighted squared error the impurity decrease of a
+ * split is SSE(parent) - SSE(left) - SSE(right) = GL^2/HL + GR^2/HR - G^2/H, i.e. the split loss
+ * of O6 (with lambda = 0; the regularised loss otherwise).  raw[t][f] = sum over the trees in
+ * order, and over each tree's nodes in index order, of the loss of every split on f (fp64);
+ * normalised: raw / sum_f raw (all zeros stay zero). */
+void orc_importance(int32_t n_trees, int32_t max_depth, int32_t F, const int32_t* feat, const double* gain,
+                    int32_t normalize, double* out /* 2 x F */) {
+  const int64_t n_nodes = ((int64_t)1 << (max_depth + 1)) - 1;
+  for (int target = 0; target < 2; ++target) {
+    double* o = out + (int64_t)target * F;
+    for (int32_t f = 0; f < F; ++f) o[f] = 0.0;
+    for (int32_t t = 0; t < n_trees; ++t) {
+      const int64_t off = ((int64_t)target * n_trees + t) * n_nodes;
+      for (int64_t k = 0; k < n_nodes; ++k)
+        if (feat[off + k] >= 0) o[feat[off + k]] += gain[off + k];
+    }
+    if (normalize) {
+      double tot = 0.0;
+      for (int32_t f = 0; f < F; ++f) tot += o[f];
+      if (tot > 0.0)
+        for (int32_t f = 0; f < F; ++f) o[f] = o[f] / tot;
+    }
+  }
 }
 
 /* ------------------------------------------------------------------------------------------ */

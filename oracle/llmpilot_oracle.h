@@ -78,6 +78,19 @@ int orc_fit(const float* X, const float* y, const float* w_in, const int32_t* ll
             float* base, int32_t* feat, int32_t* bin, float* thr, float* val, float* train_pred,
             int32_t n_trees_limit /* <=0: all; else fit only the first k trees of each target */);
 
+/* orc_fit plus gain [2][n_trees][nodes] (may be NULL): the loss of every split node, 0 elsewhere */
+int orc_fit_gain(const float* X, const float* y, const float* w_in, const int32_t* llm_id, const int32_t* prof_id,
+                 int64_t n, int32_t F, int32_t users_col, int32_t n_llm, int32_t n_prof, int64_t row_offset,
+                 int64_t n_global, const orc_hparams* hp, float L1, float L2, float* cuts, int32_t* ncuts,
+                 float* base, int32_t* feat, int32_t* bin, float* thr, float* val, double* gain, float* train_pred,
+                 int32_t n_trees_limit);
+
+/* MDI feature importance: per target, the sum
+ * of the split losses on each feature over trees (in order) and nodes (index order), fp64;
+ * normalize != 0 divides by the target's total.  out: 2 x F. */
+void orc_importance(int32_t n_trees, int32_t max_depth, int32_t F, const int32_t* feat, const double* gain,
+                    int32_t normalize, double* out);
+
 /* O10 — predict: p = base; p = p + v_t(x) in tree order; x_f < thr goes left */
 void orc_predict(const float* X, int64_t n, int32_t F, int32_t n_trees, int32_t max_depth, const float* base,
                  const int32_t* feat, const float* thr, const float* val, float* out /* n x 2 */);

@@ -91,6 +91,8 @@ def lib():
         "llmpilot_model_info": [P, C.POINTER(I32), C.POINTER(I32), C.POINTER(I32), C.POINTER(I32)],
         "llmpilot_model_export": [P, P, P, P, P, P],
         "llmpilot_model_train_pred": [P, P],
+        "llmpilot_model_gains": [P, P],
+        "llmpilot_model_importance": [P, I32, P],
         "llmpilot_predict": [P, P, P, I64, P],
         "llmpilot_recommend": [P, P, P, I32, I32, P, I32, I32, P, P, P, I32, F32, F32, I64, C.POINTER(Rec), P],
         "llmpilot_cv_leave_one_llm_out": [P, C.POINTER(DatasetC), C.POINTER(HParams), I32, F32, F32, I64, P,
@@ -274,6 +276,18 @@ class Model:
         thr = np.zeros(shp, np.float32); val = np.zeros(shp, np.float32)
         _check(lib().llmpilot_model_export(self._h, *(a.ctypes.data_as(C.c_void_p) for a in (base, feat, bin_, thr, val))))
         return dict(base=base, feat=feat, bin=bin_, thr=thr, val=val)
+
+    def gains(self) -> np.ndarray:
+        """llmpilot_model_gains: [2][n_trees][nodes] split losses (fp64)."""
+        out = np.zeros((2, self.n_trees, self.n_nodes), np.float64)
+        _check(lib().llmpilot_model_gains(self._h, out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def importance(self, normalize: bool = True) -> np.ndarray:
+        """llmpilot_model_importance: MDI feature importance, 2 x F (fp64)."""
+        out = np.zeros((2, self.F), np.float64)
+        _check(lib().llmpilot_model_importance(self._h, 1 if normalize else 0, out.ctypes.data_as(C.c_void_p)))
+        return out
 
     def train_pred(self, n_rows: int) -> np.ndarray:
         out = np.zeros((n_rows, 2), np.float32)

@@ -309,6 +309,38 @@ llmpilot_status llmpilot_model_export(const llmpilot_model* m, float* base, int3
   });
 }
 
+llmpilot_status llmpilot_model_gains(const llmpilot_model* m, double* gain) {
+  return guarded([&] {
+    LLMP_REQUIRE(m && gain, "NULL argument");
+    memcpy(gain, m->m.gain.data(), m->m.gain.size() * 8);
+  });
+}
+
+// MDI: per target, split losses summed by feature over trees in order
+// and nodes in index order (fp64, the order the oracle uses), optionally divided by the total
+llmpilot_status llmpilot_model_importance(const llmpilot_model* m, int32_t normalize, double* out) {
+  return guarded([&] {
+    LLMP_REQUIRE(m && out, "NULL argument");
+    const llmp::ModelData& md = m->m;
+    const int F = md.F;
+    for (int tg = 0; tg < 2; ++tg) {
+      double* o = out + (size_t)tg * F;
+      for (int f = 0; f < F; ++f) o[f] = 0.0;
+      for (int t = 0; t < md.T; ++t) {
+        const size_t off = ((size_t)tg * md.T + t) * md.nn;
+        for (int k = 0; k < md.nn; ++k)
+          if (md.feat[off + k] >= 0) o[md.feat[off + k]] += md.gain[off + k];
+      }
+      if (normalize) {
+        double tot = 0.0;
+        for (int f = 0; f < F; ++f) tot += o[f];
+        if (tot > 0.0)
+          for (int f = 0; f < F; ++f) o[f] = o[f] / tot;
+      }
+    }
+  });
+}
+
 llmpilot_status llmpilot_model_train_pred(const llmpilot_model* m, float* train_pred) {
   return guarded([&] {
     LLMP_REQUIRE(m && train_pred, "NULL argument");

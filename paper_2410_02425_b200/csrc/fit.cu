@@ -92,6 +92,7 @@ struct FitArgs {
   int32_t* tbin;
   float* tthr;
   float* tval;
+  double* tgain;         // [T][nn] split losses (MDI importance), 0 elsewhere
   double eta, lambda, mcw;
   float subsample, colsample;
   uint64_t seed;
@@ -151,7 +152,11 @@ __device__ __forceinline__ bool root_needed(const FitArgs& a, int t) {
   return exp_of(__uint_as_float(a.maxg[t])) != exp_of(__uint_as_float(a.maxg[t - 1])) ||
          exp_of(__uint_as_float(a.maxh[t])) != exp_of(__uint_as_float(a.maxh[t - 1]));
 }
-constexpr int UPDROOT_TREE_SMEM = 512 * 6;   // s_feat (int8), s_bin (u8), s_val (f32) of one tree
+// one tree in shared memory after the histogram kernels' dynamic smem, sized for the fit's depth
+// (nnp = nn + 1 = 2^(D+1)): k_hist: s_feat (int8, nnp), s_bin (u8, nnp), s_val (f32, nnp);
+// k_hist2: the fixed-depth routing table (s_rf, s_rb: u8 x 2^D each, s_lv: f32 x 2^D).
+// Depth 8 adds 3 KB (two CTAs per SM); depth 10 adds 12 KB.
+__host__ __device__ constexpr int updroot_tree_smem(int D) { return 6 << (D + 1); }
 
 // One row of a lane's run-length aggregation: if the row's cell address `ca` differs from the
 // current run's `pa`, flush the run (two 32-bit shared reductions) and start a new one; then add
@@ -203,8 +208,8 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitPair fp, cons
   }
   // fused mode: tree t (the one just grown) in shared memory for routing
   int8_t* s_feat = reinterpret_cast<int8_t*>(smem + HIST_SMEM);
-  uint8_t* s_bin = smem + HIST_SMEM + 512;
-  float* s_val = reinterpret_cast<float*>(smem + HIST_SMEM + 1024);
+  uint8_t* s_bin = smem + HIST_SMEM + (a.nn + 1);
+  float* s_val = reinterpret_cast<float*>(smem + HIST_SMEM + 2 * (a.nn + 1));
   if (MODE == HM_UPDROOT) {
     const size_t to = (size_t)t * a.nn;
     for (int i = tid; i < a.nn; i += HIST_THREADS) {
@@ -528,17 +533,27 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
 
   for (int i = tid; i < 2 * H2_CELLS; i += H2_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
   for (int i = tid; i < 2 * kBins; i += H2_THREADS) reinterpret_cast<uint32_t*>(sug)[i] = 0u;
-  // fused mode: tree t (the one just grown) in shared memory for routing
-  int8_t* s_feat = reinterpret_cast<int8_t*>(smem + H2_SMEM);
-  uint8_t* s_bin = smem + H2_SMEM + 512;
-  float* s_val = reinterpret_cast<float*>(smem + H2_SMEM + 1024);
+  // fused mode: tree t (the one just grown) in shared memory as a fixed-depth routing table: every
+  // row descends exactly D levels.  Internal node k (depth < D): s_rf[k], s_rb[k] = its split; a leaf
+  // above depth D and everything below it get (0, 255), i.e. "always left" (no code exceeds 255), so
+  // a row reaching leaf k at depth d ends at k's leftmost depth-D descendant (k+1)·2^(D-d) - 1,
+  // whose slot in s_lv holds k's value.  No per-level leaf test.
+  uint8_t* s_rf = smem + H2_SMEM;
+  uint8_t* s_rb = smem + H2_SMEM + (a.nn + 1) / 2;
+  float* s_lv = reinterpret_cast<float*>(smem + H2_SMEM + (a.nn + 1));   // 2^D depth-D slots
+  const int n_int = (a.nn - 1) / 2;   // 2^D - 1 slots above depth D
   if (MODE == HM_UPDROOT) {
     const size_t to = (size_t)t * a.nn;
     for (int i = tid; i < a.nn; i += H2_THREADS) {
       const int f = a.tfeat[to + i];
-      s_feat[i] = (int8_t)(f < 0 ? -1 : f);
-      s_bin[i] = (uint8_t)a.tbin[to + i];
-      s_val[i] = a.tval[to + i];
+      if (i < n_int) {
+        s_rf[i] = (uint8_t)(f >= 0 ? f : 0);
+        s_rb[i] = (uint8_t)(f >= 0 ? a.tbin[to + i] : 255);
+      }
+      if (f == -1) {   // leaf at depth d = floor(log2(i + 1))
+        const int dl = 31 - __clz(i + 1);
+        s_lv[((i + 1) << (a.D - dl)) - 1 - n_int] = a.tval[to + i];
+      }
     }
   }
   // ---- piece list (virtual concatenation of the rows to histogram)
@@ -687,13 +702,11 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
         if (MODE == HM_UPDROOT && valid) {
           // O9 for tree t (route the lane's own staged row, p += v), then O4 for tree t+1
           const int64_t ridx = base + lane + poff;
+          // both children's node words are loaded together with the row's code byte, so each level
+          // costs one shared-memory round trip (a leaf keeps k; its child indices stay < nn)
           int k = 0;
-          for (int s2 = 0; s2 < a.D; ++s2) {
-            const int f = s_feat[k];
-            const int nk = 2 * k + 1 + (myrow[f & 31] > s_bin[k] ? 1 : 0);
-            k = f >= 0 ? nk : k;
-          }
-          const float pn = __fadd_rn(np_, s_val[k]);   // one fp32 rounding, tree order
+          for (int s2 = 0; s2 < a.D; ++s2) k = 2 * k + 1 + (myrow[s_rf[k]] > s_rb[k] ? 1 : 0);
+          const float pn = __fadd_rn(np_, s_lv[k - n_int]);   // one fp32 rounding, tree order
           a.p[ridx] = pn;
           if (has_next) {
             float g = __fmul_rn(nw, __fsub_rn(pn, ny));
@@ -1473,6 +1486,7 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitPair fp, con
   int32_t* const tbin = a.tbin + (size_t)t * a.nn;
   float* const tthr = a.tthr + (size_t)t * a.nn;
   float* const tval = a.tval + (size_t)t * a.nn;
+  double* const tgain = a.tgain + (size_t)t * a.nn;
   const double G = dequant(GqN, sgi), H = dequant(HqN, shi);
   const double wP = calc_weight(G, H, lo, hi, lambda, mcw);
   const int gk = (1 << d) - 1 + k;
@@ -1494,6 +1508,7 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitPair fp, con
     tbin[gk] = bs;
     tthr[gk] = a.cuts[fs * (kBins - 1) + bs];
     tval[gk] = 0.0f;
+    tgain[gk] = ml;   // the split's loss reduction (MDI)
     if (d + 1 < a.D) {
       const LevelView& N = a.lv[d + 1];
       N.cnt[2 * k] = 0;   // k_part's child cursors
@@ -1874,6 +1889,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   DevBuf& d_p = keep_train_pred ? out.d_train_pred : ctx->workspace("p", (size_t)n * 4 * 2);
   out.device = ctx->device;
   DevBuf& d_trees = ctx->workspace("trees", (size_t)2 * std::max(T, 1) * nn * 16);
+  DevBuf& d_gain = ctx->workspace("gains", (size_t)2 * std::max(T, 1) * nn * 8);
+  LLMP_CUDA(cudaMemsetAsync(d_gain.p, 0, d_gain.bytes, s));
   DevBuf& d_max = ctx->workspace("gradmax", (size_t)2 * 2 * (T + 1) * 4);
   DevBuf& d_sums = ctx->workspace("basesums", 2 * 2 * 8);
   DevBuf& d_base = ctx->workspace("base", 2 * 4);
@@ -1949,6 +1966,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     a.tbin = bin_all + (size_t)tg * T * nn;
     a.tthr = thr_all + (size_t)tg * T * nn;
     a.tval = val_all + (size_t)tg * T * nn;
+    a.tgain = d_gain.as<double>() + (size_t)tg * T * nn;
     DevBuf& d_tab = ctx->workspace("tab" + sx, tab_bytes);
     uint8_t* tb = d_tab.as<uint8_t>();
     int64_t* start = reinterpret_cast<int64_t*>(tb);
@@ -1984,15 +2002,16 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     LLMP_CUDA(cudaFuncSetAttribute(k_hist_root2, cudaFuncAttributeMaxDynamicSharedMemorySize, R2_SMEM));
     LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_ROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
     LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_LEVEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
-    LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_UPDROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   HIST_SMEM + UPDROOT_TREE_SMEM));
     LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
     LLMP_CUDA(cudaFuncSetAttribute(k_hist2<HM_ROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, H2_SMEM));
     LLMP_CUDA(cudaFuncSetAttribute(k_hist2<HM_LEVEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, H2_SMEM));
-    LLMP_CUDA(cudaFuncSetAttribute(k_hist2<HM_UPDROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   H2_SMEM + UPDROOT_TREE_SMEM));
     attr_set = true;
   }
+  // the fused update kernels' dynamic shared memory depends on the depth (the tree they route)
+  LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_UPDROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 HIST_SMEM + updroot_tree_smem(D)));
+  LLMP_CUDA(cudaFuncSetAttribute(k_hist2<HM_UPDROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 H2_SMEM + updroot_tree_smem(D)));
   const DbgArgs nodbg{};
 
   phase("state");
@@ -2083,10 +2102,10 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     if (fused) {   // update tree t + root histogram of tree t+1 (into the now free root slot)
       for (int q = 0; q < ny; ++q) LLMP_CUDA(cudaMemsetAsync(fp.t[q].H[0], 0, (size_t)SLOT * 8, st));
       if (hist1 & 4)
-        LLMP_LAUNCH(ctx, KC_UPDATE, ny * n, k_hist<HM_UPDROOT>, hg, HIST_THREADS, HIST_SMEM + UPDROOT_TREE_SMEM, fp,
+        LLMP_LAUNCH(ctx, KC_UPDATE, ny * n, k_hist<HM_UPDROOT>, hg, HIST_THREADS, HIST_SMEM + updroot_tree_smem(D), fp,
                     0, 0, nodbg);
       else
-        LLMP_LAUNCH(ctx, KC_UPDATE, ny * n, k_hist2<HM_UPDROOT>, hg, H2_THREADS, H2_SMEM + UPDROOT_TREE_SMEM, fp, 0,
+        LLMP_LAUNCH(ctx, KC_UPDATE, ny * n, k_hist2<HM_UPDROOT>, hg, H2_THREADS, H2_SMEM + updroot_tree_smem(D), fp, 0,
                     0, nodbg);
     } else {
       LLMP_LAUNCH(ctx, KC_UPDATE, ny * n, k_update, dim3(std::max(1, upd_grid * ny / 2), ny), UPD_THREADS, 0, fp);
@@ -2220,7 +2239,9 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   out.bin.resize(tot);
   out.thr.resize(tot);
   out.val.resize(tot);
+  out.gain.resize(tot);
   if (tot) {
+    LLMP_CUDA(cudaMemcpyAsync(out.gain.data(), d_gain.p, tot * 8, cudaMemcpyDeviceToHost, s));
     LLMP_CUDA(cudaMemcpyAsync(out.feat.data(), feat_all, tot * 4, cudaMemcpyDeviceToHost, s));
     LLMP_CUDA(cudaMemcpyAsync(out.bin.data(), bin_all, tot * 4, cudaMemcpyDeviceToHost, s));
     LLMP_CUDA(cudaMemcpyAsync(out.thr.data(), thr_all, tot * 4, cudaMemcpyDeviceToHost, s));

@@ -22,6 +22,7 @@ struct ModelData {
   float base[2] = {0.f, 0.f};
   std::vector<int32_t> feat, bin;  // [2][T][nn]
   std::vector<float> thr, val;
+  std::vector<double> gain;        // [2][T][nn] split losses (0 at leaves / unused slots)
   CutsData cuts;
   DevBuf d_nodes;                  // uint2 [2][T][nn]: x = thr or leaf value bits, y = feat (int)
   DevBuf d_base;                   // float [2]

@@ -44,7 +44,9 @@ def main():
     cases = [(synth.make("C1"), None, dict(n_trees=20, max_depth=4)),
              (synth.make("C2"), None, dict(n_trees=12, max_depth=7)),
              (synth.make_s1(70001, seed=5), "w", dict(n_trees=4, max_depth=8, use_eq4_weights=0)),
-             (synth.make_s1(4097, seed=6), "w", dict(n_trees=3, max_depth=6, use_eq4_weights=0))]
+             (synth.make_s1(4097, seed=6), "w", dict(n_trees=3, max_depth=6, use_eq4_weights=0)),
+             (synth.make_s1(30001, seed=7), "w", dict(n_trees=3, max_depth=10, use_eq4_weights=0,
+                                                       min_child_weight=0.0))]
     for d, wk, kw in cases:
         w = d.w if wk else None
         om, otp = oracle.fit(d.X, d.y, oracle.hparams(**kw), d.users_col, d.llm_id, d.prof_id, d.n_llm, d.n_prof,

@@ -135,12 +135,26 @@ def test_fit_parity_c1(lp, ctx):
     assert _bits_equal(out.cpu().numpy(), otp)
 
 
+def test_importance_parity(lp, ctx):
+    """MDI importance: the split losses the split kernel records and the
+    importances summed from them are bit-identical to the oracle's (C1 and C2, with colsample)."""
+    for d, kw in ((synth.make("C1"), dict(n_trees=20, max_depth=4)),
+                  (synth.make("C2"), dict(n_trees=15, max_depth=6, colsample_bytree=0.7, seed=3))):
+        om, _, gm = _fit_both(lp, ctx, d, **kw)
+        _assert_same_model(om, gm.export())
+        assert np.array_equal(om.gain, gm.gains())
+        for nrm in (False, True):
+            assert np.array_equal(oracle.importance(om, nrm), gm.importance(nrm))
+
+
 @pytest.mark.parametrize("kw", [
     dict(),
     dict(monotone_users=0),
     dict(subsample=0.7, colsample_bytree=0.6, seed=7),
     dict(max_depth=1, n_trees=10),
     dict(max_depth=7, n_trees=6),
+    dict(max_depth=9, n_trees=4, min_child_weight=0.0),
+    dict(max_depth=10, n_trees=4, min_child_weight=0.0),
     dict(max_bin=16, grad_bits=8),
     dict(lambda_=0.0, min_child_weight=0.0),
     dict(min_child_weight=5.0, eta=0.1),
