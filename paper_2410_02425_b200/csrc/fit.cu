@@ -9,7 +9,7 @@
 //                 k_split3(0)
 //                 for d = 1..D-1:
 //                   k_part(d)       partition of the split parents' row indices into children
-//                                   (4096-row tiles, one atomic reservation per child per tile);
+//                                   (2048-row tiles, one atomic reservation per child per tile);
 //                                   zeroes the built-child histograms
 //                   k_hist<LEVEL>   histogram of the smaller child of each split parent (codes
 //                                   and packed gradient pairs gathered by row index)
@@ -1073,28 +1073,51 @@ __global__ void __launch_bounds__(R2_THREADS, 2) k_hist_root2(const FitPair fp) 
 
 // ---------------------------------------------------------------------------------------------
 // Row partition of the split parents (level d-1) into their children (level d): see k_part.
-constexpr int PT_THREADS = 256;
+constexpr int PT_THREADS = 128;
 constexpr int PT_ITEMS = 16;
-constexpr int PT_TILE = PT_THREADS * PT_ITEMS;   // 4096 rows
+constexpr int PT_TILE = PT_THREADS * PT_ITEMS;   // 2048 rows
 constexpr int PT_WORDS = PT_TILE / 32;           // bitmask words per tile
+constexpr int PT_WPL = PT_WORDS / 32;            // words per lane in the group-prefix warp
+constexpr int PT_PPT = MAX_PIECES / PT_THREADS;  // parents per thread in parent_prefixes
+static_assert(PT_WORDS % 32 == 0 && MAX_PIECES % PT_THREADS == 0, "partition tile shape");
 
-// tile and row prefixes over the level's split parents (computed by each CTA; NP <= 512)
+// tile and row prefixes over the level's split parents (computed by each CTA; NP <= 512); also
+// caches every parent's split, start and count in shared memory (s_pp), so the per-tile lookups
+// are shared-memory loads instead of a chain of dependent global loads
+struct PartParent {
+  int64_t start, cnt;
+  int32_t f, b;
+};
 __device__ __forceinline__ void parent_prefixes(const FitArgs& a, int d, int* s_tile_pref, int64_t* s_seq_pref,
-                                                int* s_w, int64_t* s_w64) {
+                                                int* s_w, int64_t* s_w64, PartParent* s_pp) {
   const int NP = 1 << (d - 1);
   const LevelView& P = a.lv[d - 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int tl[2] = {0, 0};
-  int64_t rl[2] = {0, 0};
-  for (int q = 0; q < 2; ++q) {
-    const int j = tid * 2 + q;
-    if (j < NP && P.split_f[j] >= 0) {
-      rl[q] = (d == 1) ? a.n : P.cnt[j];
-      tl[q] = (int)((rl[q] + PT_TILE - 1) / PT_TILE);
+  int tl[PT_PPT];
+  int64_t rl[PT_PPT];
+  int tv = 0;
+  int64_t rv = 0;
+#pragma unroll
+  for (int q = 0; q < PT_PPT; ++q) {
+    const int j = tid * PT_PPT + q;
+    tl[q] = 0;
+    rl[q] = 0;
+    if (j < NP) {
+      const int f = P.split_f[j];
+      PartParent pp;
+      pp.f = f;
+      pp.b = f >= 0 ? P.split_b[j] : 0;
+      pp.start = (d == 1) ? 0 : P.start[j];
+      pp.cnt = (f < 0) ? 0 : (d == 1) ? a.n : P.cnt[j];
+      s_pp[j] = pp;
+      if (f >= 0) {
+        rl[q] = pp.cnt;
+        tl[q] = (int)((rl[q] + PT_TILE - 1) / PT_TILE);
+      }
     }
+    tv += tl[q];
+    rv += rl[q];
   }
-  const int tv = tl[0] + tl[1];
-  const int64_t rv = rl[0] + rl[1];
   int tinc = tv;
   int64_t rinc = rv;
   for (int o = 1; o < 32; o <<= 1) {
@@ -1118,8 +1141,9 @@ __device__ __forceinline__ void parent_prefixes(const FitArgs& a, int d, int* s_
   }
   int te = toff + tinc - tv;
   int64_t re = roff + rinc - rv;
-  for (int q = 0; q < 2; ++q) {
-    const int j = tid * 2 + q;
+#pragma unroll
+  for (int q = 0; q < PT_PPT; ++q) {
+    const int j = tid * PT_PPT + q;
     if (j < NP) {
       s_tile_pref[j] = te;
       s_seq_pref[j] = re;
@@ -1147,7 +1171,7 @@ __device__ __forceinline__ int parent_of_tile(const int* s_tile_pref, int NP, in
 
 // ---------------------------------------------------------------------------------------------
 // Single-pass partition.  Every histogram is an integer sum, so the order of the rows inside a
-// child segment cannot change any result — only which CTA processes which rows.  Each 4096-row
+// child segment cannot change any result — only which CTA processes which rows.  Each 2048-row
 // tile of a split parent j therefore reserves its block of each child with one global atomic per
 // child instead of waiting for a prefix over all tiles: the left child fills the parent's own range
 // [s_j, s_j + n_j) of the other ping-pong buffer from the bottom (cursor C.cnt[2j]), the right child
@@ -1156,7 +1180,7 @@ __device__ __forceinline__ int parent_of_tile(const int* s_tile_pref, int NP, in
 // indices are read once; the next tile's row indices are loaded while this tile waits for its
 // reservation.  The cursors start at 0 (zeroed by the split kernel of level d-1); the children's
 // starts follow from the counts (s_j and s_j + n_L; written by the level histogram kernel).
-constexpr int PT_CTAS_PER_SM = 4;
+constexpr int PT_CTAS_PER_SM = 8;
 __global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitPair fp, const int d) {
   const FitArgs& a = fp.t[blockIdx.y];
   __shared__ int s_tile_pref[MAX_PIECES + 1];
@@ -1166,6 +1190,7 @@ __global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitPa
   __shared__ __align__(16) uint32_t s_bits[2][PT_WORDS];   // the tile's ballot words, group = (q, warp); by tile parity
   __shared__ __align__(16) int s_pre[PT_WORDS];         // exclusive left prefix of each group
   __shared__ int64_t s_lb, s_rb;                        // the tile's block offsets (left from the bottom, right from the top)
+  __shared__ PartParent s_pp[MAX_PIECES];
   const int NP = 1 << (d - 1);
   const LevelView& P = a.lv[d - 1];
   const LevelView& C = a.lv[d];
@@ -1179,7 +1204,7 @@ __global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitPa
       if (P.split_f[j] >= 0) Hz[e] = make_int4(0, 0, 0, 0);
     }
   }
-  parent_prefixes(a, d, s_tile_pref, s_seq_pref, s_w, s_w64);
+  parent_prefixes(a, d, s_tile_pref, s_seq_pref, s_w, s_w64, s_pp);
   const int ntiles = s_tile_pref[NP];
   const uint32_t lt = (1u << lane) - 1u;
   const uint32_t* const rin_all = a.sr[(d - 1) & 1];
@@ -1188,10 +1213,10 @@ __global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitPa
   auto load_rows = [&](int t, uint32_t (&r)[PT_ITEMS]) {
     if (t >= ntiles) return;
     const int j = parent_of_tile(s_tile_pref, NP, t);
-    const int64_t cnt_j = (d == 1) ? a.n : P.cnt[j];
+    const int64_t cnt_j = s_pp[j].cnt;
     const int64_t o = (int64_t)(t - s_tile_pref[j]) * PT_TILE;
     const int len = (int)min((int64_t)PT_TILE, cnt_j - o);
-    const uint32_t* rin = rin_all + ((d == 1) ? 0 : P.start[j]) + o;
+    const uint32_t* rin = rin_all + s_pp[j].start + o;
 #pragma unroll
     for (int q = 0; q < PT_ITEMS; ++q) {
       const int k = q * PT_THREADS + tid;
@@ -1204,11 +1229,12 @@ __global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitPa
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x, par ^= 1) {
     uint32_t* const bits = s_bits[par];
     const int j = parent_of_tile(s_tile_pref, NP, t);
-    const int64_t cnt_j = (d == 1) ? a.n : P.cnt[j];
-    const int64_t start_j = (d == 1) ? 0 : P.start[j];
+    const PartParent pp = s_pp[j];
+    const int64_t cnt_j = pp.cnt;
+    const int64_t start_j = pp.start;
     const int64_t o = (int64_t)(t - s_tile_pref[j]) * PT_TILE;
     const int len = (int)min((int64_t)PT_TILE, cnt_j - o);
-    const int f = P.split_f[j], b = P.split_b[j];
+    const int f = pp.f, b = pp.b;
     const uint8_t* col = a.codesT + (size_t)f * a.ldT;
     uint32_t code[PT_ITEMS];
 #pragma unroll
@@ -1221,17 +1247,25 @@ __global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitPa
     }
     load_rows(t + gridDim.x, nridx);   // in flight across the reservation below
     __syncthreads();
-    if (warp == 0) {   // group prefixes: lane L takes words 4L .. 4L+3; one atomic per child
-      const uint4 m4 = reinterpret_cast<const uint4*>(bits)[lane];
-      const int c0 = __popc(m4.x), c1 = __popc(m4.y), c2 = __popc(m4.z);
-      const int lsum = c0 + c1 + c2 + __popc(m4.w);
+    if (warp == 0) {   // group prefixes: lane L takes words PT_WPL*L ..; one atomic per child
+      int c[PT_WPL];
+      int lsum = 0;
+#pragma unroll
+      for (int w2 = 0; w2 < PT_WPL; ++w2) {
+        c[w2] = __popc(bits[PT_WPL * lane + w2]);
+        lsum += c[w2];
+      }
       int inc = lsum;
       for (int off = 1; off < 32; off <<= 1) {
         const int u = __shfl_up_sync(0xffffffffu, inc, off);
         if (lane >= off) inc += u;
       }
-      const int ex = inc - lsum;
-      reinterpret_cast<int4*>(s_pre)[lane] = make_int4(ex, ex + c0, ex + c0 + c1, ex + c0 + c1 + c2);
+      int ex = inc - lsum;
+#pragma unroll
+      for (int w2 = 0; w2 < PT_WPL; ++w2) {
+        s_pre[PT_WPL * lane + w2] = ex;
+        ex += c[w2];
+      }
       if (lane == 31) {
         const int L = inc, R = len - inc;
         s_lb = (int64_t)atomicAdd(reinterpret_cast<unsigned long long*>(&C.cnt[2 * j]), (unsigned long long)L);

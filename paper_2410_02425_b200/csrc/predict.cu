@@ -80,12 +80,11 @@ __global__ void __launch_bounds__(PRED_THREADS, 2) k_predict(const PredArgs a) {
           for (int q = 0; q < PRED_R; ++q) {
             const float* x = xs + (tid + q * PRED_THREADS) * XS_STRIDE;
             int node = 0;
-            uint2 nd = tree[0];
-            while ((int)nd.y >= 0) {
+            for (int s = 0; s < a.D; ++s) {   // fixed depth (see upload_model_nodes)
+              const uint2 nd = tree[node];
               node = 2 * node + 1 + (x[nd.y] < __uint_as_float(nd.x) ? 0 : 1);  // x < thr goes left
-              nd = tree[node];
             }
-            p[q] = __fadd_rn(p[q], __uint_as_float(nd.x));
+            p[q] = __fadd_rn(p[q], __uint_as_float(tree[node].x));
           }
         }
       }
@@ -99,15 +98,36 @@ __global__ void __launch_bounds__(PRED_THREADS, 2) k_predict(const PredArgs a) {
   }
 }
 
+// Device node table: every tree as a fixed-depth complete tree, so the predictor descends exactly D
+// levels with no leaf test.  Slots above depth D: a split {thr, f}, or — for a leaf and everything
+// below it — {+inf, 0}: x < +inf always holds (X is finite), so the row keeps going left.  A leaf k at
+// depth d < D is therefore reached at its leftmost depth-D descendant (k+1)·2^(D-d) - 1, which holds
+// k's value; a depth-D leaf holds its own.  Same leaf, same value, same fp32 add as the plain walk.
 void upload_model_nodes(Ctx* ctx, ModelData& m) {
   const size_t tot = (size_t)2 * m.T * m.nn;
+  const int n_int = (m.nn - 1) / 2;
   std::vector<uint2> h(std::max<size_t>(tot, 1));
-  for (size_t i = 0; i < tot; ++i) {
-    const int f = m.feat[i];
-    float v = f >= 0 ? m.thr[i] : m.val[i];
-    uint32_t bits;
-    memcpy(&bits, &v, 4);
-    h[i] = make_uint2(bits, (uint32_t)(f >= 0 ? f : -1));
+  const float inf = INFINITY;
+  uint32_t inf_bits;
+  memcpy(&inf_bits, &inf, 4);
+  for (size_t tr = 0; tr * m.nn < tot; ++tr) {
+    const size_t o = tr * m.nn;
+    for (int k = 0; k < m.nn; ++k) h[o + k] = make_uint2(k < n_int ? inf_bits : 0u, k < n_int ? 0u : 0xffffffffu);
+    for (int k = 0; k < m.nn; ++k) {
+      const int f = m.feat[o + k];
+      if (f >= 0) {
+        uint32_t bits;
+        memcpy(&bits, &m.thr[o + k], 4);
+        h[o + k] = make_uint2(bits, (uint32_t)f);
+      } else if (f == -1) {
+        int dl = 0;
+        while (((2 << dl) - 1) <= k) ++dl;   // depth of slot k
+        const int leaf = ((k + 1) << (m.D - dl)) - 1;
+        uint32_t bits;
+        memcpy(&bits, &m.val[o + k], 4);
+        h[o + leaf] = make_uint2(bits, 0xffffffffu);
+      }
+    }
   }
   m.d_nodes.set_stream(ctx->stream);
   m.d_base.set_stream(ctx->stream);
