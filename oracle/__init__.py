@@ -101,6 +101,10 @@ def lib():
         L.orc_fit_gain.argtypes = L.orc_fit.argtypes[:22] + [P] + L.orc_fit.argtypes[22:]
         L.orc_importance.restype = None
         L.orc_importance.argtypes = [C.c_int32, C.c_int32, C.c_int32, P, P, C.c_int32, P]
+        L.orc_wg_build.restype = C.c_int
+        L.orc_wg_build.argtypes = [P, C.c_int64, C.c_int32, P, P, P, P, P]
+        L.orc_wg_sample.restype = None
+        L.orc_wg_sample.argtypes = [P, P, C.c_int64, C.c_int32, P, P, C.c_uint64, C.c_int64, C.c_int64, P]
         L.orc_predict.argtypes = [P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, P, P, P, P, P]
         L.orc_recommend.argtypes = [P, C.c_int32, C.c_int32, C.c_int32, P, P, P, C.c_float, C.c_float,
                                     C.c_int64, P]
@@ -243,6 +247,42 @@ def importance(model: Model, normalize=True) -> np.ndarray:
     D = int(np.log2(nn + 1)) - 1
     out = np.zeros((2, model.F), np.float64)
     lib().orc_importance(T, D, model.F, _p(feat), _p(_c(model.gain, np.float64)), 1 if normalize else 0, _p(out))
+    return out
+
+
+WG_BINS = 64
+
+
+class WorkloadModel:
+    """Workload-generator model (§III-B): per-parameter bins and centres and the
+    sparse joint histogram (ascending mixed-radix keys with their row counts)."""
+
+    def __init__(self, nbins, centres, keys, counts):
+        self.nbins, self.centres, self.keys, self.counts = nbins, centres, keys, counts
+
+    @property
+    def P(self):
+        return len(self.nbins)
+
+
+def wg_build(T) -> WorkloadModel:
+    T = _c(T, np.float32)
+    n, P = T.shape
+    nb = np.zeros(P, np.int32)
+    ce = np.zeros((P, WG_BINS), np.float32)
+    keys = np.zeros(n, np.uint64)
+    counts = np.zeros(n, np.int64)
+    m = C.c_int64(0)
+    if lib().orc_wg_build(_p(T), n, P, _p(nb), _p(ce), _p(keys), _p(counts), C.byref(m)):
+        raise ValueError("orc_wg_build: invalid input")
+    return WorkloadModel(nb, ce, keys[:m.value].copy(), counts[:m.value].copy())
+
+
+def wg_sample(model: WorkloadModel, n_samples, seed=0, first=0) -> np.ndarray:
+    """samples first .. first + n_samples - 1 of `seed`, n_samples x P."""
+    out = np.zeros((n_samples, model.P), np.float32)
+    lib().orc_wg_sample(_p(model.keys), _p(model.counts), len(model.keys), model.P, _p(model.nbins),
+                        _p(model.centres), seed, first, n_samples, _p(out))
     return out
 
 

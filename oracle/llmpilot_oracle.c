@@ -731,3 +731,109 @@ int orc_cv(const float* X, const float* y, const int32_t* llm_id, const int32_t*
   free(umax_truth);
   return 0;
 }
+
+/* ------------------------------------------------------------------------------------------ */
+/* Workload generator (§III-B).  Test infrastructure. */
+/* Model: per parameter p, bins = O2's cuts with B = ORC_WG_BINS (64) — one bin per distinct value
+ * when there are at most 64 ("unless the cardinality of the parameter is lower"), else
+ * equal-frequency quantiles (exact on <= 2^20 rows, strided sample beyond); the centre of bin b is
+ * (min + max) / 2 of the trace values in it (fp64, stored as float; -0 counts as +0).  Joint model
+ * (P:L128-130): key(row) = sum_p code_p * stride_p (mixed radix, stride_0 = 1, stride_{p+1} =
+ * stride_p * nbins_p); the non-empty keys in ascending order with their row counts.
+ * Sampling: sample s of seed draws r = rng4(seed, 0x5747, s, 0), t = floor(r * n / 2^64)
+ * in [0, n), picks the first key whose cumulative count exceeds t (probability count / n) and
+ * emits every parameter's bin centre. */
+static int cmp_u64(const void* a, const void* b) {
+  uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+  return (x > y) - (x < y);
+}
+
+int orc_wg_build(const float* T, int64_t n, int32_t P, int32_t* nbins, float* centres, uint64_t* keys,
+                 int64_t* counts, int64_t* m_out) {
+  if (n < 1 || P < 1 || P > ORC_MAX_F) return 1;
+  for (int64_t i = 0; i < n * P; ++i)
+    if (!isfinite(T[i])) return 1;
+  float* cuts = (float*)malloc(sizeof(float) * ORC_MAX_F * (ORC_MAX_BIN - 1));
+  int32_t ncuts[ORC_MAX_F];
+  if (orc_cuts(T, n, P, 0, n, ORC_WG_BINS, cuts, ncuts)) {
+    free(cuts);
+    return 1;
+  }
+  /* mixed-radix strides; the key space must fit 63 bits */
+  uint64_t stride[ORC_MAX_F];
+  double space = 1.0;
+  uint64_t st = 1;
+  for (int32_t p = 0; p < P; ++p) {
+    nbins[p] = ncuts[p] + 1;
+    stride[p] = st;
+    space *= (double)nbins[p];
+    st *= (uint64_t)nbins[p];
+  }
+  if (space > 9.2e18) {
+    free(cuts);
+    return 1;
+  }
+  uint8_t* codes = (uint8_t*)malloc((size_t)n * P);
+  orc_codes(T, n, P, cuts, ncuts, codes);
+  /* per-bin min / max -> centres */
+  double* mn = (double*)malloc(sizeof(double) * P * ORC_WG_BINS);
+  double* mx = (double*)malloc(sizeof(double) * P * ORC_WG_BINS);
+  for (int64_t i = 0; i < (int64_t)P * ORC_WG_BINS; ++i) {
+    mn[i] = INFINITY;
+    mx[i] = -INFINITY;
+    centres[i] = 0.0f;
+  }
+  uint64_t* k = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)n);
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t key = 0;
+    for (int32_t p = 0; p < P; ++p) {
+      int32_t c = codes[i * P + p];
+      double x = (double)T[i * P + p];
+      if (x == 0.0) x = 0.0;
+      if (x < mn[p * ORC_WG_BINS + c]) mn[p * ORC_WG_BINS + c] = x;
+      if (x > mx[p * ORC_WG_BINS + c]) mx[p * ORC_WG_BINS + c] = x;
+      key += (uint64_t)c * stride[p];
+    }
+    k[i] = key;
+  }
+  for (int32_t p = 0; p < P; ++p)
+    for (int32_t b = 0; b < nbins[p]; ++b)
+      centres[p * ORC_WG_BINS + b] = (float)((mn[p * ORC_WG_BINS + b] + mx[p * ORC_WG_BINS + b]) * 0.5);
+  /* sparse joint histogram: sorted distinct keys with counts */
+  qsort(k, (size_t)n, sizeof(uint64_t), cmp_u64);
+  int64_t m = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (i == 0 || k[i] != k[i - 1]) {
+      keys[m] = k[i];
+      counts[m] = 0;
+      ++m;
+    }
+    counts[m - 1] += 1;
+  }
+  *m_out = m;
+  free(k);
+  free(mn);
+  free(mx);
+  free(codes);
+  free(cuts);
+  return 0;
+}
+
+void orc_wg_sample(const uint64_t* keys, const int64_t* counts, int64_t m, int32_t P, const int32_t* nbins,
+                   const float* centres, uint64_t seed, int64_t first, int64_t n_samples, float* out) {
+  int64_t n = 0;
+  for (int64_t j = 0; j < m; ++j) n += counts[j];
+  for (int64_t s = 0; s < n_samples; ++s) {
+    uint64_t r = orc_rng4(seed, 0x5747u, (uint64_t)(first + s), 0);
+    uint64_t t = (uint64_t)(((unsigned __int128)r * (unsigned __int128)(uint64_t)n) >> 64);
+    /* first j with cumulative count > t (a linear walk: plain and obviously correct) */
+    int64_t j = 0, cum = counts[0];
+    while ((uint64_t)cum <= t) cum += counts[++j];
+    uint64_t key = keys[j];
+    for (int32_t p = 0; p < P; ++p) {
+      uint64_t digit = key % (uint64_t)nbins[p];
+      key /= (uint64_t)nbins[p];
+      out[s * P + p] = centres[p * ORC_WG_BINS + digit];
+    }
+  }
+}

@@ -91,6 +91,17 @@ int orc_fit_gain(const float* X, const float* y, const float* w_in, const int32_
 void orc_importance(int32_t n_trees, int32_t max_depth, int32_t F, const int32_t* feat, const double* gain,
                     int32_t normalize, double* out);
 
+/* Workload generator (§III-B): bins = O2 cuts with 64 bins,
+ * centres = (min + max)/2 of each bin's values, sparse joint histogram of mixed-radix keys.
+ * nbins: P; centres: P x 64; keys, counts: capacity n (m_out distinct keys, ascending).
+ * Returns non-zero for invalid input (non-finite values, P out of range, key space > 2^63). */
+#define ORC_WG_BINS 64
+int orc_wg_build(const float* T, int64_t n, int32_t P, int32_t* nbins, float* centres, uint64_t* keys,
+                 int64_t* counts, int64_t* m_out);
+/* samples first .. first + n_samples - 1 of `seed` -> out (n_samples x P) */
+void orc_wg_sample(const uint64_t* keys, const int64_t* counts, int64_t m, int32_t P, const int32_t* nbins,
+                   const float* centres, uint64_t seed, int64_t first, int64_t n_samples, float* out);
+
 /* O10 — predict: p = base; p = p + v_t(x) in tree order; x_f < thr goes left */
 void orc_predict(const float* X, int64_t n, int32_t F, int32_t n_trees, int32_t max_depth, const float* base,
                  const int32_t* feat, const float* thr, const float* val, float* out /* n x 2 */);

@@ -276,3 +276,31 @@ def sweep_tables(n_llm: int = 6554, seed: int = 1, profiles=PROFILES_C2, levels=
     lf = np.stack([llm[k] for k in LLM_FIELDS], axis=1).astype(np.float32)
     pf = np.stack([prof[k] for k in PROFILE_FIELDS], axis=1).astype(np.float32)
     return lf, pf, profile_cost(profiles), np.asarray(levels, np.int32)
+
+
+# ------------------------------------------------------------------------------------------
+# Synthetic inference-request traces for the workload generator (§III-A/B, Table II
+# 17.3M requests; the parameters that matter are the numbers of input and output
+# tokens, the batch size and the token-sampling parameters, strongly correlated).
+TRACE_PARAMS = ("input_tokens", "output_tokens", "batch_size", "decoding", "temperature", "top_p", "top_k",
+                "max_new_tokens")
+TRACE_ROWS_PAPER = 17_300_000
+
+
+def make_traces(n: int, seed: int = 0, first: int = 0) -> np.ndarray:
+    """n x 8 float32 requests (rows first .. first + n - 1 of `seed`, so shards regenerate exactly):
+    lognormal input tokens; output tokens correlated with the input; batch size growing with the
+    input length; greedy (0) or sampling (1) decoding; sampling parameters only when sampling
+    (temperature on a 0.05 grid, top_p, top_k from small menus); max_new_tokens the next power of
+    two above the output length.  Integer-valued parameters are exact in float32."""
+    r = np.arange(first, first + n, dtype=np.uint64)
+    z1, z2 = normal(seed, r, 901), normal(seed, r, 902)
+    inp = np.clip(np.rint(np.exp(5.5 + 1.1 * z1)), 1, 8192)
+    out = np.clip(np.rint(np.exp(3.8 + 0.35 * np.log(inp) * 0.5 + 0.9 * (0.6 * z1 + 0.8 * z2))), 1, 4096)
+    bs = np.clip(np.floor(1 + 16 * u01(seed, r, 903) * (1 + np.log2(inp) / 13)), 1, 32)
+    samp = (u01(seed, r, 904) < 0.45).astype(np.float64)
+    temp = np.where(samp > 0, np.rint((0.1 + 1.4 * u01(seed, r, 905) ** 2) * 20) / 20, 0.0)
+    top_p = np.where(samp > 0, np.array([0.8, 0.9, 0.95, 1.0])[(u01(seed, r, 906) * 4).astype(np.int64)], 1.0)
+    top_k = np.where(samp > 0, np.array([0.0, 10.0, 50.0, 100.0])[(u01(seed, r, 907) * 4).astype(np.int64)], 0.0)
+    mnt = np.minimum(2.0 ** np.ceil(np.log2(out + 1)), 4096)
+    return np.stack([inp, out, bs, samp, temp, top_p, top_k, mnt], axis=1).astype(np.float32)
