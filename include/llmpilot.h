@@ -215,6 +215,32 @@ llmpilot_status llmpilot_cv_leave_one_llm_out(llmpilot_ctx* ctx, const llmpilot_
                                               int64_t U, const double* prof_cost, llmpilot_cv_report** out);
 void llmpilot_cv_report_free(llmpilot_cv_report* r);
 
+/* ---- Workload generator (§III-B "Workload generator").
+ * Request model: for each of the P request parameters the values are divided into 64 bins of
+ * approximately equal request counts — one bin per distinct value when the parameter has at most
+ * 64 — using the same quantile rule as llmpilot_bin (exact on <= 2^20 rows, a global
+ * strided sample beyond); each bin's centre is (min + max) / 2 of the trace values in it; the joint
+ * model is the sparse histogram of the rows' bin tuples, keyed by the mixed-radix
+ * key sum_p bin_p * prod_{q<p} nbins_q (must fit 63 bits, else LLMP_EINVAL).
+ * traces: n x P floats, row-major, host or device, finite (LLMP_EINVAL otherwise); 1 <= n < 2^31,
+ * 1 <= P <= 32.  The handle owns its device buffers (release with llmpilot_wg_free). */
+typedef struct llmpilot_wg llmpilot_wg;
+llmpilot_status llmpilot_wg_build(llmpilot_ctx* ctx, const float* traces, int64_t n, int32_t P, llmpilot_wg** out);
+/* P, trace rows, number of non-empty joint bins (any pointer may be NULL). */
+llmpilot_status llmpilot_wg_info(const llmpilot_wg* w, int32_t* P, int64_t* n_rows, int64_t* n_nonempty);
+/* Host copies: nbins [P], centres [P][64] (bin b of parameter p at p*64+b), keys [n_nonempty]
+ * ascending, counts [n_nonempty] (sum = n_rows).  Any pointer may be NULL. */
+llmpilot_status llmpilot_wg_export(const llmpilot_wg* w, int32_t* nbins, float* centres, uint64_t* keys,
+                                   int64_t* counts);
+/* Sampling: request s (s = first .. first + n_samples - 1) draws r = rng4(seed, 0x5747, s, 0)
+ * (splitmix64 chain, R21), t = floor(r * n_rows / 2^64), takes the first joint bin (key
+ * order) whose cumulative count exceeds t — i.e. a bin with probability count / n_rows — and emits
+ * each parameter's bin centre.  out: n_samples x P floats, host or device.  Samples are indexed
+ * globally, so shards (first = rank * chunk) draw disjoint, reproducible requests. */
+llmpilot_status llmpilot_wg_sample(llmpilot_ctx* ctx, const llmpilot_wg* w, int64_t n_samples, uint64_t seed,
+                                   int64_t first, float* out);
+void llmpilot_wg_free(llmpilot_wg* w);
+
 /* Test hook (parity of the histogram kernel): int64 histograms
  * Hg, Hh [32][256] (host) of the rows listed in idx (device int32, m entries; NULL = all n rows
  * in order) over codes (device n x 32) with integer gradient pairs qg, qh (device int32,

@@ -99,6 +99,10 @@ def lib():
                                           C.POINTER(C.POINTER(CvReport))],
         "llmpilot_debug_histogram": [P, P, I64, P, I64, P, P, P, P],
         "llmpilot_nccl_unique_id": [P],
+        "llmpilot_wg_build": [P, P, I64, I32, C.POINTER(P)],
+        "llmpilot_wg_info": [P, C.POINTER(I32), C.POINTER(I64), C.POINTER(I64)],
+        "llmpilot_wg_export": [P, P, P, P, P],
+        "llmpilot_wg_sample": [P, P, I64, C.c_uint64, I64, P],
     }.items():
         fn = getattr(L, name)
         fn.restype = C.c_int
@@ -106,6 +110,7 @@ def lib():
     L.llmpilot_ctx_destroy.argtypes = [P]
     L.llmpilot_cuts_free.argtypes = [P]
     L.llmpilot_model_free.argtypes = [P]
+    L.llmpilot_wg_free.argtypes = [P]
     L.llmpilot_cv_report_free.argtypes = [C.POINTER(CvReport)]
     L.llmpilot_hparams_default.argtypes = [C.POINTER(HParams)]
     _lib = L
@@ -328,6 +333,49 @@ def fit(ctx: Context, X, y, hp: HParams, users_col: int, llm_id=None, prof_id=No
     h = C.c_void_p()
     _check(lib().llmpilot_fit(ctx.handle, C.byref(ds), C.byref(hp), L1, L2, C.byref(h)))
     return Model(h)
+
+
+class WorkloadGenerator:
+    """llmpilot_wg: request model of the workload generator (§III-B)."""
+
+    def __init__(self, ctx: Context, traces):
+        n, P = int(traces.shape[0]), int(traces.shape[1])
+        pt, keep = _ptr(traces, np.float32)
+        h = C.c_void_p()
+        _check(lib().llmpilot_wg_build(ctx.handle, pt, n, P, C.byref(h)))
+        self._h = h
+        Pc, nr, m = C.c_int32(), C.c_int64(), C.c_int64()
+        _check(lib().llmpilot_wg_info(h, C.byref(Pc), C.byref(nr), C.byref(m)))
+        self.P, self.n_rows, self.n_nonempty = Pc.value, nr.value, m.value
+
+    def export(self) -> dict:
+        nb = np.zeros(self.P, np.int32)
+        ce = np.zeros((self.P, 64), np.float32)
+        keys = np.zeros(self.n_nonempty, np.uint64)
+        counts = np.zeros(self.n_nonempty, np.int64)
+        _check(lib().llmpilot_wg_export(self._h, *(a.ctypes.data_as(C.c_void_p) for a in (nb, ce, keys, counts))))
+        return dict(nbins=nb, centres=ce, keys=keys, counts=counts)
+
+    def sample(self, ctx: Context, n_samples: int, seed: int = 0, first: int = 0, out=None):
+        """out: None (returns a host numpy array) or a tensor/array of n_samples x P float32."""
+        if out is None:
+            out = np.zeros((n_samples, self.P), np.float32)
+        po, keep = _ptr(out, np.float32)
+        _check(lib().llmpilot_wg_sample(ctx.handle, self._h, n_samples, seed, first, po))
+        if keep is not None and keep is not out and isinstance(out, np.ndarray):
+            out[...] = keep
+        return out
+
+    def free(self):
+        if self._h:
+            lib().llmpilot_wg_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
 
 
 def recommend(ctx: Context, model: Model, llm_feats, prof_feats, cost, user_levels, L1: float, L2: float, U: int,

@@ -17,6 +17,9 @@ struct llmpilot_cuts {
 struct llmpilot_model {
   llmp::ModelData m;
 };
+struct llmpilot_wg {
+  llmp::WgData w;
+};
 
 namespace {
 thread_local std::string g_err;
@@ -44,7 +47,7 @@ llmpilot_status guarded(Fn&& fn) {
 
 const char* kClassNames[LLMP_N_KERNEL_CLASSES] = {
     "validate", "weights", "cuts", "codes", "base_score", "hist_root", "partition", "hist_level",
-    "split", "update", "predict", "recommend", "misc", "nccl", "unused14", "unused15"};
+    "split", "update", "predict", "recommend", "misc", "nccl", "wg", "unused15"};
 
 void set_device(llmp::Ctx* c) { LLMP_CUDA(cudaSetDevice(c->device)); }
 
@@ -357,6 +360,65 @@ llmpilot_status llmpilot_model_train_pred(const llmpilot_model* m, float* train_
 }
 
 void llmpilot_model_free(llmpilot_model* m) { delete m; }
+
+// ---- workload generator (§III-B)
+llmpilot_status llmpilot_wg_build(llmpilot_ctx* ctx, const float* traces, int64_t n, int32_t P, llmpilot_wg** out) {
+  return guarded([&] {
+    LLMP_REQUIRE(ctx && traces && out, "NULL argument");
+    LLMP_REQUIRE(n >= 1 && n < (int64_t(1) << 31) && P >= 1 && P <= llmp::kMaxF, "bad sizes (n in [1, 2^31), P in [1, 32])");
+    set_device(&ctx->c);
+    llmp::DevBuf tmp;
+    const float* Td = (const float*)llmp::to_device(&ctx->c, traces, (size_t)n * P * 4, tmp);
+    llmpilot_wg* w = new llmpilot_wg();
+    try {
+      llmp::wg_build(&ctx->c, Td, n, P, w->w);
+    } catch (...) {
+      delete w;
+      throw;
+    }
+    *out = w;
+  });
+}
+
+llmpilot_status llmpilot_wg_info(const llmpilot_wg* w, int32_t* P, int64_t* n_rows, int64_t* n_nonempty) {
+  return guarded([&] {
+    LLMP_REQUIRE(w, "NULL argument");
+    if (P) *P = w->w.P;
+    if (n_rows) *n_rows = w->w.n;
+    if (n_nonempty) *n_nonempty = w->w.m;
+  });
+}
+
+llmpilot_status llmpilot_wg_export(const llmpilot_wg* w, int32_t* nbins, float* centres, uint64_t* keys,
+                                   int64_t* counts) {
+  return guarded([&] {
+    LLMP_REQUIRE(w, "NULL argument");
+    const llmp::WgData& d = w->w;
+    if (nbins) memcpy(nbins, d.nbins.data(), (size_t)d.P * 4);
+    if (centres) memcpy(centres, d.centres.data(), (size_t)d.P * 64 * 4);
+    if (keys) memcpy(keys, d.h_keys.data(), (size_t)d.m * 8);
+    if (counts) memcpy(counts, d.h_counts.data(), (size_t)d.m * 8);
+  });
+}
+
+llmpilot_status llmpilot_wg_sample(llmpilot_ctx* ctx, const llmpilot_wg* w, int64_t n_samples, uint64_t seed,
+                                   int64_t first, float* out) {
+  return guarded([&] {
+    LLMP_REQUIRE(ctx && w && (out || n_samples == 0), "NULL argument");
+    set_device(&ctx->c);
+    const size_t bytes = (size_t)n_samples * w->w.P * 4;
+    if (llmp::is_device_ptr(out)) {
+      llmp::wg_sample(&ctx->c, w->w, n_samples, seed, first, out);
+    } else {
+      llmp::DevBuf& d = ctx->c.workspace("wg_out", std::max<size_t>(bytes, 4));
+      llmp::wg_sample(&ctx->c, w->w, n_samples, seed, first, d.as<float>());
+      LLMP_CUDA(cudaMemcpyAsync(out, d.p, bytes, cudaMemcpyDeviceToHost, ctx->c.stream));
+      LLMP_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    }
+  });
+}
+
+void llmpilot_wg_free(llmpilot_wg* w) { delete w; }
 
 llmpilot_status llmpilot_predict(llmpilot_ctx* ctx, const llmpilot_model* m, const float* X, int64_t n, float* out) {
   return guarded([&] {

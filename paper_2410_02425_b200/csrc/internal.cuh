@@ -29,6 +29,21 @@ struct ModelData {
   DevBuf d_train_pred;             // float [2][n_train] (planar) training predictions, on the device
 };
 
+// workload generator (wg.cu): per-parameter bins (64-bin quantile cuts) and centres, the sparse
+// joint histogram (ascending mixed-radix keys, cumulative counts) — PAPER.md §III-B
+struct WgData {
+  int P = 0;
+  int64_t n = 0, m = 0;               // trace rows, non-empty joint bins
+  CutsData cuts;
+  std::vector<int32_t> nbins;         // [P]
+  std::vector<float> centres;         // [P][64]
+  std::vector<uint64_t> h_keys;       // [m]
+  std::vector<int64_t> h_counts;      // [m]
+  DevBuf d_keys, d_cum, d_centres, d_nbins;
+};
+void wg_build(Ctx* ctx, const float* T, int64_t n, int P, WgData& out);
+void wg_sample(Ctx* ctx, const WgData& w, int64_t count, uint64_t seed, int64_t first, float* out);
+
 // binning.cu
 void compute_cuts(Ctx* ctx, const float* X, int64_t n, int F, int64_t row_offset, int64_t n_global, int max_bin,
                   CutsData& out);

@@ -382,3 +382,34 @@ def test_c3_full_size_first_tree_parity(lp, ctx):
     # sampled predictions: every 997th row
     idx = np.arange(0, d.n, 997)
     assert _bits_equal(oracle.predict(om, d.X[idx]), gm.predict(ctx, d.X[idx]))
+
+
+# ----------------------------------------------------------------------------- workload generator
+@pytest.mark.parametrize("n,P,seed", [(1, 1, 0), (777, 3, 1), (20011, 8, 2), (1_200_000, 8, 3)])
+def test_workload_generator_parity(lp, ctx, n, P, seed):
+    """bins, centres, the sparse joint histogram (keys, counts)
+    and the sampled requests are bit-identical to the oracle's, including a ragged trace size, a
+    single row, n > 2^20 (strided-sample quantiles) and sample offsets."""
+    T = synth.make_traces(n, seed=seed)[:, :P]
+    om = oracle.wg_build(T)
+    for src in (T, torch.from_numpy(T).cuda()):
+        g = lp.WorkloadGenerator(ctx, src)
+        e = g.export()
+        assert np.array_equal(e["nbins"], om.nbins)
+        assert _bits_equal(e["centres"], om.centres)
+        assert np.array_equal(e["keys"], om.keys) and np.array_equal(e["counts"], om.counts)
+        for s_seed, first, cnt in ((0, 0, 1000), (7, 123457, 4099)):
+            ref = oracle.wg_sample(om, cnt, seed=s_seed, first=first)
+            assert _bits_equal(g.sample(ctx, cnt, seed=s_seed, first=first), ref)
+            dev = torch.zeros((cnt, P), dtype=torch.float32, device="cuda")
+            g.sample(ctx, cnt, seed=s_seed, first=first, out=dev)
+            torch.cuda.synchronize()
+            assert _bits_equal(dev.cpu().numpy(), ref)
+        g.free()
+
+
+def test_workload_generator_errors(lp, ctx):
+    with pytest.raises(lp.LLMPilotError):
+        lp.WorkloadGenerator(ctx, np.array([[1.0, np.inf]], np.float32))
+    with pytest.raises(lp.LLMPilotError):
+        lp.WorkloadGenerator(ctx, np.tile(np.arange(64, dtype=np.float32)[:, None], (1, 11)))
