@@ -99,6 +99,7 @@ struct FitArgs {
   int monotone;
   int fused_root;     // 1: k_hist<UPDROOT> builds the next root speculatively (root_needed)
   int urow;           // 1: the histogram kernels take the users column row-parallel
+  const uint32_t* cmask;  // [n/32 batches][32 lanes] precomputed change masks (k_cmask), or null
   int nn;
   FeatBest* fbest;            // [2^(D-1)][32] per-(node, feature) best split of the current level
   unsigned long long* units;  // device counters of rows processed per kernel class (instrumentation)
@@ -603,7 +604,13 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
   __syncthreads();
   const int np = s_np;
   const int64_t S = s_vstart[np];
-  const int64_t v0 = S * blockIdx.x / gridDim.x, v1 = S * (blockIdx.x + 1) / gridDim.x;
+  // identity-order modes with precomputed change masks: CTA, chunk and warp ranges start on 32-row
+  // batch boundaries, so every staged batch is one precomputed mask batch
+  constexpr bool IDN = (MODE == HM_ROOT || MODE == HM_UPDROOT);
+  const bool pre = IDN && a.cmask != nullptr;
+  const int64_t am = pre ? ~(int64_t)31 : ~(int64_t)0;
+  const int64_t v0 = (S * blockIdx.x / gridDim.x) & am;
+  const int64_t v1 = (blockIdx.x + 1 == gridDim.x) ? S : ((S * (blockIdx.x + 1) / gridDim.x) & am);
   if (v0 >= v1) return;
   if (tid == 0 && MODE != HM_DEBUG && a.units)
     atomicAdd(&a.units[MODE == HM_ROOT ? KC_HIST_ROOT : MODE == HM_UPDROOT ? KC_UPDATE : KC_HIST], (unsigned long long)(v1 - v0));
@@ -635,13 +642,14 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
     for (int64_t c0 = s0; c0 < s1; c0 += HIST_CHUNK) {
       const int64_t c1 = min(s1, c0 + HIST_CHUNK);
       const int64_t clen = c1 - c0;
-      const int64_t w0 = c0 + clen * warp / H2_WARPS, w1 = c0 + clen * (warp + 1) / H2_WARPS;
+      const int64_t w0 = c0 + ((clen * warp / H2_WARPS) & am);
+      const int64_t w1 = (warp + 1 == H2_WARPS) ? c1 : c0 + ((clen * (warp + 1) / H2_WARPS) & am);
       uint32_t cur = 0;           // pending run of feature myf: byte offset of its (bin, f) cell
       int32_t acc_g = 0;          // its sums from earlier batches
       uint32_t acc_h = 0;
       bool fresh = true;          // no previous row yet
       uint4 nc0 = make_uint4(0, 0, 0, 0), nc1 = nc0;
-      uint32_t ngp = 0, nri = 0;
+      uint32_t ngp = 0, nri = 0, nmask = 0;
       float ny = 0.f, nw = 0.f, np_ = 0.f;
       auto load_ridx = [&](int64_t vb) {
         const int64_t vi = vb + lane;
@@ -668,6 +676,7 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
           nc0 = __ldg(crow);
           nc1 = __ldg(crow + 1);
         }
+        if (pre) nmask = __ldg(a.cmask + ((vb + poff) >> 5) * 32 + lane);   // the batch's mask word of this lane
       };
       if (w0 < w1) {
         load_ridx(w0);
@@ -689,9 +698,10 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
           gp = pack_gp(quantize(g, scale_g), quantize(h, scale_h));
           a.gp_root[ridx] = gp;
         }
+        const uint32_t bmask = nmask;       // this batch's precomputed mask word (pre)
         // previous row of lane 0: the last staged row of the previous batch (read before it is overwritten)
         uint4 pv0 = nc0, pv1 = nc1;
-        if (lane == 0 && !fresh) {
+        if (!pre && lane == 0 && !fresh) {
           pv0 = *reinterpret_cast<const uint4*>(wb + 32 * H2_ROWB);
           pv1 = *reinterpret_cast<const uint4*>(wb + 32 * H2_ROWB + 16);
         }
@@ -723,7 +733,7 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
         }
         __syncwarp();
         const uint4 cc0 = nc0, cc1 = nc1;   // this batch's row (the prefetch below overwrites nc*)
-        if (lane > 0) {
+        if (!pre && lane > 0) {
           pv0 = *reinterpret_cast<const uint4*>(myrow - H2_ROWB);
           pv1 = *reinterpret_cast<const uint4*>(myrow - H2_ROWB + 16);
         }
@@ -734,7 +744,7 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
         if (!hist_on) continue;
         // ---- row side: change mask of this lane's row (bit 8j+7-q = feature 4q+j)
         uint32_t m = 0;
-        if (valid) {
+        if (!pre && valid) {
           m = byte_ne_hi(cc0.x ^ pv0.x) | (byte_ne_hi(cc0.y ^ pv0.y) >> 1) | (byte_ne_hi(cc0.z ^ pv0.z) >> 2) |
               (byte_ne_hi(cc0.w ^ pv0.w) >> 3) | (byte_ne_hi(cc1.x ^ pv1.x) >> 4) | (byte_ne_hi(cc1.y ^ pv1.y) >> 5) |
               (byte_ne_hi(cc1.z ^ pv1.z) >> 6) | (byte_ne_hi(cc1.w ^ pv1.w) >> 7);
@@ -761,7 +771,7 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
         const int32_t tot_g = __shfl_sync(0xffffffffu, pg, 31);
         const uint32_t tot_h = __shfl_sync(0xffffffffu, ph, 31);
         // ---- feature side
-        uint32_t M = warp_transpose32(m, lane);
+        uint32_t M = pre ? (fresh ? bmask & ~1u : bmask) : warp_transpose32(m, lane);
         if (fresh) {
           if (active) cur = (uint32_t)(wb[H2_ROWB + myf] * H2_PAD + myf) * 4u;   // run starts at row 0
           fresh = false;
@@ -850,6 +860,28 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
       atomicMax(&a.maxg[t + 1], __float_as_uint(mg));
       atomicMax(&a.maxh[t + 1], __float_as_uint(mh));
     }
+  }
+}
+
+// Change masks of the identity row order, once per fit (the codes never change during a fit): word
+// L of batch B (rows 32B .. 32B+31) has bit r set iff feature h2_feat(L)'s code at row 32B+r differs
+// from the one at row 32B+r-1 (bit 0 of batch 0: 0; rows >= n: 0) — exactly the transposed mask
+// k_hist2 would build per batch, so the identity-order passes (root, fused update) load one word
+// per lane instead of recomputing it every tree (4 B per row read, ~80 instructions per batch saved)
+__global__ void __launch_bounds__(256) k_cmask(const uint8_t* codes, int64_t n, uint32_t* cmask) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nb = (n + 31) / 32;
+  for (int64_t B = ((int64_t)blockIdx.x * 256 + threadIdx.x) >> 5; B < nb; B += ((int64_t)gridDim.x * 256) >> 5) {
+    const int64_t r = B * 32 + lane;
+    uint32_t m = 0;
+    if (r < n && r > 0) {
+      const uint4* c = reinterpret_cast<const uint4*>(codes + (size_t)r * kMaxF);
+      const uint4 c0 = __ldg(c), c1 = __ldg(c + 1), p0 = __ldg(c - 2), p1 = __ldg(c - 1);
+      m = byte_ne_hi(c0.x ^ p0.x) | (byte_ne_hi(c0.y ^ p0.y) >> 1) | (byte_ne_hi(c0.z ^ p0.z) >> 2) |
+          (byte_ne_hi(c0.w ^ p0.w) >> 3) | (byte_ne_hi(c1.x ^ p1.x) >> 4) | (byte_ne_hi(c1.y ^ p1.y) >> 5) |
+          (byte_ne_hi(c1.z ^ p1.z) >> 6) | (byte_ne_hi(c1.w ^ p1.w) >> 7);
+    }
+    cmask[B * 32 + lane] = warp_transpose32(m, lane);
   }
 }
 
@@ -1952,6 +1984,14 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   static const bool use_root2 = getenv("LLMP_ROOT2") && atoi(getenv("LLMP_ROOT2")) != 0;
   static const bool fused = !use_root2 && !(getenv("LLMP_NOFUSE") && atoi(getenv("LLMP_NOFUSE")) != 0);
   static const bool urow = !(getenv("LLMP_NO_UROW") && atoi(getenv("LLMP_NO_UROW")) != 0);
+  static const bool use_cmask = !(getenv("LLMP_CMASK") && atoi(getenv("LLMP_CMASK")) == 0);
+  const uint32_t* cmask = nullptr;
+  if (use_cmask) {
+    DevBuf& d_cm = ctx->workspace("cmask", (size_t)((n + 31) / 32) * 32 * 4);
+    LLMP_LAUNCH(ctx, KC_CODES, n, k_cmask, grid_for(ctx, n, 256, 8), 256, 0, d_codes.as<uint8_t>(), n,
+                d_cm.as<uint32_t>());
+    cmask = d_cm.as<uint32_t>();
+  }
   static const int hist1 = hist1_mask();
   FitArgs A[2];
   for (int tg = 0; tg < 2; ++tg) {
@@ -1990,6 +2030,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     a.monotone = hp.monotone_users;
     a.fused_root = fused ? 1 : 0;
     a.urow = urow ? 1 : 0;
+    a.cmask = cmask;
     a.nn = nn;
     a.units = ctx->d_units;
     a.fbest = reinterpret_cast<FeatBest*>(ctx->workspace("featbest" + sx, (size_t)half_max * 32 * 48).p);
