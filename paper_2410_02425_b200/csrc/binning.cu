@@ -95,7 +95,7 @@ void compute_cuts(Ctx* ctx, const float* X, int64_t n, int F, int64_t row_offset
   // and a large cudaMalloc occasionally stalls for hundreds of ms)
   DevBuf& keys = ctx->workspace("cut_keys", (size_t)std::max<int64_t>(m, 1) * F * 4);
   DevBuf& sorted = ctx->workspace("cut_sorted", (size_t)std::max<int64_t>(m, 1) * F * 4);
-  if (ctx->nranks == 1) {
+  if (ctx->nccl == nullptr) {   // unsharded (a context with a communicator takes the sharded path, also at 1 rank)
     LLMP_REQUIRE(m_local == m, "sample size mismatch");
     if (m > 0)
       LLMP_LAUNCH(ctx, KC_CUTS, m, k_gather_sample, 1024, 256, 0, X, n, F, i0, stride, m, m, keys.as<float>());

@@ -1971,9 +1971,11 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   int* d_tree = ctx->workspace("tree_idx", sizeof(int)).as<int>();
 
   // the two ensembles are independent: every tree-loop kernel grows both (blockIdx.y = target)
-  // multi-rank: plain launches (the NCCL calls are never captured, in particular not into the body of
-  // a conditional graph node; the plain-launch loop is the one the 1-GPU timing mode exercises)
-  const bool graphs = T > 0 && !ctx->timing && ctx->use_graphs && ctx->nranks == 1;
+  // sharded (a communicator is attached): plain launches — the NCCL calls are never captured, in
+  // particular not into the body of a conditional graph node.  A 1-rank communicator runs this same
+  // sharded path (trivial collectives), which is how the GPU tests cover it on one device.
+  const bool sharded = ctx->nccl != nullptr;
+  const bool graphs = T > 0 && !ctx->timing && ctx->use_graphs && !sharded;
   size_t lvl_nodes = 0;
   for (int d = 0; d <= D; ++d) lvl_nodes += (size_t)1 << d;
   const size_t tab_bytes = lvl_nodes * (8 /*start*/ + 8 /*cnt*/ + 8 /*gcnt*/ + 8 + 8 /*lo,hi*/ + 4 + 4 /*split*/ +
@@ -2058,7 +2060,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       LevelView& L = a.lv[d];
       L.start = start + off;
       L.cnt = cnt + off;
-      L.gcnt = (ctx->nranks > 1) ? gcnt + off : cnt + off;
+      L.gcnt = sharded ? gcnt + off : cnt + off;
       L.lo = lo + off;
       L.hi = hi + off;
       L.split_f = sf + off;
@@ -2163,7 +2165,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       // persistent tile loop (upper bound of the level's tile count: one partial tile per parent)
       LLMP_LAUNCH(ctx, KC_PARTITION, ny * n, k_part, dim3(std::min(tiles_d, PT_CTAS_PER_SM / ny * ctx->sms), ny),
                   PT_THREADS, 0, fp, d);
-      if (ctx->nranks > 1) {   // every rank must histogram the same (globally smaller) child
+      if (sharded) {   // every rank must histogram the same (globally smaller) child
         for (int q = 0; q < ny; ++q) {
           LLMP_CUDA(cudaMemcpyAsync(fp.t[q].lv[d].gcnt, fp.t[q].lv[d].cnt, ((size_t)1 << d) * 8, cudaMemcpyDeviceToDevice, st));
           allreduce_sum_i64(ctx, fp.t[q].lv[d].gcnt, (size_t)1 << d);
@@ -2195,7 +2197,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   FPa.t[0] = A[0];
   FPb.t[0] = A[1];
   auto round = [&](const cudaGraphConditionalHandle* loop) {
-    const bool branches = branches_env && graphs && ctx->nranks == 1;
+    const bool branches = branches_env && graphs && !sharded;
     if (branches) {
       const cudaStream_t sa = ctx->stream, sb = ctx->capture_stream(1);
       LLMP_CUDA(cudaEventRecord(ctx->fork_event, sa));

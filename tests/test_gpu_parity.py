@@ -250,6 +250,26 @@ def test_kernel_variants(lp, env):
     assert p.returncode == 0 and "OK" in p.stdout, (env, p.stdout[-2000:], p.stderr[-2000:])
 
 
+def test_sharded_path_with_a_one_rank_nccl_communicator(lp):
+    """A context with a communicator takes the sharded fit path: NCCL all-reduces of
+    the Eq. (4) group maxima, base-score sums, gradient maxima, child counts and built-child
+    histograms, the all-gathered global cut sample, plain launches instead of graphs.  With one
+    rank every collective is trivial, so the models must be the oracle's bit for bit — this runs
+    the multi-GPU code path (and real NCCL calls) on one device."""
+    ctx1 = lp.Context(0, torch.cuda.current_stream(), lp.nccl_unique_id(), 0, 1)
+    try:
+        ctx1.reset_stats()
+        for d, w, kw in ((synth.make("C2"), None, dict(n_trees=12, max_depth=6)),
+                         (synth.make_s1(30001, seed=5), "w", dict(n_trees=4, max_depth=8, use_eq4_weights=0))):
+            om, otp, gm = _fit_both(lp, ctx1, d, w=None if w is None else d.w, **kw)
+            _assert_same_model(om, gm.export())
+            assert _bits_equal(otp, gm.train_pred(d.n))
+            gm.free()
+        assert ctx1.stats()["classes"]["nccl"]["launches"] > 0
+    finally:
+        ctx1.close()
+
+
 def test_fit_host_and_device_inputs_identical_and_deterministic(lp, ctx):
     d = synth.make("C2")
     hp = lp.hparams(n_trees=10, max_depth=6)

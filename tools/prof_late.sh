@@ -14,11 +14,10 @@ ncu --set full --clock-control none --import-source on --kernel-name regex:"k_hi
     --launch-skip $((TREE * 24)) -c 24 -o /tmp/$TAG \
     python tools/profile_fit.py --trees $TREES --repeat 1 > ${OUT}_fit.log 2>&1
 python tools/ncu_summary.py $REP $OUT "tree $TREE of a $TREES-tree C3 fit, both targets paired ($TAG)"
-for k in 1 3 5 7; do
-  ncu -i $REP --page source --csv --print-source sass --kernel-name "regex:k_hist<1>" --launch-skip $((k - 1)) \
-      --launch-count 1 > ${OUT}_sass_level$k.csv 2>/dev/null
-  python tools/ncu_stalls.py ${OUT}_sass_level$k.csv > ${OUT}_stalls_level$k.txt 2>&1
+# report-local launch indices: k_hist* = root (0), levels 1..7, fused update (8); k_part = levels 0..6
+for spec in "k_hist:1" "k_hist:3" "k_hist:5" "k_hist:7" "k_hist:8" "k_part:2" "k_part:5" "k_split3:4"; do
+  k=${spec%%:*}; i=${spec##*:}
+  ncu -i $REP --page source --csv --print-source sass --kernel-name "regex:$k" --launch-skip $i --launch-count 1 \
+      > ${OUT}_sass_${k}_$i.csv 2>/dev/null
+  python tools/ncu_stalls.py ${OUT}_sass_${k}_$i.csv > ${OUT}_stalls_${k}_$i.txt 2>&1
 done
-ncu -i $REP --page source --csv --print-source sass --kernel-name "regex:k_hist2<3>" --launch-count 1 \
-    > ${OUT}_sass_update.csv 2>/dev/null
-python tools/ncu_stalls.py ${OUT}_sass_update.csv > ${OUT}_stalls_update.txt 2>&1
