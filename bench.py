@@ -485,9 +485,9 @@ def main():
 
     # ---- workload generator: build the request model from a
     # Table II-sized synthetic trace (17.3M requests) resident in HBM, then draw requests;
-    # rank 0 only, outside the fit's timed region
+    # N = 1 only (it does not shard), outside the fit's timed region
     wg = None
-    if rank == 0 and not args.no_wg:
+    if rank == 0 and world == 1 and not args.no_wg:
         wg = bench_wg(lp, ctx, stream, dev, args)
 
     # ---- CPU baseline: the oracle as it stands, rank 0, N = 1, bounded sample

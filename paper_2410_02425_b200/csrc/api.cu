@@ -228,7 +228,7 @@ llmpilot_status llmpilot_bin(llmpilot_ctx* ctx, const float* X, int64_t n, int32
     } else {
       made = new llmpilot_cuts();
       try {
-        llmp::compute_cuts(&ctx->c, Xd, n, F, 0, n, max_bin, made->d);
+        llmp::compute_cuts(&ctx->c, Xd, n, F, 0, n, max_bin, made->d, false);   // this rank's X only
       } catch (...) {
         delete made;
         throw;

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(CUT_THREADS) k_select_cuts(const float* sorted
 }
 
 void compute_cuts(Ctx* ctx, const float* X, int64_t n, int F, int64_t row_offset, int64_t n_global, int max_bin,
-                  CutsData& out) {
+                  CutsData& out, bool sharded) {
   LLMP_REQUIRE(F >= 1 && F <= kMaxF, "n_features must be in [1, 32]");
   LLMP_REQUIRE(max_bin >= 2 && max_bin <= kBins, "max_bin must be in [2, 256]");
   LLMP_REQUIRE(n >= 1 && n_global >= n, "bad row counts");
@@ -95,7 +95,8 @@ void compute_cuts(Ctx* ctx, const float* X, int64_t n, int F, int64_t row_offset
   // and a large cudaMalloc occasionally stalls for hundreds of ms)
   DevBuf& keys = ctx->workspace("cut_keys", (size_t)std::max<int64_t>(m, 1) * F * 4);
   DevBuf& sorted = ctx->workspace("cut_sorted", (size_t)std::max<int64_t>(m, 1) * F * 4);
-  if (ctx->nccl == nullptr) {   // unsharded (a context with a communicator takes the sharded path, also at 1 rank)
+  LLMP_REQUIRE(!sharded || ctx->nccl != nullptr, "sharded cuts need a communicator");
+  if (!sharded) {
     LLMP_REQUIRE(m_local == m, "sample size mismatch");
     if (m > 0)
       LLMP_LAUNCH(ctx, KC_CUTS, m, k_gather_sample, 1024, 256, 0, X, n, F, i0, stride, m, m, keys.as<float>());

@@ -1936,7 +1936,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
 
   phase("weights");
   // ---- cuts + codes (row-major for histograms/routing, column-major for partitions)
-  compute_cuts(ctx, ds.X, n, F, ds.row_offset, ds.n_global, hp.max_bin, out.cuts);
+  compute_cuts(ctx, ds.X, n, F, ds.row_offset, ds.n_global, hp.max_bin, out.cuts, ctx->nccl != nullptr);
   DevBuf& d_codes = ctx->workspace("codes", (size_t)n * kMaxF);
   const int64_t ldT = (n + 31) / 32 * 32;
   DevBuf& d_codesT = ctx->workspace("codesT", (size_t)ldT * kMaxF);

@@ -45,8 +45,10 @@ void wg_build(Ctx* ctx, const float* T, int64_t n, int P, WgData& out);
 void wg_sample(Ctx* ctx, const WgData& w, int64_t count, uint64_t seed, int64_t first, float* out);
 
 // binning.cu
+// sharded = true: this rank holds rows [row_offset, row_offset + n) of n_global and the global sample is
+// all-gathered over the context's communicator (every rank must call); false: X is the whole data
 void compute_cuts(Ctx* ctx, const float* X, int64_t n, int F, int64_t row_offset, int64_t n_global, int max_bin,
-                  CutsData& out);
+                  CutsData& out, bool sharded);
 // codes: row-major n x 32 (may be null); codesT: column-major 32 x n (may be null).
 // flag (device int, may be null) is set to 1 when X holds a non-finite value.
 // codesT leading dimension ldT >= n (bytes between features; the fit pads it to a multiple of 32)

@@ -138,7 +138,7 @@ void wg_build(Ctx* ctx, const float* T, int64_t n, int P, WgData& out) {
   cudaStream_t s = ctx->stream;
   out.P = P;
   out.n = n;
-  compute_cuts(ctx, T, n, P, 0, n, WG_BINS, out.cuts);
+  compute_cuts(ctx, T, n, P, 0, n, WG_BINS, out.cuts, false);   // local: no collective
   LLMP_CUDA(cudaStreamSynchronize(s));
   WgKeyArgs a{};
   double space = 1.0;
