@@ -168,12 +168,15 @@ __device__ __forceinline__ void run_flush(uint32_t pa, int32_t ag, uint32_t ah) 
   asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(pa), "r"(ag) : "memory");
   asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(pa), "r"(ah), "n"(HH_OFF) : "memory");
 }
-__device__ __forceinline__ void run_step(uint32_t& pa, int32_t& ag, uint32_t& ah, uint32_t ca, uint2 gh) {
-  if (ca != pa) {
-    run_flush(pa, ag, ah);
+// The run is tracked by its code byte; the cell address sbase + code * cstride is formed only when a run
+// is flushed (the users lane reads a never-written padding byte, so its run never changes).
+__device__ __forceinline__ void run_step(uint32_t& pc, int32_t& ag, uint32_t& ah, uint32_t c, uint2 gh,
+                                         uint32_t sbase, uint32_t cstride) {
+  if (c != pc) {
+    run_flush(sbase + pc * cstride, ag, ah);
     ag = 0;
     ah = 0;
-    pa = ca;
+    pc = c;
   }
   ag += (int32_t)gh.x;
   ah += gh.y;
@@ -207,6 +210,10 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitPair fp, cons
     sug[i] = 0;
     suh[i] = 0;
   }
+  // staged-row padding bytes 40..47 are never written afterwards: zero them once (the users lane
+  // compares byte 40 of every row, which must therefore never change)
+  for (int i = tid; i < HIST_WARPS * 32; i += HIST_THREADS)
+    *reinterpret_cast<uint2*>(smem + 2 * HH_OFF + i * ROWBUF_STRIDE + 40) = make_uint2(0u, 0u);
   // fused mode: tree t (the one just grown) in shared memory for routing
   int8_t* s_feat = reinterpret_cast<int8_t*>(smem + HIST_SMEM);
   uint8_t* s_bin = smem + HIST_SMEM + (a.nn + 1);
@@ -315,7 +322,8 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitPair fp, cons
       const bool ulane = lane == ucol;
       const uint32_t sbase = ulane ? sg0 + (uint32_t)(kBins * 128) + (uint32_t)lane * 4u : sg0 + (uint32_t)lane * 4u;
       const uint32_t cstride = ulane ? 0u : 128u;
-      uint32_t pa = kNoRun;       // shared address of the current run's (bin, feature) cell
+      const int ccol = ulane ? 40 : lane;   // staged byte this lane compares (40: row padding, never written)
+      uint32_t rc = kNoRun;       // code of the current run's (bin, feature) cell
       int32_t ag = 0;             // run sums
       uint32_t ah = 0;
       // register prefetch of the first batch
@@ -409,24 +417,24 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitPair fp, cons
           asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(ua), "r"((int32_t)ghu.x) : "memory");
           asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(ua), "r"(ghu.y), "n"(kBins * 4) : "memory");
         }
-        if (pa == kNoRun) pa = sbase + (uint32_t)rowbuf[lane] * cstride;
+        if (rc == kNoRun) rc = rowbuf[ccol];
         int r = 0;
         for (; r + 4 <= cnt; r += 4) {   // the group's shared loads first, then 4 branch-free steps
           uint32_t ca[4];
           uint2 gh[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            ca[q] = sbase + (uint32_t)rowbuf[(r + q) * ROWBUF_STRIDE + lane] * cstride;
+            ca[q] = rowbuf[(r + q) * ROWBUF_STRIDE + ccol];
             gh[q] = *reinterpret_cast<const uint2*>(rowbuf + (r + q) * ROWBUF_STRIDE + 32);
           }
 #pragma unroll
-          for (int q = 0; q < 4; ++q) run_step(pa, ag, ah, ca[q], gh[q]);
+          for (int q = 0; q < 4; ++q) run_step(rc, ag, ah, ca[q], gh[q], sbase, cstride);
         }
         for (; r < cnt; ++r)
-          run_step(pa, ag, ah, sbase + (uint32_t)rowbuf[r * ROWBUF_STRIDE + lane] * cstride,
-                   *reinterpret_cast<const uint2*>(rowbuf + r * ROWBUF_STRIDE + 32));
+          run_step(rc, ag, ah, rowbuf[r * ROWBUF_STRIDE + ccol], *reinterpret_cast<const uint2*>(rowbuf + r * ROWBUF_STRIDE + 32),
+                   sbase, cstride);
       }
-      if (pa != kNoRun) run_flush(pa, ag, ah);
+      if (rc != kNoRun) run_flush(sbase + rc * cstride, ag, ah);
       __syncthreads();
       if (ucol >= 0) {   // the users column's cells (left zero by its lane) from the dense histogram
         for (int b = tid; b < kBins; b += HIST_THREADS) {
