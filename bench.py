@@ -265,6 +265,19 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------- reference
+def arm_config(args, world):
+    """The workload both arms report (BASELINE.json configs[2]/[3] shape, weak-scaled per GPU)."""
+    rows = args.llms_per_gpu * 8 * 16
+    sweep_rows = args.sweep_llms * 8 * 16
+    return {"workload": "C3 per GPU (C4 family when N > 1): %d rows/GPU = %d LLMs x 8 profiles x 16 user levels, "
+                        "32 features, 256 bins, 2 targets x %d trees, depth %d; recommend sweep %d unseen LLMs/GPU"
+                        % (rows, args.llms_per_gpu, args.trees, args.depth, args.sweep_llms),
+            "rows_global": rows * world, "rows_per_gpu": rows, "features": 32, "bins": 256, "trees": args.trees,
+            "depth": args.depth, "targets": 2, "sweep_rows_per_gpu": sweep_rows, "global_batch": rows * world,
+            "parallelism": "row-sharded dp%d, NCCL int64 histogram all-reduce" % world,
+            "l2": "inputs larger than L2 (codes %d MB + state per GPU), no flush" % (rows * 32 // 2 ** 20)}
+
+
 def run_reference(args, rank, world):
     """The reference arm for this tier is the CPU oracle, as it stands, on a bounded sample."""
     if rank != 0:
@@ -291,8 +304,7 @@ def run_reference(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * total / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8/i64",
         "data": "synthetic (seeded, synth/)",
-        "config": {"workload": "C3 scaled synthetic fit (oracle sample)", "rows": d.n, "features": 32,
-                   "bins": 256, "trees_timed": 1, "depth": args.depth, "targets": 2},
+        "config": dict(arm_config(args, world), sample=sample),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -511,15 +523,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u8/i64",
             "data": "synthetic (seeded counter-based generator, synth/; shapes of the paper's dataset)",
-            "config": {"workload": "C3 per GPU (C4 family when N > 1): %d rows/GPU = %d LLMs x 8 profiles x 16 user "
-                                   "levels, 32 features, 256 bins, 2 targets x %d trees, depth %d; recommend sweep %d "
-                                   "unseen LLMs/GPU" % (d.n, args.llms_per_gpu, args.trees, args.depth,
-                                                        args.sweep_llms),
-                       "rows_global": n_global, "rows_per_gpu": d.n, "features": 32, "bins": 256,
-                       "trees": args.trees, "depth": args.depth, "targets": 2,
-                       "sweep_rows_per_gpu": sweep_rows, "global_batch": n_global,
-                       "parallelism": "row-sharded dp%d, NCCL int64 histogram all-reduce" % world,
-                       "l2": "inputs larger than L2 (codes %d MB + state per GPU), no flush" % (d.n * 32 // 2 ** 20)},
+            "config": arm_config(args, world),
             "predict": {"value": predict_rows / (pred_ms / 1000.0), "unit": "rows/s", "rows_per_step": sweep_rows * world,
                         "ms_per_step": pred_ms / args.steps},
             "fit": {"value": row_iters / (fit_ms / 1000.0), "unit": UNIT, "ms_per_step": fit_ms / args.steps},
