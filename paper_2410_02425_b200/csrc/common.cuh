@@ -135,6 +135,8 @@ const void* to_device(Ctx* ctx, const void* p, size_t bytes, DevBuf& tmp);
 
 // multi-GPU collectives (nccl.cu); no-ops for one rank
 void allreduce_sum_i64(Ctx* ctx, int64_t* buf, size_t count);
+void nccl_group_start(Ctx* ctx);
+void nccl_group_end(Ctx* ctx);
 void allreduce_max_u32(Ctx* ctx, uint32_t* buf, size_t count);
 void allreduce_max_u64(Ctx* ctx, uint64_t* buf, size_t count);
 void allgather_bytes(Ctx* ctx, const void* send, void* recv, size_t bytes_per_rank);

@@ -54,7 +54,7 @@ __device__ __forceinline__ double exp2i(int e) {  // exact 2^e for e in [-1022, 
 struct LevelView {
   int64_t* start;    // [2^d] segment start in the row-index buffer (a child lies inside its parent's range)
   int64_t* cnt;      // [2^d] local rows
-  int64_t* gcnt;     // [2^d] global rows (== cnt for one rank)
+  int64_t* gcnt;     // [2^d] (unused: kept for the table layout)
   double* lo;        // [2^d] monotone bounds
   double* hi;
   int32_t* split_f;  // [2^d] -1 = leaf / absent
@@ -99,6 +99,7 @@ struct FitArgs {
   int monotone;
   int fused_root;     // 1: k_hist<UPDROOT> builds the next root speculatively (root_needed)
   int urow;           // 1: the histogram kernels take the users column row-parallel
+  int built_by_h;     // 1 (sharded): the split kernel picks the built child by hessian sum
   const uint32_t* cmask;  // [n/32 batches][32 lanes] precomputed change masks (k_cmask), or null
   int nn;
   FeatBest* fbest;            // [2^(D-1)][32] per-(node, feature) best split of the current level
@@ -239,8 +240,8 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitPair fp, cons
     if (tid < NP) {
       sp = P.split_f[tid] >= 0;
       if (sp) {
-        const int64_t nL = C.gcnt[2 * tid], nR = C.gcnt[2 * tid + 1];
-        side = (nL <= nR) ? 0 : 1;       // build the smaller child (global row count), ties -> left
+        const int64_t nL = C.cnt[2 * tid], nR = C.cnt[2 * tid + 1];
+        side = a.built_by_h ? C.built[tid] : (nL <= nR) ? 0 : 1;   // the smaller child (rows; hessian when sharded)
         len = C.cnt[2 * tid + side];
         // k_part: left child at the parent's start, right child after it
         const int64_t ps = (d == 1) ? 0 : P.start[tid], cl = C.cnt[2 * tid];
@@ -573,8 +574,8 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
     int64_t len = 0, pst = 0;
     int side = 0;
     if (tid < NP && P.split_f[tid] >= 0) {
-      const int64_t nL = C.gcnt[2 * tid], nR = C.gcnt[2 * tid + 1];
-      side = (nL <= nR) ? 0 : 1;       // build the smaller child (global row count), ties -> left
+      const int64_t nL = C.cnt[2 * tid], nR = C.cnt[2 * tid + 1];
+      side = a.built_by_h ? C.built[tid] : (nL <= nR) ? 0 : 1;   // the smaller child (rows; hessian when sharded)
       len = C.cnt[2 * tid + side];
       // k_part: left child at the parent's start, right child after it
       const int64_t ps = (d == 1) ? 0 : P.start[tid], cl = C.cnt[2 * tid];
@@ -1585,6 +1586,10 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitPair fp, con
     tgain[gk] = ml;   // the split's loss reduction (MDI)
     if (d + 1 < a.D) {
       const LevelView& N = a.lv[d + 1];
+      // sharded fits build the child with the smaller hessian sum (an exact global integer, so every
+      // rank makes the same choice without exchanging child counts); unsharded ones the smaller
+      // row count (decided by the level histogram kernel) — either way sibling = parent - built
+      if (a.built_by_h) N.built[k] = (HLs <= HqN - HLs) ? 0 : 1;
       N.cnt[2 * k] = 0;   // k_part's child cursors
       N.cnt[2 * k + 1] = 0;
       N.lo[2 * k] = loL;
@@ -2040,6 +2045,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     a.monotone = hp.monotone_users;
     a.fused_root = fused ? 1 : 0;
     a.urow = urow ? 1 : 0;
+    a.built_by_h = sharded ? 1 : 0;
     a.cmask = cmask;
     a.nn = nn;
     a.units = ctx->d_units;
@@ -2068,7 +2074,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       LevelView& L = a.lv[d];
       L.start = start + off;
       L.cnt = cnt + off;
-      L.gcnt = sharded ? gcnt + off : cnt + off;
+      L.gcnt = gcnt + off;
       L.lo = lo + off;
       L.hi = hi + off;
       L.split_f = sf + off;
@@ -2166,22 +2172,20 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     if (use_root2) LLMP_LAUNCH(ctx, KC_HIST_ROOT, ny * n, k_hist_root2, hg, R2_THREADS, R2_SMEM, fp);
     else if (hist1 & 1) LLMP_LAUNCH(ctx, KC_HIST_ROOT, ny * n, k_hist<HM_ROOT>, hg, HIST_THREADS, HIST_SMEM, fp, 0, 0, nodbg);
     else LLMP_LAUNCH(ctx, KC_HIST_ROOT, ny * n, k_hist2<HM_ROOT>, hg, H2_THREADS, H2_SMEM, fp, 0, 0, nodbg);
+    nccl_group_start(ctx);
     for (int q = 0; q < ny; ++q) allreduce_sum_i64(ctx, fp.t[q].H[0], SLOT);
+    nccl_group_end(ctx);
     split(fp, ny, 0);
     for (int d = 1; d < D; ++d) {
       const int tiles_d = (int)((n + PT_TILE - 1) / PT_TILE) + (1 << (d - 1));
       // persistent tile loop (upper bound of the level's tile count: one partial tile per parent)
       LLMP_LAUNCH(ctx, KC_PARTITION, ny * n, k_part, dim3(std::min(tiles_d, PT_CTAS_PER_SM / ny * ctx->sms), ny),
                   PT_THREADS, 0, fp, d);
-      if (sharded) {   // every rank must histogram the same (globally smaller) child
-        for (int q = 0; q < ny; ++q) {
-          LLMP_CUDA(cudaMemcpyAsync(fp.t[q].lv[d].gcnt, fp.t[q].lv[d].cnt, ((size_t)1 << d) * 8, cudaMemcpyDeviceToDevice, st));
-          allreduce_sum_i64(ctx, fp.t[q].lv[d].gcnt, (size_t)1 << d);
-        }
-      }
       if (hist1 & 2) LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hg, HIST_THREADS, HIST_SMEM, fp, d, 0, nodbg);
       else LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist2<HM_LEVEL>, hg, H2_THREADS, H2_SMEM, fp, d, 0, nodbg);
+      nccl_group_start(ctx);   // both targets' built-child histograms in one NCCL launch
       for (int q = 0; q < ny; ++q) allreduce_sum_i64(ctx, fp.t[q].H[d & 1], (size_t)SLOT << (d - 1));
+      nccl_group_end(ctx);
       split(fp, ny, d);
     }
     if (fused) {   // update tree t + root histogram of tree t+1 (into the now free root slot)

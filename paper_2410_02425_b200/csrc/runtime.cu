@@ -115,6 +115,8 @@ struct NcclApi {
   ncclResult_t (*allReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*allGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
 };
 NcclApi g_nccl;
 void load_nccl() {
@@ -128,7 +130,10 @@ void load_nccl() {
   g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(h, "ncclAllReduce");
   g_nccl.allGather = (decltype(g_nccl.allGather))dlsym(h, "ncclAllGather");
   g_nccl.getErrorString = (decltype(g_nccl.getErrorString))dlsym(h, "ncclGetErrorString");
-  if (!g_nccl.commInitRank || !g_nccl.allReduce || !g_nccl.allGather || !g_nccl.commDestroy)
+  g_nccl.groupStart = (decltype(g_nccl.groupStart))dlsym(h, "ncclGroupStart");
+  g_nccl.groupEnd = (decltype(g_nccl.groupEnd))dlsym(h, "ncclGroupEnd");
+  if (!g_nccl.commInitRank || !g_nccl.allReduce || !g_nccl.allGather || !g_nccl.commDestroy || !g_nccl.groupStart ||
+      !g_nccl.groupEnd)
     fail(LLMP_ENCCL, "libnccl.so.2 lacks the needed symbols");
   g_nccl.loaded = true;
 }
@@ -158,6 +163,14 @@ void nccl_destroy(Ctx* ctx) {
   ctx->nccl = nullptr;
 }
 static void coll_before(Ctx* ctx, cudaEvent_t* ev) { ctx->before(KC_NCCL, ev); }
+// several collectives issued between these become one NCCL launch (no-ops without a communicator,
+// and while per-launch event timing is on, so every collective keeps its own events)
+void nccl_group_start(Ctx* ctx) {
+  if (ctx->nccl && !ctx->timing) nccl_check(g_nccl.groupStart(), "ncclGroupStart");
+}
+void nccl_group_end(Ctx* ctx) {
+  if (ctx->nccl && !ctx->timing) nccl_check(g_nccl.groupEnd(), "ncclGroupEnd");
+}
 void allreduce_sum_i64(Ctx* ctx, int64_t* buf, size_t count) {
   if (!ctx->nccl || count == 0) return;
   cudaEvent_t ev = nullptr;
