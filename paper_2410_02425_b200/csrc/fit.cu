@@ -1251,9 +1251,11 @@ __global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitPa
   const uint32_t* const rin_all = a.sr[(d - 1) & 1];
   uint32_t* const rout = a.sr[d & 1];
   // row indices of tile t (the parent's segment in the input buffer; identity at d = 1)
-  auto load_rows = [&](int t, uint32_t (&r)[PT_ITEMS]) {
+  // the parent of each tile is found once (when its row indices are loaded) and carried along
+  auto load_rows = [&](int t, uint32_t (&r)[PT_ITEMS], int& jt) {
     if (t >= ntiles) return;
     const int j = parent_of_tile(s_tile_pref, NP, t);
+    jt = j;
     const int64_t cnt_j = s_pp[j].cnt;
     const int64_t o = (int64_t)(t - s_tile_pref[j]) * PT_TILE;
     const int len = (int)min((int64_t)PT_TILE, cnt_j - o);
@@ -1265,11 +1267,12 @@ __global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitPa
     }
   };
   uint32_t ridx[PT_ITEMS], nridx[PT_ITEMS];
-  load_rows(blockIdx.x, ridx);
+  int jcur = 0, jnext = 0;
+  load_rows(blockIdx.x, ridx, jcur);
   int par = 0;
   for (int t = blockIdx.x; t < ntiles; t += gridDim.x, par ^= 1) {
     uint32_t* const bits = s_bits[par];
-    const int j = parent_of_tile(s_tile_pref, NP, t);
+    const int j = jcur;
     const PartParent pp = s_pp[j];
     const int64_t cnt_j = pp.cnt;
     const int64_t start_j = pp.start;
@@ -1286,7 +1289,7 @@ __global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitPa
       const unsigned mw = __ballot_sync(0xffffffffu, k < len && code[q] <= (uint32_t)b);
       if (lane == 0) bits[q * (PT_THREADS / 32) + warp] = mw;
     }
-    load_rows(t + gridDim.x, nridx);   // in flight across the reservation below
+    load_rows(t + gridDim.x, nridx, jnext);   // in flight across the reservation below
     __syncthreads();
     if (warp == 0) {   // group prefixes: lane L takes words PT_WPL*L ..; one atomic per child
       int c[PT_WPL];
@@ -1329,6 +1332,7 @@ __global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitPa
     }
 #pragma unroll
     for (int q = 0; q < PT_ITEMS; ++q) ridx[q] = nridx[q];
+    jcur = jnext;
     // (no barrier: s_bits is double-buffered; the next writes of s_pre / s_lb follow the next
     // tile's first barrier)
   }
