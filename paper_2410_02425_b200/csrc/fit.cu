@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
   // identity-order modes with precomputed change masks: CTA, chunk and warp ranges start on 32-row
   // batch boundaries, so every staged batch is one precomputed mask batch
   constexpr bool IDN = (MODE == HM_ROOT || MODE == HM_UPDROOT);
-  const bool pre = IDN && a.cmask != nullptr;
+  constexpr bool pre = IDN;   // identity order always uses the fit's precomputed masks (k_cmask)
   const int64_t am = pre ? ~(int64_t)31 : ~(int64_t)0;
   const int64_t v0 = (S * blockIdx.x / gridDim.x) & am;
   const int64_t v1 = (blockIdx.x + 1 == gridDim.x) ? S : ((S * (blockIdx.x + 1) / gridDim.x) & am);
@@ -2003,14 +2003,10 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   static const bool use_root2 = getenv("LLMP_ROOT2") && atoi(getenv("LLMP_ROOT2")) != 0;
   static const bool fused = !use_root2 && !(getenv("LLMP_NOFUSE") && atoi(getenv("LLMP_NOFUSE")) != 0);
   static const bool urow = !(getenv("LLMP_NO_UROW") && atoi(getenv("LLMP_NO_UROW")) != 0);
-  static const bool use_cmask = !(getenv("LLMP_CMASK") && atoi(getenv("LLMP_CMASK")) == 0);
-  const uint32_t* cmask = nullptr;
-  if (use_cmask) {
-    DevBuf& d_cm = ctx->workspace("cmask", (size_t)((n + 31) / 32) * 32 * 4);
-    LLMP_LAUNCH(ctx, KC_CODES, n, k_cmask, grid_for(ctx, n, 256, 8), 256, 0, d_codes.as<uint8_t>(), n,
-                d_cm.as<uint32_t>());
-    cmask = d_cm.as<uint32_t>();
-  }
+  DevBuf& d_cm = ctx->workspace("cmask", (size_t)((n + 31) / 32) * 32 * 4);
+  LLMP_LAUNCH(ctx, KC_CODES, n, k_cmask, grid_for(ctx, n, 256, 8), 256, 0, d_codes.as<uint8_t>(), n,
+              d_cm.as<uint32_t>());
+  const uint32_t* cmask = d_cm.as<uint32_t>();
   static const int hist1 = hist1_mask();
   FitArgs A[2];
   for (int tg = 0; tg < 2; ++tg) {
