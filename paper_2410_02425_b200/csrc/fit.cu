@@ -521,7 +521,7 @@ __device__ __forceinline__ void red2(uint32_t addr, int32_t g, uint32_t h) {
   asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(addr), "r"(h), "n"(H2_HH) : "memory");
 }
 
-template <int MODE>
+template <int MODE, int DC = 0>   // DC: compile-time tree depth of the fused update's routing (0 = a.D)
 __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const int d, const int t_in, const DbgArgs dbg) {
   const FitArgs& a = fp.t[blockIdx.y];
   const int t = (MODE == HM_ROOT || MODE == HM_UPDROOT) ? *a.d_tree : t_in;   // graph replays: tree index from the device
@@ -724,7 +724,10 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
           // both children's node words are loaded together with the row's code byte, so each level
           // costs one shared-memory round trip (a leaf keeps k; its child indices stay < nn)
           int k = 0;
-          for (int s2 = 0; s2 < a.D; ++s2) k = 2 * k + 1 + (myrow[s_rf[k]] > s_rb[k] ? 1 : 0);
+          const int D = DC ? DC : a.D;
+#pragma unroll
+          for (int s2 = 0; s2 < (DC ? DC : kMaxDepth); ++s2)
+            if (DC || s2 < D) k = 2 * k + 1 + (myrow[s_rf[k]] > s_rb[k] ? 1 : 0);
           const float pn = __fadd_rn(np_, s_lv[k - n_int]);   // one fp32 rounding, tree order
           a.p[ridx] = pn;
           if (has_next) {
@@ -892,6 +895,14 @@ __global__ void __launch_bounds__(256) k_cmask(const uint8_t* codes, int64_t n, 
     }
     cmask[B * 32 + lane] = warp_transpose32(m, lane);
   }
+}
+
+// the fused update kernel for a depth: compile-time routing depth for the configs' depths (6, 8)
+using Hist2Kernel = void (*)(const FitPair, const int, const int, const DbgArgs);
+static Hist2Kernel updroot2_kernel(int D) {
+  if (D == 8) return k_hist2<HM_UPDROOT, 8>;
+  if (D == 6) return k_hist2<HM_UPDROOT, 6>;
+  return k_hist2<HM_UPDROOT, 0>;
 }
 
 // histogram inner loop per mode: change-mask k_hist2 or run-length k_hist.  LLMP_HIST2 is a bit mask
@@ -2101,8 +2112,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   // the fused update kernels' dynamic shared memory depends on the depth (the tree they route)
   LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_UPDROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  HIST_SMEM + updroot_tree_smem(D)));
-  LLMP_CUDA(cudaFuncSetAttribute(k_hist2<HM_UPDROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 H2_SMEM + updroot_tree_smem(D)));
+  const Hist2Kernel k_upd2 = updroot2_kernel(D);
+  LLMP_CUDA(cudaFuncSetAttribute(k_upd2, cudaFuncAttributeMaxDynamicSharedMemorySize, H2_SMEM + updroot_tree_smem(D)));
   const DbgArgs nodbg{};
 
   phase("state");
@@ -2194,8 +2205,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
         LLMP_LAUNCH(ctx, KC_UPDATE, ny * n, k_hist<HM_UPDROOT>, hg, HIST_THREADS, HIST_SMEM + updroot_tree_smem(D), fp,
                     0, 0, nodbg);
       else
-        LLMP_LAUNCH(ctx, KC_UPDATE, ny * n, k_hist2<HM_UPDROOT>, hg, H2_THREADS, H2_SMEM + updroot_tree_smem(D), fp, 0,
-                    0, nodbg);
+        LLMP_LAUNCH(ctx, KC_UPDATE, ny * n, k_upd2, hg, H2_THREADS, H2_SMEM + updroot_tree_smem(D), fp, 0, 0, nodbg);
     } else {
       LLMP_LAUNCH(ctx, KC_UPDATE, ny * n, k_update, dim3(std::max(1, upd_grid * ny / 2), ny), UPD_THREADS, 0, fp);
     }
