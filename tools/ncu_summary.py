@@ -25,8 +25,13 @@ CLASS = {"k_hist<0>": "hist_root", "k_hist<1>": "hist_level", "k_hist<3>": "upda
          "k_part": "partition", "k_hist2<0>": "hist_root", "k_hist2<1>": "hist_level", "k_hist2<3>": "update"}
 
 
+HIST_MODE = {"0": "hist_root", "1": "hist_level", "3": "update"}
+
+
 def kclass(name):
     base = name.split("(")[0].replace("void ", "").replace("llmp::", "").strip()
+    if base.startswith("k_hist<") or base.startswith("k_hist2<"):   # first template argument = the mode
+        return HIST_MODE.get(base.split("<")[1].split(",")[0].split(">")[0].strip(), base), base
     return CLASS.get(base, base), base
 
 
@@ -65,6 +70,13 @@ def main(rep, prefix, sass=()):
         w = csv.DictWriter(f, fieldnames=["kernel", "class"] + METRICS)
         w.writeheader()
         w.writerows(recs)
+    summarise(recs, prefix, os.path.basename(rep), sys.argv[3] if len(sys.argv) > 3 else "one tree of both ensembles")
+    if sass:
+        dump_sass(rep, prefix, recs, sass)
+
+
+def summarise(recs, prefix, rep_name, what):
+    """per-class totals -> PREFIX_ncu_summary.txt and ncu_traffic.json next to it"""
     agg = {}
     for r in recs:
         a = agg.setdefault(r["class"], {"launches": 0, "us": 0.0, "dram": 0.0, "inst": 0.0})
@@ -73,7 +85,7 @@ def main(rep, prefix, sass=()):
         a["dram"] += ((r["dram__bytes_read.sum"] or 0) + (r["dram__bytes_write.sum"] or 0)) * 1e6  # Mbyte -> B
         a["inst"] += r["smsp__inst_executed.sum"] or 0.0
     lines = ["ncu --set full --clock-control none, %s (C3: 10M rows, depth 8); cold cache, serialised launches"
-             % (sys.argv[3] if len(sys.argv) > 3 else "one tree of both ensembles"), ""]
+             % what, ""]
     traffic = {}
     for c, a in sorted(agg.items(), key=lambda x: -x[1]["us"]):
         per = a["dram"] / a["launches"]
@@ -82,15 +94,31 @@ def main(rep, prefix, sass=()):
                         a["dram"] / (a["us"] * 1e-6) / 1e12, a["inst"] / 1e6))
         traffic[c] = {"dram_bytes_per_launch": per, "avg_duration_us": a["us"] / a["launches"],
                       "launches_profiled": a["launches"],
-                      "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch from %s" % os.path.basename(rep)}
+                      "note": "dram__bytes_read.sum + dram__bytes_write.sum per launch from %s" % rep_name}
     with open(prefix + "_ncu_summary.txt", "w") as f:
         f.write("\n".join(lines) + "\n")
     with open(os.path.join(os.path.dirname(prefix), "ncu_traffic.json"), "w") as f:
         json.dump(traffic, f, indent=1)
     print("\n".join(lines))
-    if sass:
-        dump_sass(rep, prefix, recs, sass)
+
+
+def from_csv(csv_path, prefix, what):
+    """re-classify an existing PREFIX_ncu_launches.csv (e.g. after the class table changed)"""
+    recs = []
+    for r in csv.DictReader(open(csv_path)):
+        cls, base = kclass(r["kernel"])
+        rec = {"kernel": base, "class": cls}
+        for m in METRICS:
+            try:
+                rec[m] = float(r[m])
+            except (TypeError, ValueError):
+                rec[m] = None
+        recs.append(rec)
+    summarise(recs, prefix, os.path.basename(csv_path).replace("_ncu_launches.csv", ".ncu-rep"), what)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], sys.argv[4].split(",") if len(sys.argv) > 4 else ())
+    if sys.argv[1] == "--from-csv":
+        from_csv(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else "re-summarised launches")
+    else:
+        main(sys.argv[1], sys.argv[2], sys.argv[4].split(",") if len(sys.argv) > 4 else ())
