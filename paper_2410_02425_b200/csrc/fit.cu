@@ -42,7 +42,8 @@ constexpr int MAX_PIECES = 512;            // built children per level (2^(kMaxD
 // a dummy cell row (the users lane's run target, see k_hist)
 constexpr int HH_OFF = (kBins + 1) * kMaxF * 4;   // byte offset of the q_h half (32,896)
 constexpr int U_OFF = 2 * HH_OFF + HIST_WARPS * 32 * ROWBUF_STRIDE;     // users column: [256] q_g, [256] q_h
-constexpr int HIST_SMEM = U_OFF + 2 * kBins * 4;                             // 64.3 KB + 24 KB + 2 KB
+constexpr int GS_OFF = U_OFF + 2 * kBins * 4;                                // per warp: 8 four-row group sums (uint2)
+constexpr int HIST_SMEM = GS_OFF + HIST_WARPS * 8 * 8;                       // 64.3 KB + 24 KB + 2 KB + 1 KB
 
 constexpr int SLOT = 2 * kHistBins;        // int64 per histogram slot (g then h)
 
@@ -99,6 +100,7 @@ struct FitArgs {
   int monotone;
   int fused_root;     // 1: k_hist<UPDROOT> builds the next root speculatively (root_needed)
   int urow;           // 1: the histogram kernels take the users column row-parallel
+  int hist_swar;      // 1: k_hist's four-row fast path (group sums when no run changes)
   int built_by_h;     // 1 (sharded): the split kernel picks the built child by hessian sum
   const uint32_t* cmask;  // [n/32 batches][32 lanes] precomputed change masks (k_cmask), or null
   int nn;
@@ -195,6 +197,7 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitPair fp, cons
   uint32_t* sh = reinterpret_cast<uint32_t*>(smem + HH_OFF);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   uint8_t* rowbuf = smem + 2 * HH_OFF + warp * 32 * ROWBUF_STRIDE;
+  uint2* gsum = reinterpret_cast<uint2*>(smem + GS_OFF) + warp * 8;
 
   __shared__ int64_t s_vstart[MAX_PIECES + 1];
   __shared__ int64_t s_pstart[MAX_PIECES];
@@ -405,6 +408,15 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitPair fp, cons
           }
         }
         *reinterpret_cast<uint2*>(rowbuf + lane * ROWBUF_STRIDE + 32) = make_uint2((uint32_t)gp_g(gp), (uint32_t)gp_h(gp));
+        if (a.hist_swar) {   // (q_g, q_h) sums of the batch's four-row groups (lane = row)
+          int32_t gx = lane < cnt ? gp_g(gp) : 0;
+          uint32_t hx = lane < cnt ? (uint32_t)gp_h(gp) : 0u;
+          gx += __shfl_xor_sync(0xffffffffu, gx, 1);
+          hx += __shfl_xor_sync(0xffffffffu, hx, 1);
+          gx += __shfl_xor_sync(0xffffffffu, gx, 2);
+          hx += __shfl_xor_sync(0xffffffffu, hx, 2);
+          if ((lane & 3) == 0) gsum[lane >> 2] = make_uint2((uint32_t)gx, hx);
+        }
         __syncwarp();
         if (base + 32 < w1) {   // prefetch the next batch (and the row indices of the one after)
           load_batch(base + 32);
@@ -422,12 +434,20 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitPair fp, cons
         int r = 0;
         for (; r + 4 <= cnt; r += 4) {   // the group's shared loads first, then 4 branch-free steps
           uint32_t ca[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) ca[q] = rowbuf[(r + q) * ROWBUF_STRIDE + ccol];
+          // four-row fast path: when no lane's run changes inside the group (most groups of the
+          // child lists), every lane adds the group's precomputed sums in one step
+          if (a.hist_swar &&
+              __all_sync(0xffffffffu, (ca[0] == rc) & (ca[1] == rc) & (ca[2] == rc) & (ca[3] == rc))) {
+            const uint2 gs = gsum[r >> 2];
+            ag += (int32_t)gs.x;
+            ah += gs.y;
+            continue;
+          }
           uint2 gh[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            ca[q] = rowbuf[(r + q) * ROWBUF_STRIDE + ccol];
-            gh[q] = *reinterpret_cast<const uint2*>(rowbuf + (r + q) * ROWBUF_STRIDE + 32);
-          }
+          for (int q = 0; q < 4; ++q) gh[q] = *reinterpret_cast<const uint2*>(rowbuf + (r + q) * ROWBUF_STRIDE + 32);
 #pragma unroll
           for (int q = 0; q < 4; ++q) run_step(rc, ag, ah, ca[q], gh[q], sbase, cstride);
         }
@@ -2014,6 +2034,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   static const bool use_root2 = getenv("LLMP_ROOT2") && atoi(getenv("LLMP_ROOT2")) != 0;
   static const bool fused = !use_root2 && !(getenv("LLMP_NOFUSE") && atoi(getenv("LLMP_NOFUSE")) != 0);
   static const bool urow = !(getenv("LLMP_NO_UROW") && atoi(getenv("LLMP_NO_UROW")) != 0);
+  static const bool hist_swar = !(getenv("LLMP_HIST_SWAR") && atoi(getenv("LLMP_HIST_SWAR")) == 0);
   DevBuf& d_cm = ctx->workspace("cmask", (size_t)((n + 31) / 32) * 32 * 4);
   LLMP_LAUNCH(ctx, KC_CODES, n, k_cmask, grid_for(ctx, n, 256, 8), 256, 0, d_codes.as<uint8_t>(), n,
               d_cm.as<uint32_t>());
@@ -2056,6 +2077,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     a.monotone = hp.monotone_users;
     a.fused_root = fused ? 1 : 0;
     a.urow = urow ? 1 : 0;
+    a.hist_swar = hist_swar ? 1 : 0;
     a.built_by_h = sharded ? 1 : 0;
     a.cmask = cmask;
     a.nn = nn;
