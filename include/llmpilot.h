@@ -61,6 +61,14 @@ typedef struct llmpilot_model llmpilot_model;
 llmpilot_status llmpilot_ctx_create(int device, void* cuda_stream, const void* nccl_unique_id, int rank, int nranks,
                                     llmpilot_ctx** out);
 void llmpilot_ctx_destroy(llmpilot_ctx* ctx);
+/* Test / emulation communicator: nranks contexts on ONE device in one process (NCCL refuses two
+ * ranks on one GPU), each with its own library-created stream.  Collectives go through device
+ * memory with host barriers, so every rank must be driven by its own host thread, and all ranks
+ * must issue the same sequence of calls (like NCCL).  Models are bit-identical to a one-context
+ * fit of the whole data.  out: nranks handles, destroyed individually with llmpilot_ctx_destroy.
+ * Errors: LLMP_EINVAL for nranks outside [1, 64]; LLMP_ECUDA if a context cannot be created. */
+llmpilot_status llmpilot_ctx_create_local_group(int device, int nranks, llmpilot_ctx** out);
+
 /* Write a fresh 128-byte ncclUniqueId into out (rank 0 calls it, then broadcasts the bytes to
  * the other ranks, e.g. over a torch.distributed process group).  LLMP_ENCCL if NCCL is absent. */
 llmpilot_status llmpilot_nccl_unique_id(void* out);

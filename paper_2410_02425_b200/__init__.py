@@ -99,6 +99,7 @@ def lib():
                                           C.POINTER(C.POINTER(CvReport))],
         "llmpilot_debug_histogram": [P, P, I64, P, I64, P, P, P, P],
         "llmpilot_nccl_unique_id": [P],
+        "llmpilot_ctx_create_local_group": [C.c_int, C.c_int, P],
         "llmpilot_wg_build": [P, P, I64, I32, C.POINTER(P)],
         "llmpilot_wg_info": [P, C.POINTER(I32), C.POINTER(I64), C.POINTER(I64)],
         "llmpilot_wg_export": [P, P, P, P, P],
@@ -124,6 +125,14 @@ def _check(st):
 
 def version() -> str:
     return lib().llmpilot_version().decode()
+
+
+def local_group(device: int, nranks: int) -> list:
+    """llmpilot_ctx_create_local_group: nranks Contexts on one device sharing an in-process
+    communicator (drive each from its own thread, same call sequence on every rank)."""
+    hs = (C.c_void_p * nranks)()
+    _check(lib().llmpilot_ctx_create_local_group(device, nranks, hs))
+    return [Context._wrap(C.c_void_p(hs[r]), device, r, nranks) for r in range(nranks)]
 
 
 def nccl_unique_id() -> bytes:
@@ -177,6 +186,12 @@ class Context:
             uid = C.create_string_buffer(bytes(nccl_unique_id), 128)
         _check(lib().llmpilot_ctx_create(device, _stream_handle(stream), uid, rank, nranks, C.byref(self._h)))
         self.device, self.rank, self.nranks = device, rank, nranks
+
+    @classmethod
+    def _wrap(cls, h, device, rank, nranks):
+        c = cls.__new__(cls)
+        c._h, c.device, c.rank, c.nranks = h, device, rank, nranks
+        return c
 
     @property
     def handle(self):

@@ -124,6 +124,34 @@ llmpilot_status llmpilot_ctx_create(int device, void* cuda_stream, const void* n
   });
 }
 
+llmpilot_status llmpilot_ctx_create_local_group(int device, int nranks, llmpilot_ctx** out) {
+  return guarded([&] {
+    LLMP_REQUIRE(out != nullptr, "out is NULL");
+    LLMP_REQUIRE(nranks >= 1 && nranks <= 64, "nranks must be in [1, 64]");
+    for (int r = 0; r < nranks; ++r) out[r] = nullptr;
+    llmp::LocalGroup* g = llmp::local_group_create(nranks);
+    int made = 0;
+    try {
+      for (int r = 0; r < nranks; ++r) {
+        llmpilot_ctx* c = nullptr;
+        const llmpilot_status st = llmpilot_ctx_create(device, nullptr, nullptr, 0, 1, &c);
+        if (st != LLMP_OK) llmp::fail(st, g_err);
+        c->c.rank = r;
+        c->c.nranks = nranks;
+        c->c.lgroup = g;
+        LLMP_CUDA(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
+        c->c.own_stream = true;
+        out[r] = c;
+        ++made;
+      }
+    } catch (...) {
+      for (int r = 0; r < made; ++r) llmpilot_ctx_destroy(out[r]);   // each release drops one reference
+      for (int r = made; r < nranks; ++r) llmp::local_group_release(g);
+      throw;
+    }
+  });
+}
+
 llmpilot_status llmpilot_nccl_unique_id(void* out) {
   return guarded([&] {
     LLMP_REQUIRE(out != nullptr, "out is NULL");
@@ -139,6 +167,8 @@ void llmpilot_ctx_destroy(llmpilot_ctx* ctx) {
   }
   for (auto e : ctx->c.free_events) cudaEventDestroy(e);
   llmp::nccl_destroy(&ctx->c);
+  llmp::local_group_release(ctx->c.lgroup);
+  if (ctx->c.own_stream && ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
   if (ctx->c.d_units) cudaFree(ctx->c.d_units);
   for (auto st : ctx->c.cap_stream)
     if (st) cudaStreamDestroy(st);

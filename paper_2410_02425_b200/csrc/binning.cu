@@ -95,7 +95,7 @@ void compute_cuts(Ctx* ctx, const float* X, int64_t n, int F, int64_t row_offset
   // and a large cudaMalloc occasionally stalls for hundreds of ms)
   DevBuf& keys = ctx->workspace("cut_keys", (size_t)std::max<int64_t>(m, 1) * F * 4);
   DevBuf& sorted = ctx->workspace("cut_sorted", (size_t)std::max<int64_t>(m, 1) * F * 4);
-  LLMP_REQUIRE(!sharded || ctx->nccl != nullptr, "sharded cuts need a communicator");
+  LLMP_REQUIRE(!sharded || ctx->sharded(), "sharded cuts need a communicator");
   if (!sharded) {
     LLMP_REQUIRE(m_local == m, "sample size mismatch");
     if (m > 0)

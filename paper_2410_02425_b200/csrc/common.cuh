@@ -75,11 +75,15 @@ struct DevBuf {
 // context
 struct EventPair { cudaEvent_t a, b; int cls; };
 
+struct LocalGroup;   // runtime.cu: N ranks on one device in one process (test/emulation communicator)
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   int rank = 0, nranks = 1;
   void* nccl = nullptr;   // ncclComm_t (dlopen'ed NCCL), null for one GPU
+  LocalGroup* lgroup = nullptr;   // set instead of nccl by llmpilot_ctx_create_local_group
+  bool own_stream = false;        // the stream was created by the library (local groups)
+  bool sharded() const { return nccl != nullptr || lgroup != nullptr; }
   int sms = 148;
   unsigned long long* d_units = nullptr;  // [LLMP_N_KERNEL_CLASSES] device-side unit counters
   bool timing = false;
@@ -140,6 +144,8 @@ void nccl_group_end(Ctx* ctx);
 void allreduce_max_u32(Ctx* ctx, uint32_t* buf, size_t count);
 void allreduce_max_u64(Ctx* ctx, uint64_t* buf, size_t count);
 void allgather_bytes(Ctx* ctx, const void* send, void* recv, size_t bytes_per_rank);
+LocalGroup* local_group_create(int nranks);
+void local_group_release(LocalGroup* g);   // the last rank's release deletes it
 void nccl_init(Ctx* ctx, const void* unique_id);
 void nccl_unique_id(void* out);
 void nccl_destroy(Ctx* ctx);

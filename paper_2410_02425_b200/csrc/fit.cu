@@ -1984,7 +1984,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
 
   phase("weights");
   // ---- cuts + codes (row-major for histograms/routing, column-major for partitions)
-  compute_cuts(ctx, ds.X, n, F, ds.row_offset, ds.n_global, hp.max_bin, out.cuts, ctx->nccl != nullptr);
+  compute_cuts(ctx, ds.X, n, F, ds.row_offset, ds.n_global, hp.max_bin, out.cuts, ctx->sharded());
   DevBuf& d_codes = ctx->workspace("codes", (size_t)n * kMaxF);
   const int64_t ldT = (n + 31) / 32 * 32;
   DevBuf& d_codesT = ctx->workspace("codesT", (size_t)ldT * kMaxF);
@@ -2022,7 +2022,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   // sharded (a communicator is attached): plain launches — the NCCL calls are never captured, in
   // particular not into the body of a conditional graph node.  A 1-rank communicator runs this same
   // sharded path (trivial collectives), which is how the GPU tests cover it on one device.
-  const bool sharded = ctx->nccl != nullptr;
+  const bool sharded = ctx->sharded();
   const bool graphs = T > 0 && !ctx->timing && ctx->use_graphs && !sharded;
   size_t lvl_nodes = 0;
   for (int d = 0; d <= D; ++d) lvl_nodes += (size_t)1 << d;

@@ -3,7 +3,11 @@
 #include <dlfcn.h>
 #include <string.h>
 
+#include <algorithm>
+#include <condition_variable>
+#include <mutex>
 #include <stdexcept>
+#include <vector>
 
 #include "common.cuh"
 
@@ -163,6 +167,87 @@ void nccl_destroy(Ctx* ctx) {
   ctx->nccl = nullptr;
 }
 static void coll_before(Ctx* ctx, cudaEvent_t* ev) { ctx->before(KC_NCCL, ev); }
+
+// ---------------------------------------------------------------------------------------------
+// Local group: N ranks (contexts) on ONE device in one process, each driven by its own host thread.
+// NCCL refuses two ranks on one GPU, so this is how the multi-rank fit path (shard geometry, the
+// all-gathered cut sample, hessian-chosen built children, summed partial histograms) is exercised
+// on one B200.  A collective: every rank synchronises its stream and publishes its buffer; rank 0
+// reduces the others' buffers into its own on the device; the rest copy the result back; host
+// barriers separate the phases.  Slow by design (host round trips), exact like NCCL's integer sums.
+struct LocalGroup {
+  int n = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0, refs = 0;
+  uint64_t gen = 0;
+  std::vector<const void*> ptr;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const uint64_t g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+LocalGroup* local_group_create(int nranks) {
+  auto* g = new LocalGroup();
+  g->n = nranks;
+  g->refs = nranks;
+  g->ptr.assign(nranks, nullptr);
+  return g;
+}
+void local_group_release(LocalGroup* g) {
+  if (!g) return;
+  bool last;
+  {
+    std::lock_guard<std::mutex> lk(g->m);
+    last = --g->refs == 0;
+  }
+  if (last) delete g;
+}
+enum { LG_SUM_I64 = 0, LG_MAX_U32 = 1, LG_MAX_U64 = 2 };
+__global__ void k_lg_reduce(void* dst, const void* src, size_t n, int op) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    if (op == LG_SUM_I64) static_cast<int64_t*>(dst)[i] += static_cast<const int64_t*>(src)[i];
+    else if (op == LG_MAX_U32)
+      static_cast<uint32_t*>(dst)[i] = max(static_cast<uint32_t*>(dst)[i], static_cast<const uint32_t*>(src)[i]);
+    else static_cast<uint64_t*>(dst)[i] = max(static_cast<uint64_t*>(dst)[i], static_cast<const uint64_t*>(src)[i]);
+  }
+}
+static void lg_allreduce(Ctx* ctx, void* buf, size_t count, size_t esize, int op) {
+  LocalGroup* g = ctx->lgroup;
+  LLMP_CUDA(cudaStreamSynchronize(ctx->stream));
+  g->ptr[ctx->rank] = buf;
+  g->barrier();
+  if (ctx->rank == 0) {
+    for (int r = 1; r < g->n; ++r)
+      k_lg_reduce<<<(int)std::min<size_t>((count + 255) / 256, 1024), 256, 0, ctx->stream>>>(buf, g->ptr[r], count, op);
+    LLMP_CUDA(cudaGetLastError());
+    LLMP_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  g->barrier();
+  if (ctx->rank != 0) {
+    LLMP_CUDA(cudaMemcpyAsync(buf, g->ptr[0], count * esize, cudaMemcpyDeviceToDevice, ctx->stream));
+    LLMP_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  g->barrier();   // rank 0's buffer stays untouched until every rank has its copy
+}
+static void lg_allgather(Ctx* ctx, const void* send, void* recv, size_t bytes) {
+  LocalGroup* g = ctx->lgroup;
+  LLMP_CUDA(cudaStreamSynchronize(ctx->stream));
+  g->ptr[ctx->rank] = send;
+  g->barrier();
+  for (int r = 0; r < g->n; ++r)
+    LLMP_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(recv) + (size_t)r * bytes, g->ptr[r], bytes,
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+  LLMP_CUDA(cudaStreamSynchronize(ctx->stream));
+  g->barrier();
+}
 // several collectives issued between these become one NCCL launch (no-ops without a communicator,
 // and while per-launch event timing is on, so every collective keeps its own events)
 void nccl_group_start(Ctx* ctx) {
@@ -172,27 +257,34 @@ void nccl_group_end(Ctx* ctx) {
   if (ctx->nccl && !ctx->timing) nccl_check(g_nccl.groupEnd(), "ncclGroupEnd");
 }
 void allreduce_sum_i64(Ctx* ctx, int64_t* buf, size_t count) {
-  if (!ctx->nccl || count == 0) return;
+  if (count == 0) return;
+  if (ctx->lgroup) return lg_allreduce(ctx, buf, count, 8, LG_SUM_I64);
+  if (!ctx->nccl) return;
   cudaEvent_t ev = nullptr;
   coll_before(ctx, &ev);
   nccl_check(g_nccl.allReduce(buf, buf, count, ncclInt64, ncclSum, (ncclComm_t)ctx->nccl, ctx->stream), "ncclAllReduce");
   ctx->after(KC_NCCL, ev, (double)count * 8);
 }
 void allreduce_max_u32(Ctx* ctx, uint32_t* buf, size_t count) {
-  if (!ctx->nccl || count == 0) return;
+  if (count == 0) return;
+  if (ctx->lgroup) return lg_allreduce(ctx, buf, count, 4, LG_MAX_U32);
+  if (!ctx->nccl) return;
   cudaEvent_t ev = nullptr;
   coll_before(ctx, &ev);
   nccl_check(g_nccl.allReduce(buf, buf, count, ncclUint32, ncclMax, (ncclComm_t)ctx->nccl, ctx->stream), "ncclAllReduce");
   ctx->after(KC_NCCL, ev, (double)count * 4);
 }
 void allreduce_max_u64(Ctx* ctx, uint64_t* buf, size_t count) {
-  if (!ctx->nccl || count == 0) return;
+  if (count == 0) return;
+  if (ctx->lgroup) return lg_allreduce(ctx, buf, count, 8, LG_MAX_U64);
+  if (!ctx->nccl) return;
   cudaEvent_t ev = nullptr;
   coll_before(ctx, &ev);
   nccl_check(g_nccl.allReduce(buf, buf, count, ncclUint64, ncclMax, (ncclComm_t)ctx->nccl, ctx->stream), "ncclAllReduce");
   ctx->after(KC_NCCL, ev, (double)count * 8);
 }
 void allgather_bytes(Ctx* ctx, const void* send, void* recv, size_t bytes_per_rank) {
+  if (ctx->lgroup) return lg_allgather(ctx, send, recv, bytes_per_rank);
   if (!ctx->nccl) {
     if (send != recv) LLMP_CUDA(cudaMemcpyAsync(recv, send, bytes_per_rank, cudaMemcpyDeviceToDevice, ctx->stream));
     return;

@@ -270,6 +270,44 @@ def test_sharded_path_with_a_one_rank_nccl_communicator(lp):
         ctx1.close()
 
 
+@pytest.mark.parametrize("nranks,n_llm", [(2, 200), (3, 131)])
+def test_multi_rank_sharded_fit_on_one_device(lp, nranks, n_llm):
+    """The N > 1 fit path on one B200: nranks contexts of an in-process communicator
+    (llmpilot_ctx_create_local_group; NCCL refuses two ranks on one device), each fitting its
+    contiguous LLM-block shard from its own thread — all-gathered global cut sample, all-reduced
+    group maxima / base sums / gradient maxima / partial histograms, built children chosen by the
+    split's hessian sums.  Every rank's model equals the oracle's unsharded fit bit for bit
+    (uneven shards with 3 ranks; n_global > 2^20 is covered by the strided-sample gloo test)."""
+    import threading
+    full = synth.make_scaled(n_llm)
+    kw = dict(n_trees=8, max_depth=6, subsample=0.8, colsample_bytree=0.8, seed=5)
+    om = oracle.fit(full.X, full.y, _o_hp(**kw), full.users_col, full.llm_id, full.prof_id, full.n_llm, full.n_prof,
+                    L1, L2)
+    ctxs = lp.local_group(0, nranks)
+    res, errs = [None] * nranks, []
+
+    def run(r):
+        try:
+            sh = synth.make_scaled(n_llm, r, nranks)
+            m = lp.fit(ctxs[r], sh.X, sh.y, _g_hp(lp, **kw), sh.users_col, sh.llm_id, sh.prof_id, sh.n_llm, sh.n_prof,
+                       L1, L2, row_offset=sh.row_offset, n_global=sh.n_global)
+            res[r] = m.export()
+            m.free()
+        except Exception as e:   # noqa: BLE001
+            errs.append((r, e))
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    for c in ctxs:
+        c.close()
+    assert not errs, errs
+    for r in range(nranks):
+        _assert_same_model(om, res[r], "rank %d of %d" % (r, nranks))
+
+
 def test_fit_host_and_device_inputs_identical_and_deterministic(lp, ctx):
     d = synth.make("C2")
     hp = lp.hparams(n_trees=10, max_depth=6)
