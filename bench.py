@@ -71,6 +71,7 @@ def parse():
     ap.add_argument("--sweep-llms", type=int, default=SWEEP_LLMS_PER_GPU)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-wg", action="store_true", help="skip the workload-generator leg")
+    ap.add_argument("--no-cv", action="store_true", help="skip the paper-shaped C2 cross-validation leg")
     ap.add_argument("--wg-rows", type=int, default=17_300_000, help="trace rows of the workload-generator leg")
     ap.add_argument("--wg-samples", type=int, default=4_000_000, help="requests drawn per sampling step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -125,6 +126,38 @@ def bench_wg(lp, ctx, stream, dev, args):
         res["cpu_baseline"] = {"kind": "oracle", "cores": 1, "build": {"value": n_o / (t1 - t0), "unit": "rows/s"},
                                "sample": {"value": 1000 / (t2 - t1), "unit": "requests/s"},
                                "sample_note": "build on the first %d trace rows, 1000 requests (linear CDF walk)" % n_o}
+    return res
+
+
+def bench_cv_c2(lp, ctx, args):
+    """BASELINE.json configs[1]: C2 (30 LLMs x 10 profiles x 16 user levels, memory-masked), 1000
+    trees depth 6, full nested leave-one-LLM-out CV (grid of one) + cheapest-feasible recommendation
+    per held-out LLM; wall time of one llmpilot_cv_leave_one_llm_out call (it synchronises) after a
+    warm-up call.  The oracle is timed on one fold's fit for context (rank 0, 1 core)."""
+    import synth
+    d = synth.make("C2")
+    grid = [lp.hparams(n_trees=1000, max_depth=6)]
+    lp.cv(ctx, d.X, d.y, d.llm_id, d.prof_id, d.users_col, d.n_llm, d.n_prof, grid, L1, L2, U, d.cost)
+    t0 = time.perf_counter()
+    folds, S, O, SO = lp.cv(ctx, d.X, d.y, d.llm_id, d.prof_id, d.users_col, d.n_llm, d.n_prof, grid, L1, L2, U,
+                            d.cost)
+    dt = time.perf_counter() - t0
+    fit_rows = sum(int((d.llm_id != f["llm"]).sum()) for f in folds)   # each fold refits on the other LLMs' rows
+    res = {"workload": "C2 paper-shaped: %d rows (%d LLMs x %d profiles x 16 user levels, memory-masked), 2 targets "
+                       "x 1000 trees, depth 6, %d-fold leave-one-LLM-out CV + recommendation" % (d.n, d.n_llm, d.n_prof,
+                                                                                              len(folds)),
+           "seconds": dt, "folds": len(folds), "fits_per_s": len(folds) / dt,
+           "row_iters_per_s": 2.0 * 1000 * fit_rows / dt, "S": S, "O": O, "SO": SO}
+    if not args.no_cpu_baseline:
+        import oracle
+        keep = d.llm_id != folds[0]["llm"]
+        t0 = time.perf_counter()
+        oracle.fit(d.X[keep], d.y[keep], oracle.hparams(n_trees=1000, max_depth=6), d.users_col, d.llm_id[keep],
+                   d.prof_id[keep], d.n_llm, d.n_prof, L1, L2)
+        t1 = time.perf_counter()
+        res["cpu_baseline"] = {"kind": "oracle", "cores": 1, "seconds_one_fold_fit": t1 - t0,
+                               "row_iters_per_s": 2.0 * 1000 * int(keep.sum()) / (t1 - t0),
+                               "sample": "the oracle's fit of the first fold (1000 trees x 2 targets)"}
     return res
 
 
@@ -501,6 +534,10 @@ def main():
     wg = None
     if rank == 0 and world == 1 and not args.no_wg:
         wg = bench_wg(lp, ctx, stream, dev, args)
+    # ---- the paper-shaped config (BASELINE.json configs[1]): full leave-one-LLM-out CV of C2
+    cv_c2 = None
+    if rank == 0 and world == 1 and not args.no_cv:
+        cv_c2 = bench_cv_c2(lp, ctx, args)
 
     # ---- CPU baseline: the oracle as it stands, rank 0, N = 1, bounded sample
     cpu = None
@@ -539,6 +576,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "workload_generator": wg,
+            "cv_c2": cv_c2,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

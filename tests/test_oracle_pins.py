@@ -338,6 +338,27 @@ def test_mdi_importance_invariants_c1():
     assert np.array_equal(oracle.importance(m0), np.zeros((2, d.X.shape[1])))
 
 
+def test_boosting_loop_matches_sklearn_hist_gbrt():
+    """O3-O9 boosting loop (base score, squared-error gradients, eta, lambda, leaf values, p += v)
+    against an independent library: with exact binning (few distinct values), unit weights and no
+    monotone constraint, scikit-learn's HistGradientBoostingRegressor (same depth, learning rate,
+    l2 regularisation, min hessian 1) gives the same training predictions up to the oracle's
+    gradient quantisation (K = 14: ~2^-14 of max|g| per tree)."""
+    from sklearn.ensemble import HistGradientBoostingRegressor
+    rng = np.random.default_rng(0)
+    n = 2000
+    a = rng.integers(0, 10, n).astype(np.float32)
+    u = rng.choice([1, 2, 4, 8, 16, 32, 64, 128], n).astype(np.float32)
+    y = (a + 1) * u * 0.5 + 3
+    X = np.stack([a, u], 1).astype(np.float32)
+    for T in (1, 3, 10):
+        _, tp = oracle.fit(X, np.stack([y, y], 1), oracle.hparams(n_trees=T, max_depth=4, use_eq4_weights=0,
+                                                                  monotone_users=0), 1, return_train_pred=True)
+        sk = HistGradientBoostingRegressor(max_iter=T, max_depth=4, learning_rate=0.3, l2_regularization=1.0,
+                                           min_samples_leaf=1, early_stopping=False).fit(X, y)
+        assert np.abs(tp[:, 0] - sk.predict(X)).max() < 1e-4 * y.max(), T
+
+
 def _leaf_ids(model, X):
     feat, thr = model.feat[0, 0], model.thr[0, 0]
     out = []
