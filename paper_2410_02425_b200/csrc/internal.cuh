@@ -24,7 +24,7 @@ struct ModelData {
   std::vector<float> thr, val;
   std::vector<double> gain;        // [2][T][nn] split losses (0 at leaves / unused slots)
   CutsData cuts;
-  DevBuf d_nodes;                  // uint2 [2][T][nn]: x = thr or leaf value bits, y = feat (int)
+  DevBuf d_nodes;                  // [2][T] fixed-depth routing tables on bin codes (predict.cu)
   DevBuf d_base;                   // float [2]
   DevBuf d_train_pred;             // float [2][n_train] (planar) training predictions, on the device
 };

@@ -1,11 +1,15 @@
 // predict.cu — batched ensemble predictor and the cheapest-feasible argmin, Eq. (1)-(3)
 // (P:L166-183).
 //
-// Predictor: trees are streamed through shared memory in chunks (node = {thr | leaf value, feat},
-// 8 B) while each thread keeps R rows' features in shared memory; a row's prediction is
-// base + sum of leaf values in tree order (one fp32 rounding per tree, identical to training).
-// Recommendation rows [llm feats | profile feats | u] are assembled on the fly from the two small
-// feature tables, never materialised in HBM.
+// Predictor on bin codes: routing a row by `x_f < cuts_f[b]` is identical to `code_f(x) <= b`
+// (O2/O10, R15), so rows are binned once with the model's cuts (32 code bytes per row)
+// and the trees are walked on codes.  A CTA stages 1024 rows' codes in shared memory (36-byte
+// stride: conflict-free) and streams the trees through shared memory in 32 KB chunks of compact
+// fixed-depth routing tables (u16 node word f | b << 8, padded leaf subtrees route left on b = 255;
+// then the 2^D leaf values at the leftmost-descendant slots), 4 rows per thread.  A row's prediction
+// is base + the leaf values in tree order (one fp32 rounding per tree, identical to training).
+// Recommendation rows [llm feats | profile feats | u] are assembled from the three small code tables
+// of the LLM features, the profile features and the user levels, never materialised in HBM.
 #include <math.h>
 
 #include <algorithm>
@@ -14,125 +18,132 @@
 
 namespace llmp {
 
-constexpr int PRED_THREADS = 256;
-constexpr int PRED_R = 2;                          // rows per thread
-constexpr int PRED_ROWS = PRED_THREADS * PRED_R;   // rows per CTA pass
-constexpr int XS_STRIDE = kMaxF + 1;               // floats per staged row
-constexpr int TREE_SMEM = 32768;                   // bytes of tree nodes per chunk
-constexpr int PRED_SMEM = PRED_ROWS * XS_STRIDE * 4 + TREE_SMEM;
+constexpr int PC_THREADS = 256;
+constexpr int PC_R = 4;                            // rows per thread (independent tree walks)
+constexpr int PC_ROWS = PC_THREADS * PC_R;         // rows per CTA pass
+constexpr int PC_RSTRIDE = 36;                     // bytes per staged row (9 words: distinct banks per lane)
+constexpr int PC_TREE_SMEM = 32768;                // bytes of routing tables per chunk
+constexpr int PC_SMEM = PC_ROWS * PC_RSTRIDE + PC_TREE_SMEM;
+
+__host__ __device__ inline int rtab_inner_bytes(int D) { return ((((1 << D) - 1) * 2) + 3) / 4 * 4; }
+__host__ __device__ inline int rtab_bytes(int D) { return rtab_inner_bytes(D) + (4 << D); }
 
 struct PredArgs {
-  const uint2* nodes;  // [2][T][nn]
-  int T, D, nn, F;
+  const uint8_t* rtab;  // [2][T] routing tables of rtab_bytes(D) each
+  int T, D;
   float base0, base1;
   int64_t n;
-  // plain rows
-  const float* X;
-  // assembled rows (recommendation)
-  const float* llm_feats;
-  const float* prof_feats;
-  const int32_t* levels;
-  int F_llm, F_prof, n_prof, n_levels;
+  const uint8_t* codes;        // plain rows: n x 32 codes
+  const uint8_t* llm_codes;    // assembled rows: n_llm x F_llm, n_prof x F_prof, n_levels codes
+  const uint8_t* prof_codes;
+  const uint8_t* level_codes;
+  int F_llm, F_prof, n_prof, n_levels, users_col;
   float* out;  // n x 2
 };
 
 template <bool ASSEMBLE>
-__global__ void __launch_bounds__(PRED_THREADS, 2) k_predict(const PredArgs a) {
+__global__ void __launch_bounds__(PC_THREADS) k_predict(const PredArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  float* xs = reinterpret_cast<float*>(smem);
-  uint2* tn = reinterpret_cast<uint2*>(smem + PRED_ROWS * XS_STRIDE * 4);
+  uint8_t* rows = smem;
+  uint8_t* tabs = smem + PC_ROWS * PC_RSTRIDE;
   const int tid = threadIdx.x;
-  const int trees_per_chunk = max(1, TREE_SMEM / (a.nn * 8));
-  for (int64_t r0 = (int64_t)blockIdx.x * PRED_ROWS; r0 < a.n; r0 += (int64_t)gridDim.x * PRED_ROWS) {
-    // stage rows (coalesced over the row block)
-    const int rows = (int)min((int64_t)PRED_ROWS, a.n - r0);
-    for (int e = tid; e < rows * a.F; e += PRED_THREADS) {
-      const int r = e / a.F, f = e % a.F;
-      const int64_t row = r0 + r;
-      float x;
-      if (!ASSEMBLE) {
-        x = a.X[row * a.F + f];
-      } else {
-        const int64_t per_llm = (int64_t)a.n_prof * a.n_levels;
+  const int tb = rtab_bytes(a.D), tin = rtab_inner_bytes(a.D);
+  const int n_int = (1 << a.D) - 1;
+  const int trees_per_chunk = max(1, PC_TREE_SMEM / tb);
+  for (int64_t r0 = (int64_t)blockIdx.x * PC_ROWS; r0 < a.n; r0 += (int64_t)gridDim.x * PC_ROWS) {
+    const int nr = (int)min((int64_t)PC_ROWS, a.n - r0);
+    __syncthreads();   // previous pass done with the staged rows
+    if (!ASSEMBLE) {   // 8 words per row, coalesced
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(a.codes + r0 * kMaxF);
+      for (int e = tid; e < nr * 8; e += PC_THREADS)
+        *reinterpret_cast<uint32_t*>(rows + (e >> 3) * PC_RSTRIDE + (e & 7) * 4) = __ldg(src + e);
+    } else {
+      const int64_t per_llm = (int64_t)a.n_prof * a.n_levels;
+      for (int e = tid; e < nr * kMaxF; e += PC_THREADS) {
+        const int r = e >> 5, f = e & 31;
+        const int64_t row = r0 + r;
         const int64_t i = row / per_llm;
         const int g = (int)((row / a.n_levels) % a.n_prof);
         const int lv = (int)(row % a.n_levels);
-        if (f < a.F_llm) x = a.llm_feats[i * a.F_llm + f];
-        else if (f < a.F_llm + a.F_prof) x = a.prof_feats[(int64_t)g * a.F_prof + (f - a.F_llm)];
-        else x = (float)a.levels[lv];
+        uint8_t c = 0;
+        if (f < a.F_llm) c = a.llm_codes[i * a.F_llm + f];
+        else if (f < a.F_llm + a.F_prof) c = a.prof_codes[(int64_t)g * a.F_prof + (f - a.F_llm)];
+        else if (f == a.users_col) c = a.level_codes[lv];
+        rows[r * PC_RSTRIDE + f] = c;
       }
-      xs[r * XS_STRIDE + f] = x;
     }
     for (int target = 0; target < 2; ++target) {
-      float p[PRED_R];
+      float p[PC_R];
 #pragma unroll
-      for (int q = 0; q < PRED_R; ++q) p[q] = target == 0 ? a.base0 : a.base1;
-      const uint2* tt = a.nodes + (size_t)target * a.T * a.nn;
+      for (int q = 0; q < PC_R; ++q) p[q] = target == 0 ? a.base0 : a.base1;
+      const uint8_t* tt = a.rtab + (size_t)target * a.T * tb;
       for (int c0 = 0; c0 < a.T; c0 += trees_per_chunk) {
         const int nt = min(trees_per_chunk, a.T - c0);
         __syncthreads();
-        const uint2* src = tt + (size_t)c0 * a.nn;   // 8-byte aligned (T * nn may be odd)
-        for (int e = tid; e < nt * a.nn; e += PRED_THREADS) tn[e] = __ldg(src + e);
+        const uint4* src = reinterpret_cast<const uint4*>(tt + (size_t)c0 * tb);   // tb is a multiple of 16 for D >= 2
+        if ((tb & 15) == 0) {
+          for (int e = tid; e < nt * tb / 16; e += PC_THREADS) reinterpret_cast<uint4*>(tabs)[e] = __ldg(src + e);
+        } else {
+          const uint32_t* s4 = reinterpret_cast<const uint32_t*>(tt + (size_t)c0 * tb);
+          for (int e = tid; e < nt * tb / 4; e += PC_THREADS) reinterpret_cast<uint32_t*>(tabs)[e] = __ldg(s4 + e);
+        }
         __syncthreads();
         for (int k = 0; k < nt; ++k) {
-          const uint2* tree = tn + k * a.nn;
+          const uint16_t* inode = reinterpret_cast<const uint16_t*>(tabs + k * tb);
+          const float* lval = reinterpret_cast<const float*>(tabs + k * tb + tin);
+          int node[PC_R];
 #pragma unroll
-          for (int q = 0; q < PRED_R; ++q) {
-            const float* x = xs + (tid + q * PRED_THREADS) * XS_STRIDE;
-            int node = 0;
-            for (int s = 0; s < a.D; ++s) {   // fixed depth (see upload_model_nodes)
-              const uint2 nd = tree[node];
-              node = 2 * node + 1 + (x[nd.y] < __uint_as_float(nd.x) ? 0 : 1);  // x < thr goes left
+          for (int q = 0; q < PC_R; ++q) node[q] = 0;
+          for (int s = 0; s < a.D; ++s) {   // fixed depth; the PC_R walks are independent
+#pragma unroll
+            for (int q = 0; q < PC_R; ++q) {
+              const uint32_t w = inode[node[q]];
+              const uint32_t c = rows[(tid + q * PC_THREADS) * PC_RSTRIDE + (w & 0xffu)];
+              node[q] = 2 * node[q] + 1 + (c > (w >> 8) ? 1 : 0);   // code <= b  <=>  x < cuts_f[b]: left
             }
-            p[q] = __fadd_rn(p[q], __uint_as_float(tree[node].x));
           }
+#pragma unroll
+          for (int q = 0; q < PC_R; ++q) p[q] = __fadd_rn(p[q], lval[node[q] - n_int]);
         }
       }
 #pragma unroll
-      for (int q = 0; q < PRED_R; ++q) {
-        const int r = tid + q * PRED_THREADS;
-        if (r < rows) a.out[(r0 + r) * 2 + target] = p[q];
+      for (int q = 0; q < PC_R; ++q) {
+        const int r = tid + q * PC_THREADS;
+        if (r < nr) a.out[(r0 + r) * 2 + target] = p[q];
       }
     }
-    __syncthreads();
   }
 }
 
-// Device node table: every tree as a fixed-depth complete tree, so the predictor descends exactly D
-// levels with no leaf test.  Slots above depth D: a split {thr, f}, or — for a leaf and everything
-// below it — {+inf, 0}: x < +inf always holds (X is finite), so the row keeps going left.  A leaf k at
-// depth d < D is therefore reached at its leftmost depth-D descendant (k+1)·2^(D-d) - 1, which holds
-// k's value; a depth-D leaf holds its own.  Same leaf, same value, same fp32 add as the plain walk.
+// Device routing tables (see the header comment): per tree the 2^D - 1 node words of the slots above
+// depth D — a split {f, b}, or {0, 255} ("always left") for a leaf and everything below it — then
+// the 2^D leaf values: a leaf k at depth d < D is reached at its leftmost depth-D descendant
+// (k+1)·2^(D-d) - 1.  Same leaf, same value, same fp32 add as walking the tree on raw x.
 void upload_model_nodes(Ctx* ctx, ModelData& m) {
-  const size_t tot = (size_t)2 * m.T * m.nn;
-  const int n_int = (m.nn - 1) / 2;
-  std::vector<uint2> h(std::max<size_t>(tot, 1));
-  const float inf = INFINITY;
-  uint32_t inf_bits;
-  memcpy(&inf_bits, &inf, 4);
-  for (size_t tr = 0; tr * m.nn < tot; ++tr) {
+  const int D = m.D, n_int = (1 << D) - 1;
+  const size_t tb = (size_t)rtab_bytes(D), tin = (size_t)rtab_inner_bytes(D);
+  const size_t ntrees = (size_t)2 * m.T;
+  std::vector<uint8_t> h(std::max<size_t>(ntrees * tb, 16), 0);
+  for (size_t tr = 0; tr < ntrees; ++tr) {
+    uint16_t* inode = reinterpret_cast<uint16_t*>(h.data() + tr * tb);
+    float* lval = reinterpret_cast<float*>(h.data() + tr * tb + tin);
     const size_t o = tr * m.nn;
-    for (int k = 0; k < m.nn; ++k) h[o + k] = make_uint2(k < n_int ? inf_bits : 0u, k < n_int ? 0u : 0xffffffffu);
+    for (int k = 0; k < n_int; ++k) inode[k] = (uint16_t)(255u << 8);
     for (int k = 0; k < m.nn; ++k) {
       const int f = m.feat[o + k];
       if (f >= 0) {
-        uint32_t bits;
-        memcpy(&bits, &m.thr[o + k], 4);
-        h[o + k] = make_uint2(bits, (uint32_t)f);
+        inode[k] = (uint16_t)((uint32_t)f | ((uint32_t)(m.bin[o + k] & 0xff) << 8));
       } else if (f == -1) {
         int dl = 0;
         while (((2 << dl) - 1) <= k) ++dl;   // depth of slot k
-        const int leaf = ((k + 1) << (m.D - dl)) - 1;
-        uint32_t bits;
-        memcpy(&bits, &m.val[o + k], 4);
-        h[o + leaf] = make_uint2(bits, 0xffffffffu);
+        lval[((k + 1) << (D - dl)) - 1 - n_int] = m.val[o + k];
       }
     }
   }
   m.d_nodes.set_stream(ctx->stream);
   m.d_base.set_stream(ctx->stream);
-  m.d_nodes.ensure(h.size() * 8);
-  LLMP_CUDA(cudaMemcpyAsync(m.d_nodes.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, ctx->stream));
+  m.d_nodes.ensure(h.size());
+  LLMP_CUDA(cudaMemcpyAsync(m.d_nodes.p, h.data(), h.size(), cudaMemcpyHostToDevice, ctx->stream));
   m.d_base.ensure(8);
   LLMP_CUDA(cudaMemcpyAsync(m.d_base.p, m.base, 8, cudaMemcpyHostToDevice, ctx->stream));
   LLMP_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -141,28 +152,56 @@ void upload_model_nodes(Ctx* ctx, ModelData& m) {
 static void launch_predict(Ctx* ctx, const PredArgs& a, bool assemble, int cls) {
   static bool attr = false;
   if (!attr) {
-    LLMP_CUDA(cudaFuncSetAttribute(k_predict<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, PRED_SMEM));
-    LLMP_CUDA(cudaFuncSetAttribute(k_predict<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, PRED_SMEM));
+    LLMP_CUDA(cudaFuncSetAttribute(k_predict<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, PC_SMEM));
+    LLMP_CUDA(cudaFuncSetAttribute(k_predict<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, PC_SMEM));
     attr = true;
   }
-  int64_t blocks = (a.n + PRED_ROWS - 1) / PRED_ROWS;
-  int grid = (int)std::min<int64_t>(std::max<int64_t>(blocks, 1), (int64_t)ctx->sms * 2);
-  if (assemble) LLMP_LAUNCH(ctx, cls, a.n, k_predict<true>, grid, PRED_THREADS, PRED_SMEM, a);
-  else LLMP_LAUNCH(ctx, cls, a.n, k_predict<false>, grid, PRED_THREADS, PRED_SMEM, a);
+  int64_t blocks = (a.n + PC_ROWS - 1) / PC_ROWS;
+  int grid = (int)std::min<int64_t>(std::max<int64_t>(blocks, 1), (int64_t)ctx->sms * 3);
+  if (assemble) LLMP_LAUNCH(ctx, cls, a.n, k_predict<true>, grid, PC_THREADS, PC_SMEM, a);
+  else LLMP_LAUNCH(ctx, cls, a.n, k_predict<false>, grid, PC_THREADS, PC_SMEM, a);
+}
+
+// codes of a small table whose columns are the model's features col0 .. col0 + ncols - 1
+__global__ void k_table_codes(const float* t, int64_t nrows, int ncols, int col0, const float* cuts,
+                              const int32_t* ncuts, uint8_t* out, int* flag) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nrows * ncols; e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % ncols), f = col0 + c;
+    const float x = t[e];
+    if (!isfinite(x)) atomicExch(flag, 1);
+    const float* cf = cuts + (size_t)f * (kBins - 1);
+    int lo = 0, hi = ncuts[f];   // number of cuts <= x
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (cf[mid] <= x) lo = mid + 1;
+      else hi = mid;
+    }
+    out[e] = (uint8_t)lo;
+  }
+}
+
+static void check_flag(Ctx* ctx, DevBuf& flag, const char* what) {
+  int h = 0;
+  LLMP_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  LLMP_CUDA(cudaStreamSynchronize(ctx->stream));
+  LLMP_REQUIRE(h == 0, what);
 }
 
 void predict_impl(Ctx* ctx, const ModelData& m, const float* X, int64_t n, float* out) {
   if (n == 0) return;
+  DevBuf& codes = ctx->workspace("pred_codes", (size_t)n * kMaxF);
+  DevBuf& flag = ctx->workspace("pred_flag", sizeof(int));
+  LLMP_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx->stream));
+  compute_codes(ctx, X, n, m.F, m.cuts, codes.as<uint8_t>(), nullptr, n, flag.as<int>());
+  check_flag(ctx, flag, "X holds a non-finite value");
   PredArgs a{};
-  a.nodes = m.d_nodes.as<uint2>();
+  a.rtab = m.d_nodes.as<uint8_t>();
   a.T = m.T;
   a.D = m.D;
-  a.nn = m.nn;
-  a.F = m.F;
   a.base0 = m.base[0];
   a.base1 = m.base[1];
   a.n = n;
-  a.X = X;
+  a.codes = codes.as<uint8_t>();
   a.out = out;
   launch_predict(ctx, a, false, KC_PREDICT);
 }
@@ -239,24 +278,42 @@ void recommend_impl(Ctx* ctx, const ModelData& m, const float* llm_feats, int n_
   const int64_t n = (int64_t)n_llm * n_prof * n_levels;
   float* pred = pred_out_dev ? pred_out_dev
                              : ctx->workspace("rec_pred", (size_t)std::max<int64_t>(n, 1) * 8).as<float>();
-  DevBuf& d_lv = ctx->workspace("rec_levels", (size_t)n_levels * 4);
-  LLMP_CUDA(cudaMemcpyAsync(d_lv.p, levels, (size_t)n_levels * 4, cudaMemcpyHostToDevice, ctx->stream));
+  // codes of the three small tables (columns: LLM features, then profile features, then users)
+  LLMP_REQUIRE(F_llm + F_prof + 1 == m.F && m.users_col == F_llm + F_prof, "feature layout does not match the model");
+  DevBuf& c_llm = ctx->workspace("rec_c_llm", std::max<size_t>((size_t)n_llm * F_llm, 1));
+  DevBuf& c_prof = ctx->workspace("rec_c_prof", std::max<size_t>((size_t)n_prof * F_prof, 1));
+  DevBuf& c_lv = ctx->workspace("rec_c_lv", std::max<size_t>((size_t)n_levels, 1));
+  DevBuf& d_lvf = ctx->workspace("rec_levels_f", (size_t)n_levels * 4);
+  DevBuf& flag = ctx->workspace("pred_flag", sizeof(int));
+  std::vector<float> lvf(levels, levels + n_levels);
+  LLMP_CUDA(cudaMemcpyAsync(d_lvf.p, lvf.data(), (size_t)n_levels * 4, cudaMemcpyHostToDevice, ctx->stream));
+  LLMP_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), ctx->stream));
+  const float* cuts = m.cuts.d_cuts.as<float>();
+  const int32_t* ncuts = m.cuts.d_ncuts.as<int32_t>();
+  if ((int64_t)n_llm * F_llm > 0)
+    LLMP_LAUNCH(ctx, KC_CODES, 0, k_table_codes, 64, 256, 0, llm_feats, (int64_t)n_llm, F_llm, 0, cuts, ncuts,
+                c_llm.as<uint8_t>(), flag.as<int>());
+  if ((int64_t)n_prof * F_prof > 0)
+    LLMP_LAUNCH(ctx, KC_CODES, 0, k_table_codes, 64, 256, 0, prof_feats, (int64_t)n_prof, F_prof, F_llm, cuts, ncuts,
+                c_prof.as<uint8_t>(), flag.as<int>());
+  LLMP_LAUNCH(ctx, KC_CODES, 0, k_table_codes, 1, 256, 0, d_lvf.as<float>(), (int64_t)n_levels, 1, m.users_col, cuts,
+              ncuts, c_lv.as<uint8_t>(), flag.as<int>());
+  check_flag(ctx, flag, "feature tables hold a non-finite value");
   PredArgs a{};
-  a.nodes = m.d_nodes.as<uint2>();
+  a.rtab = m.d_nodes.as<uint8_t>();
   a.T = m.T;
   a.D = m.D;
-  a.nn = m.nn;
-  a.F = m.F;
   a.base0 = m.base[0];
   a.base1 = m.base[1];
   a.n = n;
-  a.llm_feats = llm_feats;
-  a.prof_feats = prof_feats;
-  a.levels = d_lv.as<int32_t>();
+  a.llm_codes = c_llm.as<uint8_t>();
+  a.prof_codes = c_prof.as<uint8_t>();
+  a.level_codes = c_lv.as<uint8_t>();
   a.F_llm = F_llm;
   a.F_prof = F_prof;
   a.n_prof = n_prof;
   a.n_levels = n_levels;
+  a.users_col = m.users_col;
   a.out = pred;
   if (n > 0) launch_predict(ctx, a, true, KC_PREDICT);
   argmin_impl(ctx, pred, n_llm, n_prof, n_levels, levels, cost, allowed, L1, L2, U, out);
