@@ -19,11 +19,10 @@
 namespace llmp {
 
 constexpr int PC_THREADS = 256;
-constexpr int PC_R = 4;                            // rows per thread (independent tree walks)
-constexpr int PC_ROWS = PC_THREADS * PC_R;         // rows per CTA pass
 constexpr int PC_RSTRIDE = 36;                     // bytes per staged row (9 words: distinct banks per lane)
 constexpr int PC_TREE_SMEM = 32768;                // bytes of routing tables per chunk
-constexpr int PC_SMEM = PC_ROWS * PC_RSTRIDE + PC_TREE_SMEM;
+// PC_R rows per thread (independent tree walks), PC_THREADS * PC_R rows per CTA pass
+__host__ __device__ constexpr int pc_smem(int R) { return PC_THREADS * R * PC_RSTRIDE + PC_TREE_SMEM; }
 
 __host__ __device__ inline int rtab_inner_bytes(int D) { return ((((1 << D) - 1) * 2) + 3) / 4 * 4; }
 __host__ __device__ inline int rtab_bytes(int D) { return rtab_inner_bytes(D) + (4 << D); }
@@ -41,8 +40,9 @@ struct PredArgs {
   float* out;  // n x 2
 };
 
-template <bool ASSEMBLE>
+template <bool ASSEMBLE, int PC_R>
 __global__ void __launch_bounds__(PC_THREADS) k_predict(const PredArgs a) {
+  constexpr int PC_ROWS = PC_THREADS * PC_R;
   extern __shared__ __align__(16) uint8_t smem[];
   uint8_t* rows = smem;
   uint8_t* tabs = smem + PC_ROWS * PC_RSTRIDE;
@@ -149,17 +149,23 @@ void upload_model_nodes(Ctx* ctx, ModelData& m) {
   LLMP_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
-static void launch_predict(Ctx* ctx, const PredArgs& a, bool assemble, int cls) {
+template <int R>
+static void launch_predict_r(Ctx* ctx, const PredArgs& a, bool assemble, int cls) {
   static bool attr = false;
   if (!attr) {
-    LLMP_CUDA(cudaFuncSetAttribute(k_predict<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, PC_SMEM));
-    LLMP_CUDA(cudaFuncSetAttribute(k_predict<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, PC_SMEM));
+    LLMP_CUDA(cudaFuncSetAttribute(k_predict<false, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, pc_smem(R)));
+    LLMP_CUDA(cudaFuncSetAttribute(k_predict<true, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, pc_smem(R)));
     attr = true;
   }
-  int64_t blocks = (a.n + PC_ROWS - 1) / PC_ROWS;
-  int grid = (int)std::min<int64_t>(std::max<int64_t>(blocks, 1), (int64_t)ctx->sms * 3);
-  if (assemble) LLMP_LAUNCH(ctx, cls, a.n, k_predict<true>, grid, PC_THREADS, PC_SMEM, a);
-  else LLMP_LAUNCH(ctx, cls, a.n, k_predict<false>, grid, PC_THREADS, PC_SMEM, a);
+  const int64_t rows = (int64_t)PC_THREADS * R;
+  const int per_sm = std::max(1, (int)(220000 / (pc_smem(R) + 1024)));
+  int grid = (int)std::min<int64_t>(std::max<int64_t>((a.n + rows - 1) / rows, 1), (int64_t)ctx->sms * per_sm);
+  if (assemble) LLMP_LAUNCH(ctx, cls, a.n, (k_predict<true, R>), grid, PC_THREADS, pc_smem(R), a);
+  else LLMP_LAUNCH(ctx, cls, a.n, (k_predict<false, R>), grid, PC_THREADS, pc_smem(R), a);
+}
+// 4 rows per thread: 188.6 M rows/s on the bench sweep vs 177.6 (2) and 145.8 (8; tools/ab_predict.py)
+static void launch_predict(Ctx* ctx, const PredArgs& a, bool assemble, int cls) {
+  launch_predict_r<4>(ctx, a, assemble, cls);
 }
 
 // codes of a small table whose columns are the model's features col0 .. col0 + ncols - 1
