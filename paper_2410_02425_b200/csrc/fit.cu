@@ -2036,7 +2036,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   static const bool urow = !(getenv("LLMP_NO_UROW") && atoi(getenv("LLMP_NO_UROW")) != 0);
   static const bool hist_swar = !(getenv("LLMP_HIST_SWAR") && atoi(getenv("LLMP_HIST_SWAR")) == 0);
   DevBuf& d_cm = ctx->workspace("cmask", (size_t)((n + 31) / 32) * 32 * 4);
-  LLMP_LAUNCH(ctx, KC_CODES, n, k_cmask, grid_for(ctx, n, 256, 8), 256, 0, d_codes.as<uint8_t>(), n,
+  LLMP_LAUNCH(ctx, KC_MISC, n, k_cmask, grid_for(ctx, n, 256, 8), 256, 0, d_codes.as<uint8_t>(), n,
               d_cm.as<uint32_t>());
   const uint32_t* cmask = d_cm.as<uint32_t>();
   static const int hist1 = hist1_mask();

@@ -297,12 +297,12 @@ void recommend_impl(Ctx* ctx, const ModelData& m, const float* llm_feats, int n_
   const float* cuts = m.cuts.d_cuts.as<float>();
   const int32_t* ncuts = m.cuts.d_ncuts.as<int32_t>();
   if ((int64_t)n_llm * F_llm > 0)
-    LLMP_LAUNCH(ctx, KC_CODES, 0, k_table_codes, 64, 256, 0, llm_feats, (int64_t)n_llm, F_llm, 0, cuts, ncuts,
+    LLMP_LAUNCH(ctx, KC_RECOMMEND, 0, k_table_codes, 64, 256, 0, llm_feats, (int64_t)n_llm, F_llm, 0, cuts, ncuts,
                 c_llm.as<uint8_t>(), flag.as<int>());
   if ((int64_t)n_prof * F_prof > 0)
-    LLMP_LAUNCH(ctx, KC_CODES, 0, k_table_codes, 64, 256, 0, prof_feats, (int64_t)n_prof, F_prof, F_llm, cuts, ncuts,
+    LLMP_LAUNCH(ctx, KC_RECOMMEND, 0, k_table_codes, 64, 256, 0, prof_feats, (int64_t)n_prof, F_prof, F_llm, cuts, ncuts,
                 c_prof.as<uint8_t>(), flag.as<int>());
-  LLMP_LAUNCH(ctx, KC_CODES, 0, k_table_codes, 1, 256, 0, d_lvf.as<float>(), (int64_t)n_levels, 1, m.users_col, cuts,
+  LLMP_LAUNCH(ctx, KC_RECOMMEND, 0, k_table_codes, 1, 256, 0, d_lvf.as<float>(), (int64_t)n_levels, 1, m.users_col, cuts,
               ncuts, c_lv.as<uint8_t>(), flag.as<int>());
   check_flag(ctx, flag, "feature tables hold a non-finite value");
   PredArgs a{};
