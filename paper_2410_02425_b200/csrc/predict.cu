@@ -40,7 +40,7 @@ struct PredArgs {
   float* out;  // n x 2
 };
 
-template <bool ASSEMBLE, int PC_R>
+template <bool ASSEMBLE, int PC_R, int DC>   // DC: compile-time depth (0 = a.D)
 __global__ void __launch_bounds__(PC_THREADS) k_predict(const PredArgs a) {
   constexpr int PC_ROWS = PC_THREADS * PC_R;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(PC_THREADS) k_predict(const PredArgs a) {
           int node[PC_R];
 #pragma unroll
           for (int q = 0; q < PC_R; ++q) node[q] = 0;
-          for (int s = 0; s < a.D; ++s) {   // fixed depth; the PC_R walks are independent
+#pragma unroll
+          for (int s = 0; s < (DC ? DC : a.D); ++s) {   // fixed depth; the PC_R walks are independent
 #pragma unroll
             for (int q = 0; q < PC_R; ++q) {
               const uint32_t w = inode[node[q]];
@@ -149,23 +150,27 @@ void upload_model_nodes(Ctx* ctx, ModelData& m) {
   LLMP_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
-template <int R>
+template <int R, int DC>
 static void launch_predict_r(Ctx* ctx, const PredArgs& a, bool assemble, int cls) {
   static bool attr = false;
   if (!attr) {
-    LLMP_CUDA(cudaFuncSetAttribute(k_predict<false, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, pc_smem(R)));
-    LLMP_CUDA(cudaFuncSetAttribute(k_predict<true, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, pc_smem(R)));
+    LLMP_CUDA(cudaFuncSetAttribute(k_predict<false, R, DC>, cudaFuncAttributeMaxDynamicSharedMemorySize, pc_smem(R)));
+    LLMP_CUDA(cudaFuncSetAttribute(k_predict<true, R, DC>, cudaFuncAttributeMaxDynamicSharedMemorySize, pc_smem(R)));
     attr = true;
   }
   const int64_t rows = (int64_t)PC_THREADS * R;
   const int per_sm = std::max(1, (int)(220000 / (pc_smem(R) + 1024)));
   int grid = (int)std::min<int64_t>(std::max<int64_t>((a.n + rows - 1) / rows, 1), (int64_t)ctx->sms * per_sm);
-  if (assemble) LLMP_LAUNCH(ctx, cls, a.n, (k_predict<true, R>), grid, PC_THREADS, pc_smem(R), a);
-  else LLMP_LAUNCH(ctx, cls, a.n, (k_predict<false, R>), grid, PC_THREADS, pc_smem(R), a);
+  if (assemble) LLMP_LAUNCH(ctx, cls, a.n, (k_predict<true, R, DC>), grid, PC_THREADS, pc_smem(R), a);
+  else LLMP_LAUNCH(ctx, cls, a.n, (k_predict<false, R, DC>), grid, PC_THREADS, pc_smem(R), a);
 }
-// 4 rows per thread: 188.6 M rows/s on the bench sweep vs 177.6 (2) and 145.8 (8; tools/ab_predict.py)
+// 4 rows per thread: 188.6 M rows/s on the bench sweep vs 177.6 (2) and 145.8 (8; tools/ab_predict.py);
+// compile-time depth for the configs' depths (6, 8)
 static void launch_predict(Ctx* ctx, const PredArgs& a, bool assemble, int cls) {
-  launch_predict_r<4>(ctx, a, assemble, cls);
+  static const bool dct = !(getenv("LLMP_PRED_DC") && atoi(getenv("LLMP_PRED_DC")) == 0);
+  if (dct && a.D == 8) launch_predict_r<4, 8>(ctx, a, assemble, cls);
+  else if (dct && a.D == 6) launch_predict_r<4, 6>(ctx, a, assemble, cls);
+  else launch_predict_r<4, 0>(ctx, a, assemble, cls);
 }
 
 // codes of a small table whose columns are the model's features col0 .. col0 + ncols - 1

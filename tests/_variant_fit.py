@@ -1,5 +1,6 @@
 """Subprocess helper for test_gpu_parity.test_kernel_variants: the kernel-variant switches
-(LLMP_NOFUSE, LLMP_ROOT2, LLMP_SPLIT_CLUSTER, LLMP_NO_UROW, LLMP_HIST2, LLMP_PAIRED, LLMP_GRAPH_REPLAY) are read once per process, so each variant is checked in
+(LLMP_NOFUSE, LLMP_ROOT2, LLMP_SPLIT_CLUSTER, LLMP_NO_UROW, LLMP_HIST2, LLMP_PAIRED, LLMP_GRAPH_REPLAY,
+LLMP_HIST_SWAR, LLMP_PRED_DC) are read once per process, so each variant is checked in
 its own interpreter.  Fits paper-shaped (C1 with 12 features, C2) and random (S1, ragged) data through the
 C-ABI in both execution modes (graph replay, instrumented plain launches) and compares with the oracle;
 checks the histogram test hook (the variant's histogram kernel) against brute-force sums."""
@@ -62,6 +63,10 @@ def main():
             if not np.array_equal(np.asarray(otp, np.float32).view(np.uint32),
                                   np.asarray(gm.train_pred(d.n), np.float32).view(np.uint32)):
                 print("MISMATCH train_pred n=%d timing=%d" % (d.n, every))
+                return 1
+            if not np.array_equal(np.asarray(otp, np.float32).view(np.uint32),
+                                  np.asarray(gm.predict(ctx, d.X), np.float32).view(np.uint32)):
+                print("MISMATCH predict n=%d timing=%d" % (d.n, every))
                 return 1
             gm.free()
     print("OK")
