@@ -490,7 +490,9 @@ def main():
                     "frac": kd["achieved_gbs"] / peak, "peak_source": peak_src,
                     "bytes_per_unit": kd["bytes_per_unit"], "units_per_launch": kd["units"] / kd["launches"],
                     "traffic": tr.get("dram_bytes_per_launch") if tr else None,
-                    "traffic_note": tr.get("note") if tr else "no ncu capture committed"}
+                    "traffic_note": (tr.get("note") + "; the ncu sample is one steady-state tree (tree 100 of a "
+                                     "102-tree fit, tools/prof_late.sh), whose launches need not hold the 500-tree "
+                                     "average units_per_launch") if tr else "no ncu capture committed"}
 
     # ---- end to end through the public API with pinned host buffers
     e2e = None
