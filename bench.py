@@ -489,10 +489,11 @@ def main():
         roofline = {"kernel": dom, "bound": "hbm", "achieved": kd["achieved_gbs"], "peak": peak, "unit": "GB/s",
                     "frac": kd["achieved_gbs"] / peak, "peak_source": peak_src,
                     "bytes_per_unit": kd["bytes_per_unit"], "units_per_launch": kd["units"] / kd["launches"],
-                    "traffic": tr.get("dram_bytes_per_launch") if tr else None,
-                    "traffic_note": (tr.get("note") + "; the ncu sample is one steady-state tree (tree 100 of a "
-                                     "102-tree fit, tools/prof_late.sh), whose launches need not hold the 500-tree "
-                                     "average units_per_launch") if tr else "no ncu capture committed"}
+                    "traffic": ((tr["dram_bytes_per_unit"] * kd["units"] / kd["launches"]) if tr and
+                                "dram_bytes_per_unit" in tr else tr.get("dram_bytes_per_launch") if tr else None),
+                    "traffic_note": ((tr.get("note") + "; scaled to this run's units_per_launch")
+                                     if tr and "dram_bytes_per_unit" in tr else tr.get("note") if tr
+                                     else "no ncu capture committed")}
 
     # ---- end to end through the public API with pinned host buffers
     e2e = None
