@@ -174,7 +174,8 @@ llmpilot_status llmpilot_model_importance(const llmpilot_model* m, int32_t norma
 void llmpilot_model_free(llmpilot_model* m);
 
 /* Predict both targets: out[i] = (nTTFT, ITL) = base + sum over trees in order.
- * X: n x F (host or device); out: n x 2 (host or device). */
+ * X: n x F (host or device), finite (the rows are binned with the model's cuts and routed on codes,
+ * code <= b <=> x < cut: LLMP_EINVAL for NaN/Inf); out: n x 2 (host or device). */
 llmpilot_status llmpilot_predict(llmpilot_ctx* ctx, const llmpilot_model* m, const float* X, int64_t n, float* out);
 
 /* Recommendation (Eq. 1-3): for each unseen LLM i, rows [llm_feats[i] | prof_feats[g] | u]
@@ -184,6 +185,7 @@ llmpilot_status llmpilot_predict(llmpilot_ctx* ctx, const llmpilot_model* m, con
  * llm_feats: n_llm x F_llm, prof_feats: n_prof x F_prof (host or device); F_llm + F_prof + 1
  * must equal the model's F with users at column F_llm + F_prof.  prof_cost: host, > 0.
  * allowed: host n_llm x n_prof mask or NULL.  user_levels: host, strictly increasing, > 0.
+ * The feature tables must be finite (LLMP_EINVAL otherwise).
  * out: host n_llm records; infeasible => profile -1, n_pods 0, cost +inf, u_max 0.
  * pred_out (optional, host or device): n_llm x n_prof x n_levels x 2 predictions. */
 typedef struct {

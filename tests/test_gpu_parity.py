@@ -420,6 +420,17 @@ def test_errors(lp, ctx):
     m = lp.fit(ctx, d.X, d.y, lp.hparams(n_trees=2, max_depth=2), d.users_col, d.llm_id, d.prof_id, d.n_llm, d.n_prof)
     with pytest.raises(lp.LLMPilotError, match="EINVAL"):
         lp.recommend(ctx, m, d.X[:2, :6], d.X[:2, 6:11], [1.0, 1.0], [4, 2], L1, L2, U)   # levels not increasing
+    # the predictor bins rows with the model's cuts: a non-finite feature (which routes differently as
+    # a float than as a code) is rejected, in plain rows and in the recommendation tables alike (R17)
+    Xn = d.X[:7].copy()
+    Xn[3, 2] = np.nan
+    with pytest.raises(lp.LLMPilotError, match="EINVAL"):
+        m.predict(ctx, Xn)
+    lfn = d.X[:2, :6].copy()
+    lfn[1, 0] = np.inf
+    with pytest.raises(lp.LLMPilotError, match="EINVAL"):
+        lp.recommend(ctx, m, lfn, d.X[:2, 6:11], [1.0, 1.0], [2, 4], L1, L2, U)
+    assert m.predict(ctx, d.X[:0]).shape == (0, 2)   # empty batch
     # zero trees: predictions are the base scores
     m0 = lp.fit(ctx, d.X, d.y, lp.hparams(n_trees=0), d.users_col, d.llm_id, d.prof_id, d.n_llm, d.n_prof)
     p0 = m0.predict(ctx, d.X)
