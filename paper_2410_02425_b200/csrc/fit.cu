@@ -2195,7 +2195,9 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   // one tree of the targets in `fp` (ny = 2: both as blockIdx.y = 0, 1; ny = 1: fp.t[0] only)
   auto trees = [&](const FitPair& fp, int ny) {
     const cudaStream_t st = ctx->stream;
-    const dim3 hg(ctx->sms * 2 / ny, ny);   // histogram kernels: 2 CTAs per SM in total
+    // histogram kernels: 2 CTAs per SM in total, but no more CTAs than 2048-row slices of the data
+    // (small fits would otherwise launch hundreds of CTAs that only zero their shared histograms)
+    const dim3 hg((unsigned)std::min<int64_t>(ctx->sms * 2 / ny, std::max<int64_t>(1, (n + 2047) / 2048)), ny);
     // fused: the previous round's update pass built this root already unless root_needed
     if (fused) {
       LLMP_LAUNCH(ctx, KC_MISC, 0, k_root_fix, dim3(1, ny), 1024, 0, fp);
