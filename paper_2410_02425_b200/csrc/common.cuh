@@ -90,6 +90,7 @@ struct Ctx {
   int timing_every = 1;                    // time every k-th launch of each class
   uint64_t timed[LLMP_N_KERNEL_CLASSES] = {};
   bool use_graphs = true;                  // replay each tree from a CUDA graph (off while timing)
+  bool pdl = false;                        // programmatic dependent launch inside the tree loop
   cudaStream_t cap_stream[2] = {nullptr, nullptr};   // private streams used only for graph capture
   cudaEvent_t fork_event = nullptr, join_event = nullptr;
   cudaStream_t capture_stream(int i) {
@@ -130,6 +131,32 @@ struct Ctx {
     kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);              \
     LLMP_CUDA(cudaGetLastError());                                                \
     (ctx)->after((cls), _ev, (double)(nrows));                                    \
+  } while (0)
+
+// Programmatic dependent launch (LLMP_PDL): the kernel may be scheduled while its predecessor in the
+// stream finishes; every kernel launched this way calls pdl_wait() (griddepcontrol.wait) before it
+// touches memory, so only the launch latency overlaps.  Without the attribute the wait is a no-op.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#define LLMP_LAUNCH_PDL(ctx, cls, nrows, kernel, grid, block, smem, ...)                         \
+  do {                                                                                           \
+    if (!(ctx)->pdl) {                                                                           \
+      LLMP_LAUNCH(ctx, cls, nrows, kernel, grid, block, smem, __VA_ARGS__);                      \
+      break;                                                                                     \
+    }                                                                                            \
+    cudaEvent_t _ev = nullptr;                                                                   \
+    (ctx)->before((cls), &_ev);                                                                  \
+    cudaLaunchConfig_t _cfg = {};                                                                \
+    _cfg.gridDim = dim3(grid);                                                                   \
+    _cfg.blockDim = dim3(block);                                                                 \
+    _cfg.dynamicSmemBytes = (smem);                                                              \
+    _cfg.stream = (ctx)->stream;                                                                 \
+    cudaLaunchAttribute _at[1];                                                                  \
+    _at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                              \
+    _at[0].val.programmaticStreamSerializationAllowed = 1;                                       \
+    _cfg.attrs = _at;                                                                            \
+    _cfg.numAttrs = 1;                                                                           \
+    LLMP_CUDA(cudaLaunchKernelEx(&_cfg, kernel, __VA_ARGS__));                                   \
+    (ctx)->after((cls), _ev, (double)(nrows));                                                   \
   } while (0)
 
 // copy a bulk array to the device if it is a host pointer; returns a device pointer (either the

@@ -187,6 +187,7 @@ __device__ __forceinline__ void run_step(uint32_t& pc, int32_t& ag, uint32_t& ah
 
 template <int MODE>
 __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitPair fp, const int d, const int t_in, const DbgArgs dbg) {
+  pdl_wait();
   const FitArgs& a = fp.t[blockIdx.y];
   const int t = (MODE == HM_ROOT || MODE == HM_UPDROOT) ? *a.d_tree : t_in;   // graph replays: tree index from the device
   if (MODE == HM_ROOT && !root_needed(a, t)) return;   // built speculatively by the previous update pass
@@ -543,6 +544,7 @@ __device__ __forceinline__ void red2(uint32_t addr, int32_t g, uint32_t h) {
 
 template <int MODE, int DC = 0>   // DC: compile-time tree depth of the fused update's routing (0 = a.D)
 __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const int d, const int t_in, const DbgArgs dbg) {
+  pdl_wait();
   const FitArgs& a = fp.t[blockIdx.y];
   const int t = (MODE == HM_ROOT || MODE == HM_UPDROOT) ? *a.d_tree : t_in;   // graph replays: tree index from the device
   if (MODE == HM_ROOT && !root_needed(a, t)) return;   // built speculatively by the previous update pass
@@ -936,6 +938,7 @@ static bool use_hist1() { return (hist1_mask() & 2) != 0; }   // the test hook f
 
 // zero the root histogram slot when k_hist<ROOT> is going to (re)build it (see root_needed)
 __global__ void k_root_fix(const FitPair fp) {
+  pdl_wait();
   const FitArgs& a = fp.t[blockIdx.y];
   if (!root_needed(a, *a.d_tree)) return;
   int64_t* H = a.H[0];
@@ -1254,6 +1257,7 @@ __device__ __forceinline__ int parent_of_tile(const int* s_tile_pref, int NP, in
 // starts follow from the counts (s_j and s_j + n_L; written by the level histogram kernel).
 constexpr int PT_CTAS_PER_SM = 8;
 __global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitPair fp, const int d) {
+  pdl_wait();
   const FitArgs& a = fp.t[blockIdx.y];
   __shared__ int s_tile_pref[MAX_PIECES + 1];
   __shared__ int64_t s_seq_pref[MAX_PIECES + 1];
@@ -1383,6 +1387,7 @@ constexpr int SP3_WARPS = 4;
 constexpr int SP3_CLUSTER = 32 / SP3_WARPS;   // 8 CTAs = the node's 32 features
 template <bool CL>
 __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitPair fp, const int d) {
+  pdl_wait();
   const FitArgs& a = fp.t[blockIdx.y];
   __shared__ FeatBest s_fb[SP3_WARPS];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1817,7 +1822,10 @@ __global__ void __launch_bounds__(BASE_THREADS) k_base_init(const FitArgs a, con
   }
 }
 
-__global__ void k_next_tree(int* d_tree) { *d_tree += 1; }
+__global__ void k_next_tree(int* d_tree) {
+  pdl_wait();
+  *d_tree += 1;
+}
 __global__ void k_stamp(unsigned long long* stamps) {
   unsigned long long ns;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
@@ -1825,6 +1833,7 @@ __global__ void k_stamp(unsigned long long* stamps) {
 }
 // graph form: advance the tree index and keep the device-side while loop running while t < T
 __global__ void k_next_tree_cond(int* d_tree, int T, cudaGraphConditionalHandle h, unsigned long long* stamps) {
+  pdl_wait();
   const int t = *d_tree + 1;
   *d_tree = t;
   cudaGraphSetConditional(h, t < T ? 1u : 0u);
@@ -2034,6 +2043,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   static const bool use_root2 = getenv("LLMP_ROOT2") && atoi(getenv("LLMP_ROOT2")) != 0;
   static const bool fused = !use_root2 && !(getenv("LLMP_NOFUSE") && atoi(getenv("LLMP_NOFUSE")) != 0);
   static const bool urow = !(getenv("LLMP_NO_UROW") && atoi(getenv("LLMP_NO_UROW")) != 0);
+  static const bool pdl_env = !(getenv("LLMP_PDL") && atoi(getenv("LLMP_PDL")) == 0);
+  ctx->pdl = pdl_env && !ctx->sharded();   // (NCCL calls sit between the kernels when sharded)
   static const bool hist_swar = !(getenv("LLMP_HIST_SWAR") && atoi(getenv("LLMP_HIST_SWAR")) == 0);
   DevBuf& d_cm = ctx->workspace("cmask", (size_t)((n + 31) / 32) * 32 * 4);
   LLMP_LAUNCH(ctx, KC_MISC, n, k_cmask, grid_for(ctx, n, 256, 8), 256, 0, d_codes.as<uint8_t>(), n,
@@ -2168,7 +2179,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   auto split = [&](const FitPair& fp, int ny, int d) {
     const dim3 grid((1 << d) * SP3_CLUSTER, ny);
     if (!split_cluster) {
-      LLMP_LAUNCH(ctx, KC_SPLIT, ny << d, k_split3<false>, grid, SP3_WARPS * 32, 0, fp, d);
+      LLMP_LAUNCH_PDL(ctx, KC_SPLIT, ny << d, k_split3<false>, grid, SP3_WARPS * 32, 0, fp, d);
       return;
     }
     cudaLaunchConfig_t cfg = {};
@@ -2200,13 +2211,13 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     const dim3 hg((unsigned)std::min<int64_t>(ctx->sms * 2 / ny, std::max<int64_t>(1, (n + 2047) / 2048)), ny);
     // fused: the previous round's update pass built this root already unless root_needed
     if (fused) {
-      LLMP_LAUNCH(ctx, KC_MISC, 0, k_root_fix, dim3(1, ny), 1024, 0, fp);
+      LLMP_LAUNCH_PDL(ctx, KC_MISC, 0, k_root_fix, dim3(1, ny), 1024, 0, fp);
     } else {
       for (int q = 0; q < ny; ++q) LLMP_CUDA(cudaMemsetAsync(fp.t[q].H[0], 0, (size_t)SLOT * 8, st));
     }
     if (use_root2) LLMP_LAUNCH(ctx, KC_HIST_ROOT, ny * n, k_hist_root2, hg, R2_THREADS, R2_SMEM, fp);
     else if (hist1 & 1) LLMP_LAUNCH(ctx, KC_HIST_ROOT, ny * n, k_hist<HM_ROOT>, hg, HIST_THREADS, HIST_SMEM, fp, 0, 0, nodbg);
-    else LLMP_LAUNCH(ctx, KC_HIST_ROOT, ny * n, k_hist2<HM_ROOT>, hg, H2_THREADS, H2_SMEM, fp, 0, 0, nodbg);
+    else LLMP_LAUNCH_PDL(ctx, KC_HIST_ROOT, ny * n, k_hist2<HM_ROOT>, hg, H2_THREADS, H2_SMEM, fp, 0, 0, nodbg);
     nccl_group_start(ctx);
     for (int q = 0; q < ny; ++q) allreduce_sum_i64(ctx, fp.t[q].H[0], SLOT);
     nccl_group_end(ctx);
@@ -2214,9 +2225,9 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     for (int d = 1; d < D; ++d) {
       const int tiles_d = (int)((n + PT_TILE - 1) / PT_TILE) + (1 << (d - 1));
       // persistent tile loop (upper bound of the level's tile count: one partial tile per parent)
-      LLMP_LAUNCH(ctx, KC_PARTITION, ny * n, k_part, dim3(std::min(tiles_d, PT_CTAS_PER_SM / ny * ctx->sms), ny),
+      LLMP_LAUNCH_PDL(ctx, KC_PARTITION, ny * n, k_part, dim3(std::min(tiles_d, PT_CTAS_PER_SM / ny * ctx->sms), ny),
                   PT_THREADS, 0, fp, d);
-      if (hist1 & 2) LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hg, HIST_THREADS, HIST_SMEM, fp, d, 0, nodbg);
+      if (hist1 & 2) LLMP_LAUNCH_PDL(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hg, HIST_THREADS, HIST_SMEM, fp, d, 0, nodbg);
       else LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist2<HM_LEVEL>, hg, H2_THREADS, H2_SMEM, fp, d, 0, nodbg);
       nccl_group_start(ctx);   // both targets' built-child histograms in one NCCL launch
       for (int q = 0; q < ny; ++q) allreduce_sum_i64(ctx, fp.t[q].H[d & 1], (size_t)SLOT << (d - 1));
@@ -2229,7 +2240,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
         LLMP_LAUNCH(ctx, KC_UPDATE, ny * n, k_hist<HM_UPDROOT>, hg, HIST_THREADS, HIST_SMEM + updroot_tree_smem(D), fp,
                     0, 0, nodbg);
       else
-        LLMP_LAUNCH(ctx, KC_UPDATE, ny * n, k_upd2, hg, H2_THREADS, H2_SMEM + updroot_tree_smem(D), fp, 0, 0, nodbg);
+        LLMP_LAUNCH_PDL(ctx, KC_UPDATE, ny * n, k_upd2, hg, H2_THREADS, H2_SMEM + updroot_tree_smem(D), fp, 0, 0, nodbg);
     } else {
       LLMP_LAUNCH(ctx, KC_UPDATE, ny * n, k_update, dim3(std::max(1, upd_grid * ny / 2), ny), UPD_THREADS, 0, fp);
     }
@@ -2260,7 +2271,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     // next tree's gradient maxima of both targets (contiguous; past slots are already equal on
     // every rank, future ones 0)
     allreduce_max_u32(ctx, A[0].maxg, (size_t)4 * (T + 1));
-    if (loop) LLMP_LAUNCH(ctx, KC_MISC, 0, k_next_tree_cond, 1, 1, 0, d_tree, T, *loop, stamps);
+    if (loop) LLMP_LAUNCH_PDL(ctx, KC_MISC, 0, k_next_tree_cond, 1, 1, 0, d_tree, T, *loop, stamps);
     else LLMP_LAUNCH(ctx, KC_MISC, 0, k_next_tree, 1, 1, 0, d_tree);
   };
   LLMP_CUDA(cudaMemsetAsync(d_tree, 0, sizeof(int), s));
