@@ -14,7 +14,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def child(trees, reps, llms):
-    sys.path.insert(0, ROOT)
+    # AB_ROOT=<dir>: load the package (and its built library) from another tree, e.g. a copy of
+    # the previous build, so two builds can be compared on the same box
+    sys.path.insert(0, os.environ.get("AB_ROOT", ROOT))
     import torch
 
     import paper_2410_02425_b200 as lp
