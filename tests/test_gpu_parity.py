@@ -392,6 +392,23 @@ def test_cv_grid_parity_c1(lp, ctx):
     assert of == gf and (oS, oO, oSO) == (gS, gO, gSO)
 
 
+def test_cv_hand_fixture_on_gpu(lp, ctx, golden):
+    """The O12 hand fixture (tests/golden/o12_cv_hand_fixture.json: S = 1/3, O = 0.5, SO = 0.4,
+    P:L277, Eq. (6), Eq. (7)) through llmpilot_cv_leave_one_llm_out."""
+    from _cv_fixture import cv_hand_fixture_rows
+    g = golden("o12_cv_hand_fixture.json")
+    X, y, li, pi, uc, n_llm, n_prof = cv_hand_fixture_rows(g)
+    h = g["hparams"]
+    hp = lp.hparams(n_trees=h["n_trees"], max_depth=h["max_depth"], eta=h["eta"], lambda_=h["lambda_"],
+                    min_child_weight=h["min_child_weight"], use_eq4_weights=h["use_eq4_weights"],
+                    monotone_users=h["monotone_users"])
+    gf, gS, gO, gSO = lp.cv(ctx, X, y, li, pi, uc, n_llm, n_prof, [hp], g["L1"], g["L2"], g["U"], g["cost"])
+    for f, e in zip(gf, g["folds"]):
+        assert f["rec"] == tuple(e["rec"]) and f["truth"] == tuple(e["truth"])
+        assert f["success"] == e["success"] and f["overspend"] == e["overspend"]
+    assert gS == g["S_num"] / g["S_den"] and gO == g["O"] and gSO == pytest.approx(g["SO"], rel=1e-15)
+
+
 def test_cv_parity_c2_short(lp, ctx):
     d = synth.make("C2")
     of, oS, oO, oSO = oracle.cv(d.X, d.y, d.llm_id, d.prof_id, d.users_col, d.n_llm, d.n_prof,

@@ -579,3 +579,87 @@ def test_o12_cv_grid_selects_min_error():
                                 200, d.cost)
     # the heavily under-fitted configuration never wins the inner wMAPE comparison
     assert all(f["hp_index"] == 1 for f in folds)
+
+
+def _fixture_hp(mod, h):
+    return mod.hparams(n_trees=h["n_trees"], max_depth=h["max_depth"], eta=h["eta"], lambda_=h["lambda_"],
+                       min_child_weight=h["min_child_weight"], use_eq4_weights=h["use_eq4_weights"],
+                       monotone_users=h["monotone_users"])
+
+
+def test_o12_cv_hand_fixture(golden):
+    """3-LLM hand fixture (P:L277 S_M, Eq. (6) O_M, Eq. (7) SO): every fold's recommendation, truth,
+    success and overspend and the aggregates S = 1/3, O = 0.5, SO = 0.4 derived by hand in the
+    golden file.  Folds A and B recommend n = 2 pods of a profile whose TRUE u_max is 4 (predicted 8),
+    so S_M taken from the predicted u_max would score them as successes; fold C over-provisions
+    (3 pods for a true optimum of 2), so O_M divided by the recommended cost would give 1/3."""
+    from _cv_fixture import cv_hand_fixture_rows
+    g = golden("o12_cv_hand_fixture.json")
+    X, y, li, pi, uc, n_llm, n_prof = cv_hand_fixture_rows(g)
+    folds, S, O, SO = oracle.cv(X, y, li, pi, uc, n_llm, n_prof, [_fixture_hp(oracle, g["hparams"])], g["L1"],
+                                g["L2"], g["U"], g["cost"])
+    assert len(folds) == 3
+    for f, e in zip(folds, g["folds"]):
+        assert f["llm"] == e["llm"]
+        assert f["rec"] == tuple(e["rec"]) and f["truth"] == tuple(e["truth"])
+        assert f["success"] == e["success"] and f["overspend"] == e["overspend"]
+    assert S == g["S_num"] / g["S_den"] and O == g["O"]
+    assert SO == pytest.approx(g["SO"], rel=1e-15)
+
+
+def _rederive_fold(d, M, hp, L1, L2, U):
+    """S_M and O_M of held-out LLM M re-derived from separate oracle calls (fit on the other LLMs,
+    predict M's rows, Eq. (1)-(3) on the predicted and on the measured (profile x users) tables),
+    following P:L277 and Eq. (6) directly rather than orc_cv's own scoring code."""
+    tr = d.llm_id != M
+    te = ~tr
+    m = oracle.fit(d.X[tr], d.y[tr], hp, d.users_col, d.llm_id[tr], d.prof_id[tr], d.n_llm, d.n_prof, L1, L2)
+    pred = oracle.predict(m, d.X[te])
+    Xm, ym, pm = d.X[te], d.y[te], d.prof_id[te]
+    levels = np.unique(Xm[:, d.users_col]).astype(np.int32)
+    ptab = np.zeros((1, d.n_prof, len(levels), 2), np.float32)
+    ttab = np.zeros_like(ptab)
+    allowed = np.zeros((1, d.n_prof), np.uint8)
+    for i in range(len(Xm)):
+        k = int(np.searchsorted(levels, int(Xm[i, d.users_col])))
+        ptab[0, pm[i], k] = pred[i]
+        ttab[0, pm[i], k] = ym[i]
+        allowed[0, pm[i]] = 1
+    rec = oracle.recommend(ptab, levels, d.cost, L1, L2, U, allowed)[0]
+    truth = oracle.recommend(ttab, levels, d.cost, L1, L2, U, allowed)[0]
+    success, over = 0, 0.0
+    if truth[0] >= 0 and rec[0] >= 0:
+        only = np.zeros_like(allowed)
+        only[0, rec[0]] = 1
+        on_g = oracle.recommend(ttab, levels, d.cost, L1, L2, U, only)[0]   # true u_max on the recommended profile
+        u_true = on_g[3] if on_g[0] == rec[0] else 0
+        if u_true > 0 and rec[1] * u_true >= U:                           # P:L277
+            success = 1
+            over = (rec[2] - truth[2]) / truth[2]                         # Eq. (6)
+    return rec, truth, success, over
+
+
+def test_o12_cv_folds_rederived_independently():
+    """orc_cv's per-fold S_M and O_M equal a re-derivation from oracle.fit / oracle.predict /
+    oracle.recommend (truth u_max on G* via a single-profile mask on the measured table).  The C1
+    configuration (10 trees, depth 3) has both failures whose predicted u_max exceeds the true one
+    and successes with a positive overspend, so a mutation of either S_M or Eq. (6)'s denominator
+    fails this test."""
+    d = synth.make("C1")
+    hp = oracle.hparams(n_trees=10, max_depth=3, eta=0.3)
+    L1, L2, U = 100.0, 50.0, 200
+    folds, S, O, SO = oracle.cv(d.X, d.y, d.llm_id, d.prof_id, d.users_col, d.n_llm, d.n_prof, [hp], L1, L2, U,
+                                d.cost)
+    n_over = n_fail_opt = 0
+    succ, overs = 0, []
+    for f in folds:
+        rec, truth, success, over = _rederive_fold(d, f["llm"], hp, L1, L2, U)
+        assert f["rec"] == rec and f["truth"] == truth
+        assert f["success"] == success and f["overspend"] == over
+        n_over += success and over > 0
+        n_fail_opt += (not success) and rec[0] >= 0 and rec[3] * rec[1] >= U   # feasible by the predicted u_max
+        succ += success
+        overs += [over] if success else []
+    assert n_over >= 1 and n_fail_opt >= 1   # the fixture discriminates both mutations
+    assert S == succ / len(folds) and O == sum(overs) / len(overs)
+    assert SO == oracle.so_score(S, O)
