@@ -167,6 +167,27 @@ def _ptr(a, dtype):
     return arr.ctypes.data_as(C.c_void_p), arr
 
 
+def _out_ptr(out, shape, what):
+    """Pointer of a caller-supplied OUTPUT buffer: it must be C-contiguous float32 of exactly `shape`
+    (the library writes through the pointer, so a converted copy would silently lose the result)."""
+    if out is None:
+        return None
+    if tuple(out.shape) != tuple(shape):
+        raise ValueError("%s must have shape %s, got %s" % (what, tuple(shape), tuple(out.shape)))
+    try:
+        import torch
+        if isinstance(out, torch.Tensor):
+            if out.dtype != torch.float32 or not out.is_contiguous():
+                raise ValueError("%s must be a contiguous float32 tensor" % what)
+            return C.c_void_p(out.data_ptr())
+    except ImportError:
+        pass
+    if not isinstance(out, np.ndarray) or out.dtype != np.float32 or not out.flags["C_CONTIGUOUS"] \
+            or not out.flags["WRITEABLE"]:
+        raise ValueError("%s must be a writeable C-contiguous float32 array" % what)
+    return out.ctypes.data_as(C.c_void_p)
+
+
 def _stream_handle(stream):
     if stream is None:
         return None
@@ -317,10 +338,12 @@ class Model:
     def predict(self, ctx: Context, X, out=None):
         """out: None (returns a host numpy array) or a tensor/array of n x 2 float32."""
         n = int(X.shape[0])
+        if X.ndim != 2 or int(X.shape[1]) != self.F:
+            raise ValueError("X must be n x %d (the model's feature count), got %s" % (self.F, tuple(X.shape)))
         px, keep = _ptr(X, np.float32)
         if out is None:
             out = np.zeros((n, 2), np.float32)
-        po, keep2 = _ptr(out, np.float32)
+        po = _out_ptr(out, (n, 2), "out")
         _check(lib().llmpilot_predict(ctx.handle, self._h, px, n, po))
         return out
 
@@ -403,7 +426,7 @@ def recommend(ctx: Context, model: Model, llm_feats, prof_feats, cost, user_leve
     cs = np.ascontiguousarray(cost, np.float64)
     lv = np.ascontiguousarray(user_levels, np.int32)
     al = None if allowed is None else np.ascontiguousarray(allowed, np.uint8)
-    po, k3 = _ptr(pred_out, np.float32)
+    po = _out_ptr(pred_out, (n_llm * n_prof * len(lv), 2), "pred_out")
     out = (Rec * max(n_llm, 1))()
     _check(lib().llmpilot_recommend(ctx.handle, model._h, pl, n_llm, F_llm, pp, n_prof, F_prof,
                                     cs.ctypes.data_as(C.c_void_p), None if al is None else al.ctypes.data_as(C.c_void_p),

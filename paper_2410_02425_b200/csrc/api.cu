@@ -494,18 +494,14 @@ llmpilot_status llmpilot_recommend(llmpilot_ctx* ctx, const llmpilot_model* m, c
     const float* pf =
         (const float*)llmp::to_device(&ctx->c, prof_feats, (size_t)n_prof * F_prof * 4, ctx->c.ws["rec_prof"]);
     const int64_t nrows = (int64_t)n_llm * n_prof * n_levels;
-    float* pred_dev = nullptr;
+    // predictions requested on the host: one pass into a device buffer, then one copy
     const bool pred_is_dev = pred_out && llmp::is_device_ptr(pred_out);
-    if (pred_is_dev) pred_dev = pred_out;
+    if (pred_out && !pred_is_dev) tpred.ensure((size_t)nrows * 8);
+    float* pred_dev = pred_is_dev ? pred_out : (pred_out ? tpred.as<float>() : nullptr);
     llmp::RecOut r;
     llmp::recommend_impl(&ctx->c, m->m, lf, n_llm, F_llm, pf, n_prof, F_prof, prof_cost, allowed, user_levels, n_levels,
                          L1, L2, U, r, pred_dev);
     if (pred_out && !pred_is_dev) {
-      // predictions were requested on the host: recompute into a device buffer and copy
-      tpred.ensure((size_t)nrows * 8);
-      llmp::RecOut r2;
-      llmp::recommend_impl(&ctx->c, m->m, lf, n_llm, F_llm, pf, n_prof, F_prof, prof_cost, allowed, user_levels,
-                           n_levels, L1, L2, U, r2, tpred.as<float>());
       LLMP_CUDA(cudaMemcpyAsync(pred_out, tpred.p, (size_t)nrows * 8, cudaMemcpyDeviceToHost, ctx->c.stream));
       LLMP_CUDA(cudaStreamSynchronize(ctx->c.stream));
     }

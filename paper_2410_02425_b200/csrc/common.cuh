@@ -162,6 +162,8 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // copy a bulk array to the device if it is a host pointer; returns a device pointer (either the
 // original or `tmp`'s storage)
 bool is_device_ptr(const void* p);
+// per-device, thread-safe opt-in to `bytes` of dynamic shared memory for a kernel (only grows)
+void ensure_smem_attr(const void* func, int bytes);
 const void* to_device(Ctx* ctx, const void* p, size_t bytes, DevBuf& tmp);
 
 // multi-GPU collectives (nccl.cu); no-ops for one rank

@@ -1855,10 +1855,11 @@ __global__ void k_fill_trees(int32_t* feat, int32_t* bin, float* thr, float* val
 
 // ---------------------------------------------------------------------------------------------
 // Eq. (4) weights and input validation
-__global__ void k_validate(const float* X, const float* y, const int32_t* llm, const int32_t* prof, int64_t n, int F,
-                           int n_llm, int n_prof, int* flag) {
+__global__ void k_validate(const float* X, const float* y, const int32_t* llm, const int32_t* prof, const float* w,
+                           int64_t n, int F, int n_llm, int n_prof, int* flag) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     bool bad = !isfinite(y[2 * i]) || !isfinite(y[2 * i + 1]);
+    if (w && !(isfinite(w[i]) && w[i] >= 0.0f)) bad = true;   // explicit weights: finite and >= 0
     for (int f = 0; f < F; ++f) bad |= !isfinite(X[i * F + f]);
     if (llm && (llm[i] < 0 || llm[i] >= n_llm)) bad = true;
     if (prof && (prof[i] < 0 || prof[i] >= n_prof)) bad = true;
@@ -1945,7 +1946,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   LLMP_REQUIRE(n >= 1 && n < (int64_t(1) << 30), "n_rows must be in [1, 2^30)");
   LLMP_REQUIRE(F >= 1 && F <= kMaxF, "n_features must be in [1, 32]");
   LLMP_REQUIRE(ds.users_col >= 0 && ds.users_col < F, "users_col out of range");
-  LLMP_REQUIRE(isfinite(L1) && isfinite(L2), "L1, L2 must be finite");
+  LLMP_REQUIRE(isfinite(L1) && isfinite(L2) && L1 > 0.f && L2 > 0.f, "L1, L2 must be positive and finite");
   const bool eq4 = hp.use_eq4_weights != 0;
   LLMP_REQUIRE(!eq4 || (ds.llm && ds.prof && ds.n_llm >= 1 && ds.n_prof >= 1),
                "Eq. (4) weights need llm_id/profile_id and n_llm, n_prof >= 1");
@@ -1965,11 +1966,13 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   DevBuf& d_flag = ctx->workspace("flag", sizeof(int));
   LLMP_CUDA(cudaMemsetAsync(d_flag.p, 0, sizeof(int), s));
   LLMP_LAUNCH(ctx, KC_VALIDATE, n, k_validate, grid_for(ctx, n, 256, 8), 256, 0, ds.X, ds.y, eq4 ? ds.llm : nullptr,
-              eq4 ? ds.prof : nullptr, n, F, ds.n_llm, ds.n_prof, d_flag.as<int>());
+              eq4 ? ds.prof : nullptr, eq4 ? nullptr : ds.w, n, F, ds.n_llm, ds.n_prof, d_flag.as<int>());
+  // sharded: every rank must take the same decision, or the others would block in the next collective
+  allreduce_max_u32(ctx, reinterpret_cast<uint32_t*>(d_flag.p), 1);
   int h_flag = 0;
   LLMP_CUDA(cudaMemcpyAsync(&h_flag, d_flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   LLMP_CUDA(cudaStreamSynchronize(s));
-  LLMP_REQUIRE(h_flag == 0, "dataset holds a non-finite X or y value or an id out of range");
+  LLMP_REQUIRE(h_flag == 0, "dataset holds a non-finite X or y value, a negative or non-finite weight or an id out of range (on some rank)");
 
   phase("validate");
   // ---- weights (Eq. 4) + de-interleaved targets
@@ -2132,21 +2135,15 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
 
   const int upd_grid = grid_for(ctx, n, UPD_THREADS, 8);
   const int base_grid = grid_for(ctx, n, BASE_THREADS, 8);
-  static bool attr_set = false;
-  if (!attr_set) {
-    LLMP_CUDA(cudaFuncSetAttribute(k_hist_root2, cudaFuncAttributeMaxDynamicSharedMemorySize, R2_SMEM));
-    LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_ROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
-    LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_LEVEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
-    LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
-    LLMP_CUDA(cudaFuncSetAttribute(k_hist2<HM_ROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, H2_SMEM));
-    LLMP_CUDA(cudaFuncSetAttribute(k_hist2<HM_LEVEL>, cudaFuncAttributeMaxDynamicSharedMemorySize, H2_SMEM));
-    attr_set = true;
-  }
+  ensure_smem_attr((const void*)k_hist_root2, R2_SMEM);
+  ensure_smem_attr((const void*)k_hist<HM_ROOT>, HIST_SMEM);
+  ensure_smem_attr((const void*)k_hist<HM_LEVEL>, HIST_SMEM);
+  ensure_smem_attr((const void*)k_hist2<HM_ROOT>, H2_SMEM);
+  ensure_smem_attr((const void*)k_hist2<HM_LEVEL>, H2_SMEM);
   // the fused update kernels' dynamic shared memory depends on the depth (the tree they route)
-  LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_UPDROOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 HIST_SMEM + updroot_tree_smem(D)));
+  ensure_smem_attr((const void*)k_hist<HM_UPDROOT>, HIST_SMEM + updroot_tree_smem(D));
   const Hist2Kernel k_upd2 = updroot2_kernel(D);
-  LLMP_CUDA(cudaFuncSetAttribute(k_upd2, cudaFuncAttributeMaxDynamicSharedMemorySize, H2_SMEM + updroot_tree_smem(D)));
+  ensure_smem_attr((const void*)k_upd2, H2_SMEM + updroot_tree_smem(D));
   const DbgArgs nodbg{};
 
   phase("state");
@@ -2400,12 +2397,8 @@ void debug_histogram(Ctx* ctx, const uint8_t* codes, int64_t n, const int32_t* i
   DevBuf& d_out = ctx->workspace("dbg_hist", (size_t)SLOT * 8);
   LLMP_CUDA(cudaMemsetAsync(d_out.p, 0, d_out.bytes, ctx->stream));
   DbgArgs dbg{idx, qg, qh, idx ? m : n, d_out.as<int64_t>()};
-  static bool attr_set = false;
-  if (!attr_set) {
-    LLMP_CUDA(cudaFuncSetAttribute(k_hist<HM_DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize, HIST_SMEM));
-    LLMP_CUDA(cudaFuncSetAttribute(k_hist2<HM_DEBUG>, cudaFuncAttributeMaxDynamicSharedMemorySize, H2_SMEM));
-    attr_set = true;
-  }
+  ensure_smem_attr((const void*)k_hist<HM_DEBUG>, HIST_SMEM);
+  ensure_smem_attr((const void*)k_hist2<HM_DEBUG>, H2_SMEM);
   FitPair fp;
   fp.t[0] = a;
   if (use_hist1())

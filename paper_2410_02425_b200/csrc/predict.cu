@@ -152,12 +152,8 @@ void upload_model_nodes(Ctx* ctx, ModelData& m) {
 
 template <int R, int DC>
 static void launch_predict_r(Ctx* ctx, const PredArgs& a, bool assemble, int cls) {
-  static bool attr = false;
-  if (!attr) {
-    LLMP_CUDA(cudaFuncSetAttribute(k_predict<false, R, DC>, cudaFuncAttributeMaxDynamicSharedMemorySize, pc_smem(R)));
-    LLMP_CUDA(cudaFuncSetAttribute(k_predict<true, R, DC>, cudaFuncAttributeMaxDynamicSharedMemorySize, pc_smem(R)));
-    attr = true;
-  }
+  ensure_smem_attr((const void*)k_predict<false, R, DC>, pc_smem(R));
+  ensure_smem_attr((const void*)k_predict<true, R, DC>, pc_smem(R));
   const int64_t rows = (int64_t)PC_THREADS * R;
   const int per_sm = std::max(1, (int)(220000 / (pc_smem(R) + 1024)));
   int grid = (int)std::min<int64_t>(std::max<int64_t>((a.n + rows - 1) / rows, 1), (int64_t)ctx->sms * per_sm);

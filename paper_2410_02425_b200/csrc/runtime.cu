@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <condition_variable>
+#include <map>
 #include <mutex>
 #include <stdexcept>
 #include <vector>
@@ -85,6 +86,22 @@ void Ctx::collect() {
   pending.clear();
 }
 
+// Max dynamic shared memory opt-in, per (device, kernel): cudaFuncSetAttribute applies to the
+// current device only, and contexts on several devices (or several host threads) may launch the same
+// kernel, so the record is keyed by device and guarded by a lock.  Only grows.
+void ensure_smem_attr(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> done;
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev), "cudaGetDevice", __FILE__, __LINE__);
+  std::lock_guard<std::mutex> lk(mu);
+  int& cur = done[std::make_pair(dev, func)];
+  if (cur >= bytes) return;
+  check_cuda(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes),
+             "cudaFuncSetAttribute(MaxDynamicSharedMemorySize)", __FILE__, __LINE__);
+  cur = bytes;
+}
+
 bool is_device_ptr(const void* p) {
   if (!p) return false;
   cudaPointerAttributes at;
@@ -123,7 +140,9 @@ struct NcclApi {
   ncclResult_t (*groupEnd)() = nullptr;
 };
 NcclApi g_nccl;
+std::mutex g_nccl_mu;
 void load_nccl() {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);   // contexts may be created from several host threads
   if (g_nccl.loaded) return;
   void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
   if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);

@@ -270,17 +270,22 @@ def test_sharded_path_with_a_one_rank_nccl_communicator(lp):
         ctx1.close()
 
 
-@pytest.mark.parametrize("nranks,n_llm", [(2, 200), (3, 131)])
-def test_multi_rank_sharded_fit_on_one_device(lp, nranks, n_llm):
+@pytest.mark.parametrize("nranks,n_llm,big", [(2, 200, False), (3, 131, False), (3, 16411, True)])
+def test_multi_rank_sharded_fit_on_one_device(lp, nranks, n_llm, big):
     """The N > 1 fit path on one B200: nranks contexts of an in-process communicator
     (llmpilot_ctx_create_local_group; NCCL refuses two ranks on one device), each fitting its
     contiguous LLM-block shard from its own thread — all-gathered global cut sample, all-reduced
     group maxima / base sums / gradient maxima / partial histograms, built children chosen by the
     split's hessian sums.  Every rank's model equals the oracle's unsharded fit bit for bit
-    (uneven shards with 3 ranks; n_global > 2^20 is covered by the strided-sample gloo test)."""
+    (uneven shards with 3 ranks).  The big case has n_global = 2,100,608 > 2^21 rows, so the
+    global cut sample is strided (s = ceil(n_global / 2^20) = 3, O2 / P:L209) and every rank
+    contributes the rows i = 0 (mod 3) of its own shard at their global indices."""
     import threading
     full = synth.make_scaled(n_llm)
     kw = dict(n_trees=8, max_depth=6, subsample=0.8, colsample_bytree=0.8, seed=5)
+    if big:
+        assert full.n > 2 ** 21
+        kw = dict(n_trees=2, max_depth=5, subsample=0.8, colsample_bytree=0.8, seed=7)
     om = oracle.fit(full.X, full.y, _o_hp(**kw), full.users_col, full.llm_id, full.prof_id, full.n_llm, full.n_prof,
                     L1, L2)
     ctxs = lp.local_group(0, nranks)
@@ -306,6 +311,41 @@ def test_multi_rank_sharded_fit_on_one_device(lp, nranks, n_llm):
     assert not errs, errs
     for r in range(nranks):
         _assert_same_model(om, res[r], "rank %d of %d" % (r, nranks))
+
+
+def test_concurrent_contexts_stress(lp):
+    """8 host threads, one context and stream each, fitting (CUDA-graph tree loop with its capture),
+    predicting and freeing concurrently on one device: every model is the oracle's bit for bit and
+    no call fails (shared per-device kernel attributes and workspace growth under concurrency)."""
+    import threading
+    d = synth.make("C2")
+    kw = dict(n_trees=10, max_depth=6)
+    om, otp = oracle.fit(d.X, d.y, _o_hp(**kw), d.users_col, d.llm_id, d.prof_id, d.n_llm, d.n_prof, L1, L2,
+                         return_train_pred=True)
+    errs, res = [], {}
+
+    def run(i):
+        try:
+            st = torch.cuda.Stream()
+            c = lp.Context(0, st)
+            for rep in range(3):
+                m = lp.fit(c, d.X, d.y, _g_hp(lp, **kw), d.users_col, d.llm_id, d.prof_id, d.n_llm, d.n_prof, L1, L2)
+                res[(i, rep)] = (m.export(), m.predict(c, d.X))
+                m.free()
+            c.close()
+        except Exception as e:   # noqa: BLE001
+            errs.append((i, repr(e)))
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(8)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not errs, errs
+    assert len(res) == 24
+    for k, (e, p) in res.items():
+        _assert_same_model(om, e, str(k))
+        assert _bits_equal(otp, p), k
 
 
 def test_fit_host_and_device_inputs_identical_and_deterministic(lp, ctx):
