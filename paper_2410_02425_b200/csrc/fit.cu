@@ -919,6 +919,8 @@ __global__ void __launch_bounds__(256) k_cmask(const uint8_t* codes, int64_t n, 
   }
 }
 
+#include "hist3.cuh"
+
 // the fused update kernel for a depth: compile-time routing depth for the configs' depths (6, 8)
 using Hist2Kernel = void (*)(const FitPair, const int, const int, const DbgArgs);
 static Hist2Kernel updroot2_kernel(int D) {
@@ -934,7 +936,12 @@ static int hist1_mask() {
   static const int v = 7 & ~(getenv("LLMP_HIST2") ? atoi(getenv("LLMP_HIST2")) : 5);
   return v;
 }
-static bool use_hist1() { return (hist1_mask() & 2) != 0; }   // the test hook follows the level kernel
+// level-histogram kernel: LLMP_LEVEL = 3 (default) change-row k_hist3; 1 run-length k_hist; 2 change-mask
+// k_hist2.  The test hook (llmpilot_debug_histogram) follows the same choice.
+static int level_kernel() {
+  static const int v = getenv("LLMP_LEVEL") ? atoi(getenv("LLMP_LEVEL")) : 3;
+  return (v == 1 || v == 2) ? v : 3;
+}
 
 // zero the root histogram slot when k_hist<ROOT> is going to (re)build it (see root_needed)
 __global__ void k_root_fix(const FitPair fp) {
@@ -2054,6 +2061,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
               d_cm.as<uint32_t>());
   const uint32_t* cmask = d_cm.as<uint32_t>();
   static const int hist1 = hist1_mask();
+  const int lvk = level_kernel();
   FitArgs A[2];
   for (int tg = 0; tg < 2; ++tg) {
     // per-target workspaces: the fused update pass leaves the next tree's root histogram and
@@ -2140,6 +2148,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   ensure_smem_attr((const void*)k_hist<HM_LEVEL>, HIST_SMEM);
   ensure_smem_attr((const void*)k_hist2<HM_ROOT>, H2_SMEM);
   ensure_smem_attr((const void*)k_hist2<HM_LEVEL>, H2_SMEM);
+  ensure_smem_attr((const void*)k_hist3<HM_LEVEL>, H3_SMEM);
   // the fused update kernels' dynamic shared memory depends on the depth (the tree they route)
   ensure_smem_attr((const void*)k_hist<HM_UPDROOT>, HIST_SMEM + updroot_tree_smem(D));
   const Hist2Kernel k_upd2 = updroot2_kernel(D);
@@ -2206,6 +2215,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     // histogram kernels: 2 CTAs per SM in total, but no more CTAs than 2048-row slices of the data
     // (small fits would otherwise launch hundreds of CTAs that only zero their shared histograms)
     const dim3 hg((unsigned)std::min<int64_t>(ctx->sms * 2 / ny, std::max<int64_t>(1, (n + 2047) / 2048)), ny);
+    // k_hist3: one CTA per SM
+    const dim3 hg3((unsigned)std::min<int64_t>(std::max(1, ctx->sms / ny), std::max<int64_t>(1, (n + 2047) / 2048)), ny);
     // fused: the previous round's update pass built this root already unless root_needed
     if (fused) {
       LLMP_LAUNCH_PDL(ctx, KC_MISC, 0, k_root_fix, dim3(1, ny), 1024, 0, fp);
@@ -2224,7 +2235,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       // persistent tile loop (upper bound of the level's tile count: one partial tile per parent)
       LLMP_LAUNCH_PDL(ctx, KC_PARTITION, ny * n, k_part, dim3(std::min(tiles_d, PT_CTAS_PER_SM / ny * ctx->sms), ny),
                   PT_THREADS, 0, fp, d);
-      if (hist1 & 2) LLMP_LAUNCH_PDL(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hg, HIST_THREADS, HIST_SMEM, fp, d, 0, nodbg);
+      if (lvk == 3) LLMP_LAUNCH_PDL(ctx, KC_HIST, 0, k_hist3<HM_LEVEL>, hg3, H3_THREADS, H3_SMEM, fp, d, nodbg);
+      else if (lvk == 1) LLMP_LAUNCH_PDL(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hg, HIST_THREADS, HIST_SMEM, fp, d, 0, nodbg);
       else LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist2<HM_LEVEL>, hg, H2_THREADS, H2_SMEM, fp, d, 0, nodbg);
       nccl_group_start(ctx);   // both targets' built-child histograms in one NCCL launch
       for (int q = 0; q < ny; ++q) allreduce_sum_i64(ctx, fp.t[q].H[d & 1], (size_t)SLOT << (d - 1));
@@ -2399,9 +2411,12 @@ void debug_histogram(Ctx* ctx, const uint8_t* codes, int64_t n, const int32_t* i
   DbgArgs dbg{idx, qg, qh, idx ? m : n, d_out.as<int64_t>()};
   ensure_smem_attr((const void*)k_hist<HM_DEBUG>, HIST_SMEM);
   ensure_smem_attr((const void*)k_hist2<HM_DEBUG>, H2_SMEM);
+  ensure_smem_attr((const void*)k_hist3<HM_DEBUG>, H3_SMEM);
   FitPair fp;
   fp.t[0] = a;
-  if (use_hist1())
+  if (level_kernel() == 3)
+    LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist3<HM_DEBUG>, ctx->sms, H3_THREADS, H3_SMEM, fp, 0, dbg);
+  else if (level_kernel() == 1)
     LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist<HM_DEBUG>, 2 * ctx->sms, HIST_THREADS, HIST_SMEM, fp, 0, 0, dbg);
   else
     LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist2<HM_DEBUG>, 2 * ctx->sms, H2_THREADS, H2_SMEM, fp, 0, 0, dbg);
