@@ -2215,8 +2215,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     // histogram kernels: 2 CTAs per SM in total, but no more CTAs than 2048-row slices of the data
     // (small fits would otherwise launch hundreds of CTAs that only zero their shared histograms)
     const dim3 hg((unsigned)std::min<int64_t>(ctx->sms * 2 / ny, std::max<int64_t>(1, (n + 2047) / 2048)), ny);
-    // k_hist3: one CTA per SM
-    const dim3 hg3((unsigned)std::min<int64_t>(std::max(1, ctx->sms / ny), std::max<int64_t>(1, (n + 2047) / 2048)), ny);
+    // k_hist3: one CTA per SM; one launch covers the built children of every ensemble in fp
+    const dim3 hg3((unsigned)std::min<int64_t>(ctx->sms, std::max<int64_t>(1, (n * ny + 2047) / 2048)));
     // fused: the previous round's update pass built this root already unless root_needed
     if (fused) {
       LLMP_LAUNCH_PDL(ctx, KC_MISC, 0, k_root_fix, dim3(1, ny), 1024, 0, fp);
@@ -2235,7 +2235,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       // persistent tile loop (upper bound of the level's tile count: one partial tile per parent)
       LLMP_LAUNCH_PDL(ctx, KC_PARTITION, ny * n, k_part, dim3(std::min(tiles_d, PT_CTAS_PER_SM / ny * ctx->sms), ny),
                   PT_THREADS, 0, fp, d);
-      if (lvk == 3) LLMP_LAUNCH_PDL(ctx, KC_HIST, 0, k_hist3<HM_LEVEL>, hg3, H3_THREADS, H3_SMEM, fp, d, nodbg);
+      if (lvk == 3) LLMP_LAUNCH_PDL(ctx, KC_HIST, 0, k_hist3<HM_LEVEL>, hg3, H3_THREADS, H3_SMEM, fp, ny, d, nodbg);
       else if (lvk == 1) LLMP_LAUNCH_PDL(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hg, HIST_THREADS, HIST_SMEM, fp, d, 0, nodbg);
       else LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist2<HM_LEVEL>, hg, H2_THREADS, H2_SMEM, fp, d, 0, nodbg);
       nccl_group_start(ctx);   // both targets' built-child histograms in one NCCL launch
@@ -2415,7 +2415,7 @@ void debug_histogram(Ctx* ctx, const uint8_t* codes, int64_t n, const int32_t* i
   FitPair fp;
   fp.t[0] = a;
   if (level_kernel() == 3)
-    LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist3<HM_DEBUG>, ctx->sms, H3_THREADS, H3_SMEM, fp, 0, dbg);
+    LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist3<HM_DEBUG>, ctx->sms, H3_THREADS, H3_SMEM, fp, 1, 0, dbg);
   else if (level_kernel() == 1)
     LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist<HM_DEBUG>, 2 * ctx->sms, HIST_THREADS, HIST_SMEM, fp, 0, 0, dbg);
   else

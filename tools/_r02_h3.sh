@@ -1,0 +1,6 @@
+set -x
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/h3_build.log 2>&1
+timeout 900 python -m pytest tests -q -m gpu -x -k "histogram_parity or fit_parity or sharded or cv_parity_c1 or variants" > gpurun_out/h3_pytest.log 2>&1; tail -3 gpurun_out/h3_pytest.log
+timeout 600 python bench.py --no-wg --no-cv --no-e2e --no-cpu-baseline > gpurun_out/h3_bench.json 2> gpurun_out/h3_bench.err; head -c 300 gpurun_out/h3_bench.json
+LLMP_LEVEL=1 timeout 600 python bench.py --no-wg --no-cv --no-e2e --no-cpu-baseline > gpurun_out/h1_bench.json 2> gpurun_out/h1_bench.err; head -c 300 gpurun_out/h1_bench.json

@@ -30,7 +30,7 @@ HIST_MODE = {"0": "hist_root", "1": "hist_level", "3": "update"}
 
 def kclass(name):
     base = name.split("(")[0].replace("void ", "").replace("llmp::", "").strip()
-    if base.startswith("k_hist<") or base.startswith("k_hist2<"):   # first template argument = the mode
+    if base.startswith("k_hist<") or base.startswith("k_hist2<") or base.startswith("k_hist3<"):   # first template argument = the mode
         return HIST_MODE.get(base.split("<")[1].split(",")[0].split(">")[0].strip(), base), base
     return CLASS.get(base, base), base
 
