@@ -47,7 +47,7 @@ llmpilot_status guarded(Fn&& fn) {
 
 const char* kClassNames[LLMP_N_KERNEL_CLASSES] = {
     "validate", "weights", "cuts", "codes", "base_score", "hist_root", "partition", "hist_level",
-    "split", "update", "predict", "recommend", "misc", "nccl", "wg", "unused15"};
+    "split", "update", "predict", "recommend", "misc", "nccl", "wg", "fit_small"};
 
 void set_device(llmp::Ctx* c) { LLMP_CUDA(cudaSetDevice(c->device)); }
 

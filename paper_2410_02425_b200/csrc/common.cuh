@@ -23,7 +23,7 @@ constexpr int kMaxGradBits = 14; // |q_g| <= 2^14 fits int16; q_h <= 2^14 fits u
 // kernel classes for instrumentation (llmpilot_kernel_class_name)
 enum KernelClass {
   KC_VALIDATE = 0, KC_WEIGHTS, KC_CUTS, KC_CODES, KC_BASE, KC_HIST_ROOT, KC_PARTITION, KC_HIST, KC_SPLIT,
-  KC_UPDATE, KC_PREDICT, KC_RECOMMEND, KC_MISC, KC_NCCL, KC_WG, KC_COUNT
+  KC_UPDATE, KC_PREDICT, KC_RECOMMEND, KC_MISC, KC_NCCL, KC_WG, KC_FIT_SMALL, KC_COUNT
 };
 
 // ---------------------------------------------------------------------------------------------

@@ -81,6 +81,125 @@ double wmape(const std::vector<float>& pred, const std::vector<int32_t>& rows, c
   }
   return den > 0.0 ? num / den : 0.0;
 }
+// ---------------------------------------------------------------------------------------------
+// Batched small fits (fit_small.cu): every fit of a CV stage in ONE launch, one thread block per
+// (fit, ensemble).  A fit is (training rows, held-out rows, hparams); its cuts (O2) come from its
+// own training rows, its codes are built with them for both row sets.
+struct BatchFit {
+  std::vector<int32_t> tr, te;   // row indices into the full dataset (ascending)
+  int hp;                        // index into the grid
+};
+
+SmallFitHp small_hp(const llmpilot_hparams& h, const DatasetDev& ds) {
+  SmallFitHp s{};
+  s.T = h.n_trees;
+  s.D = h.max_depth;
+  s.K = h.grad_bits;
+  s.F = ds.F;
+  s.users_col = ds.users_col;
+  s.monotone = h.monotone_users;
+  s.eta = (double)h.eta;
+  s.lambda = (double)h.lambda;
+  s.mcw = (double)h.min_child_weight;
+  s.subsample = h.subsample;
+  s.colsample = h.colsample_bytree;
+  s.seed = h.seed;
+  return s;
+}
+
+bool small_path_ok(const DatasetDev& ds, const llmpilot_hparams* grid, int n_grid) {
+  static const bool off = getenv("LLMP_CV_SMALL") && atoi(getenv("LLMP_CV_SMALL")) == 0;
+  if (off || ds.n > (int64_t)fit_small_max_rows()) return false;
+  for (int g = 0; g < n_grid; ++g)
+    if (grid[g].max_depth > 8) return false;
+  return true;
+}
+
+// predictions (m x 2 per fit, host) of every fit, in order
+void run_batch(Ctx* ctx, const DatasetDev& ds, const std::vector<float>& w_host, const llmpilot_hparams* grid,
+               const std::vector<BatchFit>& fits, std::vector<std::vector<float>>& preds) {
+  const int F = ds.F;
+  cudaStream_t s = ctx->stream;
+  std::vector<SmallFitHp> hps;
+  for (size_t g = 0; g < (size_t)(std::max_element(fits.begin(), fits.end(), [](const BatchFit& a, const BatchFit& b) {
+                                   return a.hp < b.hp; })->hp + 1); ++g)
+    hps.push_back(small_hp(grid[g], ds));
+  // arena: per fit codes (train + test), y, w, ncuts, predictions
+  std::vector<size_t> o_ctr(fits.size()), o_cte(fits.size()), o_y(fits.size()), o_w(fits.size()), o_nc(fits.size()),
+      o_pr(fits.size());
+  size_t tot = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = tot;
+    tot += (bytes + 255) & ~(size_t)255;
+    return o;
+  };
+  size_t max_rows = 1;
+  for (size_t i = 0; i < fits.size(); ++i) {
+    const size_t n = fits[i].tr.size(), m = fits[i].te.size();
+    o_ctr[i] = take(n * kMaxF);
+    o_cte[i] = take(std::max<size_t>(m, 1) * kMaxF);
+    o_y[i] = take(n * 8);
+    o_w[i] = take(n * 4);
+    o_nc[i] = take(kMaxF * 4);
+    o_pr[i] = take(std::max<size_t>(m, 1) * 8);
+    max_rows = std::max(max_rows, n + m);
+  }
+  DevBuf& arena = ctx->workspace("cvb_arena", tot);
+  uint8_t* A = arena.as<uint8_t>();
+  DevBuf& d_idx = ctx->workspace("cvb_idx", max_rows * 4);
+  DevBuf& d_X = ctx->workspace("cvb_X", max_rows * F * 4);
+  DevBuf& d_y = ctx->workspace("cvb_y", max_rows * 8);
+  DevBuf& d_l = ctx->workspace("cvb_l", max_rows * 4);
+  DevBuf& d_p = ctx->workspace("cvb_p", max_rows * 4);
+  std::vector<float> wsub;
+  std::vector<int32_t> idx;
+  std::vector<SmallFitItem> items;
+  for (size_t i = 0; i < fits.size(); ++i) {
+    const BatchFit& bf = fits[i];
+    const int64_t n = (int64_t)bf.tr.size(), m = (int64_t)bf.te.size();
+    idx.assign(bf.tr.begin(), bf.tr.end());
+    idx.insert(idx.end(), bf.te.begin(), bf.te.end());
+    LLMP_CUDA(cudaMemcpyAsync(d_idx.p, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice, s));
+    const int grid_g = (int)std::min<int64_t>((n + m + 255) / 256, (int64_t)ctx->sms * 4);
+    LLMP_LAUNCH(ctx, KC_MISC, n + m, k_gather_rows, grid_g, 256, 0, d_idx.as<int32_t>(), n + m, F, ds.X, ds.y, ds.llm,
+                ds.prof, d_X.as<float>(), d_y.as<float>(), d_l.as<int32_t>(), d_p.as<int32_t>());
+    LLMP_CUDA(cudaMemcpyAsync(A + o_y[i], d_y.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, s));
+    wsub.resize(n);
+    // Eq. (4) weights are per (LLM, profile) group, so a subset's weights are the full set's (O1);
+    // use_eq4_weights = 0: w = 1 (a CV subset carries no explicit weights)
+    const bool eq4 = grid[bf.hp].use_eq4_weights != 0;
+    for (int64_t k = 0; k < n; ++k) wsub[k] = eq4 ? w_host[bf.tr[k]] : 1.0f;
+    LLMP_CUDA(cudaMemcpyAsync(A + o_w[i], wsub.data(), (size_t)n * 4, cudaMemcpyHostToDevice, s));
+    CutsData cuts;
+    compute_cuts(ctx, d_X.as<float>(), n, F, 0, n, grid[bf.hp].max_bin, cuts, false);   // O2 on the fit's rows
+    compute_codes(ctx, d_X.as<float>(), n, F, cuts, A + o_ctr[i], nullptr, 0, nullptr);
+    if (m > 0) compute_codes(ctx, d_X.as<float>() + (size_t)n * F, m, F, cuts, A + o_cte[i], nullptr, 0, nullptr);
+    LLMP_CUDA(cudaMemcpyAsync(A + o_nc[i], cuts.d_ncuts.p, kMaxF * 4, cudaMemcpyDeviceToDevice, s));
+    LLMP_CUDA(cudaStreamSynchronize(s));   // wsub / cuts are reused by the next fit
+    for (int tg = 0; tg < 2; ++tg) {
+      SmallFitItem itm{};
+      itm.n = (int)n;
+      itm.m_test = (int)m;
+      itm.target = tg;
+      itm.hp = bf.hp;
+      itm.codes = A + o_ctr[i];
+      itm.codes_test = A + o_cte[i];
+      itm.y = reinterpret_cast<const float*>(A + o_y[i]);
+      itm.w = reinterpret_cast<const float*>(A + o_w[i]);
+      itm.ncuts = reinterpret_cast<const int32_t*>(A + o_nc[i]);
+      itm.pred_test = reinterpret_cast<float*>(A + o_pr[i]);
+      items.push_back(itm);
+    }
+  }
+  fit_small_run(ctx, items, hps);
+  preds.assign(fits.size(), {});
+  for (size_t i = 0; i < fits.size(); ++i) {
+    preds[i].resize(fits[i].te.size() * 2);
+    if (!fits[i].te.empty())
+      LLMP_CUDA(cudaMemcpyAsync(preds[i].data(), A + o_pr[i], preds[i].size() * 4, cudaMemcpyDeviceToHost, s));
+  }
+  LLMP_CUDA(cudaStreamSynchronize(s));
+}
 }  // namespace
 
 void cv_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams* grid, int n_grid, float L1, float L2, int64_t U,
@@ -123,41 +242,109 @@ void cv_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams* grid, int n
   Subset tr, te, trV, teV;
   DevBuf pred_dev;
   std::vector<float> pred;
+  // batched path (all fits of a stage in one launch, fit_small.cu) for small datasets
+  const bool batched = small_path_ok(ds, grid, n_grid);
+  std::vector<int> llms;
+  for (int M = 0; M < ds.n_llm; ++M)
+    if (present[M]) llms.push_back(M);
+  std::vector<std::vector<int32_t>> rows_of(ds.n_llm);
+  for (int64_t i = 0; i < n; ++i) rows_of[llm[i]].push_back((int32_t)i);
+  std::vector<int> best_of(ds.n_llm, 0);
+  std::vector<std::vector<float>> outer_pred;
+  if (batched) {
+    if (n_grid > 1) {   // inner stage: (M, V, hp) for every ordered pair of distinct LLMs
+      std::vector<BatchFit> inner;
+      for (int M : llms)
+        for (int V : llms) {
+          if (V == M) continue;
+          BatchFit bf;
+          for (int64_t i = 0; i < n; ++i)
+            if (llm[i] != M && llm[i] != V) bf.tr.push_back((int32_t)i);
+          if (bf.tr.empty()) continue;
+          bf.te = rows_of[V];
+          for (int h = 0; h < n_grid; ++h) {
+            bf.hp = h;
+            inner.push_back(bf);
+          }
+        }
+      std::vector<std::vector<float>> ip;
+      run_batch(ctx, ds, w, grid, inner, ip);
+      // err(hp) = mean over V of (wMAPE_1 + wMAPE_2)/2, V ascending (O12), first minimum wins
+      size_t q = 0;
+      for (int M : llms) {
+        std::vector<double> err_sum(n_grid, 0.0);
+        std::vector<int> nv(n_grid, 0);
+        for (int V : llms) {
+          if (V == M) continue;
+          if (q >= inner.size() || inner[q].te != rows_of[V]) continue;   // V skipped (no training rows)
+          for (int h = 0; h < n_grid; ++h, ++q) {
+            err_sum[h] += 0.5 * (wmape(ip[q], rows_of[V], y, w, 0) + wmape(ip[q], rows_of[V], y, w, 1));
+            ++nv[h];
+          }
+        }
+        double best_err = INFINITY;
+        for (int h = 0; h < n_grid; ++h) {
+          const double err = nv[h] > 0 ? err_sum[h] / nv[h] : 0.0;
+          if (err < best_err) {
+            best_err = err;
+            best_of[M] = h;
+          }
+        }
+      }
+    }
+    std::vector<BatchFit> outer;
+    for (int M : llms) {
+      BatchFit bf;
+      for (int64_t i = 0; i < n; ++i)
+        if (llm[i] != M) bf.tr.push_back((int32_t)i);
+      LLMP_REQUIRE(!bf.tr.empty(), "leave-one-LLM-out needs at least two LLMs");
+      bf.te = rows_of[M];
+      bf.hp = best_of[M];
+      outer.push_back(bf);
+    }
+    run_batch(ctx, ds, w, grid, outer, outer_pred);
+  }
+  size_t mi = 0;
   for (int M = 0; M < ds.n_llm; ++M) {
     if (!present[M]) continue;
     std::vector<int32_t> rows_tr, rows_M;
     for (int64_t i = 0; i < n; ++i) (llm[i] == M ? rows_M : rows_tr).push_back((int32_t)i);
     LLMP_REQUIRE(!rows_tr.empty(), "leave-one-LLM-out needs at least two LLMs");
     int best_hp = 0;
-    if (n_grid > 1) {
-      double best_err = INFINITY;
-      for (int h = 0; h < n_grid; ++h) {
-        double err_sum = 0.0;
-        int nv = 0;
-        for (int V = 0; V < ds.n_llm; ++V) {
-          if (!present[V] || V == M) continue;
-          std::vector<int32_t> r_tr, r_v;
-          for (int64_t i = 0; i < n; ++i) {
-            if (llm[i] == V) r_v.push_back((int32_t)i);
-            else if (llm[i] != M) r_tr.push_back((int32_t)i);
+    if (batched) {
+      best_hp = best_of[M];
+      pred = outer_pred[mi++];
+    } else {
+      if (n_grid > 1) {
+        double best_err = INFINITY;
+        for (int h = 0; h < n_grid; ++h) {
+          double err_sum = 0.0;
+          int nv = 0;
+          for (int V = 0; V < ds.n_llm; ++V) {
+            if (!present[V] || V == M) continue;
+            std::vector<int32_t> r_tr, r_v;
+            for (int64_t i = 0; i < n; ++i) {
+              if (llm[i] == V) r_v.push_back((int32_t)i);
+              else if (llm[i] != M) r_tr.push_back((int32_t)i);
+            }
+            if (r_tr.empty()) continue;
+            make_subset(ctx, ds, r_tr, trV);
+            make_subset(ctx, ds, r_v, teV);
+            fit_predict(ctx, trV, teV, grid[h], L1, L2, pred, pred_dev);
+            err_sum += 0.5 * (wmape(pred, r_v, y, w, 0) + wmape(pred, r_v, y, w, 1));
+            ++nv;
           }
-          if (r_tr.empty()) continue;
-          make_subset(ctx, ds, r_tr, trV);
-          make_subset(ctx, ds, r_v, teV);
-          fit_predict(ctx, trV, teV, grid[h], L1, L2, pred, pred_dev);
-          err_sum += 0.5 * (wmape(pred, r_v, y, w, 0) + wmape(pred, r_v, y, w, 1));
-          ++nv;
-        }
-        const double err = nv > 0 ? err_sum / nv : 0.0;
-        if (err < best_err) {
-          best_err = err;
-          best_hp = h;
+          const double err = nv > 0 ? err_sum / nv : 0.0;
+          if (err < best_err) {
+            best_err = err;
+            best_hp = h;
+          }
         }
       }
+      make_subset(ctx, ds, rows_tr, tr);
+      make_subset(ctx, ds, rows_M, te);
+      fit_predict(ctx, tr, te, grid[best_hp], L1, L2, pred, pred_dev);
     }
-    make_subset(ctx, ds, rows_tr, tr);
-    make_subset(ctx, ds, rows_M, te);
-    fit_predict(ctx, tr, te, grid[best_hp], L1, L2, pred, pred_dev);
     // M's measured grid: profiles present x user levels (regular grid required)
     std::vector<int32_t> levels;
     for (int32_t i : rows_M) levels.push_back((int32_t)X[(size_t)i * F + ds.users_col]);

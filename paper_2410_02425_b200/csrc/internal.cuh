@@ -88,6 +88,28 @@ void recommend_impl(Ctx* ctx, const ModelData& m, const float* llm_feats, int n_
                     const int32_t* levels, int n_levels, float L1, float L2, int64_t U, RecOut& out,
                     float* pred_out_dev);
 
+// fit_small.cu: one thread block per (fit, ensemble) for n <= fit_small_max_rows() rows (the CV's
+// fits).  Each item fits one ensemble on its rows (codes with the fit's own cuts) and writes the
+// predictions of its held-out rows (column `target` of pred_test, n_test x 2).
+struct SmallFitHp {
+  int T, D, K, F, users_col, monotone;
+  double eta, lambda, mcw;
+  float subsample, colsample;
+  uint64_t seed;
+};
+struct SmallFitItem {
+  int n, m_test, target, hp;
+  int n_cap;                    // set by fit_small_run (shared-memory stride)
+  const uint8_t* codes;         // n x 32, row-major (the fit's cuts)
+  const uint8_t* codes_test;    // m_test x 32 (the same cuts)
+  const float* y;               // n x 2
+  const float* w;               // n (Eq. 4 or explicit weights)
+  const int32_t* ncuts;         // [32] cuts per feature of the fit
+  float* pred_test;             // m_test x 2
+};
+int fit_small_max_rows();
+void fit_small_run(Ctx* ctx, const std::vector<SmallFitItem>& items, const std::vector<SmallFitHp>& hps);
+
 // cv.cu
 struct CvFold {
   int llm, hp_index;
