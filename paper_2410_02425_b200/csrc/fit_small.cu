@@ -79,6 +79,10 @@ __global__ void __launch_bounds__(SF_THREADS, 1) k_fit_small(const SmallFitItem*
   const int hist_bytes = smem_bytes - (int)(s_hist - smem);
 
   __shared__ int s_off[kMaxF + 1];          // compact cell offset of feature f (C = s_off[F])
+  __shared__ int8_t s_pkw[kMaxF];           // split-evaluation feature packs (see below)
+  __shared__ int8_t s_pkf[kMaxF][4];
+  __shared__ int s_npk;
+  __shared__ uint32_t s_inpk;
   __shared__ int s_nc[kMaxF];
   __shared__ int8_t s_tf[SF_MAX_NN];        // tree being grown: feature (-1 leaf, -2 absent)
   __shared__ uint8_t s_tb[SF_MAX_NN];
@@ -105,6 +109,31 @@ __global__ void __launch_bounds__(SF_THREADS, 1) k_fit_small(const SmallFitItem*
       o += (f < F) ? s_nc[f] + 1 : 0;
     }
     s_off[kMaxF] = o;
+    // feature packs for the split evaluation: features with <= 8 / <= 16 / <= 32 bins share a warp
+    // four / two / one at a time (width = lanes per feature); > 32 bins: a warp of 8 bins per lane
+    // (width 64 marks it); features with one bin have no threshold and are left out, except feature
+    // 0, whose pass also yields the node totals
+    int np_ = 0;
+    uint32_t inpk = 0;
+    for (int wdt = 8; wdt <= 64; wdt <<= 1) {
+      const int per = wdt >= 32 ? 1 : 32 / wdt;
+      int fill = per;
+      for (int f = 0; f < F; ++f) {
+        const int nb = s_nc[f] + 1;
+        const int want = nb > 32 ? 64 : nb > 16 ? 32 : nb > 8 ? 16 : 8;
+        if (want != wdt || (nb == 1 && f != 0)) continue;
+        if (fill == per) {
+          s_pkw[np_] = (int8_t)wdt;
+          for (int q = 0; q < 4; ++q) s_pkf[np_][q] = -1;
+          ++np_;
+          fill = 0;
+        }
+        s_pkf[np_ - 1][fill++] = (int8_t)f;
+        inpk |= 1u << f;
+      }
+    }
+    s_npk = np_;
+    s_inpk = inpk;
   }
   __syncthreads();
   const int C = s_off[kMaxF];
@@ -337,92 +366,152 @@ __global__ void __launch_bounds__(SF_THREADS, 1) k_fit_small(const SmallFitItem*
           asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a + (uint32_t)C * 4u), "r"(acc_h) : "memory");
         }
         __syncthreads();
-        // ---- O6 per (node, feature): one warp each; lane l owns bins 8l .. 8l+7
-        for (int task = warp; task < np * F; task += SF_WARPS) {
-          const int sl = task / F, f = task % F;
+        // ---- O6 per (node, feature pack): one warp evaluates up to four features of one node, lane
+        // = bin within a segment of 8, 16 or 32 lanes (segmented scans and argmax); features with
+        // more than 32 bins get a warp each, lane l owning bins 8l .. 8l+7.  A node's sums fit 32
+        // bits (|sum q| <= n 2^K <= 2^27), so prefix sums are 32-bit.
+        for (int task = warp; task < np * s_npk; task += SF_WARPS) {
+          const int sl = task / s_npk, pk = task % s_npk;
+          const int W = s_pkw[pk];
+          const bool wide = W > 32;
+          const int Wl = wide ? 32 : W;
+          const int seg = lane / Wl, bl_ = lane % Wl;
+          const int f = s_pkf[pk][seg];
+          const int nb = f >= 0 ? s_nc[f] + 1 : 0;
+          const int nthr = nb - 1;
+          const bool fin = f >= 0 && ((s_colmask >> f) & 1u);
           const int k = s_list[j0 + sl];
-          const int nb = s_nc[f] + 1;
-          const int32_t* Gs = reinterpret_cast<const int32_t*>(hg) + (size_t)sl * 2 * C + s_off[f];
-          const uint32_t* Hs = hg + (size_t)sl * 2 * C + C + s_off[f];
-          int64_t g8[8], h8[8];
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int bq = lane * 8 + q;
-            g8[q] = bq < nb ? (int64_t)Gs[bq] : 0;
-            h8[q] = bq < nb ? (int64_t)Hs[bq] : 0;
-          }
-#pragma unroll
-          for (int q = 1; q < 8; ++q) {
-            g8[q] += g8[q - 1];
-            h8[q] += h8[q - 1];
-          }
-          int64_t ig = g8[7], ih = h8[7];
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int64_t ug = __shfl_up_sync(0xffffffffu, ig, o), uh = __shfl_up_sync(0xffffffffu, ih, o);
-            if (lane >= o) {
-              ig += ug;
-              ih += uh;
-            }
-          }
-          const int64_t bgp = ig - g8[7], bhp = ih - h8[7];
-          const int64_t Gq = __shfl_sync(0xffffffffu, ig, 31), Hq = __shfl_sync(0xffffffffu, ih, 31);
-          const bool fin = (s_colmask >> f) & 1u;
+          const int32_t* Gs = reinterpret_cast<const int32_t*>(hg) + (size_t)sl * 2 * C + (f >= 0 ? s_off[f] : 0);
+          const uint32_t* Hs = hg + (size_t)sl * 2 * C + C + (f >= 0 ? s_off[f] : 0);
           const double lo = s_lo[par][k], hi = s_hi[par][k];
           double bl = -INFINITY;
           int bb = 0x7fffffff;
-          int64_t bGL = 0, bHL = 0;
-          const int nthr = nb - 1;
-          if (fin && lane * 8 < nthr) {
-            const double G = dequant(Gq, sgi), H = dequant(Hq, shi);
-            const double gainP = calc_gain(G, H, calc_weight(G, H, lo, hi, hp.lambda, hp.mcw), hp.lambda);
+          int32_t Gq, wGL;
+          uint32_t Hq, wHL;
+          // one threshold's loss (O6), or -inf when the candidate is invalid
+          auto cand = [&](int32_t GLq, uint32_t HLq, double gainP) -> double {
+            const double GL = dequant(GLq, sgi), HL = dequant(HLq, shi);
+            const double GR = dequant(Gq - GLq, sgi), HR = dequant(Hq - HLq, shi);
+            if (!(HL >= hp.mcw && HR >= hp.mcw)) return -INFINITY;
+            const double wl = calc_weight(GL, HL, lo, hi, hp.lambda, hp.mcw);
+            const double wr = calc_weight(GR, HR, lo, hi, hp.lambda, hp.mcw);
+            if (hp.monotone && f == hp.users_col && wl > wr) return -INFINITY;
+            return __dsub_rn(__dadd_rn(calc_gain(GL, HL, wl, hp.lambda), calc_gain(GR, HR, wr, hp.lambda)), gainP);
+          };
+          if (!wide) {   // lane = bin of its segment's feature
+            int32_t ig = (bl_ < nb) ? Gs[bl_] : 0;
+            uint32_t ih = (bl_ < nb) ? Hs[bl_] : 0u;
+            for (int o = 1; o < Wl; o <<= 1) {
+              const int32_t ug = __shfl_up_sync(0xffffffffu, ig, o, Wl);
+              const uint32_t uh = __shfl_up_sync(0xffffffffu, ih, o, Wl);
+              if (bl_ >= o) {
+                ig += ug;
+                ih += uh;
+              }
+            }
+            Gq = __shfl_sync(0xffffffffu, ig, Wl - 1, Wl);
+            Hq = __shfl_sync(0xffffffffu, ih, Wl - 1, Wl);
+            // a feature with at most one non-empty bin has every candidate's loss exactly 0
+            const int32_t pg = __shfl_up_sync(0xffffffffu, ig, 1, Wl);
+            const uint32_t ph = __shfl_up_sync(0xffffffffu, ih, 1, Wl);
+            const unsigned ne = __ballot_sync(0xffffffffu, bl_ < nb && (ig != (bl_ ? pg : 0) || ih != (bl_ ? ph : 0u)));
+            const unsigned segm = (Wl == 32 ? 0xffffffffu : ((1u << Wl) - 1u)) << (seg * Wl);
+            if (fin && bl_ < nthr && __popc(ne & segm) > 1) {
+              const double G = dequant(Gq, sgi), H = dequant(Hq, shi);
+              const double gainP = calc_gain(G, H, calc_weight(G, H, lo, hi, hp.lambda, hp.mcw), hp.lambda);
+              bl = cand(ig, ih, gainP);
+              if (bl > -INFINITY) bb = bl_;
+            }
+            for (int o = Wl >> 1; o > 0; o >>= 1) {
+              const double ol = __shfl_down_sync(0xffffffffu, bl, o, Wl);
+              const int ob = __shfl_down_sync(0xffffffffu, bb, o, Wl);
+              if (ol > bl || (ol == bl && ob < bb)) {
+                bl = ol;
+                bb = ob;
+              }
+            }
+            bb = __shfl_sync(0xffffffffu, bb, 0, Wl);
+            bl = __shfl_sync(0xffffffffu, bl, 0, Wl);
+            const int own = bb == 0x7fffffff ? 0 : bb;
+            wGL = __shfl_sync(0xffffffffu, ig, own, Wl);
+            wHL = __shfl_sync(0xffffffffu, ih, own, Wl);
+          } else {          // one feature, lane l owns bins 8l .. 8l+7
+            int32_t gl[8];
+            uint32_t hl[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              const int b = lane * 8 + q;
-              if (b < nthr) {
-                const int64_t GLq = bgp + g8[q], HLq = bhp + h8[q];
-                const double GL = dequant(GLq, sgi), HL = dequant(HLq, shi);
-                const double GR = dequant(Gq - GLq, sgi), HR = dequant(Hq - HLq, shi);
-                if (HL >= hp.mcw && HR >= hp.mcw) {
-                  const double wl = calc_weight(GL, HL, lo, hi, hp.lambda, hp.mcw);
-                  const double wr = calc_weight(GR, HR, lo, hi, hp.lambda, hp.mcw);
-                  if (!(hp.monotone && f == hp.users_col && wl > wr)) {
-                    const double loss = __dsub_rn(
-                        __dadd_rn(calc_gain(GL, HL, wl, hp.lambda), calc_gain(GR, HR, wr, hp.lambda)), gainP);
-                    if (loss > bl) {   // b ascending within the lane: strict keeps the smaller b
-                      bl = loss;
-                      bb = b;
-                      bGL = GLq;
-                      bHL = HLq;
-                    }
+              const int bq = lane * 8 + q;
+              gl[q] = bq < nb ? Gs[bq] : 0;
+              hl[q] = bq < nb ? Hs[bq] : 0u;
+            }
+#pragma unroll
+            for (int q = 1; q < 8; ++q) {
+              gl[q] += gl[q - 1];
+              hl[q] += hl[q - 1];
+            }
+            int32_t ig = gl[7];
+            uint32_t ih = hl[7];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int32_t ug = __shfl_up_sync(0xffffffffu, ig, o);
+              const uint32_t uh = __shfl_up_sync(0xffffffffu, ih, o);
+              if (lane >= o) {
+                ig += ug;
+                ih += uh;
+              }
+            }
+            const int32_t bgp = ig - gl[7];
+            const uint32_t bhp = ih - hl[7];
+            Gq = __shfl_sync(0xffffffffu, ig, 31);
+            Hq = __shfl_sync(0xffffffffu, ih, 31);
+            int32_t myg = 0;
+            uint32_t myh = 0;
+            if (fin && lane * 8 < nthr) {
+              const double G = dequant(Gq, sgi), H = dequant(Hq, shi);
+              const double gainP = calc_gain(G, H, calc_weight(G, H, lo, hi, hp.lambda, hp.mcw), hp.lambda);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const int b = lane * 8 + q;
+                if (b < nthr) {
+                  const double loss = cand(bgp + gl[q], bhp + hl[q], gainP);
+                  if (loss > bl) {   // b ascending within the lane: strict keeps the smaller b
+                    bl = loss;
+                    bb = b;
+                    myg = bgp + gl[q];
+                    myh = bhp + hl[q];
                   }
                 }
               }
             }
-          }
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const double ol = __shfl_down_sync(0xffffffffu, bl, o);
-            const int ob = __shfl_down_sync(0xffffffffu, bb, o);
-            const int64_t oG = __shfl_down_sync(0xffffffffu, bGL, o), oH = __shfl_down_sync(0xffffffffu, bHL, o);
-            if (ol > bl || (ol == bl && ob < bb)) {
-              bl = ol;
-              bb = ob;
-              bGL = oG;
-              bHL = oH;
+            for (int o = 16; o > 0; o >>= 1) {
+              const double ol = __shfl_down_sync(0xffffffffu, bl, o);
+              const int ob = __shfl_down_sync(0xffffffffu, bb, o);
+              const int32_t og = __shfl_down_sync(0xffffffffu, myg, o);
+              const uint32_t oh = __shfl_down_sync(0xffffffffu, myh, o);
+              if (ol > bl || (ol == bl && ob < bb)) {
+                bl = ol;
+                bb = ob;
+                myg = og;
+                myh = oh;
+              }
             }
+            bb = __shfl_sync(0xffffffffu, bb, 0);
+            bl = __shfl_sync(0xffffffffu, bl, 0);
+            wGL = __shfl_sync(0xffffffffu, myg, 0);
+            wHL = __shfl_sync(0xffffffffu, myh, 0);
           }
-          if (lane == 0) {
+          if (bl_ == 0 && f >= 0 && (!wide || lane == 0)) {
             SFRes r;
             r.loss = bl;
             r.b = bb;
             r.valid = bl > -INFINITY ? 1 : 0;
-            r.GLq = bGL;
-            r.HLq = bHL;
+            r.GLq = wGL;
+            r.HLq = (int64_t)wHL;
             res[sl * kMaxF + f] = r;
             if (f == 0) {   // node totals (every feature's bins sum to them)
               s_tot[sl][0] = Gq;
-              s_tot[sl][1] = Hq;
+              s_tot[sl][1] = (long long)Hq;
             }
           }
         }
@@ -432,7 +521,7 @@ __global__ void __launch_bounds__(SF_THREADS, 1) k_fit_small(const SmallFitItem*
           const int k = s_list[j0 + sl];
           double ml = -INFINITY;
           int mf = lane, mb = 0x7fffffff;
-          if (lane < F) {
+          if (lane < F && ((s_inpk >> lane) & 1u)) {
             const SFRes r = res[sl * kMaxF + lane];
             if (r.valid) {
               ml = r.loss;

@@ -449,6 +449,38 @@ def test_cv_hand_fixture_on_gpu(lp, ctx, golden):
     assert gS == g["S_num"] / g["S_den"] and gO == g["O"] and gSO == pytest.approx(g["SO"], rel=1e-15)
 
 
+@pytest.mark.parametrize("batched", [True, False])
+def test_cv_grid5_parity_c1(lp, batched):
+    """A 5-point grid of the HPs P:L207-209 names (trees, depth, learning rate, subsampling ratio,
+    bins; plus column sampling and min child weight) through the nested leave-one-LLM-out CV, on the
+    batched small-fit path (one thread block per fit) and on the sequential path (LLMP_CV_SMALL=0,
+    one full fit per call): folds, chosen HPs, S, O, SO equal the oracle's."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import os, sys
+sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
+import torch, oracle, synth, paper_2410_02425_b200 as lp
+d = synth.make("C1")
+gk = [dict(n_trees=12, max_depth=3, eta=0.3), dict(n_trees=8, max_depth=5, eta=0.5, max_bin=4),
+      dict(n_trees=15, max_depth=4, eta=0.2, subsample=0.7, seed=3), dict(n_trees=10, max_depth=2, eta=0.6, colsample_bytree=0.5, seed=9),
+      dict(n_trees=10, max_depth=4, eta=0.3, min_child_weight=4.0, lambda_=2.0)]
+of = oracle.cv(d.X, d.y, d.llm_id, d.prof_id, d.users_col, d.n_llm, d.n_prof, [oracle.hparams(**k) for k in gk], 100.0, 50.0, 200, d.cost)
+ctx = lp.Context(0, torch.cuda.current_stream())
+gf = lp.cv(ctx, d.X, d.y, d.llm_id, d.prof_id, d.users_col, d.n_llm, d.n_prof, [lp.hparams(**k) for k in gk], 100.0, 50.0, 200, d.cost)
+assert of == gf, (of, gf)
+assert len({f["hp_index"] for f in of[0]}) >= 1
+print("OK", sorted({f["hp_index"] for f in of[0]}))
+'''
+    env = dict(os.environ)
+    if not batched:
+        env["LLMP_CV_SMALL"] = "0"
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0 and "OK" in p.stdout, (p.stdout[-2000:], p.stderr[-3000:])
+
+
 def test_cv_parity_c2_short(lp, ctx):
     d = synth.make("C2")
     of, oS, oO, oSO = oracle.cv(d.X, d.y, d.llm_id, d.prof_id, d.users_col, d.n_llm, d.n_prof,
