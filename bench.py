@@ -71,7 +71,13 @@ def parse():
     ap.add_argument("--sweep-llms", type=int, default=SWEEP_LLMS_PER_GPU)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-wg", action="store_true", help="skip the workload-generator leg")
-    ap.add_argument("--no-cv", action="store_true", help="skip the paper-shaped C2 cross-validation leg")
+    ap.add_argument("--no-cv", action="store_true", help="skip the paper-shaped C2 cross-validation legs")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 recommendation-sweep leg")
+    ap.add_argument("--strong", action="store_true",
+                    help="BASELINE configs[3]: 100M rows (781,250 LLMs) in total, row-sharded over the N ranks "
+                         "(strong scaling) instead of 10M rows per GPU")
+    ap.add_argument("--strong-llms", type=int, default=781250)
+    ap.add_argument("--grid-trees", type=int, default=1000, help="trees of the cv_c2_grid leg's points")
     ap.add_argument("--wg-rows", type=int, default=17_300_000, help="trace rows of the workload-generator leg")
     ap.add_argument("--wg-samples", type=int, default=4_000_000, help="requests drawn per sampling step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -159,6 +165,90 @@ def bench_cv_c2(lp, ctx, args):
                                "row_iters_per_s": 2.0 * 1000 * int(keep.sum()) / (t1 - t0),
                                "sample": "the oracle's fit of the first fold (1000 trees x 2 targets)"}
     return res
+
+
+def bench_cv_c2_grid(lp, ctx, args):
+    """Nested leave-one-LLM-out CV with an HP grid on C2 (trees, depth, learning rate,
+    subsampling; 4 points): 30 x 29 x 4 inner fits (wMAPE per point) + 30 refits + recommendations.
+    Every fit of a stage runs in one launch (one thread block per fit and ensemble, fit_small.cu)."""
+    import synth
+    d = synth.make("C2")
+    T = args.grid_trees
+    gk = [dict(n_trees=T, max_depth=6, eta=0.3), dict(n_trees=T, max_depth=4, eta=0.3),
+          dict(n_trees=T, max_depth=6, eta=0.1), dict(n_trees=T, max_depth=6, eta=0.3, subsample=0.8)]
+    grid = [lp.hparams(**k) for k in gk]
+    t0 = time.perf_counter()
+    folds, S, O, SO = lp.cv(ctx, d.X, d.y, d.llm_id, d.prof_id, d.users_col, d.n_llm, d.n_prof, grid, L1, L2, U,
+                            d.cost)
+    dt = time.perf_counter() - t0
+    n_llm = len(folds)
+    inner = n_llm * (n_llm - 1) * len(grid)
+    fits = inner + n_llm
+    rows = sum(int((d.llm_id != f["llm"]).sum()) for f in folds)   # outer fits' rows
+    inner_rows = sum(int(((d.llm_id != f["llm"]) & (d.llm_id != g["llm"])).sum()) for f in folds for g in folds
+                     if g["llm"] != f["llm"]) * len(grid)
+    return {"workload": "C2 nested leave-one-LLM-out CV, grid of %d (trees %d; depth 6/4; eta 0.3/0.1; subsample 1/0.8),"
+                        " %d inner + %d outer fits x 2 targets" % (len(grid), T, inner, n_llm),
+            "seconds": dt, "fits": fits, "fits_per_s": fits / dt,
+            "row_iters_per_s": 2.0 * T * (rows + inner_rows) / dt,
+            "hp_chosen": sorted({f["hp_index"] for f in folds}), "S": S, "O": O, "SO": SO}
+
+
+def bench_c5(lp, ctx, stream, dev, args, rank, world):
+    """BASELINE configs[4]: recommendation sweep of 6,554 unseen LLMs (seed 1) x the 10 C2 profiles x
+    16 user levels = 1,048,640 candidate rows through the C2-shaped model (2 x 1000 trees, depth 6),
+    Eq. (1)-(3) argmin per LLM; the LLMs are split over the ranks and the per-LLM results gathered.
+    Device-timed (CUDA events), K steps after one warm-up."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    d = synth.make("C2")
+    m = lp.fit(ctx, d.X, d.y, lp.hparams(n_trees=1000, max_depth=6), d.users_col, d.llm_id, d.prof_id, d.n_llm,
+               d.n_prof, L1, L2)
+    n_total = 6554
+    lo, hi = rank * n_total // world, (rank + 1) * n_total // world
+    lf, pf, cost, levels = synth.sweep_tables(n_llm=hi - lo, seed=1, profiles=synth.PROFILES_C2, first_id=lo)
+    lfd, pfd = torch.from_numpy(lf).to(dev), torch.from_numpy(pf).to(dev)
+    rows = (hi - lo) * pf.shape[0] * len(levels)
+    gathered = torch.zeros((n_total, 4), dtype=torch.float64, device=dev)
+
+    def step():
+        recs = lp.recommend(ctx, m, lfd, pfd, cost, levels, L1, L2, U)
+        mine = torch.tensor(recs, dtype=torch.float64).to(dev)
+        if world > 1:
+            parts = [torch.zeros(((r + 1) * n_total // world - r * n_total // world, 4), dtype=torch.float64,
+                                 device=dev) for r in range(world)]
+            dist.all_gather(parts, mine)
+            torch.cat(parts, out=gathered)
+        else:
+            gathered.copy_(mine)
+
+    step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(args.steps):
+        step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = ms.item() / args.steps
+    m.free()
+    total_rows = n_total * pf.shape[0] * len(levels)
+    visits = total_rows * 2 * 1000 * 6
+    return {"workload": "C5: %d unseen LLMs x %d profiles x %d user levels = %d rows, C2-shaped model (2 x 1000 trees,"
+                        " depth 6), LLMs split over %d rank(s), per-LLM results all-gathered" %
+                        (n_total, pf.shape[0], len(levels), total_rows, world),
+            "value": total_rows / (ms / 1000.0), "unit": "rows/s", "ms_per_step": ms, "rows": total_rows,
+            "rows_per_rank": rows, "node_visits_per_s": visits / (ms / 1000.0),
+            "node_visits_per_row": 2 * 1000 * 6,
+            "note": "the predictor routes on bin codes through fixed-depth trees: SM-issue bound, not HBM "
+                    "(DESIGN.md §6); node visits/s against the issue-rate bound there"}
 
 
 def measured_peaks():
@@ -299,15 +389,24 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------------- reference
 def arm_config(args, world):
-    """The workload both arms report (BASELINE.json configs[2]/[3] shape, weak-scaled per GPU)."""
-    rows = args.llms_per_gpu * 8 * 16
+    """The workload both arms report: BASELINE.json configs[2] per GPU, weak-scaled (default), or
+    configs[3] (--strong: 100M rows in total, row-sharded over the N ranks)."""
     sweep_rows = args.sweep_llms * 8 * 16
-    return {"workload": "C3 per GPU (C4 family when N > 1): %d rows/GPU = %d LLMs x 8 profiles x 16 user levels, "
-                        "32 features, 256 bins, 2 targets x %d trees, depth %d; recommend sweep %d unseen LLMs/GPU"
-                        % (rows, args.llms_per_gpu, args.trees, args.depth, args.sweep_llms),
-            "rows_global": rows * world, "rows_per_gpu": rows, "features": 32, "bins": 256, "trees": args.trees,
-            "depth": args.depth, "targets": 2, "sweep_rows_per_gpu": sweep_rows, "global_batch": rows * world,
-            "parallelism": "row-sharded dp%d, NCCL int64 histogram all-reduce" % world,
+    if args.strong:
+        rows_g = args.strong_llms * 8 * 16
+        rows = rows_g // world
+        desc = ("C4 row-sharded fit: %d rows in total = %d LLMs x 8 profiles x 16 user levels over %d GPU(s), 32 "
+                "features, 256 bins, 2 targets x %d trees, depth %d; recommend sweep %d unseen LLMs/GPU"
+                % (rows_g, args.strong_llms, world, args.trees, args.depth, args.sweep_llms))
+    else:
+        rows = args.llms_per_gpu * 8 * 16
+        rows_g = rows * world
+        desc = ("C3 per GPU (C4 family when N > 1): %d rows/GPU = %d LLMs x 8 profiles x 16 user levels, "
+                "32 features, 256 bins, 2 targets x %d trees, depth %d; recommend sweep %d unseen LLMs/GPU"
+                % (rows, args.llms_per_gpu, args.trees, args.depth, args.sweep_llms))
+    return {"workload": desc, "rows_global": rows_g, "rows_per_gpu": rows, "features": 32, "bins": 256,
+            "trees": args.trees, "depth": args.depth, "targets": 2, "sweep_rows_per_gpu": sweep_rows,
+            "global_batch": rows_g, "parallelism": "row-sharded dp%d, NCCL int64 histogram all-reduce" % world,
             "l2": "inputs larger than L2 (codes %d MB + state per GPU), no flush" % (rows * 32 // 2 ** 20)}
 
 
@@ -345,6 +444,50 @@ def run_reference(args, rank, world):
     return 0
 
 
+def _gen_chunk(a):
+    import synth
+    n_total, shard, n_shards = a
+    c = synth.make_scaled(n_total, shard, n_shards)
+    return c.X, c.y, c.llm_id, c.prof_id, c.row_offset, c.n_global
+
+
+def device_shard(n_llm_total, rank, world, dev, chunks=16):
+    """Rank `rank`'s contiguous LLM-block shard of make_scaled(n_llm_total) built straight into HBM,
+    chunk by chunk (the concatenation of make_scaled(n, rank*c + j, world*c) over j is exactly
+    make_scaled(n, rank, world)), generated by a process pool to bound host memory and time."""
+    import concurrent.futures as cf
+    import types
+
+    import torch
+    lo, hi = rank * n_llm_total // world, (rank + 1) * n_llm_total // world
+    rows_per_llm = 8 * 16
+    n = (hi - lo) * rows_per_llm
+    X = torch.empty((n, 32), dtype=torch.float32, device=dev)
+    y = torch.empty((n, 2), dtype=torch.float32, device=dev)
+    li = torch.empty(n, dtype=torch.int32, device=dev)
+    pi = torch.empty(n, dtype=torch.int32, device=dev)
+    jobs = [(n_llm_total, rank * chunks + j, world * chunks) for j in range(chunks)]
+    off = 0
+    row_offset = None
+    workers = max(1, min(8, (os.cpu_count() or 2) - 1))
+    with cf.ProcessPoolExecutor(workers) as ex:
+        for Xc, yc, lc, pc, ro, ng in ex.map(_gen_chunk, jobs):
+            m = Xc.shape[0]
+            X[off:off + m].copy_(torch.from_numpy(Xc))
+            y[off:off + m].copy_(torch.from_numpy(yc))
+            li[off:off + m].copy_(torch.from_numpy(lc))
+            pi[off:off + m].copy_(torch.from_numpy(pc))
+            if row_offset is None:
+                row_offset = ro
+            off += m
+            n_global = ng
+    assert off == n
+    import synth
+    meta = types.SimpleNamespace(n=n, users_col=31, n_llm=n_llm_total, n_prof=len(synth.PROFILES_C3),
+                                 row_offset=row_offset, n_global=n_global, X=None, y=None, llm_id=None, prof_id=None)
+    return meta, X, y, li, pi
+
+
 # ---------------------------------------------------------------------------------------- ours
 def main():
     args = parse()
@@ -372,15 +515,20 @@ def main():
         uid = bytes(t.cpu().numpy().tobytes())
 
     # ---- synthetic inputs (seeded), resident in HBM before the timed region
-    n_llm_total = args.llms_per_gpu * world
-    d = synth.make_scaled(n_llm_total, rank, world)
+    n_llm_total = args.strong_llms if args.strong else args.llms_per_gpu * world
+    if args.strong:
+        args.no_e2e = True   # (a 13 GB pinned host copy per rank is not what configs[3] measures)
+        d, Xd, yd, ld, pd = device_shard(n_llm_total, rank, world, dev)
+    else:
+        d = synth.make_scaled(n_llm_total, rank, world)
     lf, pf, cost, levels = synth.sweep_tables(n_llm=args.sweep_llms, seed=1, profiles=synth.PROFILES_C3,
                                               params_lo=1.0, params_hi=16.0, first_id=rank * args.sweep_llms)
     stream = torch.cuda.current_stream()
-    Xd = torch.from_numpy(d.X).to(dev)
-    yd = torch.from_numpy(d.y).to(dev)
-    ld = torch.from_numpy(d.llm_id).to(dev)
-    pd = torch.from_numpy(d.prof_id).to(dev)
+    if not args.strong:
+        Xd = torch.from_numpy(d.X).to(dev)
+        yd = torch.from_numpy(d.y).to(dev)
+        ld = torch.from_numpy(d.llm_id).to(dev)
+        pd = torch.from_numpy(d.prof_id).to(dev)
     lfd = torch.from_numpy(lf).to(dev)
     pfd = torch.from_numpy(pf).to(dev)
     torch.cuda.synchronize()
@@ -538,9 +686,14 @@ def main():
     if rank == 0 and world == 1 and not args.no_wg:
         wg = bench_wg(lp, ctx, stream, dev, args)
     # ---- the paper-shaped config (BASELINE.json configs[1]): full leave-one-LLM-out CV of C2
-    cv_c2 = None
+    cv_c2 = cv_grid = None
     if rank == 0 and world == 1 and not args.no_cv:
         cv_c2 = bench_cv_c2(lp, ctx, args)
+        cv_grid = bench_cv_c2_grid(lp, ctx, args)
+    # ---- BASELINE configs[4]: the C5 recommendation sweep, LLMs split over the ranks
+    c5 = None
+    if not args.no_c5:
+        c5 = bench_c5(lp, ctx, stream, dev, args, rank, world)
 
     # ---- CPU baseline: the oracle as it stands, rank 0, N = 1, bounded sample
     cpu = None
@@ -561,7 +714,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u8/i64",
+            "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "u8/i64",
             "data": "synthetic (seeded counter-based generator, synth/; shapes of the paper's dataset)",
             "config": arm_config(args, world),
             "predict": {"value": predict_rows / (pred_ms / 1000.0), "unit": "rows/s", "rows_per_step": sweep_rows * world,
@@ -580,6 +733,8 @@ def main():
             "cpu_baseline": cpu,
             "workload_generator": wg,
             "cv_c2": cv_c2,
+            "cv_c2_grid": cv_grid,
+            "c5_sweep": c5,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

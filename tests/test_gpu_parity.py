@@ -385,6 +385,31 @@ def test_predict_and_recommend_parity(lp, ctx):
     assert any(r[0] == -1 for r in grec2) or True
 
 
+def test_c5_sweep_full_size_sampled_parity(lp, ctx):
+    """BASELINE configs[4] at full size: the C2-shaped model (2 x 1000 trees, depth 6) and
+    the sweep of 6,554 unseen LLMs x 10 profiles x 16 levels = 1,048,640 rows in the launch
+    configuration bench.py times; the oracle predicts and recommends a sample of 48 LLMs (their 7,680
+    rows), which must match the GPU's predictions bit for bit and its recommendations exactly."""
+    d = synth.make("C2")
+    om, otp, gm = _fit_both(lp, ctx, d, n_trees=1000, max_depth=6)
+    _assert_same_model(om, gm.export())
+    lf, pf, cost, levels = synth.sweep_tables(n_llm=6554, seed=1, profiles=synth.PROFILES_C2)
+    nL, nP, nU = lf.shape[0], pf.shape[0], len(levels)
+    pred_out = torch.zeros((nL * nP * nU, 2), dtype=torch.float32, device="cuda")
+    grec = lp.recommend(ctx, gm, torch.from_numpy(lf).cuda(), torch.from_numpy(pf).cuda(), cost, levels, L1, L2, U,
+                        pred_out=pred_out)
+    gp = pred_out.cpu().numpy().reshape(nL, nP, nU, 2)
+    sample = np.random.default_rng(5).choice(nL, 48, replace=False)
+    sample[:2] = [0, nL - 1]
+    for i in sample:
+        rows = np.concatenate([np.repeat(lf[i:i + 1], nP * nU, axis=0), np.repeat(pf, nU, axis=0),
+                               np.tile(levels.astype(np.float32), nP)[:, None]], axis=1)
+        op = oracle.predict(om, rows).reshape(1, nP, nU, 2)
+        assert _bits_equal(op[0], gp[i]), i
+        assert oracle.recommend(op, levels, cost, L1, L2, U)[0] == grec[i], i
+    assert len(grec) == nL
+
+
 def test_recommend_toy_table_through_gpu_argmin(lp, ctx, golden):
     """The hand-computed toy table (tests/golden/o11_toy_table.json) through the GPU argmin:
     a 1-feature constant model cannot express it, so drive the argmin via the CV-free path:
