@@ -213,9 +213,18 @@ def bench_c5(lp, ctx, stream, dev, args, rank, world):
     rows = (hi - lo) * pf.shape[0] * len(levels)
     gathered = torch.zeros((n_total, 4), dtype=torch.float64, device=dev)
 
-    def step():
-        recs = lp.recommend(ctx, m, lfd, pfd, cost, levels, L1, L2, U)
-        mine = torch.tensor(recs, dtype=torch.float64).to(dev)
+    rec_ms = []
+
+    def step(record=False):
+        if record:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        recs = lp.recommend(ctx, m, lfd, pfd, cost, levels, L1, L2, U, as_array=True)
+        if record:
+            e1.record(stream)
+            rec_ms.append((e0, e1))
+        mine = torch.from_numpy(np.stack([recs["profile"].astype(np.float64), recs["n_pods"].astype(np.float64),
+                                          recs["cost"], recs["u_max"].astype(np.float64)], axis=1)).to(dev)
         if world > 1:
             parts = [torch.zeros(((r + 1) * n_total // world - r * n_total // world, 4), dtype=torch.float64,
                                  device=dev) for r in range(world)]
@@ -231,9 +240,10 @@ def bench_c5(lp, ctx, stream, dev, args, rank, world):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
     for _ in range(args.steps):
-        step()
+        step(record=True)
     b.record(stream)
     torch.cuda.synchronize()
+    call_ms = sum(x.elapsed_time(y) for x, y in rec_ms) / args.steps
     ms = torch.tensor([a.elapsed_time(b)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
@@ -246,6 +256,7 @@ def bench_c5(lp, ctx, stream, dev, args, rank, world):
                         (n_total, pf.shape[0], len(levels), total_rows, world),
             "value": total_rows / (ms / 1000.0), "unit": "rows/s", "ms_per_step": ms, "rows": total_rows,
             "rows_per_rank": rows, "node_visits_per_s": visits / (ms / 1000.0),
+            "recommend_call_ms": call_ms,
             "node_visits_per_row": 2 * 1000 * 6,
             "note": "the predictor routes on bin codes through fixed-depth trees: SM-issue bound, not HBM "
                     "(DESIGN.md §6); node visits/s against the issue-rate bound there"}

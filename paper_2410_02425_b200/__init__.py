@@ -416,9 +416,16 @@ class WorkloadGenerator:
             pass
 
 
+REC_DTYPE = np.dtype({"names": ["profile", "n_pods", "cost", "u_max"], "formats": [np.int32, np.int64, np.float64,
+                                                                                    np.int32],
+                      "offsets": [Rec.profile.offset, Rec.n_pods.offset, Rec.cost.offset, Rec.u_max.offset],
+                      "itemsize": C.sizeof(Rec)})
+
+
 def recommend(ctx: Context, model: Model, llm_feats, prof_feats, cost, user_levels, L1: float, L2: float, U: int,
-              allowed=None, pred_out=None):
-    """Eq. (1)-(3) for every row of llm_feats.  Returns a list of (profile, n_pods, cost, u_max)."""
+              allowed=None, pred_out=None, as_array: bool = False):
+    """Eq. (1)-(3) for every row of llm_feats.  Returns a list of (profile, n_pods, cost, u_max), or
+    with as_array=True a numpy structured array (REC_DTYPE) over the library's output records."""
     n_llm, F_llm = int(llm_feats.shape[0]), int(llm_feats.shape[1])
     n_prof, F_prof = int(prof_feats.shape[0]), int(prof_feats.shape[1])
     pl, k1 = _ptr(llm_feats, np.float32)
@@ -431,6 +438,8 @@ def recommend(ctx: Context, model: Model, llm_feats, prof_feats, cost, user_leve
     _check(lib().llmpilot_recommend(ctx.handle, model._h, pl, n_llm, F_llm, pp, n_prof, F_prof,
                                     cs.ctypes.data_as(C.c_void_p), None if al is None else al.ctypes.data_as(C.c_void_p),
                                     lv.ctypes.data_as(C.c_void_p), len(lv), L1, L2, U, out, po))
+    if as_array:
+        return np.frombuffer(out, dtype=REC_DTYPE, count=n_llm).copy()
     return [(r.profile, r.n_pods, r.cost, r.u_max) for r in out[:n_llm]]
 
 

@@ -7,6 +7,7 @@
 // j = 1..B-1, dropping c_j == v[0] and duplicates.  codes: code(x) = #{c in cuts_f : c <= x}.
 #include <cub/device/device_segmented_sort.cuh>
 
+#include "bulk.cuh"
 #include "internal.cuh"
 
 namespace llmp {
@@ -160,66 +161,142 @@ void compute_cuts(Ctx* ctx, const float* X, int64_t n, int F, int64_t row_offset
   LLMP_CUDA(cudaStreamSynchronize(s));
 }
 
-// codes: CTA of 256 threads per 128-row tile; warp = row, lane = feature; cuts transposed in smem
-// ([bin][feature]) so the 32 lanes' binary searches never share a bank.
+// codes: persistent CTAs of 256 threads over 128-row tiles, every transfer a bulk copy (TMA engine):
+// the tile's X rows (128 x F floats, contiguous) land in a double-buffered shared-memory stage through
+// cp.async.bulk + an mbarrier while the previous tile is binned; the codes leave as bulk stores — the
+// row-major tile (128 x 32 B, contiguous) and, column-major, one 128-byte run per feature.  Binning:
+// warp = row, lane = feature, binary search over the feature's cuts transposed in shared memory
+// ([bin][feature]: the 32 lanes' searches never share a bank), 16 rows per warp in flight.
 constexpr int CODE_ROWS = 128;
-__global__ void __launch_bounds__(256) k_codes(const float* __restrict__ X, int64_t n, int F,
-                                               const float* __restrict__ cuts, const int32_t* __restrict__ ncuts,
-                                               uint8_t* __restrict__ codes, uint8_t* __restrict__ codesT, int64_t ldT,
-                                               int* flag) {
+constexpr int CODE_THREADS = 256;
+constexpr int CODE_TSTRIDE = CODE_ROWS + 16;   // column-major tile: 16-B aligned runs, 4-way (not 32-way) bank sharing
+constexpr int CODE_SMEM = 2 * CODE_ROWS * kMaxF * 4 + CODE_ROWS * kMaxF + kMaxF * CODE_TSTRIDE;   // 40.5 KB
+__global__ void __launch_bounds__(CODE_THREADS) k_codes(const float* __restrict__ X, int64_t n, int F,
+                                                        const float* __restrict__ cuts,
+                                                        const int32_t* __restrict__ ncuts, uint8_t* __restrict__ codes,
+                                                        uint8_t* __restrict__ codesT, int64_t ldT, int* flag, int al) {
   __shared__ float s_cut[kBins][kMaxF];
   __shared__ int s_nc[kMaxF];
-  __shared__ __align__(16) uint8_t s_tile[CODE_ROWS][kMaxF];
+  extern __shared__ __align__(128) uint8_t code_smem[];
+  float(*s_x)[CODE_ROWS * kMaxF] = reinterpret_cast<float(*)[CODE_ROWS * kMaxF]>(code_smem);       // [2] stages
+  uint8_t(*s_tile)[kMaxF] = reinterpret_cast<uint8_t(*)[kMaxF]>(code_smem + 2 * CODE_ROWS * kMaxF * 4);  // row-major
+  uint8_t(*s_tileT)[CODE_TSTRIDE] =
+      reinterpret_cast<uint8_t(*)[CODE_TSTRIDE]>(code_smem + 2 * CODE_ROWS * kMaxF * 4 + CODE_ROWS * kMaxF);   // column-major
+  __shared__ __align__(8) uint64_t s_bar[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < (kBins - 1) * kMaxF; i += 256) {
-    const int f = i / (kBins - 1), b = i % (kBins - 1);
-    s_cut[b][f] = cuts[i];
+  const int64_t ntiles = (n + CODE_ROWS - 1) / CODE_ROWS;
+  // bulk path: whole tiles whose byte count is a multiple of 16 (the tail goes through plain loads)
+  auto tile_rows = [&](int64_t t) { return (int)min((int64_t)CODE_ROWS, n - t * CODE_ROWS); };
+  // al: bit 0 X, bit 1 codes, bit 2 codesT (with ldT) are 16-byte aligned (bulk copies need it)
+  auto bulk_ok = [&](int64_t t) { return (al & 1) && ((size_t)tile_rows(t) * F * 4) % 16 == 0; };
+  if (tid == 0) {
+    mbar_init(smem_u32(&s_bar[0]), 1);
+    mbar_init(smem_u32(&s_bar[1]), 1);
+    mbar_fence_init();
   }
   if (tid < kMaxF) s_nc[tid] = ncuts[tid];
   __syncthreads();
-  const int nc = s_nc[lane];
-  for (int64_t r0 = (int64_t)blockIdx.x * CODE_ROWS; r0 < n; r0 += (int64_t)gridDim.x * CODE_ROWS) {
-    const int rows = (int)min((int64_t)CODE_ROWS, n - r0);
-    for (int r = warp; r < CODE_ROWS; r += 8) {
+  // cuts padded with NaN to 255 entries (no comparison with NaN holds): a fixed 8-step upper_bound
+  for (int i = tid; i < (kBins - 1) * kMaxF; i += CODE_THREADS) {
+    const int f = i / (kBins - 1), b = i % (kBins - 1);
+    s_cut[b][f] = b < s_nc[f] ? cuts[i] : __int_as_float(0x7fffffff);   // NaN: never <= x
+  }
+  __syncthreads();
+  auto issue = [&](int64_t t, int buf) {   // thread 0: tile t's X rows into stage buf
+    if (t < ntiles && bulk_ok(t)) {
+      const uint32_t bytes = (uint32_t)((size_t)tile_rows(t) * F * 4);
+      mbar_arrive_expect_tx(smem_u32(&s_bar[buf]), bytes);
+      bulk_g2s(smem_u32(&s_x[buf][0]), X + t * CODE_ROWS * F, bytes, smem_u32(&s_bar[buf]));
+    }
+  };
+  if (tid == 0) issue(blockIdx.x, 0);
+  uint32_t phase[2] = {0u, 0u};
+  int k = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    const int buf = k & 1;
+    const int rows = tile_rows(t);
+    const int64_t r0 = t * CODE_ROWS;
+    const bool bulk = bulk_ok(t);
+    if (tid == 0) {
+      bulk_wait_read0();   // the previous tile's bulk stores have read s_tile / s_tileT
+      issue(t + gridDim.x, buf ^ 1);   // next tile's stage was consumed in the previous iteration
+    }
+    if (bulk) {
+      mbar_wait(smem_u32(&s_bar[buf]), phase[buf]);
+      phase[buf] ^= 1u;
+    }
+    __syncthreads();   // (s_tile free again: thread 0's wait above is ordered before every write below)
+    float xv[CODE_ROWS / 8];
+#pragma unroll
+    for (int j = 0; j < CODE_ROWS / 8; ++j) {
+      const int r = warp + 8 * j;
+      xv[j] = 0.f;
+      if (r < rows && lane < F) xv[j] = bulk ? s_x[buf][r * F + lane] : X[(r0 + r) * F + lane];
+    }
+#pragma unroll
+    for (int j = 0; j < CODE_ROWS / 8; ++j) {
+      const int r = warp + 8 * j;
       uint8_t code = 0;
       if (r < rows && lane < F) {
-        const float x = X[(r0 + r) * F + lane];
+        const float x = xv[j];
         if (flag && !isfinite(x)) atomicOr(flag, 1);
-        int lo = 0, hi = nc;   // upper_bound over the feature's cuts
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (s_cut[mid][lane] <= x) lo = mid + 1;
-          else hi = mid;
-        }
-        code = (uint8_t)lo;
+        int pos = 0;   // upper_bound: #{cuts <= x} over the 255 padded cuts
+#pragma unroll
+        for (int st = 128; st >= 1; st >>= 1)
+          if (s_cut[pos + st - 1][lane] <= x) pos += st;
+        code = (uint8_t)pos;
       }
       s_tile[r][lane] = code;
+      s_tileT[lane][r] = code;
     }
+    fence_proxy_async_smem();   // the code tiles are read by the bulk stores below
     __syncthreads();
-    if (codes) {
-      // row-major: rows * 32 contiguous bytes, 16 B per thread
-      uint4* dst = reinterpret_cast<uint4*>(codes + r0 * kMaxF);
-      const uint4* src = reinterpret_cast<const uint4*>(&s_tile[0][0]);
-      for (int i = tid; i < rows * 2; i += 256) dst[i] = src[i];
+    // one bulk store per destination run: thread 0 the row-major tile, the lanes of warp 1 the 32
+    // column-major 128-byte runs (a tail tile or an unaligned destination: plain stores)
+    const bool full = rows == CODE_ROWS;
+    if (full && codes && (al & 2) && tid == 0) {
+      bulk_s2g(codes + r0 * kMaxF, smem_u32(&s_tile[0][0]), CODE_ROWS * kMaxF);
+      bulk_commit();
     }
-    if (codesT) {
-      // column-major: feature f, rows r0..r0+rows; 4 rows per thread-word when aligned
-      for (int i = tid; i < kMaxF * CODE_ROWS; i += 256) {
-        const int f = i / CODE_ROWS, r = i % CODE_ROWS;
-        if (r < rows) codesT[(int64_t)f * ldT + r0 + r] = s_tile[r][f];
+    if (full && codesT && (al & 4) && warp == 1) {
+      bulk_s2g(codesT + (int64_t)lane * ldT + r0, smem_u32(&s_tileT[lane][0]), CODE_ROWS);
+      bulk_commit();
+    }
+    {
+      if (codes && !(full && (al & 2))) {
+        if (al & 2) {
+          uint4* dst = reinterpret_cast<uint4*>(codes + r0 * kMaxF);
+          const uint4* src = reinterpret_cast<const uint4*>(&s_tile[0][0]);
+          for (int i = tid; i < rows * 2; i += CODE_THREADS) dst[i] = src[i];
+        } else {
+          for (int i = tid; i < rows * kMaxF; i += CODE_THREADS) codes[r0 * kMaxF + i] = (&s_tile[0][0])[i];
+        }
       }
+      if (codesT && !(full && (al & 4)))
+        for (int i = tid; i < kMaxF * rows; i += CODE_THREADS) {
+          const int f = i / rows, r = i % rows;
+          codesT[(int64_t)f * ldT + r0 + r] = s_tileT[f][r];
+        }
     }
+    if (warp == 1) bulk_wait_read0();   // warp 1's column stores have read s_tileT
     __syncthreads();
   }
+  if (tid == 0 || warp == 1) bulk_wait0();
 }
 
 void compute_codes(Ctx* ctx, const float* X, int64_t n, int F, const CutsData& cuts, uint8_t* codes, uint8_t* codesT,
                    int64_t ldT, int* flag) {
   int64_t tiles = (n + CODE_ROWS - 1) / CODE_ROWS;
-  int grid = (int)std::min<int64_t>(tiles, (int64_t)ctx->sms * 8);
+  const int al = ((((uintptr_t)X & 15) == 0) ? 1 : 0) | ((((uintptr_t)codes & 15) == 0) ? 2 : 0) |
+                 (((((uintptr_t)codesT | (uintptr_t)ldT) & 15) == 0) ? 4 : 0);
+  ensure_smem_attr((const void*)k_codes, CODE_SMEM);
+  int per_sm = 1;   // persistent CTAs: exactly the resident count (no partial second wave)
+  LLMP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_codes, CODE_THREADS, CODE_SMEM));
+  int grid = (int)std::min<int64_t>(tiles, (int64_t)ctx->sms * std::max(1, per_sm));
   if (grid < 1) grid = 1;
-  LLMP_LAUNCH(ctx, KC_CODES, n, k_codes, grid, 256, 0, X, n, F, cuts.d_cuts.as<float>(), cuts.d_ncuts.as<int32_t>(),
-              codes, codesT, ldT, flag);
+  // (unaligned buffers, and tiles whose byte count is not a multiple of 16, take plain loads / stores)
+  LLMP_LAUNCH(ctx, KC_CODES, n, k_codes, grid, CODE_THREADS, CODE_SMEM, X, n, F, cuts.d_cuts.as<float>(),
+              cuts.d_ncuts.as<int32_t>(), codes, codesT, ldT, flag, al);
 }
 
 }  // namespace llmp
