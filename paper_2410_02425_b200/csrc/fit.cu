@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <chrono>
 
+#include "bulk.cuh"
 #include "internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -923,6 +924,19 @@ __global__ void __launch_bounds__(256) k_cmask(const uint8_t* codes, int64_t n, 
 
 // the fused update kernel for a depth: compile-time routing depth for the configs' depths (6, 8)
 using Hist2Kernel = void (*)(const FitPair, const int, const int, const DbgArgs);
+using Upd3Kernel = void (*)(const FitPair);
+static Upd3Kernel upd3_kernel(int D) {
+  if (D == 8) return k_upd3<8>;
+  if (D == 6) return k_upd3<6>;
+  return k_upd3<0>;
+}
+// fused update kernel: LLMP_UPD = 2 (default) change-mask k_hist2 with the precomputed masks; 3 the
+// bulk-staged change-row k_upd3 (measured slower: 385 vs 311 us per paired launch on C3 — the pass is
+// issue-bound, and the precomputed masks cost less than per-batch change tests)
+static int upd_kernel() {
+  static const int v = getenv("LLMP_UPD") ? atoi(getenv("LLMP_UPD")) : 2;
+  return v == 3 ? 3 : 2;
+}
 static Hist2Kernel updroot2_kernel(int D) {
   if (D == 8) return k_hist2<HM_UPDROOT, 8>;
   if (D == 6) return k_hist2<HM_UPDROOT, 6>;
@@ -2153,6 +2167,9 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   ensure_smem_attr((const void*)k_hist<HM_UPDROOT>, HIST_SMEM + updroot_tree_smem(D));
   const Hist2Kernel k_upd2 = updroot2_kernel(D);
   ensure_smem_attr((const void*)k_upd2, H2_SMEM + updroot_tree_smem(D));
+  const Upd3Kernel k_up3 = upd3_kernel(D);
+  ensure_smem_attr((const void*)k_up3, U3_SMEM + updroot_tree_smem(D));
+  const int updk = upd_kernel();
   const DbgArgs nodbg{};
 
   phase("state");
@@ -2215,6 +2232,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     // histogram kernels: 2 CTAs per SM in total, but no more CTAs than 2048-row slices of the data
     // (small fits would otherwise launch hundreds of CTAs that only zero their shared histograms)
     const dim3 hg((unsigned)std::min<int64_t>(ctx->sms * 2 / ny, std::max<int64_t>(1, (n + 2047) / 2048)), ny);
+    // k_upd3: one CTA per SM and ensemble
+    const dim3 hu3((unsigned)std::min<int64_t>(std::max(1, ctx->sms / ny), std::max<int64_t>(1, (n + 2047) / 2048)), ny);
     // k_hist3: one CTA per SM; one launch covers the built children of every ensemble in fp
     const dim3 hg3((unsigned)std::min<int64_t>(ctx->sms, std::max<int64_t>(1, (n * ny + 2047) / 2048)));
     // fused: the previous round's update pass built this root already unless root_needed
@@ -2248,6 +2267,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       if (hist1 & 4)
         LLMP_LAUNCH(ctx, KC_UPDATE, ny * n, k_hist<HM_UPDROOT>, hg, HIST_THREADS, HIST_SMEM + updroot_tree_smem(D), fp,
                     0, 0, nodbg);
+      else if (updk == 3)
+        LLMP_LAUNCH_PDL(ctx, KC_UPDATE, ny * n, k_up3, hu3, U3_THREADS, U3_SMEM + updroot_tree_smem(D), fp);
       else
         LLMP_LAUNCH_PDL(ctx, KC_UPDATE, ny * n, k_upd2, hg, H2_THREADS, H2_SMEM + updroot_tree_smem(D), fp, 0, 0, nodbg);
     } else {

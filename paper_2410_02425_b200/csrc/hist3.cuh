@@ -320,3 +320,272 @@ __global__ void __launch_bounds__(H3_THREADS, 1) k_hist3(const FitPair fp, const
     }
   }
 }
+
+// ---------------------------------------------------------------------------------------------
+// k_upd3: fused update of tree t + root histogram of tree t+1 (HM_UPDROOT semantics, see k_hist2:
+// O9 p += v for every row, then O4 for tree t+1 quantised with tree t's exponents — the speculation
+// that k_root_fix / k_hist2<ROOT> undo when an exponent changed — and O5 over all rows), rows in
+// identity order.  Every input moves by bulk copy (TMA engine): per warp (32 per CTA, one CTA per
+// SM) a 3-stage ring, one stage =
+// one 32-row batch = its code rows (1 KB, contiguous) and its y, w, p (128 B each), issued by lane 0
+// with cp.async.bulk on the stage's mbarrier two batches ahead of use.  Per batch, lane = row routes
+// its row through tree t (fixed-depth table), updates p, computes and quantises tree t+1's pair;
+// then the root histogram takes the change-row form of k_hist3 (a ballot of the rows whose codes
+// differ from the previous row, lanes = features flushing runs only there; users row-parallel).
+constexpr int U3_THREADS = 1024;
+constexpr int U3_WARPS = U3_THREADS / 32;
+constexpr int U3_STAGES = 3;
+constexpr int U3_AHEAD = 2;                              // batches in flight ahead of the one in use
+                                                         // (lane 0's previous row is kept in registers)
+constexpr int U3_Y = 32 * 32, U3_W = U3_Y + 128, U3_P = U3_W + 128;
+constexpr int U3_STAGE = U3_P + 128;                     // 1,408 B
+constexpr int U3_RING_OFF = H3_RING_OFF;                 // histogram channels + users column first
+constexpr int U3_SMEM = U3_RING_OFF + U3_WARPS * U3_STAGES * U3_STAGE;   // 66 + 132 KB (+ the tree)
+
+template <int DC>
+__global__ void __launch_bounds__(U3_THREADS, 1) k_upd3(const FitPair fp) {
+  pdl_wait();
+  const FitArgs& a = fp.t[blockIdx.y];
+  const int t = *a.d_tree;
+  const bool has_next = t + 1 < a.T;
+  const int ucol = (a.users_col >= 0 && a.users_col < kMaxF) ? a.users_col : -1;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ __align__(8) uint64_t s_bar[U3_WARPS][U3_STAGES];
+  {   // zero both histogram channels and the users column
+    uint4* z = reinterpret_cast<uint4*>(smem);
+    for (int i = tid; i < H3_RING_OFF / 16; i += U3_THREADS) z[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  if (lane == 0) {
+    for (int s = 0; s < U3_STAGES; ++s) mbar_init(smem_u32(&s_bar[warp][s]), 1);
+    mbar_fence_init();
+  }
+  // tree t as a fixed-depth routing table (as in k_hist2): internal slots above depth D hold their
+  // split, leaves and everything below them "always left" (0, 255); 2^D leaf values
+  uint8_t* s_rf = smem + U3_SMEM;
+  uint8_t* s_rb = s_rf + (a.nn + 1) / 2;
+  float* s_lv = reinterpret_cast<float*>(smem + U3_SMEM + (a.nn + 1));
+  const int n_int = (a.nn - 1) / 2;
+  {
+    const size_t to = (size_t)t * a.nn;
+    for (int i = tid; i < a.nn; i += U3_THREADS) {
+      const int f = a.tfeat[to + i];
+      if (i < n_int) {
+        s_rf[i] = (uint8_t)(f >= 0 ? f : 0);
+        s_rb[i] = (uint8_t)(f >= 0 ? a.tbin[to + i] : 255);
+      }
+      if (f == -1) {
+        const int dl = 31 - __clz(i + 1);
+        s_lv[((i + 1) << (a.D - dl)) - 1 - n_int] = a.tval[to + i];
+      }
+    }
+  }
+  __syncthreads();
+  const int64_t n = a.n;
+  const int64_t nb_all = (n + 31) / 32;
+  const int64_t v0 = (nb_all * blockIdx.x / gridDim.x) * 32, v1 = min(n, (nb_all * (blockIdx.x + 1) / gridDim.x) * 32);
+  if (v0 >= v1) return;
+  if (tid == 0 && a.units) atomicAdd(&a.units[KC_UPDATE], (unsigned long long)(v1 - v0));
+  const double scale_g = exp2i(a.K - exp_of(__uint_as_float(a.maxg[t])));
+  const double scale_h = exp2i(a.K - exp_of(__uint_as_float(a.maxh[t])));
+  float mg = 0.f, mh = 0.f;
+  const uint32_t sgb = smem_u32(smem);
+  const uint32_t sub = sgb + H3_U_OFF;
+  const uint32_t ring = sgb + U3_RING_OFF + (uint32_t)(warp * U3_STAGES * U3_STAGE);
+  const bool active = lane < a.F && lane != ucol;
+  uint32_t um[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) um[j] = (ucol >= 0 && (ucol >> 2) == j) ? ~(0xffu << (8 * (ucol & 3))) : 0xffffffffu;
+  uint32_t phase = 0;   // bit s: parity of stage s's barrier
+  for (int64_t c0 = v0; c0 < v1; c0 += HIST_CHUNK) {
+    const int64_t c1 = min(v1, c0 + HIST_CHUNK);
+    const int64_t nbc = (c1 - c0 + 31) / 32;
+    const int64_t w0 = c0 + (nbc * warp / U3_WARPS) * 32, w1 = min(c1, c0 + (nbc * (warp + 1) / U3_WARPS) * 32);
+    const int nb = (int)((w1 - w0 + 31) >> 5);
+    auto rows_of = [&](int b) { return (int)min((int64_t)32, w1 - (w0 + 32 * (int64_t)b)); };
+    // lane 0: batch b into its stage (full batches by bulk copy; a partial last batch of the data
+    // — its byte counts need not be multiples of 16 — by the whole warp with plain loads)
+    auto issue = [&](int b) {
+      if (b >= nb) return;
+      const int cnt = rows_of(b);
+      const int s = b % U3_STAGES;
+      const uint32_t st = ring + (uint32_t)(s * U3_STAGE);
+      const int64_t r0 = w0 + 32 * (int64_t)b;
+      // bulk copies need 16-byte aligned sources (p of the second ensemble starts at p + n)
+      const bool al = ((((uintptr_t)(a.y + r0)) | ((uintptr_t)(a.w + r0)) | ((uintptr_t)(a.p + r0))) & 15) == 0;
+      if (cnt == 32 && al) {
+        if (lane == 0) {
+          const uint32_t bar = smem_u32(&s_bar[warp][s]);
+          mbar_arrive_expect_tx(bar, 32 * 32 + 3 * 128);
+          bulk_g2s(st, a.codes + r0 * kMaxF, 32 * 32, bar);
+          bulk_g2s(st + U3_Y, a.y + r0, 128, bar);
+          bulk_g2s(st + U3_W, a.w + r0, 128, bar);
+          bulk_g2s(st + U3_P, a.p + r0, 128, bar);
+        }
+      } else {
+        if (lane < cnt) {
+          const uint4* cr = reinterpret_cast<const uint4*>(a.codes + (r0 + lane) * kMaxF);
+          const uint4 q0 = cr[0], q1 = cr[1];
+          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(st + lane * 32), "r"(q0.x), "r"(q0.y), "r"(q0.z),
+                       "r"(q0.w) : "memory");
+          asm volatile("st.shared.v4.u32 [%0+16], {%1, %2, %3, %4};" ::"r"(st + lane * 32), "r"(q1.x), "r"(q1.y),
+                       "r"(q1.z), "r"(q1.w) : "memory");
+          sts32(st + U3_Y + lane * 4, __float_as_uint(a.y[r0 + lane]));
+          sts32(st + U3_W + lane * 4, __float_as_uint(a.w[r0 + lane]));
+          sts32(st + U3_P + lane * 4, __float_as_uint(a.p[r0 + lane]));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(smem_u32(&s_bar[warp][s]), 0);   // completes the phase
+      }
+    };
+#pragma unroll
+    for (int k = 0; k < U3_AHEAD; ++k) issue(k);
+    uint32_t cur = 0;
+    int32_t acc_g = 0;
+    uint32_t acc_h = 0;
+    bool fresh = true;
+    uint32_t prv[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};   // row 31 of the previous batch
+    for (int b = 0; b < nb; ++b) {
+      __syncwarp();   // the stage being refilled (batch b-1's) is consumed by every lane
+      issue(b + U3_AHEAD);
+      const int s = b % U3_STAGES;
+      const uint32_t st = ring + (uint32_t)(s * U3_STAGE);
+      mbar_wait(smem_u32(&s_bar[warp][s]), (phase >> s) & 1u);
+      phase ^= 1u << s;
+      const int cnt = rows_of(b);
+      const bool valid = lane < cnt;
+      const int64_t ridx = w0 + 32 * (int64_t)b + lane;
+      // ---- O9 for tree t: route the lane's row (fixed depth), p += v (one fp32 rounding)
+      const uint32_t myrow = st + (uint32_t)(lane * 32);
+      int k = 0;
+      const int D = DC ? DC : a.D;
+#pragma unroll
+      for (int s2 = 0; s2 < (DC ? DC : kMaxDepth); ++s2)
+        if (DC || s2 < D) k = 2 * k + 1 + (lds8(myrow + s_rf[k]) > s_rb[k] ? 1 : 0);
+      const float pv = __uint_as_float(lds32(st + U3_P + lane * 4));
+      const float yv = __uint_as_float(lds32(st + U3_Y + lane * 4));
+      const float wv = __uint_as_float(lds32(st + U3_W + lane * 4));
+      const float pn = __fadd_rn(pv, s_lv[k - n_int]);
+      uint32_t gp = 0u;
+      if (valid) {
+        a.p[ridx] = pn;
+        if (has_next) {   // O4 for tree t+1 with tree t's exponents (speculation)
+          float g = __fmul_rn(wv, __fsub_rn(pn, yv));
+          float h = wv;
+          if (row_sampled_out(a.seed, a.target, t + 1, a.row_offset + ridx, a.subsample)) {
+            g = 0.f;
+            h = 0.f;
+          }
+          mg = fmaxf(mg, fabsf(g));
+          mh = fmaxf(mh, h);
+          gp = pack_gp(quantize(g, scale_g), quantize(h, scale_h));
+          a.gp_root[ridx] = gp;
+        }
+      }
+      if (!has_next) continue;   // last tree: update only
+      // ---- O5 root histogram of tree t+1: change-row form
+      const uint4 c0v = lds128(myrow), c1v = lds128(myrow + 16);
+      uint4 p0 = lds128(st + (uint32_t)((lane ? lane - 1 : 0) * 32)), p1 = lds128(st + (uint32_t)((lane ? lane - 1 : 0) * 32 + 16));
+      if (lane == 0) {   // the previous batch's last row (its stage may already be refilled)
+        p0 = make_uint4(prv[0], prv[1], prv[2], prv[3]);
+        p1 = make_uint4(prv[4], prv[5], prv[6], prv[7]);
+      }
+      {
+        const uint32_t cw[8] = {c0v.x, c0v.y, c0v.z, c0v.w, c1v.x, c1v.y, c1v.z, c1v.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) prv[j] = __shfl_sync(0xffffffffu, cw[j], 31);
+      }
+      const uint32_t dx = ((c0v.x ^ p0.x) & um[0]) | ((c0v.y ^ p0.y) & um[1]) | ((c0v.z ^ p0.z) & um[2]) |
+                          ((c0v.w ^ p0.w) & um[3]) | ((c1v.x ^ p1.x) & um[4]) | ((c1v.y ^ p1.y) & um[5]) |
+                          ((c1v.z ^ p1.z) & um[6]) | ((c1v.w ^ p1.w) & um[7]);
+      unsigned B = __ballot_sync(0xffffffffu, valid && (dx != 0u || (fresh && lane == 0)));
+      const int32_t qg = valid ? gp_g(gp) : 0;
+      const uint32_t qh = valid ? (uint32_t)gp_h(gp) : 0u;
+      if (ucol >= 0 && valid) {
+        const uint32_t ua = sub + lds8(myrow + ucol) * 4u;
+        asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(ua), "r"(qg) : "memory");
+        asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(ua), "r"(qh), "n"(kBins * 4) : "memory");
+      }
+      if (fresh) {
+        cur = (lds8(st + lane) * 32u + (uint32_t)lane) * 4u;
+        fresh = false;
+        B &= ~1u;
+      }
+      int32_t bg = 0;
+      uint32_t bh = 0;
+      while (B) {
+        const int r1 = __ffs(B) - 1;
+        B &= B - 1u;
+        const bool two = B != 0u;
+        const int r2 = two ? __ffs(B) - 1 : r1;
+        B &= B - 1u;
+        const uint32_t cc1 = lds8(st + (uint32_t)(r1 * 32 + lane));
+        const uint32_t cc2 = lds8(st + (uint32_t)(r2 * 32 + lane));
+        const int32_t vg1 = (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)(lane < r1 ? qg : 0));
+        const uint32_t vh1 = __reduce_add_sync(0xffffffffu, lane < r1 ? qh : 0u);
+        const int32_t vg2 = (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)(lane < r2 ? qg : 0));
+        const uint32_t vh2 = __reduce_add_sync(0xffffffffu, lane < r2 ? qh : 0u);
+        const uint32_t na1 = (cc1 * 32u + (uint32_t)lane) * 4u;
+        if (active && na1 != cur) {
+          red2_h3(sgb + cur, acc_g + (vg1 - bg), acc_h + (vh1 - bh));
+          acc_g = 0;
+          acc_h = 0;
+          bg = vg1;
+          bh = vh1;
+          cur = na1;
+        }
+        const uint32_t na2 = (cc2 * 32u + (uint32_t)lane) * 4u;
+        if (two && active && na2 != cur) {
+          red2_h3(sgb + cur, acc_g + (vg2 - bg), acc_h + (vh2 - bh));
+          acc_g = 0;
+          acc_h = 0;
+          bg = vg2;
+          bh = vh2;
+          cur = na2;
+        }
+      }
+      acc_g += (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)qg) - bg;
+      acc_h += __reduce_add_sync(0xffffffffu, qh) - bh;
+    }
+    if (!has_next) continue;
+    if (active && !fresh && (acc_g | (int32_t)acc_h)) red2_h3(sgb + cur, acc_g, acc_h);
+    __syncthreads();
+    int32_t* sg = reinterpret_cast<int32_t*>(smem);
+    uint32_t* sh = reinterpret_cast<uint32_t*>(smem + H3_HH);
+    int32_t* sug = reinterpret_cast<int32_t*>(smem + H3_U_OFF);
+    uint32_t* suh = reinterpret_cast<uint32_t*>(smem + H3_U_OFF + kBins * 4);
+    if (ucol >= 0) {
+      for (int bb = tid; bb < kBins; bb += U3_THREADS) {
+        sg[bb * 32 + ucol] = sug[bb];
+        sh[bb * 32 + ucol] = suh[bb];
+        sug[bb] = 0;
+        suh[bb] = 0;
+      }
+      __syncthreads();
+    }
+    int64_t* Hg = a.H[0];
+    int64_t* Hh = Hg + kHistBins;
+    for (int i = tid; i < kHistBins; i += U3_THREADS) {
+      const int32_t g = sg[i];
+      const uint32_t h = sh[i];
+      if (g != 0 || h != 0) {
+        const int bb = i >> 5, f = i & 31;
+        atomicAdd(reinterpret_cast<unsigned long long*>(&Hg[f * kBins + bb]), (unsigned long long)(long long)g);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&Hh[f * kBins + bb]), (unsigned long long)h);
+        sg[i] = 0;
+        sh[i] = 0;
+      }
+    }
+    __syncthreads();
+  }
+  if (has_next) {
+    for (int o = 16; o > 0; o >>= 1) {
+      mg = fmaxf(mg, __shfl_xor_sync(0xffffffffu, mg, o));
+      mh = fmaxf(mh, __shfl_xor_sync(0xffffffffu, mh, o));
+    }
+    if (lane == 0) {
+      atomicMax(&a.maxg[t + 1], __float_as_uint(mg));
+      atomicMax(&a.maxh[t + 1], __float_as_uint(mh));
+    }
+  }
+}
