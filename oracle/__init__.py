@@ -41,15 +41,30 @@ class Hparams(C.Structure):
                 ("grad_bits", C.c_int32), ("eta", C.c_float), ("lambda_", C.c_float),
                 ("min_child_weight", C.c_float), ("subsample", C.c_float),
                 ("colsample_bytree", C.c_float), ("seed", C.c_uint64),
-                ("use_eq4_weights", C.c_int32), ("monotone_users", C.c_int32)]
+                ("use_eq4_weights", C.c_int32), ("monotone_users", C.c_int32),
+                ("model", C.c_int32), ("max_features", C.c_float), ("rf_bootstrap", C.c_int32)]
 
 
 def hparams(n_trees=20, max_depth=4, max_bin=256, grad_bits=14, eta=0.3, lambda_=1.0,
             min_child_weight=1.0, subsample=1.0, colsample_bytree=1.0, seed=0, use_eq4_weights=1,
-            monotone_users=1) -> Hparams:
-    """Defaults = XGBoost defaults (SURVEY §8c #12) with K = 14 gradient bits (DESIGN.md)."""
+            monotone_users=1, model=0, max_features=1.0, rf_bootstrap=1) -> Hparams:
+    """Defaults = XGBoost defaults with K = 14 gradient bits.
+    model=1: random forest (DESIGN R33-R36)."""
     return Hparams(n_trees, max_depth, max_bin, grad_bits, eta, lambda_, min_child_weight,
-                   subsample, colsample_bytree, seed, use_eq4_weights, monotone_users)
+                   subsample, colsample_bytree, seed, use_eq4_weights, monotone_users, model, max_features,
+                   rf_bootstrap)
+
+
+def rf_hparams(n_trees=20, max_depth=8, max_bin=256, max_features=1.0, min_child_weight=0.0, seed=0,
+               use_eq4_weights=0, bootstrap=1, grad_bits=14) -> Hparams:
+    """Random-forest regressor: lambda 0, no monotone constraint, no row subsampling."""
+    return hparams(n_trees=n_trees, max_depth=max_depth, max_bin=max_bin, grad_bits=grad_bits, eta=1.0, lambda_=0.0,
+                   min_child_weight=min_child_weight, seed=seed, use_eq4_weights=use_eq4_weights, monotone_users=0,
+                   model=1, max_features=max_features, rf_bootstrap=bootstrap)
+
+
+def poisson1(seed, t, i) -> int:
+    return lib().orc_poisson1(seed, t, i)
 
 
 class Split(C.Structure):
@@ -79,6 +94,8 @@ def lib():
         L = _lib
         L.orc_rng4.restype = C.c_uint64
         L.orc_rng4.argtypes = [C.c_uint64] * 4
+        L.orc_poisson1.restype = C.c_int32
+        L.orc_poisson1.argtypes = [C.c_uint64, C.c_int32, C.c_int64]
         L.orc_weights.argtypes = [C.c_int64, P, P, P, C.c_int32, C.c_int32, C.c_float, C.c_float, P]
         L.orc_cuts.restype = C.c_int
         L.orc_cuts.argtypes = [P, C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.c_int32, P, P]

@@ -32,6 +32,22 @@ uint64_t orc_rng4(uint64_t seed, uint64_t a, uint64_t b, uint64_t c) {
  *   w_t(M,G,u) = 1 - |l_t(M,G,u) - L_t| / max_{v in U} |l_t(M,G,v) - L_t|,   t in {1,2}
  *   w = (w_1 + w_2) / 2   ("We combine both weights using arithmetic mean")
  * Group = (llm_id, profile_id).  Zero denominator => weight 1 (reading R6).      */
+/* Poisson(1) by inversion (DESIGN R34): k = min{k : u < F(k)}, F(k) = sum_{j<=k} e^-1 / j!, with
+ * the terms and the running sum in fp64 in exactly this order (p_0 = e^-1, p_k = p_{k-1} / k); capped
+ * at 16 (F(16) rounds to 1 in fp64) */
+int32_t orc_poisson1(uint64_t seed, int32_t t, int64_t i) {
+  double u = (double)(orc_rng4(seed, 0x5246u, (uint64_t)t, (uint64_t)i) >> 11) * 0x1.0p-53;
+  double p = 0x1.78b56362cef38p-2; /* e^-1 rounded to double */
+  double F = p;
+  int32_t k = 0;
+  while (u >= F && k < 16) {
+    ++k;
+    p = p / (double)k;
+    F = F + p;
+  }
+  return k;
+}
+
 void orc_weights(int64_t n, const float* y, const int32_t* llm_id, const int32_t* prof_id, int32_t n_llm,
                  int32_t n_prof, float L1, float L2, float* w_out) {
   int64_t ng = (int64_t)n_llm * n_prof;
@@ -236,7 +252,9 @@ static int fit_one_target(const uint8_t* codes, const float* y, const float* w, 
   int32_t nbins[ORC_MAX_F];
   for (int32_t f = 0; f < F; ++f) nbins[f] = ncuts[f] + 1;
 
-  /* O3 — base score: quantise g = w*(0 - y), h = w (no subsampling); base = -G/H (lambda = 0) */
+  const int rf = hp->model == 1;
+  /* O3 — base score: quantise g = w*(0 - y), h = w (no subsampling); base = -G/H (lambda = 0).
+   * Random forest (R33): no intercept, base 0 (every tree predicts the mean of its bootstrap). */
   for (int64_t i = 0; i < n; ++i) {
     float d = 0.0f - y[i * 2 + target];
     g[i] = w[i] * d;
@@ -250,6 +268,7 @@ static int fit_one_target(const uint8_t* codes, const float* y, const float* w, 
   }
   double G0 = ldexp((double)Gq, eg - K), H0 = ldexp((double)Hq, eh - K);
   float base = H0 > 0.0 ? (float)(-G0 / H0) : 0.0f;
+  if (rf) base = 0.0f;
   *base_out = base;
   for (int64_t i = 0; i < n; ++i) p[i] = base;
 
@@ -272,8 +291,17 @@ static int fit_one_target(const uint8_t* codes, const float* y, const float* w, 
       tv[k] = 0.0f;
       if (tgn) tgn[k] = 0.0;
     }
-    /* O4 — gradients of weighted squared error, fp32; row subsampling */
+    /* O4 — gradients of weighted squared error, fp32; row subsampling.
+     * Random forest (R33, R34): every tree fits y itself (p = 0 in the gradient, no boosting) with
+     * the row's Poisson(1) bootstrap count as an integer weight: w_t = c_t,i * w (fp32). */
     for (int64_t i = 0; i < n; ++i) {
+      if (rf) {
+        const float c = hp->rf_bootstrap ? (float)orc_poisson1(hp->seed, t, row_offset + i) : 1.0f;
+        const float wt = c * w[i];
+        g[i] = wt * (0.0f - y[i * 2 + target]);
+        h[i] = wt;
+        continue;
+      }
       float d = p[i] - y[i * 2 + target];
       g[i] = w[i] * d;
       h[i] = w[i];
@@ -328,14 +356,33 @@ static int fit_one_target(const uint8_t* codes, const float* y, const float* w, 
         orc_split sp;
         int split = 0;
         if (d < D) {
+          if (rf) {
+            /* R35 — random forest: the node's own feature sample, the ceil(max_features F) features
+             * with the smallest keys rng4(seed, 2 target + 1, t, (k + 1) * 32 + f), ties by f */
+            int32_t mk = (int32_t)ceil((double)hp->max_features * (double)F);
+            if (mk < 1) mk = 1;
+            for (int32_t f = 0; f < F; ++f) {
+              uint64_t kf = orc_rng4(hp->seed, (uint64_t)(2 * target + 1), (uint64_t)t,
+                                     (uint64_t)(nd->k + 1) * 32u + (uint64_t)f);
+              int32_t rank = 0;
+              for (int32_t f2 = 0; f2 < F; ++f2) {
+                uint64_t k2 = orc_rng4(hp->seed, (uint64_t)(2 * target + 1), (uint64_t)t,
+                                       (uint64_t)(nd->k + 1) * 32u + (uint64_t)f2);
+                if (k2 < kf || (k2 == kf && f2 < f)) ++rank;
+              }
+              fmask[f] = (uint8_t)(rank < mk);
+            }
+          }
           orc_node_hist(codes, F, nd->rows, nd->m, qg, qh, Hg, Hh);
           split = orc_best_split(Hg, Hh, F, nbins, fmask, users_col, hp->monotone_users, eg, eh, K, nd->lo, nd->hi,
                                  lambda, mcw, &sp);
         }
         if (!split) {
-          /* O8 — leaf value v = (float)(eta * W(G,H,lo,hi)) */
+          /* O8 — leaf value v = (float)(eta * W(G,H,lo,hi)); random forest (R36): (float)(W / T), so
+           * the prediction base + sum_t v_t is the average of the trees */
           double Gd = ldexp((double)Gn, eg - K), Hd = ldexp((double)Hn, eh - K);
-          float v = (float)(eta * orc_calc_weight(Gd, Hd, nd->lo, nd->hi, lambda, mcw));
+          double Wl = orc_calc_weight(Gd, Hd, nd->lo, nd->hi, lambda, mcw);
+          float v = rf ? (float)(Wl / (double)hp->n_trees) : (float)(eta * Wl);
           tf[nd->k] = -1;
           tv[nd->k] = v;
           for (int64_t r = 0; r < nd->m; ++r) leaf_of[nd->rows[r]] = nd->k;
@@ -413,6 +460,10 @@ int orc_fit_gain(const float* X, const float* y, const float* w_in, const int32_
   if (n < 1 || F < 1 || F > ORC_MAX_F || users_col < 0 || users_col >= F) return 1;
   if (hp->max_depth < 1 || hp->max_depth > 12 || hp->n_trees < 0 || hp->grad_bits < 2 || hp->grad_bits > 14) return 1;
   if (hp->max_bin < 2 || hp->max_bin > 256) return 1;
+  if (hp->model != 0 && hp->model != 1) return 1;
+  if (hp->model == 1 && (!(hp->max_features > 0.0f && hp->max_features <= 1.0f) || hp->subsample != 1.0f ||
+                         hp->monotone_users != 0))
+    return 1;
   for (int64_t i = 0; i < n * F; ++i)
     if (!isfinite(X[i])) return 1;
   for (int64_t i = 0; i < n * 2; ++i)

@@ -26,7 +26,17 @@ typedef struct {
   float eta, lambda, min_child_weight, subsample, colsample_bytree;
   uint64_t seed;
   int32_t use_eq4_weights, monotone_users;
+  /* model = 1: random-forest regressor (DESIGN R33-R36):
+   * trees fit independently on Poisson(1) bootstrap counts, max_features sampled per node, leaf =
+   * weighted mean / n_trees, no boosting, base 0.  rf_bootstrap = 0 disables the bootstrap (c = 1). */
+  int32_t model;
+  float max_features;
+  int32_t rf_bootstrap;
 } orc_hparams;
+
+/* RF bootstrap count of (tree t, global row i): Poisson(1) by inversion of u = top 53 bits of
+ * rng4(seed, 0x5246, t, i) / 2^53 (DESIGN R34) */
+int32_t orc_poisson1(uint64_t seed, int32_t t, int64_t i);
 
 /* counter-based generator: sm64 finaliser chained over (seed, a, b, c) */
 uint64_t orc_rng4(uint64_t seed, uint64_t a, uint64_t b, uint64_t c);
