@@ -73,6 +73,7 @@ def parse():
     ap.add_argument("--no-wg", action="store_true", help="skip the workload-generator leg")
     ap.add_argument("--no-cv", action="store_true", help="skip the paper-shaped C2 cross-validation legs")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 recommendation-sweep leg")
+    ap.add_argument("--no-rf", action="store_true", help="skip the random-forest trace-importance leg")
     ap.add_argument("--strong", action="store_true",
                     help="BASELINE configs[3]: 100M rows (781,250 LLMs) in total, row-sharded over the N ranks "
                          "(strong scaling) instead of 10M rows per GPU")
@@ -260,6 +261,42 @@ def bench_c5(lp, ctx, stream, dev, args, rank, world):
             "node_visits_per_row": 2 * 1000 * 6,
             "note": "the predictor routes on bin codes through fixed-depth trees: SM-issue bound, not HBM "
                     "(DESIGN.md §6); node visits/s against the issue-rate bound there"}
+
+
+def bench_rf_traces(lp, ctx, stream, dev, args):
+    """The paper's random-forest importance study (§III-A): an RF regressor predicting the
+    latency of every request of a Table II-sized trace (17.3M requests x 8 parameters)
+    from its parameters, then the MDI importance.  100 trees, depth 10, half the parameters per node,
+    Poisson(1) bootstrap (DESIGN R33-R36); device-timed fit after one warm-up fit."""
+    import torch
+
+    import synth
+    n = args.wg_rows
+    T = synth.make_traces(n, seed=0)
+    y = synth.trace_latency(T, seed=0)
+    Td, yd = torch.from_numpy(T).to(dev), torch.from_numpy(y).to(dev)
+    hp = lp.rf_hparams(n_trees=100, max_depth=10, max_features=0.5, seed=1)
+    lp.fit(ctx, Td, yd, lp.rf_hparams(n_trees=2, max_depth=10, max_features=0.5, seed=1), T.shape[1] - 1).free()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    m = lp.fit(ctx, Td, yd, hp, T.shape[1] - 1)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    imp = m.importance()
+    pred = m.predict(ctx, Td[: 1 << 20])
+    yt = y[: 1 << 20, 0].astype(np.float64)
+    r2 = 1.0 - float(((pred[:, 0] - yt) ** 2).sum() / ((yt - yt.mean()) ** 2).sum())
+    m.free()
+    order = [synth.TRACE_PARAMS[i] for i in np.argsort(-imp[0])]
+    return {"workload": "RF regressor on %d synthetic trace requests x %d parameters, 2 targets (latency, latency "
+                        "per output token) x 100 trees, depth 10, max_features 0.5, Poisson(1) bootstrap" %
+                        (n, T.shape[1]),
+            "value": 2.0 * 100 * n / (ms / 1000.0), "unit": "row-iters/s", "ms": ms,
+            "r2_latency_train_first_1M": r2, "mdi_order_latency": order,
+            "paper_context": "R^2 ~ 0.93 on the real traces; MDI: output tokens, then input tokens, batch size, "
+                             "sampling parameters (P:L120)"}
 
 
 def measured_peaks():
@@ -696,6 +733,9 @@ def main():
     wg = None
     if rank == 0 and world == 1 and not args.no_wg:
         wg = bench_wg(lp, ctx, stream, dev, args)
+    rf = None
+    if rank == 0 and world == 1 and not args.no_rf:
+        rf = bench_rf_traces(lp, ctx, stream, dev, args)
     # ---- the paper-shaped config (BASELINE.json configs[1]): full leave-one-LLM-out CV of C2
     cv_c2 = cv_grid = None
     if rank == 0 and world == 1 and not args.no_cv:
@@ -743,6 +783,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "workload_generator": wg,
+            "rf_traces": rf,
             "cv_c2": cv_c2,
             "cv_c2_grid": cv_grid,
             "c5_sweep": c5,

@@ -126,10 +126,21 @@ typedef struct {
   uint64_t seed;            /* counter-based RNG seed for the two subsamplings */
   int32_t use_eq4_weights;  /* 1 = paper's Eq. (4) sample weights; 0 = dataset.w or 1 */
   int32_t monotone_users;   /* 1 = paper's monotone constraint on users */
+  /* model = 1: random-forest regressor, the model of the paper's MDI importance studies ("a
+   * RF regressor ... to predict the latency", "a RF regressor to predict the TTFT and ITL";
+   * DESIGN R33-R36): every tree fits y itself on Poisson(1) bootstrap counts of the rows (integer
+   * weights, counter-based per (tree, global row)), with ceil(max_features F) features sampled per
+   * node; leaf = (float)(W / n_trees) (lambda as given, so the prediction base(0) + sum_t v_t is the
+   * average of the trees); eta and colsample_bytree are ignored; requires subsample = 1 and
+   * monotone_users = 0.  rf_bootstrap = 0 fits every tree on the plain weights. */
+  int32_t model;            /* 0 = gradient-boosted trees (the paper's performance model), 1 = random forest */
+  float max_features;       /* RF: fraction of the features sampled per node, (0, 1] */
+  int32_t rf_bootstrap;     /* RF: 1 = Poisson(1) bootstrap (default), 0 = none */
 } llmpilot_hparams;
 void llmpilot_hparams_default(llmpilot_hparams* hp); /* n_trees 100, depth 6, bins 256, K 14, eta .3,
                                                          lambda 1, mcw 1, subsample 1, colsample 1,
-                                                         seed 0, eq4 1, monotone 1 */
+                                                         seed 0, eq4 1, monotone 1, model 0 (GBDT),
+                                                         max_features 1, rf_bootstrap 1 */
 
 /* Quantile binning: per-feature cuts from a deterministic strided sample of at
  * most 2^20 rows, then code(x) = #{cuts <= x}.  X: n x F (host or device).  cuts_in != NULL

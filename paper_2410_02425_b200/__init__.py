@@ -34,7 +34,8 @@ class HParams(C.Structure):
                 ("grad_bits", C.c_int32), ("eta", C.c_float), ("lambda_", C.c_float),
                 ("min_child_weight", C.c_float), ("subsample", C.c_float),
                 ("colsample_bytree", C.c_float), ("seed", C.c_uint64),
-                ("use_eq4_weights", C.c_int32), ("monotone_users", C.c_int32)]
+                ("use_eq4_weights", C.c_int32), ("monotone_users", C.c_int32),
+                ("model", C.c_int32), ("max_features", C.c_float), ("rf_bootstrap", C.c_int32)]
 
 
 class DatasetC(C.Structure):
@@ -252,9 +253,18 @@ class Context:
 
 
 def hparams(n_trees=100, max_depth=6, max_bin=256, grad_bits=14, eta=0.3, lambda_=1.0, min_child_weight=1.0,
-            subsample=1.0, colsample_bytree=1.0, seed=0, use_eq4_weights=1, monotone_users=1) -> HParams:
+            subsample=1.0, colsample_bytree=1.0, seed=0, use_eq4_weights=1, monotone_users=1, model=0,
+            max_features=1.0, rf_bootstrap=1) -> HParams:
     return HParams(n_trees, max_depth, max_bin, grad_bits, eta, lambda_, min_child_weight, subsample,
-                   colsample_bytree, seed, use_eq4_weights, monotone_users)
+                   colsample_bytree, seed, use_eq4_weights, monotone_users, model, max_features, rf_bootstrap)
+
+
+def rf_hparams(n_trees=100, max_depth=8, max_bin=256, max_features=1.0, min_child_weight=0.0, seed=0,
+               use_eq4_weights=0, bootstrap=1, grad_bits=14) -> HParams:
+    """Random-forest regressor (DESIGN R33-R36): lambda 0, no monotone constraint."""
+    return hparams(n_trees=n_trees, max_depth=max_depth, max_bin=max_bin, grad_bits=grad_bits, eta=1.0, lambda_=0.0,
+                   min_child_weight=min_child_weight, seed=seed, use_eq4_weights=use_eq4_weights, monotone_users=0,
+                   model=1, max_features=max_features, rf_bootstrap=bootstrap)
 
 
 def _dataset(X, y, llm_id, prof_id, users_col, n_llm, n_prof, w=None, row_offset=0, n_global=None):

@@ -239,6 +239,9 @@ void llmpilot_hparams_default(llmpilot_hparams* hp) {
   hp->seed = 0;
   hp->use_eq4_weights = 1;
   hp->monotone_users = 1;
+  hp->model = 0;
+  hp->max_features = 1.0f;
+  hp->rf_bootstrap = 1;
 }
 
 llmpilot_status llmpilot_bin(llmpilot_ctx* ctx, const float* X, int64_t n, int32_t F, int32_t max_bin,

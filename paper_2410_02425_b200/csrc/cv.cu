@@ -111,7 +111,7 @@ bool small_path_ok(const DatasetDev& ds, const llmpilot_hparams* grid, int n_gri
   static const bool off = getenv("LLMP_CV_SMALL") && atoi(getenv("LLMP_CV_SMALL")) == 0;
   if (off || ds.n > (int64_t)fit_small_max_rows()) return false;
   for (int g = 0; g < n_grid; ++g)
-    if (grid[g].max_depth > 8) return false;
+    if (grid[g].max_depth > 8 || grid[g].model != 0) return false;   // (the small-fit kernel is GBDT only)
   return true;
 }
 

@@ -103,6 +103,8 @@ struct FitArgs {
   int urow;           // 1: the histogram kernels take the users column row-parallel
   int hist_swar;      // 1: k_hist's four-row fast path (group sums when no run changes)
   int built_by_h;     // 1 (sharded): the split kernel picks the built child by hessian sum
+  int rf, rf_boot;    // random forest (DESIGN R33-R36): bootstrap weights, per-node features, leaf W / T
+  float max_features;
   const uint32_t* cmask;  // [n/32 batches][32 lanes] precomputed change masks (k_cmask), or null
   int nn;
   FeatBest* fbest;            // [2^(D-1)][32] per-(node, feature) best split of the current level
@@ -130,6 +132,45 @@ __device__ __forceinline__ bool row_sampled_out(uint64_t seed, int target, int t
   uint64_t r = rng4(seed, (uint64_t)(2 * target), (uint64_t)t, (uint64_t)gi);
   double u = (double)(r >> 11) * 0x1.0p-53;
   return u >= (double)subsample;
+}
+
+// RF bootstrap count of (tree t, global row gi) (DESIGN R34): Poisson(1) by inversion of the top 53
+// bits of rng4(seed, 0x5246, t, gi), the terms and the running sum in fp64 in the oracle's order
+__device__ __forceinline__ int poisson1(uint64_t seed, int t, int64_t gi) {
+  const double u = (double)(rng4(seed, 0x5246u, (uint64_t)t, (uint64_t)gi) >> 11) * 0x1.0p-53;
+  double p = 0x1.78b56362cef38p-2;   // e^-1 rounded to double
+  double F = p;
+  int k = 0;
+  while (u >= F && k < 16) {
+    ++k;
+    p = __ddiv_rn(p, (double)k);
+    F = __dadd_rn(F, p);
+  }
+  return k;
+}
+
+// O4 gradient pair of global row gi for tree t: weighted squared error g = w (p - y), h = w, zeroed
+// when the row is sampled out; random forest (R33, R34): every tree fits y itself (p = 0) with the
+// row's bootstrap count as an integer weight, w_t = c_t,i w
+__device__ __forceinline__ void grad_pair(const FitArgs& a, int t, int64_t gi, float y, float w, float p, float& g,
+                                          float& h) {
+  if (a.rf) {
+    const float wt = a.rf_boot ? __fmul_rn((float)poisson1(a.seed, t, gi), w) : w;
+    g = __fmul_rn(wt, __fsub_rn(0.0f, y));
+    h = wt;
+    return;
+  }
+  g = __fmul_rn(w, __fsub_rn(p, y));
+  h = w;
+  if (row_sampled_out(a.seed, a.target, t, gi, a.subsample)) {
+    g = 0.f;
+    h = 0.f;
+  }
+}
+
+// O8 leaf value: (float)(eta W); random forest (R36): (float)(W / T), the trees' average
+__device__ __forceinline__ float leaf_value(const FitArgs& a, double W) {
+  return a.rf ? (float)__ddiv_rn(W, (double)a.T) : (float)__dmul_rn(a.eta, W);
 }
 
 // slot of node k at level d inside H[d&1]: built child of parent j -> j, sibling -> 2^(d-1)+j
@@ -374,12 +415,8 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitPair fp, cons
         uint32_t gp = ngp;
         if (MODE == HM_ROOT && lane < cnt) {
           const int64_t ridx = base + lane + (s_pstart[pc] - s_vstart[pc]);
-          float g = __fmul_rn(nw, __fsub_rn(np_, ny));
-          float h = nw;
-          if (row_sampled_out(a.seed, a.target, t, a.row_offset + ridx, a.subsample)) {
-            g = 0.f;
-            h = 0.f;
-          }
+          float g, h;
+          grad_pair(a, t, a.row_offset + ridx, ny, nw, np_, g, h);
           gp = pack_gp(quantize(g, scale_g), quantize(h, scale_h));
           a.gp_root[ridx] = gp;
         }
@@ -397,12 +434,8 @@ __global__ void __launch_bounds__(HIST_THREADS, 2) k_hist(const FitPair fp, cons
           const float pn = __fadd_rn(np_, s_val[k]);   // one fp32 rounding, tree order
           a.p[ridx] = pn;
           if (has_next) {
-            float g = __fmul_rn(nw, __fsub_rn(pn, ny));
-            float h = nw;
-            if (row_sampled_out(a.seed, a.target, t + 1, a.row_offset + ridx, a.subsample)) {
-              g = 0.f;
-              h = 0.f;
-            }
+            float g, h;
+            grad_pair(a, t + 1, a.row_offset + ridx, ny, nw, pn, g, h);
             mg = fmaxf(mg, fabsf(g));
             mh = fmaxf(mh, h);
             gp = pack_gp(quantize(g, scale_g), quantize(h, scale_h));
@@ -721,12 +754,8 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
         uint32_t gp = ngp;
         if (MODE == HM_ROOT && valid) {
           const int64_t ridx = base + lane + poff;
-          float g = __fmul_rn(nw, __fsub_rn(np_, ny));
-          float h = nw;
-          if (row_sampled_out(a.seed, a.target, t, a.row_offset + ridx, a.subsample)) {
-            g = 0.f;
-            h = 0.f;
-          }
+          float g, h;
+          grad_pair(a, t, a.row_offset + ridx, ny, nw, np_, g, h);
           gp = pack_gp(quantize(g, scale_g), quantize(h, scale_h));
           a.gp_root[ridx] = gp;
         }
@@ -754,12 +783,8 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
           const float pn = __fadd_rn(np_, s_lv[k - n_int]);   // one fp32 rounding, tree order
           a.p[ridx] = pn;
           if (has_next) {
-            float g = __fmul_rn(nw, __fsub_rn(pn, ny));
-            float h = nw;
-            if (row_sampled_out(a.seed, a.target, t + 1, a.row_offset + ridx, a.subsample)) {
-              g = 0.f;
-              h = 0.f;
-            }
+            float g, h;
+            grad_pair(a, t + 1, a.row_offset + ridx, ny, nw, pn, g, h);
             mg = fmaxf(mg, fabsf(g));
             mh = fmaxf(mh, h);
             gp = pack_gp(quantize(g, scale_g), quantize(h, scale_h));
@@ -1046,12 +1071,8 @@ __global__ void __launch_bounds__(R2_THREADS, 2) k_hist_root2(const FitPair fp) 
       int32_t qg = 0, qh = 0;
       if (lane < cnt) {
         const int64_t i = base + lane;
-        float g = __fmul_rn(wv, __fsub_rn(pv, yv));
-        float h = wv;
-        if (row_sampled_out(a.seed, a.target, t, a.row_offset + i, a.subsample)) {
-          g = 0.f;
-          h = 0.f;
-        }
+        float g, h;
+        grad_pair(a, t, a.row_offset + i, yv, wv, pv, g, h);
         qg = quantize(g, scale_g);
         qh = quantize(h, scale_h);
         a.gp_root[i] = pack_gp(qg, qh);
@@ -1494,12 +1515,15 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitPair fp, con
   const int64_t bgp = ig - g8[7], bhp = ih - h8[7];
   const int64_t Gq = __shfl_sync(0xffffffffu, ig, 31), Hq = __shfl_sync(0xffffffffu, ih, 31);
   bool fin = f < a.F;
-  if (fin && a.colsample < 1.0f) {
+  if (fin && (a.rf ? a.max_features < 1.0f : a.colsample < 1.0f)) {
+    // GBDT: the tree's column sample (O6.3); random forest (R35): the node's own sample, keys
+    // rng4(seed, 2 target + 1, t, (k + 1) 32 + f) with k the node's complete-tree index
     const int F = a.F;
-    int nkeep = (int)ceil((double)a.colsample * (double)F);
+    int nkeep = (int)ceil((double)(a.rf ? a.max_features : a.colsample) * (double)F);
     if (nkeep < 1) nkeep = 1;
-    const uint64_t kf = rng4(a.seed, (uint64_t)(2 * a.target + 1), (uint64_t)t, (uint64_t)f);
-    const uint64_t kl = lane < F ? rng4(a.seed, (uint64_t)(2 * a.target + 1), (uint64_t)t, (uint64_t)lane) : ~0ull;
+    const uint64_t c0 = a.rf ? (uint64_t)((1 << d) + k) * 32u : 0u;   // (1 << d) - 1 + k + 1
+    const uint64_t kf = rng4(a.seed, (uint64_t)(2 * a.target + 1), (uint64_t)t, c0 + (uint64_t)f);
+    const uint64_t kl = lane < F ? rng4(a.seed, (uint64_t)(2 * a.target + 1), (uint64_t)t, c0 + (uint64_t)lane) : ~0ull;
     const unsigned less = __ballot_sync(0xffffffffu, lane < F && (kl < kf || (kl == kf && lane < f)));
     fin = __popc(less) < nkeep;
   }
@@ -1660,14 +1684,14 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitPair fp, con
     } else {
       // children at max depth are leaves: v = (float)(eta * W(G, H, lo, hi))
       tfeat[2 * gk + 1] = -1;
-      tval[2 * gk + 1] = (float)__dmul_rn(a.eta, calc_weight(GL, HL, loL, hiL, lambda, mcw));
+      tval[2 * gk + 1] = leaf_value(a, calc_weight(GL, HL, loL, hiL, lambda, mcw));
       tfeat[2 * gk + 2] = -1;
-      tval[2 * gk + 2] = (float)__dmul_rn(a.eta, calc_weight(GR, HR, loR, hiR, lambda, mcw));
+      tval[2 * gk + 2] = leaf_value(a, calc_weight(GR, HR, loR, hiR, lambda, mcw));
     }
   } else {
     V.split_f[k] = -1;
     tfeat[gk] = -1;
-    tval[gk] = (float)__dmul_rn(a.eta, wP);
+    tval[gk] = leaf_value(a, wP);
   }
 }
 
@@ -1755,12 +1779,8 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update(const FitPair fp) {
         const float pn = __fadd_rn(pv[q], s_val[k[q]]);  // O9: one fp32 rounding
         a.p[i] = pn;
         if (has_next) {
-          float g = __fmul_rn(wv[q], __fsub_rn(pn, yv[q]));
-          float h = wv[q];
-          if (row_sampled_out(a.seed, a.target, t + 1, a.row_offset + i, a.subsample)) {
-            g = 0.f;
-            h = 0.f;
-          }
+          float g, h;
+          grad_pair(a, t + 1, a.row_offset + i, yv[q], wv[q], pn, g, h);
           mg = fmaxf(mg, fabsf(g));
           mh = fmaxf(mh, h);
         }
@@ -1819,19 +1839,16 @@ __global__ void __launch_bounds__(BASE_THREADS) k_base_init(const FitArgs a, con
   __shared__ float s_a[BASE_THREADS / 32], s_b[BASE_THREADS / 32];
   const double G = dequant(sums[0], exp2i(exp_of(__uint_as_float(a.maxg[a.T])) - a.K));
   const double H = dequant(sums[1], exp2i(exp_of(__uint_as_float(a.maxh[a.T])) - a.K));
-  const float base = H > 0.0 ? (float)__ddiv_rn(-G, H) : 0.0f;
+  // random forest (R33): no intercept — every tree predicts the mean of its bootstrap
+  const float base = a.rf ? 0.0f : H > 0.0 ? (float)__ddiv_rn(-G, H) : 0.0f;
   if (blockIdx.x == 0 && threadIdx.x == 0) *base_out = base;
   float mg = 0.f, mh = 0.f;
   for (int64_t i = (int64_t)blockIdx.x * BASE_THREADS + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * BASE_THREADS) {
     a.p[i] = base;
     if (a.T > 0) {
       const float wv = a.w[i];
-      float g = __fmul_rn(wv, __fsub_rn(base, a.y[i]));
-      float h = wv;
-      if (row_sampled_out(a.seed, a.target, 0, a.row_offset + i, a.subsample)) {
-        g = 0.f;
-        h = 0.f;
-      }
+      float g, h;
+      grad_pair(a, 0, a.row_offset + i, a.y[i], wv, base, g, h);
       mg = fmaxf(mg, fabsf(g));
       mh = fmaxf(mh, h);
     }
@@ -1949,6 +1966,12 @@ void validate_hparams(const llmpilot_hparams& hp) {
   LLMP_REQUIRE(hp.lambda >= 0.0f && isfinite(hp.lambda), "lambda must be >= 0");
   LLMP_REQUIRE(hp.min_child_weight >= 0.0f && isfinite(hp.min_child_weight), "min_child_weight must be >= 0");
   LLMP_REQUIRE(isfinite(hp.eta), "eta must be finite");
+  LLMP_REQUIRE(hp.model == 0 || hp.model == 1, "model must be 0 (GBDT) or 1 (random forest)");
+  if (hp.model == 1) {
+    LLMP_REQUIRE(hp.max_features > 0.0f && hp.max_features <= 1.0f, "max_features must be in (0, 1]");
+    LLMP_REQUIRE(hp.subsample == 1.0f, "random forest: subsample must be 1 (the bootstrap samples the rows)");
+    LLMP_REQUIRE(hp.monotone_users == 0, "random forest: monotone_users must be 0");
+  }
 }
 
 static int grid_for(Ctx* ctx, int64_t n, int threads, int per_sm) {
@@ -2115,6 +2138,9 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     a.urow = urow ? 1 : 0;
     a.hist_swar = hist_swar ? 1 : 0;
     a.built_by_h = sharded ? 1 : 0;
+    a.rf = hp.model == 1 ? 1 : 0;
+    a.rf_boot = hp.rf_bootstrap ? 1 : 0;
+    a.max_features = hp.max_features;
     a.cmask = cmask;
     a.nn = nn;
     a.units = ctx->d_units;

@@ -470,12 +470,8 @@ __global__ void __launch_bounds__(U3_THREADS, 1) k_upd3(const FitPair fp) {
       if (valid) {
         a.p[ridx] = pn;
         if (has_next) {   // O4 for tree t+1 with tree t's exponents (speculation)
-          float g = __fmul_rn(wv, __fsub_rn(pn, yv));
-          float h = wv;
-          if (row_sampled_out(a.seed, a.target, t + 1, a.row_offset + ridx, a.subsample)) {
-            g = 0.f;
-            h = 0.f;
-          }
+          float g, h;
+          grad_pair(a, t + 1, a.row_offset + ridx, yv, wv, pn, g, h);
           mg = fmaxf(mg, fabsf(g));
           mh = fmaxf(mh, h);
           gp = pack_gp(quantize(g, scale_g), quantize(h, scale_h));

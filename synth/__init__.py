@@ -304,3 +304,18 @@ def make_traces(n: int, seed: int = 0, first: int = 0) -> np.ndarray:
     top_k = np.where(samp > 0, np.array([0.0, 10.0, 50.0, 100.0])[(u01(seed, r, 907) * 4).astype(np.int64)], 0.0)
     mnt = np.minimum(2.0 ** np.ceil(np.log2(out + 1)), 4096)
     return np.stack([inp, out, bs, samp, temp, top_p, top_k, mnt], axis=1).astype(np.float32)
+
+
+def trace_latency(T: np.ndarray, seed: int = 0, first: int = 0) -> np.ndarray:
+    """End-to-end latency (s) of each trace request, for the RF + MDI study of P:L120 (a regressor
+    predicting the latency of individual requests from their parameters): prefill proportional to
+    the input tokens, decode proportional to the output tokens times a per-token time that grows with
+    the batch size and with sampling, lognormal noise (sigma 0.1).  The ordering the paper reports —
+    output tokens, then input tokens, then batch size and the sampling parameters — follows from the
+    magnitudes.  n x 2 float32 (latency, per-output-token latency)."""
+    n = T.shape[0]
+    r = np.arange(first, first + n, dtype=np.uint64)
+    inp, out, bs, samp, temp = (T[:, k].astype(np.float64) for k in range(5))
+    tpot = 0.012 * (1.0 + 0.04 * bs) * (1.0 + 0.15 * samp + 0.05 * temp)
+    lat = (0.05 + 0.0008 * inp + out * tpot) * np.exp(0.1 * normal(seed, r, 910))
+    return np.stack([lat, lat / np.maximum(out, 1.0)], axis=1).astype(np.float32)

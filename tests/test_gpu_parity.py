@@ -615,3 +615,33 @@ def test_workload_generator_errors(lp, ctx):
         lp.WorkloadGenerator(ctx, np.array([[1.0, np.inf]], np.float32))
     with pytest.raises(lp.LLMPilotError):
         lp.WorkloadGenerator(ctx, np.tile(np.arange(64, dtype=np.float32)[:, None], (1, 11)))
+
+
+# ------------------------------------------------------------------------------ random forest
+@pytest.mark.parametrize("case", ["c2", "s1", "traces"])
+def test_random_forest_parity(lp, ctx, case):
+    """NEXT-1 (DESIGN R33-R36): the random-forest regressor — Poisson(1) bootstrap
+    counts, per-node feature samples, leaf = W / T — bit-exact with the oracle: trees, training
+    predictions, predictions, and the MDI importance."""
+    import synth as sy
+    if case == "c2":
+        d = sy.make("C2")
+        X, y, w, uc, kw = d.X, d.y, None, d.users_col, dict(n_trees=12, max_depth=6, max_features=0.5, seed=3)
+    elif case == "s1":
+        d = sy.make_s1(40001, seed=2)
+        X, y, w, uc, kw = d.X, d.y, d.w, d.users_col, dict(n_trees=6, max_depth=8, max_features=0.25, seed=9,
+                                                          min_child_weight=2.0)
+    else:
+        T = sy.make_traces(150_000, seed=0)
+        oi, ii = sy.TRACE_PARAMS.index("output_tokens"), sy.TRACE_PARAMS.index("input_tokens")
+        lat = (0.02 * T[:, oi] + 0.002 * T[:, ii]).astype(np.float32)
+        X, y, w, uc, kw = T, np.stack([lat, 2 * lat], axis=1), None, T.shape[1] - 1, dict(n_trees=8, max_depth=7,
+                                                                                         max_features=0.5, seed=1)
+    om, otp = oracle.fit(X, y, oracle.rf_hparams(**kw), uc, w=w, return_train_pred=True)
+    gm = lp.fit(ctx, torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda(), lp.rf_hparams(**kw), uc,
+                w=None if w is None else torch.from_numpy(w).cuda())
+    _assert_same_model(om, gm.export(), case)
+    assert _bits_equal(otp, gm.train_pred(len(X)))
+    assert _bits_equal(oracle.predict(om, X), gm.predict(ctx, X))
+    assert np.array_equal(oracle.importance(om), gm.importance())
+    gm.free()
