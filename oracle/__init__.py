@@ -20,7 +20,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "llmpilot_oracle.c")
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 MAX_F = 32
-MAX_BIN = 256
+MAX_BIN = 1024   # bins per feature (16-bit codes, NEXT-4)
 
 GCC_FLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-msse2", "-mfpmath=sse",
              "-fPIC", "-shared"]
@@ -42,17 +42,18 @@ class Hparams(C.Structure):
                 ("min_child_weight", C.c_float), ("subsample", C.c_float),
                 ("colsample_bytree", C.c_float), ("seed", C.c_uint64),
                 ("use_eq4_weights", C.c_int32), ("monotone_users", C.c_int32),
-                ("model", C.c_int32), ("max_features", C.c_float), ("rf_bootstrap", C.c_int32)]
+                ("model", C.c_int32), ("max_features", C.c_float), ("rf_bootstrap", C.c_int32),
+                ("tree_method", C.c_int32)]
 
 
 def hparams(n_trees=20, max_depth=4, max_bin=256, grad_bits=14, eta=0.3, lambda_=1.0,
             min_child_weight=1.0, subsample=1.0, colsample_bytree=1.0, seed=0, use_eq4_weights=1,
-            monotone_users=1, model=0, max_features=1.0, rf_bootstrap=1) -> Hparams:
+            monotone_users=1, model=0, max_features=1.0, rf_bootstrap=1, tree_method=0) -> Hparams:
     """Defaults = XGBoost defaults with K = 14 gradient bits.
     model=1: random forest (DESIGN R33-R36)."""
     return Hparams(n_trees, max_depth, max_bin, grad_bits, eta, lambda_, min_child_weight,
                    subsample, colsample_bytree, seed, use_eq4_weights, monotone_users, model, max_features,
-                   rf_bootstrap)
+                   rf_bootstrap, tree_method)
 
 
 def rf_hparams(n_trees=20, max_depth=8, max_bin=256, max_features=1.0, min_child_weight=0.0, seed=0,
@@ -156,7 +157,8 @@ def weights(y, llm_id, prof_id, n_llm, n_prof, L1, L2) -> np.ndarray:
 
 
 def cuts(X, max_bin=256, row_offset=0, n_global=None):
-    """O2 cuts -> (cuts [F, 255] float32, ncuts [F] int32)."""
+    """O2 cuts -> (cuts [F, MAX_BIN - 1] float32, ncuts [F] int32).  max_bin = 0: exact (every
+    distinct value its own bin)."""
     X = _c(X, np.float32)
     n, F = X.shape
     ct = np.zeros((MAX_F, MAX_BIN - 1), np.float32)
@@ -170,11 +172,11 @@ def cuts(X, max_bin=256, row_offset=0, n_global=None):
 def codes(X, ct, nc) -> np.ndarray:
     X = _c(X, np.float32)
     n, F = X.shape
-    ctf = np.zeros((MAX_F, MAX_BIN - 1), np.float32); ctf[:F] = ct
+    ctf = np.zeros((MAX_F, MAX_BIN - 1), np.float32); ctf[:F, :ct.shape[1]] = ct
     ncf = np.zeros(MAX_F, np.int32); ncf[:F] = nc
-    out = np.empty((n, F), np.uint8)
+    out = np.empty((n, F), np.uint16)
     lib().orc_codes(_p(X), n, F, _p(ctf), _p(ncf), _p(out))
-    return out
+    return out if out.size and out.max() > 255 else out.astype(np.uint8)
 
 
 def quantize(v, K):
@@ -193,18 +195,21 @@ def calc_gain(G, H, w, lambda_) -> float:
 
 
 def node_hist(codes_, rows, qg, qh):
-    codes_ = _c(codes_, np.uint8); rows = _c(rows, np.int64)
+    codes_ = _c(codes_, np.uint16); rows = _c(rows, np.int64)
     qg = _c(qg, np.int32); qh = _c(qh, np.int32)
     F = codes_.shape[1]
-    Hg = np.zeros((F, 256), np.int64); Hh = np.zeros((F, 256), np.int64)
+    Hg = np.zeros((F, MAX_BIN), np.int64); Hh = np.zeros((F, MAX_BIN), np.int64)
     lib().orc_node_hist(_p(codes_), F, _p(rows), len(rows), _p(qg), _p(qh), _p(Hg), _p(Hh))
     return Hg, Hh
 
 
 def best_split(Hg, Hh, nbins, users_col=-1, monotone_users=0, eg=0, eh=0, K=0, lo=-np.inf, hi=np.inf,
                lambda_=1.0, mcw=1.0, fmask=None):
+    F = np.asarray(Hg).shape[0]
+    if np.asarray(Hg).shape[1] < MAX_BIN:   # accept narrower hand-built histograms
+        Hg = np.pad(np.asarray(Hg), ((0, 0), (0, MAX_BIN - np.asarray(Hg).shape[1])))
+        Hh = np.pad(np.asarray(Hh), ((0, 0), (0, MAX_BIN - np.asarray(Hh).shape[1])))
     Hg = _c(Hg, np.int64); Hh = _c(Hh, np.int64)
-    F = Hg.shape[0]
     nb = _c(nbins, np.int32)
     fm = _c(np.ones(F) if fmask is None else fmask, np.uint8)
     s = Split()

@@ -82,7 +82,7 @@ static int cmp_float(const void* a, const void* b) {
 
 int orc_cuts(const float* X, int64_t n, int32_t F, int64_t row_offset, int64_t n_global, int32_t max_bin,
              float* cuts, int32_t* ncuts) {
-  if (F < 1 || F > ORC_MAX_F || max_bin < 2 || max_bin > ORC_MAX_BIN || n < 1) return 1;
+  if (F < 1 || F > ORC_MAX_F || !(max_bin == 0 || (max_bin >= 2 && max_bin <= ORC_MAX_BIN)) || n < 1) return 1;
   const int64_t cap = (int64_t)1 << 20;
   int64_t s = (n_global + cap - 1) / cap;
   if (s < 1) s = 1;
@@ -106,7 +106,11 @@ int orc_cuts(const float* X, int64_t n, int32_t F, int64_t row_offset, int64_t n
       if (i == 0 || v[i] != v[i - 1]) ++ndist;
     int32_t nc = 0;
     float* cf = cuts + (int64_t)f * (ORC_MAX_BIN - 1);
-    if (ndist <= max_bin) {
+    if (max_bin == 0 && ndist > ORC_MAX_BIN) { /* exact: more distinct values than codes */
+      free(v);
+      return 1;
+    }
+    if (max_bin == 0 || ndist <= max_bin) {
       /* cuts = [d_2 .. d_k] */
       for (int64_t i = 1; i < m; ++i)
         if (v[i] != v[i - 1]) cf[nc++] = v[i];
@@ -125,7 +129,7 @@ int orc_cuts(const float* X, int64_t n, int32_t F, int64_t row_offset, int64_t n
   return 0;
 }
 
-void orc_codes(const float* X, int64_t n, int32_t F, const float* cuts, const int32_t* ncuts, uint8_t* codes) {
+void orc_codes(const float* X, int64_t n, int32_t F, const float* cuts, const int32_t* ncuts, uint16_t* codes) {
   for (int64_t i = 0; i < n; ++i)
     for (int32_t f = 0; f < F; ++f) {
       const float* cf = cuts + (int64_t)f * (ORC_MAX_BIN - 1);
@@ -137,7 +141,7 @@ void orc_codes(const float* X, int64_t n, int32_t F, const float* cuts, const in
         if (cf[mid] <= x) lo = mid + 1;
         else hi = mid;
       }
-      codes[i * F + f] = (uint8_t)lo;
+      codes[i * F + f] = (uint16_t)lo;
     }
 }
 
@@ -167,16 +171,16 @@ double orc_calc_gain(double G, double H, double w, double lambda) {
 }
 
 /* O5 — Hg[f][b] = sum_{i in node, code_if = b} q_g,i ; likewise Hh */
-void orc_node_hist(const uint8_t* codes, int32_t F, const int64_t* idx, int64_t m, const int32_t* qg,
+void orc_node_hist(const uint16_t* codes, int32_t F, const int64_t* idx, int64_t m, const int32_t* qg,
                    const int32_t* qh, int64_t* Hg, int64_t* Hh) {
-  memset(Hg, 0, sizeof(int64_t) * (size_t)F * 256);
-  memset(Hh, 0, sizeof(int64_t) * (size_t)F * 256);
+  memset(Hg, 0, sizeof(int64_t) * (size_t)F * ORC_MAX_BIN);
+  memset(Hh, 0, sizeof(int64_t) * (size_t)F * ORC_MAX_BIN);
   for (int64_t j = 0; j < m; ++j) {
     int64_t i = idx[j];
     for (int32_t f = 0; f < F; ++f) {
       int32_t b = codes[i * F + f];
-      Hg[f * 256 + b] += qg[i];
-      Hh[f * 256 + b] += qh[i];
+      Hg[f * ORC_MAX_BIN + b] += qg[i];
+      Hh[f * ORC_MAX_BIN + b] += qh[i];
     }
   }
 }
@@ -186,7 +190,7 @@ int orc_best_split(const int64_t* Hg, const int64_t* Hh, int32_t F, const int32_
                    double hi, double lambda, double mcw, orc_split* out) {
   /* node totals: every feature's histogram sums to them; read feature 0 */
   int64_t Gq = 0, Hq = 0;
-  for (int32_t b = 0; b < 256; ++b) {
+  for (int32_t b = 0; b < ORC_MAX_BIN; ++b) {
     Gq += Hg[b];
     Hq += Hh[b];
   }
@@ -199,8 +203,8 @@ int orc_best_split(const int64_t* Hg, const int64_t* Hh, int32_t F, const int32_
     if (!fmask[f]) continue;
     int64_t GLq = 0, HLq = 0;
     for (int32_t b = 0; b + 1 < nbins[f]; ++b) {
-      GLq += Hg[f * 256 + b];
-      HLq += Hh[f * 256 + b];
+      GLq += Hg[f * ORC_MAX_BIN + b];
+      HLq += Hh[f * ORC_MAX_BIN + b];
       int64_t GRq = Gq - GLq, HRq = Hq - HLq;
       double GL = ldexp((double)GLq, eg - K), HL = ldexp((double)HLq, eh - K);
       double GR = ldexp((double)GRq, eg - K), HR = ldexp((double)HRq, eh - K);
@@ -236,7 +240,7 @@ typedef struct {
   double lo, hi;   /* monotone bounds */
 } orc_node;
 
-static int fit_one_target(const uint8_t* codes, const float* y, const float* w, int64_t n, int32_t F,
+static int fit_one_target(const uint16_t* codes, const float* y, const float* w, int64_t n, int32_t F,
                           int32_t users_col, int64_t row_offset, const orc_hparams* hp, const float* cuts,
                           const int32_t* ncuts, int target, float* base_out, int32_t* feat, int32_t* bin,
                           float* thr, float* val, double* gain, float* p, int32_t n_trees_fit) {
@@ -247,8 +251,8 @@ static int fit_one_target(const uint8_t* codes, const float* y, const float* w, 
   float* h = (float*)malloc(sizeof(float) * (size_t)n);
   int32_t* qg = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
   int32_t* qh = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
-  int64_t* Hg = (int64_t*)malloc(sizeof(int64_t) * (size_t)F * 256);
-  int64_t* Hh = (int64_t*)malloc(sizeof(int64_t) * (size_t)F * 256);
+  int64_t* Hg = (int64_t*)malloc(sizeof(int64_t) * (size_t)F * ORC_MAX_BIN);
+  int64_t* Hh = (int64_t*)malloc(sizeof(int64_t) * (size_t)F * ORC_MAX_BIN);
   int32_t nbins[ORC_MAX_F];
   for (int32_t f = 0; f < F; ++f) nbins[f] = ncuts[f] + 1;
 
@@ -459,7 +463,8 @@ int orc_fit_gain(const float* X, const float* y, const float* w_in, const int32_
                  int32_t n_trees_limit) {
   if (n < 1 || F < 1 || F > ORC_MAX_F || users_col < 0 || users_col >= F) return 1;
   if (hp->max_depth < 1 || hp->max_depth > 12 || hp->n_trees < 0 || hp->grad_bits < 2 || hp->grad_bits > 14) return 1;
-  if (hp->max_bin < 2 || hp->max_bin > 256) return 1;
+  if (hp->tree_method != 0 && hp->tree_method != 1) return 1;
+  if (hp->tree_method == 0 && (hp->max_bin < 2 || hp->max_bin > ORC_MAX_BIN)) return 1;
   if (hp->model != 0 && hp->model != 1) return 1;
   if (hp->model == 1 && (!(hp->max_features > 0.0f && hp->max_features <= 1.0f) || hp->subsample != 1.0f ||
                          hp->monotone_users != 0))
@@ -474,11 +479,11 @@ int orc_fit_gain(const float* X, const float* y, const float* w_in, const int32_
   } else {
     for (int64_t i = 0; i < n; ++i) w[i] = w_in ? w_in[i] : 1.0f;
   }
-  if (orc_cuts(X, n, F, row_offset, n_global, hp->max_bin, cuts, ncuts)) {
+  if (orc_cuts(X, n, F, row_offset, n_global, hp->tree_method == 1 ? 0 : hp->max_bin, cuts, ncuts)) {
     free(w);
     return 1;
   }
-  uint8_t* codes = (uint8_t*)malloc((size_t)n * F);
+  uint16_t* codes = (uint16_t*)malloc((size_t)n * F * sizeof(uint16_t));
   orc_codes(X, n, F, cuts, ncuts, codes);
   const int64_t n_nodes = ((int64_t)1 << (hp->max_depth + 1)) - 1;
   int32_t nt = hp->n_trees;
@@ -824,7 +829,7 @@ int orc_wg_build(const float* T, int64_t n, int32_t P, int32_t* nbins, float* ce
     free(cuts);
     return 1;
   }
-  uint8_t* codes = (uint8_t*)malloc((size_t)n * P);
+  uint16_t* codes = (uint16_t*)malloc((size_t)n * P * sizeof(uint16_t));
   orc_codes(T, n, P, cuts, ncuts, codes);
   /* per-bin min / max -> centres */
   double* mn = (double*)malloc(sizeof(double) * P * ORC_WG_BINS);

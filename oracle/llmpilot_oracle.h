@@ -19,7 +19,7 @@ extern "C" {
 #endif
 
 #define ORC_MAX_F 32
-#define ORC_MAX_BIN 256
+#define ORC_MAX_BIN 1024   /* bins per feature: codes are 16-bit */
 
 typedef struct {
   int32_t n_trees, max_depth, max_bin, grad_bits;
@@ -32,6 +32,9 @@ typedef struct {
   int32_t model;
   float max_features;
   int32_t rf_bootstrap;
+  /* tree building method: 0 = hist (O2 cuts with max_bin bins), 1 = exact (every distinct
+   * value of the sample its own bin, i.e. hist with unbounded max_bin; at most ORC_MAX_BIN) */
+  int32_t tree_method;
 } orc_hparams;
 
 /* RF bootstrap count of (tree t, global row i): Poisson(1) by inversion of u = top 53 bits of
@@ -46,12 +49,14 @@ void orc_weights(int64_t n, const float* y, const int32_t* llm_id, const int32_t
                  int32_t n_llm, int32_t n_prof, float L1, float L2, float* w_out);
 
 /* O2 — quantile cuts from the global-index strided sample; returns 0 on success.
- * cuts: F x 255 (row f holds ncuts[f] strictly increasing values). */
+ * cuts: F x (ORC_MAX_BIN - 1) (row f holds ncuts[f] strictly increasing values).  max_bin in
+ * [2, ORC_MAX_BIN]; max_bin = 0: exact (every distinct sample value starts a bin; fails if a
+ * feature has more than ORC_MAX_BIN distinct values). */
 int orc_cuts(const float* X, int64_t n, int32_t F, int64_t row_offset, int64_t n_global,
              int32_t max_bin, float* cuts, int32_t* ncuts);
-/* O2 — code(x) = #{c in cuts_f : c <= x}; codes n x F row-major */
+/* O2 — code(x) = #{c in cuts_f : c <= x}; codes n x F row-major (16-bit) */
 void orc_codes(const float* X, int64_t n, int32_t F, const float* cuts, const int32_t* ncuts,
-               uint8_t* codes);
+               uint16_t* codes);
 
 /* O4 — quantisation of one gradient vector: returns e (exponent) and writes q = rint(ldexpf(v, K-e)) */
 int32_t orc_quantize(int64_t n, const float* v, int32_t K, int32_t* q);
@@ -61,8 +66,8 @@ double orc_calc_weight(double G, double H, double lo, double hi, double lambda, 
 double orc_calc_gain(double G, double H, double w, double lambda);
 
 /* O5 — node histogram (int64), rows listed in idx[0..m) */
-void orc_node_hist(const uint8_t* codes, int32_t F, const int64_t* idx, int64_t m, const int32_t* qg,
-                   const int32_t* qh, int64_t* Hg /* F x 256 */, int64_t* Hh /* F x 256 */);
+void orc_node_hist(const uint16_t* codes, int32_t F, const int64_t* idx, int64_t m, const int32_t* qg,
+                   const int32_t* qh, int64_t* Hg /* F x ORC_MAX_BIN */, int64_t* Hh /* F x ORC_MAX_BIN */);
 
 /* O6 — split search on one node's histogram.  Returns 1 and fills (f,b,loss,wl,wr,...) if a split
  * with loss > 1e-6 exists among the features with fmask[f] != 0, else 0. */

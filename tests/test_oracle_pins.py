@@ -66,9 +66,11 @@ def test_o2_few_distinct_codes_are_ranks():
         assert all(codes[i, f] == rank[X[i, f]] for i in range(len(X)))
 
 
-def test_o2_equal_frequency_when_many_distinct():
+@pytest.mark.parametrize("B", [64, 256, 500, 1024])
+def test_o2_equal_frequency_when_many_distinct(B):
+    """O2 with B bins ("number of bins"; B > 256 gives 16-bit codes)."""
     rng = np.random.default_rng(1)
-    n, B = 10000, 64
+    n = 10000 if B <= 256 else 20 * B
     X = rng.standard_normal((n, 2)).astype(np.float32)
     ct, nc = oracle.cuts(X, max_bin=B)
     codes = oracle.codes(X, ct, nc)
@@ -77,6 +79,34 @@ def test_o2_equal_frequency_when_many_distinct():
         cnt = np.bincount(codes[:, f], minlength=B)
         # c_j = v[floor(j m / B)]: every bin holds floor(m/B) or ceil(m/B) sample values
         assert set(cnt.tolist()) <= {n // B, -(-n // B)}, cnt
+
+
+def test_o2_exact_tree_method_is_one_bin_per_distinct_value():
+    """P:L209 tree building method "exact" (DESIGN R13): every distinct value its own bin — the cuts
+    are the distinct values d_2..d_k (brute force), codes their ranks, identical to hist with any
+    max_bin >= k; a feature with more distinct values than 16-bit codes allow (ORC_MAX_BIN) fails;
+    a fit with tree_method = 1 equals the fit with max_bin = k."""
+    rng = np.random.default_rng(12)
+    vals = np.unique(rng.integers(-5000, 5000, 700)).astype(np.float32) / 4
+    X = rng.choice(vals, size=(6000, 2)).astype(np.float32)
+    ct, nc = oracle.cuts(X, max_bin=0)
+    codes = oracle.codes(X, ct, nc)
+    for f in range(2):
+        u = np.unique(X[:, f])
+        assert nc[f] == len(u) - 1 and np.array_equal(ct[f, :nc[f]], u[1:])
+        assert np.array_equal(codes[:, f], np.searchsorted(u, X[:, f]))
+    assert codes.dtype == np.uint16 and codes.max() > 255
+    ct2, nc2 = oracle.cuts(X, max_bin=1024)
+    assert np.array_equal(nc, nc2) and np.array_equal(ct, ct2)
+    with pytest.raises(ValueError):
+        oracle.cuts(rng.standard_normal((3000, 1)).astype(np.float32), max_bin=0)   # 3000 distinct > 1024
+    y = np.stack([X[:, 0] * 0.5 + X[:, 1], X[:, 1]], axis=1).astype(np.float32)
+    hp_e = oracle.hparams(n_trees=5, max_depth=4, tree_method=1, use_eq4_weights=0, monotone_users=0)
+    hp_h = oracle.hparams(n_trees=5, max_depth=4, max_bin=int(max(nc) + 1), use_eq4_weights=0, monotone_users=0)
+    me, mh = oracle.fit(X, y, hp_e, users_col=1), oracle.fit(X, y, hp_h, users_col=1)
+    for k in ("feat", "bin", "thr", "val", "base"):
+        assert np.array_equal(getattr(me, k), getattr(mh, k)), k
+    assert (me.bin[me.feat >= 0] > 255).any()   # thresholds beyond the 8-bit range are used
 
 
 def test_o2_code_threshold_equivalence_and_monotone():
