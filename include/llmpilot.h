@@ -116,7 +116,7 @@ typedef struct {
 typedef struct {
   int32_t n_trees;          /* >= 0 */
   int32_t max_depth;        /* 1..10 */
-  int32_t max_bin;          /* 2..256, number of histogram bins per feature */
+  int32_t max_bin;          /* 2..1024, number of histogram bins per feature (see tree_method) */
   int32_t grad_bits;        /* K: gradients quantised to K-bit integers per tree (2..14; default 14) */
   float eta;                /* learning rate */
   float lambda;             /* L2 regulariser on leaf weights */
@@ -136,11 +136,16 @@ typedef struct {
   int32_t model;            /* 0 = gradient-boosted trees (the paper's performance model), 1 = random forest */
   float max_features;       /* RF: fraction of the features sampled per node, (0, 1] */
   int32_t rf_bootstrap;     /* RF: 1 = Poisson(1) bootstrap (default), 0 = none */
+  /* tree building method: 0 = hist (max_bin bins per feature), 1 = exact (every distinct
+   * value of the cut sample its own bin = hist with unbounded max_bin).  More than 256 bins (16-bit
+   * codes, up to 1024) are supported by the cross-validation's batched small-fit path (n <= 8192
+   * rows, depth <= 8); llmpilot_fit keeps 8-bit codes and returns LLMP_EINVAL beyond 256 bins. */
+  int32_t tree_method;
 } llmpilot_hparams;
 void llmpilot_hparams_default(llmpilot_hparams* hp); /* n_trees 100, depth 6, bins 256, K 14, eta .3,
                                                          lambda 1, mcw 1, subsample 1, colsample 1,
                                                          seed 0, eq4 1, monotone 1, model 0 (GBDT),
-                                                         max_features 1, rf_bootstrap 1 */
+                                                         max_features 1, rf_bootstrap 1, tree_method 0 */
 
 /* Quantile binning: per-feature cuts from a deterministic strided sample of at
  * most 2^20 rows, then code(x) = #{cuts <= x}.  X: n x F (host or device).  cuts_in != NULL

@@ -35,7 +35,8 @@ class HParams(C.Structure):
                 ("min_child_weight", C.c_float), ("subsample", C.c_float),
                 ("colsample_bytree", C.c_float), ("seed", C.c_uint64),
                 ("use_eq4_weights", C.c_int32), ("monotone_users", C.c_int32),
-                ("model", C.c_int32), ("max_features", C.c_float), ("rf_bootstrap", C.c_int32)]
+                ("model", C.c_int32), ("max_features", C.c_float), ("rf_bootstrap", C.c_int32),
+                ("tree_method", C.c_int32)]
 
 
 class DatasetC(C.Structure):
@@ -254,9 +255,10 @@ class Context:
 
 def hparams(n_trees=100, max_depth=6, max_bin=256, grad_bits=14, eta=0.3, lambda_=1.0, min_child_weight=1.0,
             subsample=1.0, colsample_bytree=1.0, seed=0, use_eq4_weights=1, monotone_users=1, model=0,
-            max_features=1.0, rf_bootstrap=1) -> HParams:
+            max_features=1.0, rf_bootstrap=1, tree_method=0) -> HParams:
     return HParams(n_trees, max_depth, max_bin, grad_bits, eta, lambda_, min_child_weight, subsample,
-                   colsample_bytree, seed, use_eq4_weights, monotone_users, model, max_features, rf_bootstrap)
+                   colsample_bytree, seed, use_eq4_weights, monotone_users, model, max_features, rf_bootstrap,
+                   tree_method)
 
 
 def rf_hparams(n_trees=100, max_depth=8, max_bin=256, max_features=1.0, min_child_weight=0.0, seed=0,

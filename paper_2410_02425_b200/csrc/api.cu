@@ -242,6 +242,7 @@ void llmpilot_hparams_default(llmpilot_hparams* hp) {
   hp->model = 0;
   hp->max_features = 1.0f;
   hp->rf_bootstrap = 1;
+  hp->tree_method = 0;
 }
 
 llmpilot_status llmpilot_bin(llmpilot_ctx* ctx, const float* X, int64_t n, int32_t F, int32_t max_bin,

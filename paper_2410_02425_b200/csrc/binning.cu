@@ -32,11 +32,13 @@ __global__ void k_offsets(int64_t* off, int F, int64_t m) {
 
 // one CTA per feature over its sorted sample
 constexpr int CUT_THREADS = 1024;
-__global__ void __launch_bounds__(CUT_THREADS) k_select_cuts(const float* sorted, int64_t m, int B, float* cuts,
-                                                             int32_t* ncuts) {
+// B = 0: exact tree method (every distinct value its own bin; ncuts = -1 flags more distinct values
+// than the cut stride holds); stride: cuts per feature row (255 for 8-bit codes, 1023 for 16-bit)
+__global__ void __launch_bounds__(CUT_THREADS) k_select_cuts(const float* sorted, int64_t m, int B, int stride,
+                                                             float* cuts, int32_t* ncuts) {
   const int f = blockIdx.x;
   const float* v = sorted + (int64_t)f * m;
-  float* cf = cuts + (int64_t)f * (kBins - 1);
+  float* cf = cuts + (int64_t)f * stride;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ int64_t s_w[CUT_THREADS / 32];
   __shared__ int64_t s_total;
@@ -56,7 +58,9 @@ __global__ void __launch_bounds__(CUT_THREADS) k_select_cuts(const float* sorted
   if (tid == CUT_THREADS - 1) s_total = woff + inc;
   __syncthreads();
   const int64_t k = s_total;
-  if (k <= B) {
+  if (B == 0 && k - 1 > stride) {
+    if (tid == 0) ncuts[f] = -1;
+  } else if (B == 0 || k <= B) {
     // the r-th distinct value (0-based), r >= 1, is cut r-1
     int64_t r = woff + inc - cnt;
     for (int64_t i = c0; i < c1; ++i) {
@@ -79,9 +83,13 @@ __global__ void __launch_bounds__(CUT_THREADS) k_select_cuts(const float* sorted
 }
 
 void compute_cuts(Ctx* ctx, const float* X, int64_t n, int F, int64_t row_offset, int64_t n_global, int max_bin,
-                  CutsData& out, bool sharded) {
+                  CutsData& out, bool sharded, bool wide) {
   LLMP_REQUIRE(F >= 1 && F <= kMaxF, "n_features must be in [1, 32]");
-  LLMP_REQUIRE(max_bin >= 2 && max_bin <= kBins, "max_bin must be in [2, 256]");
+  const int cstride = wide ? kMaxCuts16 : kBins - 1;   // cuts per feature row
+  LLMP_REQUIRE(max_bin == 0 || (max_bin >= 2 && max_bin <= cstride + 1),
+               wide ? "max_bin must be in [2, 1024] (0: exact)"
+                    : "max_bin must be in [2, 256] (0: exact); more bins (16-bit codes) are supported by the batched "
+                      "small-fit path (cross-validation, n <= 8192 rows)");
   LLMP_REQUIRE(n >= 1 && n_global >= n, "bad row counts");
   cudaStream_t s = ctx->stream;
   const int64_t cap = int64_t(1) << 20;
@@ -146,19 +154,54 @@ void compute_cuts(Ctx* ctx, const float* X, int64_t n, int F, int64_t row_offset
   ctx->launches[KC_CUTS] += 1;
   out.F = F;
   out.max_bin = max_bin;
+  out.stride = cstride;
   out.d_cuts.set_stream(ctx->stream);
   out.d_ncuts.set_stream(ctx->stream);
-  out.d_cuts.ensure((size_t)kMaxF * (kBins - 1) * 4);
+  out.d_cuts.ensure((size_t)kMaxF * cstride * 4);
   out.d_ncuts.ensure((size_t)kMaxF * 4);
   LLMP_CUDA(cudaMemsetAsync(out.d_cuts.p, 0, out.d_cuts.bytes, s));
   LLMP_CUDA(cudaMemsetAsync(out.d_ncuts.p, 0, out.d_ncuts.bytes, s));
   LLMP_LAUNCH(ctx, KC_CUTS, m * F, k_select_cuts, F, CUT_THREADS, 0, sorted.as<float>(), m, max_bin,
-              out.d_cuts.as<float>(), out.d_ncuts.as<int32_t>());
-  out.h_cuts.assign((size_t)kMaxF * (kBins - 1), 0.f);
+              cstride, out.d_cuts.as<float>(), out.d_ncuts.as<int32_t>());
+  out.h_cuts.assign((size_t)kMaxF * cstride, 0.f);
   out.h_ncuts.assign(kMaxF, 0);
   LLMP_CUDA(cudaMemcpyAsync(out.h_cuts.data(), out.d_cuts.p, out.h_cuts.size() * 4, cudaMemcpyDeviceToHost, s));
   LLMP_CUDA(cudaMemcpyAsync(out.h_ncuts.data(), out.d_ncuts.p, kMaxF * 4, cudaMemcpyDeviceToHost, s));
   LLMP_CUDA(cudaStreamSynchronize(s));
+  for (int f = 0; f < F; ++f)
+    LLMP_REQUIRE(out.h_ncuts[f] >= 0, wide ? "exact tree method: a feature has more than 1024 distinct values"
+                                            : "exact tree method: a feature has more than 256 distinct values (the "
+                                              "8-bit code path); the small-fit path takes up to 1024");
+}
+
+// 16-bit codes with wide cuts (stride kMaxCuts16): one thread per (row, feature), binary search over
+// the feature's cuts in global memory (the small-fit path's data are small: L2-resident)
+__global__ void k_codes16(const float* __restrict__ X, int64_t n, int F, const float* __restrict__ cuts,
+                          const int32_t* __restrict__ ncuts, uint16_t* __restrict__ codes) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * kMaxF; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / kMaxF;
+    const int f = (int)(e % kMaxF);
+    uint16_t code = 0;
+    if (f < F) {
+      const float x = X[i * F + f];
+      const float* cf = cuts + (int64_t)f * kMaxCuts16;
+      int lo = 0, hi = ncuts[f];
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (cf[mid] <= x) lo = mid + 1;
+        else hi = mid;
+      }
+      code = (uint16_t)lo;
+    }
+    codes[e] = code;
+  }
+}
+
+void compute_codes16(Ctx* ctx, const float* X, int64_t n, int F, const CutsData& cuts, uint16_t* codes) {
+  LLMP_REQUIRE(cuts.stride == kMaxCuts16, "16-bit codes need wide cuts");
+  const int grid = (int)std::min<int64_t>(std::max<int64_t>((n * kMaxF + 255) / 256, 1), (int64_t)ctx->sms * 8);
+  LLMP_LAUNCH(ctx, KC_CODES, n, k_codes16, grid, 256, 0, X, n, F, cuts.d_cuts.as<float>(), cuts.d_ncuts.as<int32_t>(),
+              codes);
 }
 
 // codes: persistent CTAs of 256 threads over 128-row tiles, every transfer a bulk copy (TMA engine):
@@ -286,6 +329,7 @@ __global__ void __launch_bounds__(CODE_THREADS) k_codes(const float* __restrict_
 
 void compute_codes(Ctx* ctx, const float* X, int64_t n, int F, const CutsData& cuts, uint8_t* codes, uint8_t* codesT,
                    int64_t ldT, int* flag) {
+  LLMP_REQUIRE(cuts.stride == kBins - 1, "8-bit codes need at most 256 bins");
   int64_t tiles = (n + CODE_ROWS - 1) / CODE_ROWS;
   const int al = ((((uintptr_t)X & 15) == 0) ? 1 : 0) | ((((uintptr_t)codes & 15) == 0) ? 2 : 0) |
                  (((((uintptr_t)codesT | (uintptr_t)ldT) & 15) == 0) ? 4 : 0);

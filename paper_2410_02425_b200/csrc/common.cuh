@@ -18,6 +18,7 @@ constexpr int kMaxF = 32;        // features per row (codes padded to 32 bytes =
 constexpr int kBins = 256;       // histogram bins per feature (u8 codes)
 constexpr int kHistBins = kMaxF * kBins;  // 8192 (feature, bin) cells per node
 constexpr int kMaxDepth = 10;
+constexpr int kMaxCuts16 = 1023; // 16-bit codes (small-fit path): up to 1024 bins per feature
 constexpr int kMaxGradBits = 14; // |q_g| <= 2^14 fits int16; q_h <= 2^14 fits uint16 => 32-bit pair
 
 // kernel classes for instrumentation (llmpilot_kernel_class_name)

@@ -136,8 +136,8 @@ void run_batch(Ctx* ctx, const DatasetDev& ds, const std::vector<float>& w_host,
   size_t max_rows = 1;
   for (size_t i = 0; i < fits.size(); ++i) {
     const size_t n = fits[i].tr.size(), m = fits[i].te.size();
-    o_ctr[i] = take(n * kMaxF);
-    o_cte[i] = take(std::max<size_t>(m, 1) * kMaxF);
+    o_ctr[i] = take(n * kMaxF * 2);   // (room for 16-bit codes)
+    o_cte[i] = take(std::max<size_t>(m, 1) * kMaxF * 2);
     o_y[i] = take(n * 8);
     o_w[i] = take(n * 4);
     o_nc[i] = take(kMaxF * 4);
@@ -170,10 +170,21 @@ void run_batch(Ctx* ctx, const DatasetDev& ds, const std::vector<float>& w_host,
     const bool eq4 = grid[bf.hp].use_eq4_weights != 0;
     for (int64_t k = 0; k < n; ++k) wsub[k] = eq4 ? w_host[bf.tr[k]] : 1.0f;
     LLMP_CUDA(cudaMemcpyAsync(A + o_w[i], wsub.data(), (size_t)n * 4, cudaMemcpyHostToDevice, s));
+    // O2 on the fit's rows; more than 256 bins (or exact with more than 256 distinct values) take
+    // 16-bit codes (NEXT-4)
+    const llmpilot_hparams& hb = grid[bf.hp];
+    const bool wide = hb.tree_method == 1 || hb.max_bin > kBins;
     CutsData cuts;
-    compute_cuts(ctx, d_X.as<float>(), n, F, 0, n, grid[bf.hp].max_bin, cuts, false);   // O2 on the fit's rows
-    compute_codes(ctx, d_X.as<float>(), n, F, cuts, A + o_ctr[i], nullptr, 0, nullptr);
-    if (m > 0) compute_codes(ctx, d_X.as<float>() + (size_t)n * F, m, F, cuts, A + o_cte[i], nullptr, 0, nullptr);
+    compute_cuts(ctx, d_X.as<float>(), n, F, 0, n, hb.tree_method == 1 ? 0 : hb.max_bin, cuts, false, wide);
+    const int cw = wide ? 2 : 1;
+    if (cw == 1) {
+      compute_codes(ctx, d_X.as<float>(), n, F, cuts, A + o_ctr[i], nullptr, 0, nullptr);
+      if (m > 0) compute_codes(ctx, d_X.as<float>() + (size_t)n * F, m, F, cuts, A + o_cte[i], nullptr, 0, nullptr);
+    } else {
+      compute_codes16(ctx, d_X.as<float>(), n, F, cuts, reinterpret_cast<uint16_t*>(A + o_ctr[i]));
+      if (m > 0)
+        compute_codes16(ctx, d_X.as<float>() + (size_t)n * F, m, F, cuts, reinterpret_cast<uint16_t*>(A + o_cte[i]));
+    }
     LLMP_CUDA(cudaMemcpyAsync(A + o_nc[i], cuts.d_ncuts.p, kMaxF * 4, cudaMemcpyDeviceToDevice, s));
     LLMP_CUDA(cudaStreamSynchronize(s));   // wsub / cuts are reused by the next fit
     for (int tg = 0; tg < 2; ++tg) {
@@ -182,6 +193,7 @@ void run_batch(Ctx* ctx, const DatasetDev& ds, const std::vector<float>& w_host,
       itm.m_test = (int)m;
       itm.target = tg;
       itm.hp = bf.hp;
+      itm.cw = cw;
       itm.codes = A + o_ctr[i];
       itm.codes_test = A + o_cte[i];
       itm.y = reinterpret_cast<const float*>(A + o_y[i]);

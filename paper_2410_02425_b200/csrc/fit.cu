@@ -1666,7 +1666,7 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitPair fp, con
     V.split_b[k] = bs;
     tfeat[gk] = fs;
     tbin[gk] = bs;
-    tthr[gk] = a.cuts[fs * (kBins - 1) + bs];
+    tthr[gk] = a.cuts[fs * (kBins - 1) + bs];   // (8-bit code path: cut stride 255)
     tval[gk] = 0.0f;
     tgain[gk] = ml;   // the split's loss reduction (MDI)
     if (d + 1 < a.D) {
@@ -1959,7 +1959,9 @@ void compute_weights(Ctx* ctx, const DatasetDev& ds, float L1, float L2, float* 
 void validate_hparams(const llmpilot_hparams& hp) {
   LLMP_REQUIRE(hp.n_trees >= 0, "n_trees must be >= 0");
   LLMP_REQUIRE(hp.max_depth >= 1 && hp.max_depth <= kMaxDepth, "max_depth must be in [1, 10]");
-  LLMP_REQUIRE(hp.max_bin >= 2 && hp.max_bin <= kBins, "max_bin must be in [2, 256]");
+  LLMP_REQUIRE(hp.tree_method == 0 || hp.tree_method == 1, "tree_method must be 0 (hist) or 1 (exact)");
+  LLMP_REQUIRE(hp.tree_method == 1 || (hp.max_bin >= 2 && hp.max_bin <= kMaxCuts16 + 1),
+               "max_bin must be in [2, 1024]");
   LLMP_REQUIRE(hp.grad_bits >= 2 && hp.grad_bits <= kMaxGradBits, "grad_bits must be in [2, 14]");
   LLMP_REQUIRE(hp.subsample > 0.0f && hp.subsample <= 1.0f, "subsample must be in (0, 1]");
   LLMP_REQUIRE(hp.colsample_bytree > 0.0f && hp.colsample_bytree <= 1.0f, "colsample_bytree must be in (0, 1]");
@@ -2040,7 +2042,12 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
 
   phase("weights");
   // ---- cuts + codes (row-major for histograms/routing, column-major for partitions)
-  compute_cuts(ctx, ds.X, n, F, ds.row_offset, ds.n_global, hp.max_bin, out.cuts, ctx->sharded());
+  // this path keeps 8-bit codes (one 32-byte sector per row): at most 256 bins (exact: 256 distinct values)
+  LLMP_REQUIRE(hp.tree_method == 1 || hp.max_bin <= kBins,
+               "max_bin > 256 (16-bit codes) is supported by the batched small-fit path (cross-validation, n <= 8192 "
+               "rows, depth <= 8); this fit path takes at most 256 bins");
+  compute_cuts(ctx, ds.X, n, F, ds.row_offset, ds.n_global, hp.tree_method == 1 ? 0 : hp.max_bin, out.cuts,
+               ctx->sharded());
   DevBuf& d_codes = ctx->workspace("codes", (size_t)n * kMaxF);
   const int64_t ldT = (n + 31) / 32 * 32;
   DevBuf& d_codesT = ctx->workspace("codesT", (size_t)ldT * kMaxF);

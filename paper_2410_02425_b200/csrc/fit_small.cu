@@ -35,8 +35,9 @@ constexpr int SF_WARPS = SF_THREADS / 32;
 constexpr int SF_MAX_D = 8;
 constexpr int SF_MAX_NN = (1 << (SF_MAX_D + 1)) - 1;   // 511 tree nodes
 constexpr int SF_MAX_LVL = 1 << (SF_MAX_D - 1);        // 128 nodes at the deepest split level
-constexpr int SF_ROWB = 32;                            // staged code row
-constexpr int SF_STAGE = 32 * SF_ROWB + 32 * 4;        // per warp: 32 code rows + 32 slots
+// CW: bytes per code (1: up to 256 bins; 2: 16-bit codes, up to 1024 bins — NEXT-4)
+template <int CW> __host__ __device__ constexpr int sf_rowb() { return 32 * CW; }                    // staged code row
+template <int CW> __host__ __device__ constexpr int sf_stage() { return 32 * sf_rowb<CW>() + 32 * 4; }   // per warp: 32 rows + 32 slots
 constexpr int SF_RES = 32;                             // bytes per (node, feature) split result
 constexpr int SF_SMEM_CAP = 227 * 1024 - 24 * 1024;    // dynamic budget (static tables take the rest)
 
@@ -62,8 +63,10 @@ __device__ __forceinline__ float sf_wmax(float v) {   // warp max of non-negativ
   return v;
 }
 
+template <int CW>
 __global__ void __launch_bounds__(SF_THREADS, 1) k_fit_small(const SmallFitItem* items, const SmallFitHp* hps,
                                                              int smem_bytes) {
+  constexpr int SF_ROWB = sf_rowb<CW>(), SF_STAGE = sf_stage<CW>(), NW = 8 * CW;   // NW: 32-bit words per row
   const SmallFitItem it = items[blockIdx.x];
   const SmallFitHp hp = hps[it.hp];
   const int n = it.n, tg = it.target, F = hp.F, D = hp.D, T = hp.T, K = hp.K;
@@ -85,7 +88,7 @@ __global__ void __launch_bounds__(SF_THREADS, 1) k_fit_small(const SmallFitItem*
   __shared__ uint32_t s_inpk;
   __shared__ int s_nc[kMaxF];
   __shared__ int8_t s_tf[SF_MAX_NN];        // tree being grown: feature (-1 leaf, -2 absent)
-  __shared__ uint8_t s_tb[SF_MAX_NN];
+  __shared__ uint16_t s_tb[SF_MAX_NN];
   __shared__ float s_tv[SF_MAX_NN];
   __shared__ double s_lo[2][SF_MAX_LVL * 2], s_hi[2][SF_MAX_LVL * 2];   // bounds by level parity
   __shared__ int16_t s_list[SF_MAX_LVL];    // existing nodes of the level
@@ -93,7 +96,7 @@ __global__ void __launch_bounds__(SF_THREADS, 1) k_fit_small(const SmallFitItem*
   __shared__ long long s_tot[SF_MAX_LVL][2];   // node totals (q_g, q_h) of the pass
   __shared__ int16_t s_slot[SF_MAX_LVL];    // node -> slot of the current pass (-1: not in it)
   __shared__ int8_t s_sf[SF_MAX_LVL];       // split feature of each node of the level (-1 none)
-  __shared__ uint8_t s_sb[SF_MAX_LVL];
+  __shared__ uint16_t s_sb[SF_MAX_LVL];
   __shared__ int s_ne, s_ne_next;
   __shared__ uint32_t s_colmask;
   __shared__ unsigned s_mg, s_mh;
@@ -229,9 +232,13 @@ __global__ void __launch_bounds__(SF_THREADS, 1) k_fit_small(const SmallFitItem*
   const int uoff = ucol >= 0 ? s_off[ucol] : 0;
   // rows of this warp in identity order
   const int w0 = (int)((int64_t)n * warp / SF_WARPS), w1 = (int)((int64_t)n * (warp + 1) / SF_WARPS);
-  uint32_t um[8];   // the users byte is masked out of the change test (its column goes row-parallel)
-#pragma unroll
-  for (int j = 0; j < 8; ++j) um[j] = (ucol >= 0 && (ucol >> 2) == j) ? ~(0xffu << (8 * (ucol & 3))) : 0xffffffffu;
+  // the users code is masked out of the change test (its column goes row-parallel)
+  const int uwrd = CW == 1 ? ucol >> 2 : ucol >> 1;
+  const uint32_t umask = ucol < 0 ? 0xffffffffu
+                                  : CW == 1 ? ~(0xffu << (8 * (ucol & 3))) : ~(0xffffu << (16 * (ucol & 1)));
+  auto code_at = [&](const uint8_t* base, int64_t row, int f) -> uint32_t {   // code of (row, f) in global memory
+    return CW == 1 ? (uint32_t)base[row * kMaxF + f] : (uint32_t)reinterpret_cast<const uint16_t*>(base)[row * kMaxF + f];
+  };
 
   for (int t = 0; t < T; ++t) {
     // ---- O4: quantise tree t's pairs with its exponents; every row starts at the root
@@ -296,37 +303,46 @@ __global__ void __launch_bounds__(SF_THREADS, 1) k_fit_small(const SmallFitItem*
         for (int b0 = w0; b0 < w1; b0 += 32) {
           const int i = b0 + lane;
           const bool valid = i < w1;
-          uint4 c0 = make_uint4(0u, 0u, 0u, 0u), c1 = c0;
+          uint4 cv[2 * CW];
+#pragma unroll
+          for (int q = 0; q < 2 * CW; ++q) cv[q] = make_uint4(0u, 0u, 0u, 0u);
           int slot = -1;
           uint32_t gp = 0u;
           if (valid) {
-            const uint4* cr = reinterpret_cast<const uint4*>(codes + (size_t)i * kMaxF);
-            c0 = __ldg(cr);
-            c1 = __ldg(cr + 1);
+            const uint4* cr = reinterpret_cast<const uint4*>(codes + (size_t)i * SF_ROWB);
+#pragma unroll
+            for (int q = 0; q < 2 * CW; ++q) cv[q] = __ldg(cr + q);
             const int pk = s_pos[i];
             slot = pk >= 0 ? s_slot[pk] : -1;
             gp = slot >= 0 ? s_gp[i] : 0u;   // rows outside the pass add nothing
           }
           __syncwarp();
-          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sst + lane * SF_ROWB), "r"(c0.x), "r"(c0.y),
-                       "r"(c0.z), "r"(c0.w) : "memory");
-          asm volatile("st.shared.v4.u32 [%0+16], {%1, %2, %3, %4};" ::"r"(sst + lane * SF_ROWB), "r"(c1.x), "r"(c1.y),
-                       "r"(c1.z), "r"(c1.w) : "memory");
+#pragma unroll
+          for (int q = 0; q < 2 * CW; ++q)
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sst + lane * SF_ROWB + 16 * q), "r"(cv[q].x),
+                         "r"(cv[q].y), "r"(cv[q].z), "r"(cv[q].w) : "memory");
           asm volatile("st.shared.s32 [%0], %1;" ::"r"(sst + 32 * SF_ROWB + lane * 4), "r"(slot) : "memory");
           // change test against the previous row of the warp's range (row 0 of a batch: always flagged)
-          uint32_t pw[8];
-          const uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+          uint32_t cw[NW];
 #pragma unroll
-          for (int j = 0; j < 8; ++j) pw[j] = __shfl_up_sync(0xffffffffu, cw[j], 1);
+          for (int q = 0; q < 2 * CW; ++q) {
+            cw[4 * q] = cv[q].x;
+            cw[4 * q + 1] = cv[q].y;
+            cw[4 * q + 2] = cv[q].z;
+            cw[4 * q + 3] = cv[q].w;
+          }
           const int pslot = __shfl_up_sync(0xffffffffu, slot, 1);
           uint32_t dx = 0;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) dx |= (cw[j] ^ pw[j]) & um[j];
+          for (int j = 0; j < NW; ++j) dx |= (cw[j] ^ __shfl_up_sync(0xffffffffu, cw[j], 1)) & (j == uwrd ? umask : 0xffffffffu);
           unsigned B = __ballot_sync(0xffffffffu, valid && (lane == 0 || dx != 0u || slot != pslot));
           const int32_t qg = gp_g(gp);
           const uint32_t qh = (uint32_t)gp_h(gp);
           if (ucol >= 0 && slot >= 0) {   // users column, row-parallel
-            const uint32_t cu = (cw[ucol >> 2] >> (8 * (ucol & 3))) & 0xffu;
+            uint32_t wsel = 0;
+#pragma unroll
+            for (int j = 0; j < NW; ++j) wsel = j == uwrd ? cw[j] : wsel;
+            const uint32_t cu = CW == 1 ? (wsel >> (8 * (ucol & 3))) & 0xffu : (wsel >> (16 * (ucol & 1))) & 0xffffu;
             const uint32_t a = shg + (uint32_t)((slot * 2 * C + uoff + (int)cu) * 4);
             asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(a), "r"(qg) : "memory");
             asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(a + (uint32_t)C * 4u), "r"(qh) : "memory");
@@ -340,7 +356,8 @@ __global__ void __launch_bounds__(SF_THREADS, 1) k_fit_small(const SmallFitItem*
             int sl;
             asm volatile("ld.shared.s32 %0, [%1];" : "=r"(sl) : "r"(sst + 32 * SF_ROWB + r * 4));
             uint32_t c;
-            asm volatile("ld.shared.u8 %0, [%1];" : "=r"(c) : "r"(sst + r * SF_ROWB + lane));
+            if (CW == 1) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(c) : "r"(sst + r * SF_ROWB + lane));
+            else asm volatile("ld.shared.u16 %0, [%1];" : "=r"(c) : "r"(sst + r * SF_ROWB + 2 * lane));
             const int32_t vg = (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)(lane < r ? qg : 0));
             const uint32_t vh = __reduce_add_sync(0xffffffffu, lane < r ? qh : 0u);
             const int na = sl >= 0 ? sl * 2 * C + my_off + (int)c : -1;
@@ -367,8 +384,8 @@ __global__ void __launch_bounds__(SF_THREADS, 1) k_fit_small(const SmallFitItem*
         }
         __syncthreads();
         // ---- O6 per (node, feature pack): one warp evaluates up to four features of one node, lane
-        // = bin within a segment of 8, 16 or 32 lanes (segmented scans and argmax); features with
-        // more than 32 bins get a warp each, lane l owning bins 8l .. 8l+7.  A node's sums fit 32
+        // = bin within a segment of 8, 16 or 32 lanes (segmented scans and argmax); a feature with
+        // more than 32 bins gets a warp, lane l owning ceil(nb/32) consecutive bins.  A node's sums fit 32
         // bits (|sum q| <= n 2^K <= 2^27), so prefix sums are 32-bit.
         for (int task = warp; task < np * s_npk; task += SF_WARPS) {
           const int sl = task / s_npk, pk = task % s_npk;
@@ -435,22 +452,19 @@ __global__ void __launch_bounds__(SF_THREADS, 1) k_fit_small(const SmallFitItem*
             const int own = bb == 0x7fffffff ? 0 : bb;
             wGL = __shfl_sync(0xffffffffu, ig, own, Wl);
             wHL = __shfl_sync(0xffffffffu, ih, own, Wl);
-          } else {          // one feature, lane l owns bins 8l .. 8l+7
-            int32_t gl[8];
-            uint32_t hl[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              const int bq = lane * 8 + q;
-              gl[q] = bq < nb ? Gs[bq] : 0;
-              hl[q] = bq < nb ? Hs[bq] : 0u;
+          } else {          // one feature with nb > 32 bins: lane l owns bins [per l, per (l+1)), per = ceil(nb/32)
+            const int per = (nb + 31) >> 5;   // <= 32 (16-bit codes: up to 1024 bins)
+            int32_t lg = 0;
+            uint32_t lh = 0;
+            for (int q = 0; q < per; ++q) {
+              const int bq = lane * per + q;
+              if (bq < nb) {
+                lg += Gs[bq];
+                lh += Hs[bq];
+              }
             }
-#pragma unroll
-            for (int q = 1; q < 8; ++q) {
-              gl[q] += gl[q - 1];
-              hl[q] += hl[q - 1];
-            }
-            int32_t ig = gl[7];
-            uint32_t ih = hl[7];
+            int32_t ig = lg;
+            uint32_t ih = lh;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
               const int32_t ug = __shfl_up_sync(0xffffffffu, ig, o);
@@ -460,26 +474,26 @@ __global__ void __launch_bounds__(SF_THREADS, 1) k_fit_small(const SmallFitItem*
                 ih += uh;
               }
             }
-            const int32_t bgp = ig - gl[7];
-            const uint32_t bhp = ih - hl[7];
             Gq = __shfl_sync(0xffffffffu, ig, 31);
             Hq = __shfl_sync(0xffffffffu, ih, 31);
             int32_t myg = 0;
             uint32_t myh = 0;
-            if (fin && lane * 8 < nthr) {
+            if (fin && lane * per < nthr) {
               const double G = dequant(Gq, sgi), H = dequant(Hq, shi);
               const double gainP = calc_gain(G, H, calc_weight(G, H, lo, hi, hp.lambda, hp.mcw), hp.lambda);
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                const int b = lane * 8 + q;
-                if (b < nthr) {
-                  const double loss = cand(bgp + gl[q], bhp + hl[q], gainP);
-                  if (loss > bl) {   // b ascending within the lane: strict keeps the smaller b
-                    bl = loss;
-                    bb = b;
-                    myg = bgp + gl[q];
-                    myh = bhp + hl[q];
-                  }
+              int32_t rg = ig - lg;    // prefix before the lane's first bin
+              uint32_t rh = ih - lh;
+              for (int q = 0; q < per; ++q) {
+                const int b = lane * per + q;
+                if (b >= nthr) break;
+                rg += Gs[b];
+                rh += Hs[b];
+                const double loss = cand(rg, rh, gainP);
+                if (loss > bl) {   // b ascending within the lane: strict keeps the smaller b
+                  bl = loss;
+                  bb = b;
+                  myg = rg;
+                  myh = rh;
                 }
               }
             }
@@ -557,9 +571,9 @@ __global__ void __launch_bounds__(SF_THREADS, 1) k_fit_small(const SmallFitItem*
               loR = mid;
             }
             s_sf[k] = (int8_t)mf;
-            s_sb[k] = (uint8_t)mb;
+            s_sb[k] = (uint16_t)mb;
             s_tf[gk] = (int8_t)mf;
-            s_tb[gk] = (uint8_t)mb;
+            s_tb[gk] = (uint16_t)mb;
             if (d + 1 < D) {
               s_lo[par ^ 1][2 * k] = loL;
               s_hi[par ^ 1][2 * k] = hiL;
@@ -585,7 +599,7 @@ __global__ void __launch_bounds__(SF_THREADS, 1) k_fit_small(const SmallFitItem*
         if (pk < 0) continue;
         const int f = s_sf[pk];
         if (f >= 0) {
-          const int child = 2 * pk + (codes[(size_t)i * kMaxF + f] > s_sb[pk] ? 1 : 0);
+          const int child = 2 * pk + (code_at(codes, i, f) > s_sb[pk] ? 1 : 0);
           if (d + 1 == D) {
             s_leaf[i] = (int16_t)((1 << (d + 1)) - 1 + child);
             s_pos[i] = -1;
@@ -642,11 +656,10 @@ __global__ void __launch_bounds__(SF_THREADS, 1) k_fit_small(const SmallFitItem*
       block_max2(mg, mh);
     }
     for (int i = tid; i < it.m_test; i += SF_THREADS) {
-      const uint8_t* row = it.codes_test + (size_t)i * kMaxF;
       int k = 0;
       for (int s2 = 0; s2 < D; ++s2) {
         const int f = s_tf[k];
-        if (f >= 0) k = 2 * k + 1 + (row[f] > s_tb[k] ? 1 : 0);
+        if (f >= 0) k = 2 * k + 1 + (code_at(it.codes_test, i, f) > s_tb[k] ? 1 : 0);
       }
       it.pred_test[2 * i + tg] = __fadd_rn(it.pred_test[2 * i + tg], s_tv[k]);
     }
@@ -663,6 +676,7 @@ void fit_small_run(Ctx* ctx, const std::vector<SmallFitItem>& items, const std::
   for (const auto& itm : items) {
     LLMP_REQUIRE(itm.n >= 1 && itm.n <= SF_MAX_N, "small fit: n must be in [1, 8192]");
     LLMP_REQUIRE(itm.hp >= 0 && itm.hp < (int)hps.size(), "small fit: bad hparams index");
+    LLMP_REQUIRE(itm.cw == 1 || itm.cw == 2, "small fit: codes are 8- or 16-bit");
     n_cap = std::max(n_cap, itm.n);
   }
   for (const auto& h : hps) {
@@ -670,21 +684,34 @@ void fit_small_run(Ctx* ctx, const std::vector<SmallFitItem>& items, const std::
     LLMP_REQUIRE(h.F >= 1 && h.F <= kMaxF, "small fit: bad F");
   }
   n_cap = (n_cap + 7) & ~7;
-  std::vector<SmallFitItem> its(items);
-  for (auto& itm : its) itm.n_cap = n_cap;
-  const int fixed = 12 * n_cap + SF_WARPS * SF_STAGE;
-  const int smem = SF_SMEM_CAP;
-  LLMP_REQUIRE(fixed + 64 * 1024 <= smem, "small fit: too many rows for shared memory");
-  ensure_smem_attr((const void*)k_fit_small, smem);
-  DevBuf& d_items = ctx->workspace("sf_items", its.size() * sizeof(SmallFitItem));
   DevBuf& d_hps = ctx->workspace("sf_hps", hps.size() * sizeof(SmallFitHp));
-  LLMP_CUDA(cudaMemcpyAsync(d_items.p, its.data(), its.size() * sizeof(SmallFitItem), cudaMemcpyHostToDevice,
-                            ctx->stream));
   LLMP_CUDA(cudaMemcpyAsync(d_hps.p, hps.data(), hps.size() * sizeof(SmallFitHp), cudaMemcpyHostToDevice, ctx->stream));
-  double rows = 0;
-  for (const auto& itm : its) rows += (double)itm.n * hps[itm.hp].T;
-  LLMP_LAUNCH(ctx, KC_FIT_SMALL, rows, k_fit_small, (int)its.size(), SF_THREADS, smem, d_items.as<SmallFitItem>(),
-              d_hps.as<SmallFitHp>(), smem);
+  // one launch per code width (a template instantiation each)
+  for (int cw = 1; cw <= 2; ++cw) {
+    std::vector<SmallFitItem> its;
+    for (const auto& itm : items)
+      if (itm.cw == cw) {
+        its.push_back(itm);
+        its.back().n_cap = n_cap;
+      }
+    if (its.empty()) continue;
+    const int fixed = 12 * n_cap + SF_WARPS * (cw == 1 ? sf_stage<1>() : sf_stage<2>());
+    const int smem = SF_SMEM_CAP;
+    LLMP_REQUIRE(fixed + 64 * 1024 <= smem, "small fit: too many rows for shared memory");
+    const void* kf = cw == 1 ? (const void*)k_fit_small<1> : (const void*)k_fit_small<2>;
+    ensure_smem_attr(kf, smem);
+    DevBuf& d_items = ctx->workspace(cw == 1 ? "sf_items1" : "sf_items2", its.size() * sizeof(SmallFitItem));
+    LLMP_CUDA(cudaMemcpyAsync(d_items.p, its.data(), its.size() * sizeof(SmallFitItem), cudaMemcpyHostToDevice,
+                              ctx->stream));
+    double rows = 0;
+    for (const auto& itm : its) rows += (double)itm.n * hps[itm.hp].T;
+    if (cw == 1)
+      LLMP_LAUNCH(ctx, KC_FIT_SMALL, rows, k_fit_small<1>, (int)its.size(), SF_THREADS, smem,
+                  d_items.as<SmallFitItem>(), d_hps.as<SmallFitHp>(), smem);
+    else
+      LLMP_LAUNCH(ctx, KC_FIT_SMALL, rows, k_fit_small<2>, (int)its.size(), SF_THREADS, smem,
+                  d_items.as<SmallFitItem>(), d_hps.as<SmallFitHp>(), smem);
+  }
 }
 
 }  // namespace llmp

@@ -8,6 +8,7 @@ namespace llmp {
 struct CutsData {
   int F = 0;
   int max_bin = 256;
+  int stride = kBins - 1;   // cuts per feature row: 255 (8-bit codes) or kMaxCuts16 (16-bit codes)
   DevBuf d_cuts;    // float [32][255]
   DevBuf d_ncuts;   // int32 [32]
   std::vector<float> h_cuts;     // [32*255]
@@ -47,8 +48,10 @@ void wg_sample(Ctx* ctx, const WgData& w, int64_t count, uint64_t seed, int64_t 
 // binning.cu
 // sharded = true: this rank holds rows [row_offset, row_offset + n) of n_global and the global sample is
 // all-gathered over the context's communicator (every rank must call); false: X is the whole data
+// max_bin = 0: exact tree method; wide: 16-bit codes (up to 1024 bins, cut stride kMaxCuts16)
 void compute_cuts(Ctx* ctx, const float* X, int64_t n, int F, int64_t row_offset, int64_t n_global, int max_bin,
-                  CutsData& out, bool sharded);
+                  CutsData& out, bool sharded, bool wide = false);
+void compute_codes16(Ctx* ctx, const float* X, int64_t n, int F, const CutsData& cuts, uint16_t* codes);
 // codes: row-major n x 32 (may be null); codesT: column-major 32 x n (may be null).
 // flag (device int, may be null) is set to 1 when X holds a non-finite value.
 // codesT leading dimension ldT >= n (bytes between features; the fit pads it to a multiple of 32)
@@ -100,7 +103,8 @@ struct SmallFitHp {
 struct SmallFitItem {
   int n, m_test, target, hp;
   int n_cap;                    // set by fit_small_run (shared-memory stride)
-  const uint8_t* codes;         // n x 32, row-major (the fit's cuts)
+  int cw;                       // bytes per code: 1 (<= 256 bins) or 2 (16-bit codes, up to 1024 bins)
+  const uint8_t* codes;         // n x 32 codes of cw bytes, row-major (the fit's cuts)
   const uint8_t* codes_test;    // m_test x 32 (the same cuts)
   const float* y;               // n x 2
   const float* w;               // n (Eq. 4 or explicit weights)

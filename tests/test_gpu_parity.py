@@ -645,3 +645,50 @@ def test_random_forest_parity(lp, ctx, case):
     assert _bits_equal(oracle.predict(om, X), gm.predict(ctx, X))
     assert np.array_equal(oracle.importance(om), gm.importance())
     gm.free()
+
+
+# ------------------------------------------------------------------ >256 bins, exact tree method
+def _c1_many_distinct():
+    d = synth.make("C1")
+    X = d.X.copy()
+    X[:, 1] = np.asarray(synth.u01(4, np.arange(len(X)), 77) * 1000.0, np.float32)   # a continuous LLM-side feature
+    return d, X
+
+
+def test_cv_wide_bins_and_exact_parity(lp, ctx):
+    """NEXT-4 ("tree building method" and "number of bins"): the nested CV with 300 bins and
+    with the exact method on data with 320 distinct values in one feature — 16-bit codes in the
+    batched small-fit path — equals the oracle fold by fold."""
+    d, X = _c1_many_distinct()
+    gk = [dict(n_trees=8, max_depth=4, max_bin=300), dict(n_trees=8, max_depth=4, tree_method=1),
+          dict(n_trees=8, max_depth=4, max_bin=1024, eta=0.5)]
+    of = oracle.cv(X, d.y, d.llm_id, d.prof_id, d.users_col, d.n_llm, d.n_prof, [oracle.hparams(**k) for k in gk],
+                   L1, L2, U, d.cost)
+    gf = lp.cv(ctx, X, d.y, d.llm_id, d.prof_id, d.users_col, d.n_llm, d.n_prof, [lp.hparams(**k) for k in gk], L1,
+               L2, U, d.cost)
+    assert of == gf
+    for k in gk:   # each point alone (plain LOO) too
+        assert oracle.cv(X, d.y, d.llm_id, d.prof_id, d.users_col, d.n_llm, d.n_prof, [oracle.hparams(**k)], L1, L2,
+                         U, d.cost) == lp.cv(ctx, X, d.y, d.llm_id, d.prof_id, d.users_col, d.n_llm, d.n_prof,
+                                             [lp.hparams(**k)], L1, L2, U, d.cost)
+
+
+def test_fit_bins_limits_and_exact(lp, ctx):
+    """llmpilot_fit keeps 8-bit codes: max_bin > 256 and exact with > 256 distinct values are
+    LLMP_EINVAL; exact on paper-shaped data (<= 256 distinct values per feature) equals hist with
+    256 bins, which is exact there (DESIGN R13)."""
+    d, X = _c1_many_distinct()
+    with pytest.raises(lp.LLMPilotError, match="EINVAL"):
+        lp.fit(ctx, X, d.y, lp.hparams(n_trees=2, max_bin=300), d.users_col, d.llm_id, d.prof_id, d.n_llm, d.n_prof)
+    with pytest.raises(lp.LLMPilotError, match="EINVAL"):
+        lp.fit(ctx, X, d.y, lp.hparams(n_trees=2, tree_method=1), d.users_col, d.llm_id, d.prof_id, d.n_llm, d.n_prof)
+    d2 = synth.make("C2")
+    a = lp.fit(ctx, d2.X, d2.y, lp.hparams(n_trees=10, tree_method=1), d2.users_col, d2.llm_id, d2.prof_id, d2.n_llm,
+               d2.n_prof).export()
+    b = lp.fit(ctx, d2.X, d2.y, lp.hparams(n_trees=10), d2.users_col, d2.llm_id, d2.prof_id, d2.n_llm,
+               d2.n_prof).export()
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+    om = oracle.fit(d2.X, d2.y, oracle.hparams(n_trees=10, max_depth=6, tree_method=1), d2.users_col, d2.llm_id,
+                    d2.prof_id, d2.n_llm, d2.n_prof, L1, L2)
+    _assert_same_model(om, a)
