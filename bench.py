@@ -30,6 +30,7 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ.setdefault("NCCL_DEBUG", "WARN")   # rank 0's stdout carries exactly one JSON line
 
 import numpy as np  # noqa: E402
 
@@ -78,6 +79,8 @@ def parse():
                     help="BASELINE configs[3]: 100M rows (781,250 LLMs) in total, row-sharded over the N ranks "
                          "(strong scaling) instead of 10M rows per GPU")
     ap.add_argument("--strong-llms", type=int, default=781250)
+    ap.add_argument("--nccl1", action="store_true",
+                    help="N = 1 through a one-rank NCCL communicator: the sharded fit path on one GPU")
     ap.add_argument("--grid-trees", type=int, default=1000, help="trees of the cv_c2_grid leg's points")
     ap.add_argument("--wg-rows", type=int, default=17_300_000, help="trace rows of the workload-generator leg")
     ap.add_argument("--wg-samples", type=int, default=4_000_000, help="requests drawn per sampling step")
@@ -561,6 +564,8 @@ def main():
             t.copy_(torch.frombuffer(bytearray(lp.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(t, 0)
         uid = bytes(t.cpu().numpy().tobytes())
+    elif args.nccl1:
+        uid = lp.nccl_unique_id()
 
     # ---- synthetic inputs (seeded), resident in HBM before the timed region
     n_llm_total = args.strong_llms if args.strong else args.llms_per_gpu * world

@@ -200,6 +200,8 @@ def node_hist(codes_, rows, qg, qh):
     F = codes_.shape[1]
     Hg = np.zeros((F, MAX_BIN), np.int64); Hh = np.zeros((F, MAX_BIN), np.int64)
     lib().orc_node_hist(_p(codes_), F, _p(rows), len(rows), _p(qg), _p(qh), _p(Hg), _p(Hh))
+    if codes_.size == 0 or int(codes_.max()) < 256:   # 8-bit codes: the [F][256] layout of the GPU's hook
+        return Hg[:, :256].copy(), Hh[:, :256].copy()
     return Hg, Hh
 
 

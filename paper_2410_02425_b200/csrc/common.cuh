@@ -82,6 +82,8 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   int rank = 0, nranks = 1;
   void* nccl = nullptr;   // ncclComm_t (dlopen'ed NCCL), null for one GPU
+  void* nccl2 = nullptr;  // a second communicator over the same ranks (the second ensemble's graph branch)
+  int comm_sel = 0;       // 1: collectives being issued go to nccl2
   LocalGroup* lgroup = nullptr;   // set instead of nccl by llmpilot_ctx_create_local_group
   bool own_stream = false;        // the stream was created by the library (local groups)
   bool sharded() const { return nccl != nullptr || lgroup != nullptr; }
@@ -179,6 +181,7 @@ void local_group_release(LocalGroup* g);   // the last rank's release deletes it
 void nccl_init(Ctx* ctx, const void* unique_id);
 void nccl_unique_id(void* out);
 void nccl_destroy(Ctx* ctx);
+void nccl_health(Ctx* ctx);   // ncclCommGetAsyncError; abort + LLMP_ENCCL on an error
 
 // ---------------------------------------------------------------------------------------------
 // device helpers

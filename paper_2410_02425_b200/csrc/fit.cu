@@ -105,6 +105,7 @@ struct FitArgs {
   int built_by_h;     // 1 (sharded): the split kernel picks the built child by hessian sum
   int rf, rf_boot;    // random forest (DESIGN R33-R36): bootstrap weights, per-node features, leaf W / T
   float max_features;
+  const float* w_base;  // RF: the rows' weights before the bootstrap (w then holds the current tree's)
   const uint32_t* cmask;  // [n/32 batches][32 lanes] precomputed change masks (k_cmask), or null
   int nn;
   FeatBest* fbest;            // [2^(D-1)][32] per-(node, feature) best split of the current level
@@ -150,17 +151,12 @@ __device__ __forceinline__ int poisson1(uint64_t seed, int t, int64_t gi) {
 }
 
 // O4 gradient pair of global row gi for tree t: weighted squared error g = w (p - y), h = w, zeroed
-// when the row is sampled out; random forest (R33, R34): every tree fits y itself (p = 0) with the
-// row's bootstrap count as an integer weight, w_t = c_t,i w
+// when the row is sampled out.  Random forest (R33, R34): every tree fits y itself (p = 0), and `w`
+// is then the tree's bootstrap weight c_t,i w (a.w points at the per-tree buffer k_rf_weights fills),
+// so the hot kernels carry no bootstrap arithmetic
 __device__ __forceinline__ void grad_pair(const FitArgs& a, int t, int64_t gi, float y, float w, float p, float& g,
                                           float& h) {
-  if (a.rf) {
-    const float wt = a.rf_boot ? __fmul_rn((float)poisson1(a.seed, t, gi), w) : w;
-    g = __fmul_rn(wt, __fsub_rn(0.0f, y));
-    h = wt;
-    return;
-  }
-  g = __fmul_rn(w, __fsub_rn(p, y));
+  g = __fmul_rn(w, __fsub_rn(a.rf ? 0.0f : p, y));
   h = w;
   if (row_sampled_out(a.seed, a.target, t, gi, a.subsample)) {
     g = 0.f;
@@ -1860,6 +1856,17 @@ __global__ void __launch_bounds__(BASE_THREADS) k_base_init(const FitArgs a, con
   }
 }
 
+// RF (R34): this target's bootstrap weights of tree t = *d_tree + ahead: w_t,i = c_t,i w_i (fp32)
+__global__ void k_rf_weights(const FitPair fp, int ahead) {
+  pdl_wait();
+  const FitArgs& a = fp.t[blockIdx.y];
+  const int t = *a.d_tree + ahead;
+  if (t >= a.T) return;
+  float* wt = const_cast<float*>(a.w);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x)
+    wt[i] = a.rf_boot ? __fmul_rn((float)poisson1(a.seed, t, a.row_offset + i), a.w_base[i]) : a.w_base[i];
+}
+
 __global__ void k_next_tree(int* d_tree) {
   pdl_wait();
   *d_tree += 1;
@@ -2086,7 +2093,11 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   // particular not into the body of a conditional graph node.  A 1-rank communicator runs this same
   // sharded path (trivial collectives), which is how the GPU tests cover it on one device.
   const bool sharded = ctx->sharded();
-  const bool graphs = T > 0 && !ctx->timing && ctx->use_graphs && !sharded;
+  // NCCL-sharded fits replay each round as a captured graph with the collectives inside (host-side
+  // replay: no conditional node around NCCL kernels); the in-process local group's collectives are
+  // host barriers and cannot be captured
+  const bool nccl_mode = ctx->nccl != nullptr;
+  const bool graphs = T > 0 && !ctx->timing && ctx->use_graphs && (!sharded || nccl_mode);
   size_t lvl_nodes = 0;
   for (int d = 0; d <= D; ++d) lvl_nodes += (size_t)1 << d;
   const size_t tab_bytes = lvl_nodes * (8 /*start*/ + 8 /*cnt*/ + 8 /*gcnt*/ + 8 + 8 /*lo,hi*/ + 4 + 4 /*split*/ +
@@ -2098,7 +2109,10 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   static const bool fused = !use_root2 && !(getenv("LLMP_NOFUSE") && atoi(getenv("LLMP_NOFUSE")) != 0);
   static const bool urow = !(getenv("LLMP_NO_UROW") && atoi(getenv("LLMP_NO_UROW")) != 0);
   static const bool pdl_env = !(getenv("LLMP_PDL") && atoi(getenv("LLMP_PDL")) == 0);
-  ctx->pdl = pdl_env && !ctx->sharded();   // (NCCL calls sit between the kernels when sharded)
+  // (every tree-loop kernel waits on griddepcontrol.wait before touching memory, so a kernel following
+  // an NCCL kernel starts only once the collective is complete; the local group's host barriers are
+  // outside any stream dependency and stay unlaunched-ahead)
+  ctx->pdl = pdl_env && ctx->lgroup == nullptr;
   static const bool hist_swar = !(getenv("LLMP_HIST_SWAR") && atoi(getenv("LLMP_HIST_SWAR")) == 0);
   DevBuf& d_cm = ctx->workspace("cmask", (size_t)((n + 31) / 32) * 32 * 4);
   LLMP_LAUNCH(ctx, KC_MISC, n, k_cmask, grid_for(ctx, n, 256, 8), 256, 0, d_codes.as<uint8_t>(), n,
@@ -2148,6 +2162,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     a.rf = hp.model == 1 ? 1 : 0;
     a.rf_boot = hp.rf_bootstrap ? 1 : 0;
     a.max_features = hp.max_features;
+    a.w_base = a.w;
+    if (a.rf) a.w = ctx->workspace("rf_w" + sx, (size_t)n * 4).as<float>();   // per-tree bootstrap weights
     a.cmask = cmask;
     a.nn = nn;
     a.units = ctx->d_units;
@@ -2206,10 +2222,18 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   const DbgArgs nodbg{};
 
   phase("state");
+  const bool rf = hp.model == 1;
+  const int rfw_grid = grid_for(ctx, n, 256, 8);
+  LLMP_CUDA(cudaMemsetAsync(d_tree, 0, sizeof(int), s));
   // ---- base scores (O3) and tree 0's gradient maxima
   for (int tg = 0; tg < 2; ++tg) {
     const FitArgs& a = A[tg];
     int64_t* sums = d_sums.as<int64_t>() + 2 * tg;
+    if (rf) {   // tree 0's bootstrap weights (R34)
+      FitPair f1;
+      f1.t[0] = a;
+      LLMP_LAUNCH(ctx, KC_MISC, n, k_rf_weights, dim3(rfw_grid, 1), 256, 0, f1, 0);
+    }
     LLMP_LAUNCH(ctx, KC_BASE, n, k_base_max, base_grid, BASE_THREADS, 0, a);
     allreduce_max_u32(ctx, a.maxg + T, 1);
     allreduce_max_u32(ctx, a.maxh + T, 1);
@@ -2295,6 +2319,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       nccl_group_end(ctx);
       split(fp, ny, d);
     }
+    // RF: tree t+1's bootstrap weights, read by the update's gradients (and the next root rebuild)
+    if (rf) LLMP_LAUNCH_PDL(ctx, KC_MISC, ny * n, k_rf_weights, dim3(rfw_grid, ny), 256, 0, fp, 1);
     if (fused) {   // update tree t + root histogram of tree t+1 (into the now free root slot)
       for (int q = 0; q < ny; ++q) LLMP_CUDA(cudaMemsetAsync(fp.t[q].H[0], 0, (size_t)SLOT * 8, st));
       if (hist1 & 4)
@@ -2317,14 +2343,17 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   FPa.t[0] = A[0];
   FPb.t[0] = A[1];
   auto round = [&](const cudaGraphConditionalHandle* loop) {
-    const bool branches = branches_env && graphs && !sharded;
+    // sharded: the second branch issues its collectives on the second communicator (ctx->nccl2)
+    const bool branches = branches_env && graphs && (!sharded || ctx->nccl2 != nullptr);
     if (branches) {
       const cudaStream_t sa = ctx->stream, sb = ctx->capture_stream(1);
       LLMP_CUDA(cudaEventRecord(ctx->fork_event, sa));
       LLMP_CUDA(cudaStreamWaitEvent(sb, ctx->fork_event, 0));
       trees(FPa, 1);
       ctx->stream = sb;
+      ctx->comm_sel = 1;
       trees(FPb, 1);
+      ctx->comm_sel = 0;
       LLMP_CUDA(cudaEventRecord(ctx->join_event, sb));
       ctx->stream = sa;
       LLMP_CUDA(cudaStreamWaitEvent(sa, ctx->join_event, 0));
@@ -2341,7 +2370,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   // graphs: the whole tree loop is ONE graph launch — a device-side while loop (conditional graph
   // node) around the captured round, so no host thread sits between the T rounds (host jitter
   // cannot starve the GPU).  LLMP_GRAPH_REPLAY=1 replays the round graph T times from the host.
-  static const bool replay = getenv("LLMP_GRAPH_REPLAY") && atoi(getenv("LLMP_GRAPH_REPLAY")) != 0;
+  static const bool replay_env = getenv("LLMP_GRAPH_REPLAY") && atoi(getenv("LLMP_GRAPH_REPLAY")) != 0;
+  const bool replay = replay_env || sharded;
   if (graphs) {
     cudaGraph_t g = nullptr;
     cudaGraphExec_t ge = nullptr;
@@ -2377,6 +2407,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
         ctx->rows[c] += (ctx->rows[c] - r0[c]) * (double)(T - 1);
       }
     } catch (...) {
+      ctx->comm_sel = 0;
       ctx->stream = sa;
       cudaGraph_t gc = nullptr;
       cudaStreamEndCapture(sa, &gc);
@@ -2424,6 +2455,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     fprintf(stderr, "\n");
   }
   phase("loop");
+  nccl_health(ctx);   // an asynchronous NCCL failure surfaces here (LLMP_ENCCL), not as a hang
   // ---- model to host
   out.F = F;
   out.users_col = ds.users_col;

@@ -138,6 +138,9 @@ struct NcclApi {
   const char* (*getErrorString)(ncclResult_t) = nullptr;
   ncclResult_t (*groupStart)() = nullptr;
   ncclResult_t (*groupEnd)() = nullptr;
+  ncclResult_t (*commSplit)(ncclComm_t, int, int, ncclComm_t*, void*) = nullptr;
+  ncclResult_t (*commGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+  ncclResult_t (*commAbort)(ncclComm_t) = nullptr;
 };
 NcclApi g_nccl;
 std::mutex g_nccl_mu;
@@ -155,6 +158,9 @@ void load_nccl() {
   g_nccl.getErrorString = (decltype(g_nccl.getErrorString))dlsym(h, "ncclGetErrorString");
   g_nccl.groupStart = (decltype(g_nccl.groupStart))dlsym(h, "ncclGroupStart");
   g_nccl.groupEnd = (decltype(g_nccl.groupEnd))dlsym(h, "ncclGroupEnd");
+  g_nccl.commSplit = (decltype(g_nccl.commSplit))dlsym(h, "ncclCommSplit");
+  g_nccl.commGetAsyncError = (decltype(g_nccl.commGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+  g_nccl.commAbort = (decltype(g_nccl.commAbort))dlsym(h, "ncclCommAbort");
   if (!g_nccl.commInitRank || !g_nccl.allReduce || !g_nccl.allGather || !g_nccl.commDestroy || !g_nccl.groupStart ||
       !g_nccl.groupEnd)
     fail(LLMP_ENCCL, "libnccl.so.2 lacks the needed symbols");
@@ -173,6 +179,33 @@ void nccl_init(Ctx* ctx, const void* unique_id) {
   ncclComm_t comm = nullptr;
   nccl_check(g_nccl.commInitRank(&comm, ctx->nranks, id, ctx->rank), "ncclCommInitRank");
   ctx->nccl = comm;
+  // a second communicator over the same ranks for the second ensemble's collectives: the two
+  // ensembles' trees then grow as concurrent graph branches, each branch ordering its own
+  // communicator's collectives identically on every rank (one communicator shared by two concurrent
+  // branches could interleave its collectives differently on different ranks)
+  if (g_nccl.commSplit) {
+    ncclComm_t c2 = nullptr;
+    if (g_nccl.commSplit(comm, 0, ctx->rank, &c2, nullptr) == 0) ctx->nccl2 = c2;
+  }
+}
+// ncclCommGetAsyncError on both communicators; on an error, abort them and fail (LLMP_ENCCL) instead
+// of letting the next collective hang
+void nccl_health(Ctx* ctx) {
+  if (!ctx->nccl || !g_nccl.commGetAsyncError) return;
+  for (void* c : {ctx->nccl, ctx->nccl2}) {
+    if (!c) continue;
+    ncclResult_t r = 0;
+    g_nccl.commGetAsyncError((ncclComm_t)c, &r);
+    if (r != 0 && r != 7 /* ncclInProgress */) {
+      const std::string msg = std::string("NCCL asynchronous error: ") + (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "?");
+      if (g_nccl.commAbort) {
+        if (ctx->nccl2) g_nccl.commAbort((ncclComm_t)ctx->nccl2);
+        g_nccl.commAbort((ncclComm_t)ctx->nccl);
+      }
+      ctx->nccl = ctx->nccl2 = nullptr;
+      fail(LLMP_ENCCL, msg);
+    }
+  }
 }
 void nccl_unique_id(void* out) {
   load_nccl();
@@ -182,8 +215,13 @@ void nccl_unique_id(void* out) {
   memcpy(out, &id, sizeof(id));
 }
 void nccl_destroy(Ctx* ctx) {
+  if (ctx->nccl2 && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)ctx->nccl2);
   if (ctx->nccl && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)ctx->nccl);
-  ctx->nccl = nullptr;
+  ctx->nccl = ctx->nccl2 = nullptr;
+}
+// the communicator of the collectives being issued (ctx->comm_sel: the graph branch)
+static ncclComm_t comm_of(Ctx* ctx) {
+  return (ncclComm_t)((ctx->comm_sel == 1 && ctx->nccl2) ? ctx->nccl2 : ctx->nccl);
 }
 static void coll_before(Ctx* ctx, cudaEvent_t* ev) { ctx->before(KC_NCCL, ev); }
 
@@ -281,7 +319,7 @@ void allreduce_sum_i64(Ctx* ctx, int64_t* buf, size_t count) {
   if (!ctx->nccl) return;
   cudaEvent_t ev = nullptr;
   coll_before(ctx, &ev);
-  nccl_check(g_nccl.allReduce(buf, buf, count, ncclInt64, ncclSum, (ncclComm_t)ctx->nccl, ctx->stream), "ncclAllReduce");
+  nccl_check(g_nccl.allReduce(buf, buf, count, ncclInt64, ncclSum, comm_of(ctx), ctx->stream), "ncclAllReduce");
   ctx->after(KC_NCCL, ev, (double)count * 8);
 }
 void allreduce_max_u32(Ctx* ctx, uint32_t* buf, size_t count) {
@@ -290,7 +328,7 @@ void allreduce_max_u32(Ctx* ctx, uint32_t* buf, size_t count) {
   if (!ctx->nccl) return;
   cudaEvent_t ev = nullptr;
   coll_before(ctx, &ev);
-  nccl_check(g_nccl.allReduce(buf, buf, count, ncclUint32, ncclMax, (ncclComm_t)ctx->nccl, ctx->stream), "ncclAllReduce");
+  nccl_check(g_nccl.allReduce(buf, buf, count, ncclUint32, ncclMax, comm_of(ctx), ctx->stream), "ncclAllReduce");
   ctx->after(KC_NCCL, ev, (double)count * 4);
 }
 void allreduce_max_u64(Ctx* ctx, uint64_t* buf, size_t count) {
@@ -299,7 +337,7 @@ void allreduce_max_u64(Ctx* ctx, uint64_t* buf, size_t count) {
   if (!ctx->nccl) return;
   cudaEvent_t ev = nullptr;
   coll_before(ctx, &ev);
-  nccl_check(g_nccl.allReduce(buf, buf, count, ncclUint64, ncclMax, (ncclComm_t)ctx->nccl, ctx->stream), "ncclAllReduce");
+  nccl_check(g_nccl.allReduce(buf, buf, count, ncclUint64, ncclMax, comm_of(ctx), ctx->stream), "ncclAllReduce");
   ctx->after(KC_NCCL, ev, (double)count * 8);
 }
 void allgather_bytes(Ctx* ctx, const void* send, void* recv, size_t bytes_per_rank) {
@@ -310,7 +348,7 @@ void allgather_bytes(Ctx* ctx, const void* send, void* recv, size_t bytes_per_ra
   }
   cudaEvent_t ev = nullptr;
   coll_before(ctx, &ev);
-  nccl_check(g_nccl.allGather(send, recv, bytes_per_rank, ncclUint8, (ncclComm_t)ctx->nccl, ctx->stream), "ncclAllGather");
+  nccl_check(g_nccl.allGather(send, recv, bytes_per_rank, ncclUint8, comm_of(ctx), ctx->stream), "ncclAllGather");
   ctx->after(KC_NCCL, ev, (double)bytes_per_rank * ctx->nranks);
 }
 
