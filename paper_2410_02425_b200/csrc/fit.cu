@@ -47,6 +47,7 @@ constexpr int GS_OFF = U_OFF + 2 * kBins * 4;                                // 
 constexpr int HIST_SMEM = GS_OFF + HIST_WARPS * 8 * 8;                       // 64.3 KB + 24 KB + 2 KB + 1 KB
 
 constexpr int SLOT = 2 * kHistBins;        // int64 per histogram slot (g then h)
+constexpr int FQ_INTS = 2 + 2 * MAX_PIECES; // fold-in queue: head, tail, one slot per piece of a launch
 
 
 __device__ __forceinline__ double exp2i(int e) {  // exact 2^e for e in [-1022, 1023]
@@ -106,6 +107,7 @@ struct FitArgs {
   int rf, rf_boot;    // random forest (DESIGN R33-R36): bootstrap weights, per-node features, leaf W / T
   float max_features;
   const float* w_base;  // RF: the rows' weights before the bootstrap (w then holds the current tree's)
+  int* fq;              // fold-in work queue of the level histogram (k_hist3): [0] head, [1] tail, slots
   const uint32_t* cmask;  // [n/32 batches][32 lanes] precomputed change masks (k_cmask), or null
   int nn;
   FeatBest* fbest;            // [2^(D-1)][32] per-(node, feature) best split of the current level
@@ -941,23 +943,8 @@ __global__ void __launch_bounds__(256) k_cmask(const uint8_t* codes, int64_t n, 
   }
 }
 
-#include "hist3.cuh"
-
 // the fused update kernel for a depth: compile-time routing depth for the configs' depths (6, 8)
 using Hist2Kernel = void (*)(const FitPair, const int, const int, const DbgArgs);
-using Upd3Kernel = void (*)(const FitPair);
-static Upd3Kernel upd3_kernel(int D) {
-  if (D == 8) return k_upd3<8>;
-  if (D == 6) return k_upd3<6>;
-  return k_upd3<0>;
-}
-// fused update kernel: LLMP_UPD = 2 (default) change-mask k_hist2 with the precomputed masks; 3 the
-// bulk-staged change-row k_upd3 (measured slower: 385 vs 311 us per paired launch on C3 — the pass is
-// issue-bound, and the precomputed masks cost less than per-batch change tests)
-static int upd_kernel() {
-  static const int v = getenv("LLMP_UPD") ? atoi(getenv("LLMP_UPD")) : 2;
-  return v == 3 ? 3 : 2;
-}
 static Hist2Kernel updroot2_kernel(int D) {
   if (D == 8) return k_hist2<HM_UPDROOT, 8>;
   if (D == 6) return k_hist2<HM_UPDROOT, 6>;
@@ -1309,6 +1296,8 @@ __global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitPa
   const LevelView& P = a.lv[d - 1];
   const LevelView& C = a.lv[d];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (a.fq && blockIdx.x == 0)   // the level histogram's fold-in work queue (head, tail, slots)
+    for (int i = tid; i < FQ_INTS; i += PT_THREADS) a.fq[i] = 0;
   {   // zero the built-child histogram slots [0, NP) of this level for split parents
     int4* Hz = reinterpret_cast<int4*>(a.H[d & 1]);
     const size_t per_slot = SLOT / 2;  // int4 per slot
@@ -1423,26 +1412,25 @@ __global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitPa
 // entry (one round trip).
 constexpr int SP3_WARPS = 4;
 constexpr int SP3_CLUSTER = 32 / SP3_WARPS;   // 8 CTAs = the node's 32 features
-template <bool CL>
-__global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitPair fp, const int d) {
-  pdl_wait();
-  const FitArgs& a = fp.t[blockIdx.y];
-  __shared__ FeatBest s_fb[SP3_WARPS];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int k = blockIdx.x / SP3_CLUSTER;                  // node of level d
-  const int f = (blockIdx.x % SP3_CLUSTER) * SP3_WARPS + warp;
+// O6 for feature f of node k of level d, by one warp (lane l owns bins 8l .. 8l+7): the feature's
+// histogram (sibling = parent - built, exact int64, written back for the next level), prefix scan,
+// fp64 gains with the monotone veto, best (loss desc, b asc).  Lane 0 receives the result in r.
+// Returns false when the node does not exist (its parent did not split).
+__device__ __forceinline__ bool split_feature(const FitArgs& a, const int d, const int k, const int f, const int lane,
+                                              FeatBest& r, const int side_in = -1) {
   const LevelView& V = a.lv[d];
   const int j = k >> 1;                                     // parent (level d-1)
   // ---- independent loads, all issued up front
   const int t = *a.d_tree;
   const int pf = (d == 0) ? 0 : a.lv[d - 1].split_f[j];
-  const int side = (d == 0) ? 0 : V.built[j];
+  // (the level histogram's fold-in passes the built side it computed: V.built may not be visible yet)
+  const int side = (d == 0) ? 0 : side_in >= 0 ? side_in : V.built[j];
   const int pside = (d >= 2) ? a.lv[d - 1].built[j >> 1] : 0;
   const double lo = (d == 0) ? -INFINITY : V.lo[k], hi = (d == 0) ? INFINITY : V.hi[k];
   const int nthr = a.ncuts[f];   // thresholds b = 0 .. nbins_f - 2
-  if (d > 0 && pf < 0) {         // node absent (uniform over the cluster)
+  if (d > 0 && pf < 0) {         // node absent (uniform over the node's warps)
     if (f == 0 && lane == 0) V.split_f[k] = -1;
-    return;
+    return false;
   }
   const uint32_t mgb = a.maxg[t], mhb = a.maxh[t];
   int64_t* Hself;
@@ -1461,11 +1449,11 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitPair fp, con
       const int eg0 = (f * kBins + lane * 8) / 2, eh0 = (kHistBins + f * kBins + lane * 8) / 2;
       longlong2 pg[4], bg2[4], ph[4], bh2[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        pg[q] = Hp[eg0 + q];
-        bg2[q] = Hb[eg0 + q];
-        ph[q] = Hp[eh0 + q];
-        bh2[q] = Hb[eh0 + q];
+      for (int q = 0; q < 4; ++q) {   // (L2 loads: the built histogram may come from other CTAs' atomics)
+        pg[q] = __ldcg(Hp + eg0 + q);
+        bg2[q] = __ldcg(Hb + eg0 + q);
+        ph[q] = __ldcg(Hp + eh0 + q);
+        bh2[q] = __ldcg(Hb + eh0 + q);
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -1484,8 +1472,8 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitPair fp, con
     longlong2 gv[4], hv[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      gv[q] = G2[q];
-      hv[q] = H2[q];
+      gv[q] = __ldcg(G2 + q);
+      hv[q] = __ldcg(H2 + q);
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -1570,7 +1558,6 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitPair fp, con
     }
   }
   if (lane == 0) {
-    FeatBest r;
     r.loss = bl;
     r.b = bb;
     r.valid = (bl > -INFINITY) ? 1 : 0;
@@ -1578,48 +1565,20 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitPair fp, con
     r.HLq = bHL;
     r.Gq = Gq;
     r.Hq = Hq;
-    if (CL) s_fb[warp] = r;
-    else a.fbest[(size_t)k * 32 + f] = r;
   }
-  // ---- the node's reduction, by one warp: lane l takes feature l's result
-  int rvalid, rb;
-  double rloss;
-  int64_t rGL, rHL, rG, rH;
-  if constexpr (CL) {   // cluster launch: results exchanged through distributed shared memory
-    cg::cluster_group cluster = cg::this_cluster();
-    cluster.sync();
-    if (blockIdx.x % SP3_CLUSTER != 0 || warp != 0) {
-      cluster.sync();   // keep this CTA's s_fb readable until the reduction warp has read it
-      return;
-    }
-    const FeatBest* rf = cluster.map_shared_rank(&s_fb[0], lane / SP3_WARPS) + (lane % SP3_WARPS);
-    rvalid = rf->valid;
-    rb = rf->b;
-    rloss = rf->loss;
-    rGL = rf->GLq;
-    rHL = rf->HLq;
-    rG = rf->Gq;
-    rH = rf->Hq;
-    cluster.sync();
-  } else {              // plain launch: the node's last-arriving warp (global ticket) reduces
-    int last = 0;
-    if (lane == 0) {
-      __threadfence();
-      last = atomicAdd(&V.done[k], 1) == 31;
-    }
-    last = __shfl_sync(0xffffffffu, last, 0);
-    if (!last) return;
-    __threadfence();
-    const volatile FeatBest* rf = a.fbest + (size_t)k * 32 + lane;
-    rvalid = rf->valid;
-    rb = rf->b;
-    rloss = rf->loss;
-    rGL = rf->GLq;
-    rHL = rf->HLq;
-    rG = rf->Gq;
-    rH = rf->Hq;
-    if (lane == 0) V.done[k] = 0;
-  }
+  return true;
+}
+
+// the node's decision (O6 argmax over features, O7 children, O8 leaves), by one warp: lane l holds
+// feature l's result
+__device__ __forceinline__ void split_node(const FitArgs& a, const int d, const int k, const int lane, int rvalid,
+                                           int rb, double rloss, int64_t rGL, int64_t rHL, int64_t rG, int64_t rH) {
+  const LevelView& V = a.lv[d];
+  const int t = *a.d_tree;
+  const double lo = (d == 0) ? -INFINITY : V.lo[k], hi = (d == 0) ? INFINITY : V.hi[k];
+  const int eg = exp_of(__uint_as_float(a.maxg[t])), eh = exp_of(__uint_as_float(a.maxh[t]));
+  const double sgi = exp2i(eg - a.K), shi = exp2i(eh - a.K);
+  const double lambda = a.lambda, mcw = a.mcw;
   double ml = rvalid ? rloss : -INFINITY;
   int mf = lane, mb = rb;
   for (int o = 16; o > 0; o >>= 1) {
@@ -1691,6 +1650,78 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitPair fp, con
   }
 }
 
+template <bool CL>
+__global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitPair fp, const int d) {
+  pdl_wait();
+  const FitArgs& a = fp.t[blockIdx.y];
+  __shared__ FeatBest s_fb[SP3_WARPS];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int k = blockIdx.x / SP3_CLUSTER;                  // node of level d
+  const int f = (blockIdx.x % SP3_CLUSTER) * SP3_WARPS + warp;
+  const LevelView& V = a.lv[d];
+  FeatBest r;
+  if (!split_feature(a, d, k, f, lane, r)) return;
+  if (lane == 0) {
+    if (CL) s_fb[warp] = r;
+    else a.fbest[(size_t)k * 32 + f] = r;
+  }
+  // ---- the node's reduction, by one warp: lane l takes feature l's result
+  int rvalid, rb;
+  double rloss;
+  int64_t rGL, rHL, rG, rH;
+  if constexpr (CL) {   // cluster launch: results exchanged through distributed shared memory
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();
+    if (blockIdx.x % SP3_CLUSTER != 0 || warp != 0) {
+      cluster.sync();   // keep this CTA's s_fb readable until the reduction warp has read it
+      return;
+    }
+    const FeatBest* rf = cluster.map_shared_rank(&s_fb[0], lane / SP3_WARPS) + (lane % SP3_WARPS);
+    rvalid = rf->valid;
+    rb = rf->b;
+    rloss = rf->loss;
+    rGL = rf->GLq;
+    rHL = rf->HLq;
+    rG = rf->Gq;
+    rH = rf->Hq;
+    cluster.sync();
+  } else {              // plain launch: the node's last-arriving warp (global ticket) reduces
+    int last = 0;
+    if (lane == 0) {
+      __threadfence();
+      last = atomicAdd(&V.done[k], 1) == 31;
+    }
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
+    __threadfence();
+    const volatile FeatBest* rf = a.fbest + (size_t)k * 32 + lane;
+    rvalid = rf->valid;
+    rb = rf->b;
+    rloss = rf->loss;
+    rGL = rf->GLq;
+    rHL = rf->HLq;
+    rG = rf->Gq;
+    rH = rf->Hq;
+    if (lane == 0) V.done[k] = 0;
+  }
+  split_node(a, d, k, lane, rvalid, rb, rloss, rGL, rHL, rG, rH);
+}
+
+#include "hist3.cuh"
+
+using Upd3Kernel = void (*)(const FitPair);
+static Upd3Kernel upd3_kernel(int D) {
+  if (D == 8) return k_upd3<8>;
+  if (D == 6) return k_upd3<6>;
+  return k_upd3<0>;
+}
+// fused update kernel: LLMP_UPD = 2 (default) change-mask k_hist2 with the precomputed masks; 3 the
+// bulk-staged change-row k_upd3 (measured slower: 385 vs 311 us per paired launch on C3 — the pass is
+// issue-bound, and the precomputed masks cost less than per-batch change tests)
+static int upd_kernel() {
+  static const int v = getenv("LLMP_UPD") ? atoi(getenv("LLMP_UPD")) : 2;
+  return v == 3 ? 3 : 2;
+}
 // ---------------------------------------------------------------------------------------------
 // leaf routing + prediction update + next tree's gradient maxima
 constexpr int UPD_THREADS = 256;
@@ -1962,6 +1993,11 @@ void compute_weights(Ctx* ctx, const DatasetDev& ds, float L1, float L2, float* 
               (double)L2, d_D.as<unsigned long long>(), w, d_y0.as<float>(), d_y1.as<float>());
 }
 
+static bool split_cluster_env() {
+  static const bool v = getenv("LLMP_SPLIT_CLUSTER") && atoi(getenv("LLMP_SPLIT_CLUSTER")) != 0;
+  return v;
+}
+
 // ---------------------------------------------------------------------------------------------
 void validate_hparams(const llmpilot_hparams& hp) {
   LLMP_REQUIRE(hp.n_trees >= 0, "n_trees must be >= 0");
@@ -2120,6 +2156,13 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   const uint32_t* cmask = d_cm.as<uint32_t>();
   static const int hist1 = hist1_mask();
   const int lvk = level_kernel();
+  // split evaluation folded into k_hist3 (LLMP_FOLD=1; unsharded only: no all-reduce between the
+  // histogram and the split).  Measured slower than the separate k_split3 launch (107 vs 55 + 14 us per
+  // paired level on C3): one CTA evaluates a node's 64 (child, feature) tasks in four serial rounds
+  // (~12 us), and the last-completed pieces put that on the kernel's tail, where k_split3 spreads
+  // every node over 8 CTAs of the whole GPU
+  static const bool fold_env = getenv("LLMP_FOLD") && atoi(getenv("LLMP_FOLD")) != 0;
+  const bool fold = fold_env && lvk == 3 && !sharded && !split_cluster_env();
   FitArgs A[2];
   for (int tg = 0; tg < 2; ++tg) {
     // per-target workspaces: the fused update pass leaves the next tree's root histogram and
@@ -2163,6 +2206,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     a.rf_boot = hp.rf_bootstrap ? 1 : 0;
     a.max_features = hp.max_features;
     a.w_base = a.w;
+    a.fq = ctx->workspace("fold_q" + sx, (size_t)FQ_INTS * 4).as<int>();
     if (a.rf) a.w = ctx->workspace("rf_w" + sx, (size_t)n * 4).as<float>();   // per-tree bootstrap weights
     a.cmask = cmask;
     a.nn = nn;
@@ -2255,7 +2299,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   FitPair FP;
   FP.t[0] = A[0];
   FP.t[1] = A[1];
-  static const bool split_cluster = getenv("LLMP_SPLIT_CLUSTER") && atoi(getenv("LLMP_SPLIT_CLUSTER")) != 0;
+  static const bool split_cluster = split_cluster_env();
   auto split = [&](const FitPair& fp, int ny, int d) {
     const dim3 grid((1 << d) * SP3_CLUSTER, ny);
     if (!split_cluster) {
@@ -2311,13 +2355,14 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       // persistent tile loop (upper bound of the level's tile count: one partial tile per parent)
       LLMP_LAUNCH_PDL(ctx, KC_PARTITION, ny * n, k_part, dim3(std::min(tiles_d, PT_CTAS_PER_SM / ny * ctx->sms), ny),
                   PT_THREADS, 0, fp, d);
-      if (lvk == 3) LLMP_LAUNCH_PDL(ctx, KC_HIST, 0, k_hist3<HM_LEVEL>, hg3, H3_THREADS, H3_SMEM, fp, ny, d, nodbg);
+      if (lvk == 3) LLMP_LAUNCH_PDL(ctx, KC_HIST, 0, k_hist3<HM_LEVEL>, hg3, H3_THREADS, H3_SMEM, fp, ny, d, nodbg,
+                                    fold ? 1 : 0);
       else if (lvk == 1) LLMP_LAUNCH_PDL(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hg, HIST_THREADS, HIST_SMEM, fp, d, 0, nodbg);
       else LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist2<HM_LEVEL>, hg, H2_THREADS, H2_SMEM, fp, d, 0, nodbg);
       nccl_group_start(ctx);   // both targets' built-child histograms in one NCCL launch
       for (int q = 0; q < ny; ++q) allreduce_sum_i64(ctx, fp.t[q].H[d & 1], (size_t)SLOT << (d - 1));
       nccl_group_end(ctx);
-      split(fp, ny, d);
+      if (!fold) split(fp, ny, d);
     }
     // RF: tree t+1's bootstrap weights, read by the update's gradients (and the next root rebuild)
     if (rf) LLMP_LAUNCH_PDL(ctx, KC_MISC, ny * n, k_rf_weights, dim3(rfw_grid, ny), 256, 0, fp, 1);
@@ -2501,7 +2546,7 @@ void debug_histogram(Ctx* ctx, const uint8_t* codes, int64_t n, const int32_t* i
   FitPair fp;
   fp.t[0] = a;
   if (level_kernel() == 3)
-    LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist3<HM_DEBUG>, ctx->sms, H3_THREADS, H3_SMEM, fp, 1, 0, dbg);
+    LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist3<HM_DEBUG>, ctx->sms, H3_THREADS, H3_SMEM, fp, 1, 0, dbg, 0);
   else if (level_kernel() == 1)
     LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist<HM_DEBUG>, 2 * ctx->sms, HIST_THREADS, HIST_SMEM, fp, 0, 0, dbg);
   else

@@ -71,8 +71,34 @@ __device__ __forceinline__ void red2_h3(uint32_t addr, int32_t g, uint32_t h) {
 // (r >> 2) & 1 are swapped, so the 8 lanes of one phase of a 16-byte load hit 8 distinct bank quads
 __device__ __forceinline__ uint32_t h3_half(int r, int h) { return (uint32_t)(r * 32) + ((uint32_t)(h ^ ((r >> 2) & 1)) << 4); }
 
+// ---------------------------------------------------------------------------------------------
+// Split evaluation folded into the level histogram (unsharded fits): the CTA that
+// completes the last contribution to parent j's built child evaluates both children of j — the 64
+// (child, feature) warps of k_split3 over the CTA's 16 warps, then one warp per child for the node
+// decision — so a level costs one launch instead of two and the split's dependent-load chain
+// overlaps the other CTAs' histogram work.
+__device__ __forceinline__ void fold_split(const FitPair& fp, int tg, int d, int j, int side) {
+  const FitArgs& a = fp.t[tg];
+  __shared__ FeatBest s_fb2[2][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool split = a.lv[d - 1].split_f[j] >= 0;   // else split_feature marks both children absent
+  for (int task = warp; task < 64; task += H3_WARPS) {
+    const int c = task >> 5, f = task & 31;
+    FeatBest r;
+    const bool ok = split_feature(a, d, 2 * j + c, f, lane, r, side);
+    if (ok && lane == 0) s_fb2[c][f] = r;
+  }
+  __syncthreads();
+  if (split && warp < 2) {
+    const FeatBest q = s_fb2[warp][lane];
+    split_node(a, d, 2 * j + warp, lane, q.valid, q.b, q.loss, q.GLq, q.HLq, q.Gq, q.Hq);
+  }
+  __syncthreads();
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(H3_THREADS, 1) k_hist3(const FitPair fp, const int ny, const int d, const DbgArgs dbg) {
+__global__ void __launch_bounds__(H3_THREADS, 1) k_hist3(const FitPair fp, const int ny, const int d, const DbgArgs dbg,
+                                                         const int fold) {
   pdl_wait();
   const FitArgs& a0 = fp.t[0];   // F, users_col, codes: the same for both ensembles
   const int ucol = (a0.users_col >= 0 && a0.users_col < kMaxF) ? a0.users_col : -1;
@@ -85,7 +111,8 @@ __global__ void __launch_bounds__(H3_THREADS, 1) k_hist3(const FitPair fp, const
   __shared__ int64_t s_pstart[2 * MAX_PIECES];
   __shared__ int16_t s_slot[2 * MAX_PIECES];
   __shared__ int8_t s_tg[2 * MAX_PIECES];
-  __shared__ int s_np;
+  __shared__ int8_t s_side[2 * MAX_PIECES];   // built child of the piece's parent (fold-in)
+  __shared__ int s_np, s_last;
 
   {   // zero both histogram channels and the users column
     uint4* z = reinterpret_cast<uint4*>(smem);
@@ -101,9 +128,11 @@ __global__ void __launch_bounds__(H3_THREADS, 1) k_hist3(const FitPair fp, const
       const LevelView& P = a.lv[d - 1];
       const LevelView& C = a.lv[d];
       int64_t len = 0, pst = 0;
+      int side_of = 0;
       if (tid < NP && P.split_f[tid] >= 0) {
         const int64_t nL = C.cnt[2 * tid], nR = C.cnt[2 * tid + 1];
         const int side = a.built_by_h ? C.built[tid] : (nL <= nR) ? 0 : 1;   // smaller child (rows; hessian when sharded)
+        side_of = side;
         len = C.cnt[2 * tid + side];
         const int64_t ps = (d == 1) ? 0 : P.start[tid], cl = C.cnt[2 * tid];   // k_part: left child first
         pst = side ? ps + cl : ps;
@@ -130,6 +159,7 @@ __global__ void __launch_bounds__(H3_THREADS, 1) k_hist3(const FitPair fp, const
         s_pstart[tg * NP + tid] = pst;
         s_slot[tg * NP + tid] = (int16_t)tid;
         s_tg[tg * NP + tid] = (int8_t)tg;
+        s_side[tg * NP + tid] = (int8_t)side_of;
       }
       base = tot;
       __syncthreads();   // s_wsum is reused by the next ensemble
@@ -150,8 +180,14 @@ __global__ void __launch_bounds__(H3_THREADS, 1) k_hist3(const FitPair fp, const
   const int np = s_np;
   const int64_t S = s_vstart[np];
   const int64_t v0 = S * blockIdx.x / gridDim.x, v1 = S * (blockIdx.x + 1) / gridDim.x;
-  if (v0 >= v1) return;
-  if (tid == 0 && MODE == HM_LEVEL && a0.units) atomicAdd(&a0.units[KC_HIST], (unsigned long long)(v1 - v0));
+  if (MODE == HM_LEVEL && fold) {
+    // fold-in: pieces without rows (a parent that did not split, or an empty built child) are
+    // evaluated by CTA p mod G up front (nothing to wait for: the built slot was zeroed by k_part)
+    for (int pp = blockIdx.x; pp < np; pp += gridDim.x)
+      if (s_vstart[pp + 1] == s_vstart[pp]) fold_split(fp, s_tg[pp], d, s_slot[pp], s_side[pp]);
+  }
+  if (v0 >= v1 && !(MODE == HM_LEVEL && fold)) return;   // (fold-in: an idle CTA still evaluates queued pieces)
+  if (v0 < v1 && tid == 0 && MODE == HM_LEVEL && a0.units) atomicAdd(&a0.units[KC_HIST], (unsigned long long)(v1 - v0));
 
   const uint32_t sgb = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t sub = sgb + H3_U_OFF;
@@ -318,6 +354,63 @@ __global__ void __launch_bounds__(H3_THREADS, 1) k_hist3(const FitPair fp, const
       }
       __syncthreads();
     }
+    if (MODE == HM_LEVEL && fold) {
+      // this CTA's contribution to the piece is flushed: the CTA completing the count of CTAs that
+      // cover the piece evaluates the split of the piece's parent
+      const FitArgs& ap = fp.t[s_tg[pc]];
+      int* ticket = &ap.lv[d].done[2 * s_slot[pc]];
+      if (tid == 0) {
+        const int64_t G = gridDim.x;
+        auto cta_of = [&](int64_t v) {   // largest b with floor(S b / G) <= v: the CTA holding v
+          int lo = 0, hi = (int)G - 1;
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (S * mid / G <= v) lo = mid;
+            else hi = mid - 1;
+          }
+          return lo;
+        };
+        const int ncta = cta_of(s_vstart[pc + 1] - 1) - cta_of(s_vstart[pc]) + 1;
+        __threadfence();
+        const int prev = atomicAdd(ticket, 1);
+        s_last = prev + 1 == ncta;
+        if (s_last) {
+          *ticket = 0;   // self-resetting for the next tree
+          __threadfence();
+        }
+      }
+      __syncthreads();
+      // the piece is complete: queue its split evaluation (any CTA whose histogram work is done
+      // takes it — a CTA covering many small pieces would otherwise evaluate them all in series)
+      if (s_last && tid == 0) {
+        int* fq = fp.t[0].fq;
+        const int slot = atomicAdd(&fq[1], 1);
+        atomicExch(&fq[2 + slot], pc + 1);
+      }
+    }
+  }
+  if (MODE == HM_LEVEL && fold) {
+    // this CTA's histogram work is done: evaluate queued pieces until every non-empty piece is taken
+    int* fq = fp.t[0].fq;
+    int n_ne = 0;
+    for (int pp = 0; pp < np; ++pp) n_ne += s_vstart[pp + 1] > s_vstart[pp];
+    while (true) {
+      if (tid == 0) {
+        const int h = atomicAdd(&fq[0], 1);
+        int pc = -1;
+        if (h < n_ne) {
+          volatile int* slot = &fq[2 + h];
+          while ((pc = *slot) == 0) __nanosleep(200);   // produced by a CTA still flushing
+          __threadfence();
+          --pc;
+        }
+        s_last = pc;
+      }
+      __syncthreads();
+      const int pc = s_last;
+      if (pc < 0) break;
+      fold_split(fp, s_tg[pc], d, s_slot[pc], s_side[pc]);
+    }
   }
 }
 
@@ -349,7 +442,7 @@ __global__ void __launch_bounds__(U3_THREADS, 1) k_upd3(const FitPair fp) {
   const int t = *a.d_tree;
   const bool has_next = t + 1 < a.T;
   const int ucol = (a.users_col >= 0 && a.users_col < kMaxF) ? a.users_col : -1;
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ __align__(16) uint8_t smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   __shared__ __align__(8) uint64_t s_bar[U3_WARPS][U3_STAGES];
   {   // zero both histogram channels and the users column
