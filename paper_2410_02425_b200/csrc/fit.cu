@@ -198,7 +198,7 @@ __device__ __forceinline__ bool root_needed(const FitArgs& a, int t) {
 }
 // one tree in shared memory after the histogram kernels' dynamic smem, sized for the fit's depth
 // (nnp = nn + 1 = 2^(D+1)): k_hist: s_feat (int8, nnp), s_bin (u8, nnp), s_val (f32, nnp);
-// k_hist2: the fixed-depth routing table (s_rf, s_rb: u8 x 2^D each, s_lv: f32 x 2^D).
+// k_hist2: the fixed-depth routing table (s_rt: u16 x 2^D node words, s_lv: f32 x 2^D).
 // Depth 8 adds 3 KB (two CTAs per SM); depth 10 adds 12 KB.
 __host__ __device__ constexpr int updroot_tree_smem(int D) { return 6 << (D + 1); }
 
@@ -598,12 +598,12 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
   for (int i = tid; i < 2 * H2_CELLS; i += H2_THREADS) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
   for (int i = tid; i < 2 * kBins; i += H2_THREADS) reinterpret_cast<uint32_t*>(sug)[i] = 0u;
   // fused mode: tree t (the one just grown) in shared memory as a fixed-depth routing table: every
-  // row descends exactly D levels.  Internal node k (depth < D): s_rf[k], s_rb[k] = its split; a leaf
+  // row descends exactly D levels.  Internal node k (depth < D): s_rt[k] = its split (f | b << 8); a leaf
   // above depth D and everything below it get (0, 255), i.e. "always left" (no code exceeds 255), so
   // a row reaching leaf k at depth d ends at k's leftmost depth-D descendant (k+1)·2^(D-d) - 1,
   // whose slot in s_lv holds k's value.  No per-level leaf test.
-  uint8_t* s_rf = smem + H2_SMEM;
-  uint8_t* s_rb = smem + H2_SMEM + (a.nn + 1) / 2;
+  // one u16 word per internal node: feature | bin << 8 (a single shared load per level)
+  uint16_t* s_rt = reinterpret_cast<uint16_t*>(smem + H2_SMEM);
   float* s_lv = reinterpret_cast<float*>(smem + H2_SMEM + (a.nn + 1));   // 2^D depth-D slots
   const int n_int = (a.nn - 1) / 2;   // 2^D - 1 slots above depth D
   if (MODE == HM_UPDROOT) {
@@ -611,8 +611,7 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
     for (int i = tid; i < a.nn; i += H2_THREADS) {
       const int f = a.tfeat[to + i];
       if (i < n_int) {
-        s_rf[i] = (uint8_t)(f >= 0 ? f : 0);
-        s_rb[i] = (uint8_t)(f >= 0 ? a.tbin[to + i] : 255);
+        s_rt[i] = (uint16_t)(f >= 0 ? ((uint32_t)f | ((uint32_t)(a.tbin[to + i] & 0xff) << 8)) : (255u << 8));
       }
       if (f == -1) {   // leaf at depth d = floor(log2(i + 1))
         const int dl = 31 - __clz(i + 1);
@@ -777,7 +776,10 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
           const int D = DC ? DC : a.D;
 #pragma unroll
           for (int s2 = 0; s2 < (DC ? DC : kMaxDepth); ++s2)
-            if (DC || s2 < D) k = 2 * k + 1 + (myrow[s_rf[k]] > s_rb[k] ? 1 : 0);
+            if (DC || s2 < D) {
+              const uint32_t w = s_rt[k];
+              k = 2 * k + 1 + ((uint32_t)myrow[w & 0xffu] > (w >> 8) ? 1 : 0);
+            }
           const float pn = __fadd_rn(np_, s_lv[k - n_int]);   // one fp32 rounding, tree order
           a.p[ridx] = pn;
           if (has_next) {
@@ -2255,7 +2257,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   ensure_smem_attr((const void*)k_hist<HM_LEVEL>, HIST_SMEM);
   ensure_smem_attr((const void*)k_hist2<HM_ROOT>, H2_SMEM);
   ensure_smem_attr((const void*)k_hist2<HM_LEVEL>, H2_SMEM);
-  ensure_smem_attr((const void*)k_hist3<HM_LEVEL>, H3_SMEM);
+  ensure_smem_attr((const void*)k_hist3<HM_LEVEL, false>, H3_SMEM);
+  ensure_smem_attr((const void*)k_hist3<HM_LEVEL, true>, H3_SMEM);
   // the fused update kernels' dynamic shared memory depends on the depth (the tree they route)
   ensure_smem_attr((const void*)k_hist<HM_UPDROOT>, HIST_SMEM + updroot_tree_smem(D));
   const Hist2Kernel k_upd2 = updroot2_kernel(D);
@@ -2355,8 +2358,8 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       // persistent tile loop (upper bound of the level's tile count: one partial tile per parent)
       LLMP_LAUNCH_PDL(ctx, KC_PARTITION, ny * n, k_part, dim3(std::min(tiles_d, PT_CTAS_PER_SM / ny * ctx->sms), ny),
                   PT_THREADS, 0, fp, d);
-      if (lvk == 3) LLMP_LAUNCH_PDL(ctx, KC_HIST, 0, k_hist3<HM_LEVEL>, hg3, H3_THREADS, H3_SMEM, fp, ny, d, nodbg,
-                                    fold ? 1 : 0);
+      if (lvk == 3 && fold) LLMP_LAUNCH_PDL(ctx, KC_HIST, 0, (k_hist3<HM_LEVEL, true>), hg3, H3_THREADS, H3_SMEM, fp, ny, d, nodbg);
+      else if (lvk == 3) LLMP_LAUNCH_PDL(ctx, KC_HIST, 0, (k_hist3<HM_LEVEL, false>), hg3, H3_THREADS, H3_SMEM, fp, ny, d, nodbg);
       else if (lvk == 1) LLMP_LAUNCH_PDL(ctx, KC_HIST, 0, k_hist<HM_LEVEL>, hg, HIST_THREADS, HIST_SMEM, fp, d, 0, nodbg);
       else LLMP_LAUNCH(ctx, KC_HIST, 0, k_hist2<HM_LEVEL>, hg, H2_THREADS, H2_SMEM, fp, d, 0, nodbg);
       nccl_group_start(ctx);   // both targets' built-child histograms in one NCCL launch
@@ -2542,11 +2545,11 @@ void debug_histogram(Ctx* ctx, const uint8_t* codes, int64_t n, const int32_t* i
   DbgArgs dbg{idx, qg, qh, idx ? m : n, d_out.as<int64_t>()};
   ensure_smem_attr((const void*)k_hist<HM_DEBUG>, HIST_SMEM);
   ensure_smem_attr((const void*)k_hist2<HM_DEBUG>, H2_SMEM);
-  ensure_smem_attr((const void*)k_hist3<HM_DEBUG>, H3_SMEM);
+  ensure_smem_attr((const void*)k_hist3<HM_DEBUG, false>, H3_SMEM);
   FitPair fp;
   fp.t[0] = a;
   if (level_kernel() == 3)
-    LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist3<HM_DEBUG>, ctx->sms, H3_THREADS, H3_SMEM, fp, 1, 0, dbg, 0);
+    LLMP_LAUNCH(ctx, KC_HIST, dbg.m, (k_hist3<HM_DEBUG, false>), ctx->sms, H3_THREADS, H3_SMEM, fp, 1, 0, dbg);
   else if (level_kernel() == 1)
     LLMP_LAUNCH(ctx, KC_HIST, dbg.m, k_hist<HM_DEBUG>, 2 * ctx->sms, HIST_THREADS, HIST_SMEM, fp, 0, 0, dbg);
   else

@@ -96,9 +96,9 @@ __device__ __forceinline__ void fold_split(const FitPair& fp, int tg, int d, int
   __syncthreads();
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(H3_THREADS, 1) k_hist3(const FitPair fp, const int ny, const int d, const DbgArgs dbg,
-                                                         const int fold) {
+template <int MODE, bool FOLD = false>
+__global__ void __launch_bounds__(H3_THREADS, 1) k_hist3(const FitPair fp, const int ny, const int d, const DbgArgs dbg) {
+  constexpr bool fold = FOLD;
   pdl_wait();
   const FitArgs& a0 = fp.t[0];   // F, users_col, codes: the same for both ensembles
   const int ucol = (a0.users_col >= 0 && a0.users_col < kMaxF) ? a0.users_col : -1;
