@@ -183,6 +183,14 @@ llmpilot_status llmpilot_model_gains(const llmpilot_model* m, double* gain);
  * != 0, divided by the target's total (all zeros when the ensemble has no split).
  * Errors: LLMP_EINVAL for NULL arguments. */
 llmpilot_status llmpilot_model_importance(const llmpilot_model* m, int32_t normalize, double* out);
+/* Persist a model to a file and load it back (optional model save/load; the paper
+ * persists only its dataset).  Little-endian binary: magic "LLMPMDL1", shape (F, users_col,
+ * n_trees, max_depth), base[2], the cuts (F x 255 floats + F counts) and feat/bin/thr/val/gain
+ * [2][n_trees][nodes].  A loaded model predicts, recommends and exports bit-identically to the
+ * saved one; its device tables live on ctx's device.  Errors: LLMP_EINVAL for NULL arguments, an
+ * unreadable or malformed file (bad magic, sizes out of range, short read). */
+llmpilot_status llmpilot_model_save(const llmpilot_model* m, const char* path);
+llmpilot_status llmpilot_model_load(llmpilot_ctx* ctx, const char* path, llmpilot_model** out);
 /* Free a model.  Its device buffers are released stream-ordered (cudaFreeAsync into the
  * device's default memory pool, which keeps the memory cached) on the stream of the context
  * that fitted it: free a model before destroying that stream, and only after work that reads the

@@ -93,6 +93,8 @@ def lib():
         "llmpilot_model_info": [P, C.POINTER(I32), C.POINTER(I32), C.POINTER(I32), C.POINTER(I32)],
         "llmpilot_model_export": [P, P, P, P, P, P],
         "llmpilot_model_train_pred": [P, P],
+        "llmpilot_model_save": [P, C.c_char_p],
+        "llmpilot_model_load": [P, C.c_char_p, C.POINTER(P)],
         "llmpilot_model_gains": [P, P],
         "llmpilot_model_importance": [P, I32, P],
         "llmpilot_predict": [P, P, P, I64, P],
@@ -358,6 +360,17 @@ class Model:
         po = _out_ptr(out, (n, 2), "out")
         _check(lib().llmpilot_predict(ctx.handle, self._h, px, n, po))
         return out
+
+    def save(self, path: str):
+        """llmpilot_model_save: persist the model (binary, see include/llmpilot.h)."""
+        _check(lib().llmpilot_model_save(self._h, os.fsencode(path)))
+
+    @staticmethod
+    def load(ctx: "Context", path: str) -> "Model":
+        """llmpilot_model_load: a model saved by Model.save, its tables on ctx's device."""
+        h = C.c_void_p()
+        _check(lib().llmpilot_model_load(ctx.handle, os.fsencode(path), C.byref(h)))
+        return Model(h)
 
     def free(self):
         if self._h:

@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <new>
 
+#include <stdio.h>
+
 #include "internal.cuh"
 
 struct llmpilot_ctx {
@@ -394,6 +396,90 @@ llmpilot_status llmpilot_model_train_pred(const llmpilot_model* m, float* train_
 }
 
 void llmpilot_model_free(llmpilot_model* m) { delete m; }
+
+namespace {
+constexpr char kModelMagic[8] = {'L', 'L', 'M', 'P', 'M', 'D', 'L', '1'};
+}
+
+llmpilot_status llmpilot_model_save(const llmpilot_model* m, const char* path) {
+  return guarded([&] {
+    LLMP_REQUIRE(m && path, "NULL argument");
+    const llmp::ModelData& d = m->m;
+    LLMP_REQUIRE(d.cuts.stride == llmp::kBins - 1, "only 8-bit-code models are persisted");
+    FILE* fp = fopen(path, "wb");
+    LLMP_REQUIRE(fp != nullptr, std::string("cannot open ") + path + " for writing");
+    const int32_t hdr[4] = {d.F, d.users_col, d.T, d.D};
+    const size_t tot = (size_t)2 * d.T * d.nn;
+    bool ok = fwrite(kModelMagic, 1, 8, fp) == 8 && fwrite(hdr, 4, 4, fp) == 4 && fwrite(d.base, 4, 2, fp) == 2 &&
+              fwrite(d.cuts.h_cuts.data(), 4, (size_t)d.F * 255, fp) == (size_t)d.F * 255 &&
+              fwrite(d.cuts.h_ncuts.data(), 4, (size_t)d.F, fp) == (size_t)d.F;
+    ok = ok && fwrite(d.feat.data(), 4, tot, fp) == tot && fwrite(d.bin.data(), 4, tot, fp) == tot &&
+         fwrite(d.thr.data(), 4, tot, fp) == tot && fwrite(d.val.data(), 4, tot, fp) == tot &&
+         fwrite(d.gain.data(), 8, tot, fp) == tot;
+    ok = (fclose(fp) == 0) && ok;
+    LLMP_REQUIRE(ok, std::string("write failed: ") + path);
+  });
+}
+
+llmpilot_status llmpilot_model_load(llmpilot_ctx* ctx, const char* path, llmpilot_model** out) {
+  return guarded([&] {
+    LLMP_REQUIRE(ctx && path && out, "NULL argument");
+    FILE* fp = fopen(path, "rb");
+    LLMP_REQUIRE(fp != nullptr, std::string("cannot open ") + path);
+    auto* mo = new llmpilot_model();
+    try {
+      char mg[8];
+      int32_t hdr[4];
+      bool ok = fread(mg, 1, 8, fp) == 8 && memcmp(mg, kModelMagic, 8) == 0 && fread(hdr, 4, 4, fp) == 4;
+      LLMP_REQUIRE(ok, "not an llmpilot model file");
+      llmp::ModelData& d = mo->m;
+      d.F = hdr[0];
+      d.users_col = hdr[1];
+      d.T = hdr[2];
+      d.D = hdr[3];
+      LLMP_REQUIRE(d.F >= 1 && d.F <= llmp::kMaxF && d.users_col >= 0 && d.users_col < d.F && d.T >= 0 &&
+                       d.T <= (1 << 24) && d.D >= 1 && d.D <= llmp::kMaxDepth,
+                   "model file: shape out of range");
+      d.nn = (1 << (d.D + 1)) - 1;
+      const size_t tot = (size_t)2 * d.T * d.nn;
+      d.cuts.F = d.F;
+      d.cuts.stride = llmp::kBins - 1;
+      d.cuts.h_cuts.assign((size_t)llmp::kMaxF * 255, 0.f);
+      d.cuts.h_ncuts.assign(llmp::kMaxF, 0);
+      d.feat.resize(tot);
+      d.bin.resize(tot);
+      d.thr.resize(tot);
+      d.val.resize(tot);
+      d.gain.resize(tot);
+      ok = fread(d.base, 4, 2, fp) == 2 && fread(d.cuts.h_cuts.data(), 4, (size_t)d.F * 255, fp) == (size_t)d.F * 255 &&
+           fread(d.cuts.h_ncuts.data(), 4, (size_t)d.F, fp) == (size_t)d.F && fread(d.feat.data(), 4, tot, fp) == tot &&
+           fread(d.bin.data(), 4, tot, fp) == tot && fread(d.thr.data(), 4, tot, fp) == tot &&
+           fread(d.val.data(), 4, tot, fp) == tot && fread(d.gain.data(), 8, tot, fp) == tot;
+      LLMP_REQUIRE(ok, "model file: short read");
+      for (int f = 0; f < d.F; ++f) LLMP_REQUIRE(d.cuts.h_ncuts[f] >= 0 && d.cuts.h_ncuts[f] <= 255, "model file: bad cuts");
+      for (size_t i = 0; i < tot; ++i)
+        LLMP_REQUIRE(d.feat[i] >= -2 && d.feat[i] < d.F && d.bin[i] >= 0 && d.bin[i] <= 255, "model file: bad node");
+      fclose(fp);
+      fp = nullptr;
+      set_device(&ctx->c);
+      d.device = ctx->c.device;
+      d.cuts.d_cuts.set_stream(ctx->c.stream);
+      d.cuts.d_ncuts.set_stream(ctx->c.stream);
+      d.cuts.d_cuts.ensure((size_t)llmp::kMaxF * 255 * 4);
+      d.cuts.d_ncuts.ensure((size_t)llmp::kMaxF * 4);
+      LLMP_CUDA(cudaMemcpyAsync(d.cuts.d_cuts.p, d.cuts.h_cuts.data(), (size_t)llmp::kMaxF * 255 * 4,
+                                cudaMemcpyHostToDevice, ctx->c.stream));
+      LLMP_CUDA(cudaMemcpyAsync(d.cuts.d_ncuts.p, d.cuts.h_ncuts.data(), (size_t)llmp::kMaxF * 4, cudaMemcpyHostToDevice,
+                                ctx->c.stream));
+      llmp::upload_model_nodes(&ctx->c, d);   // (synchronises the stream)
+      *out = mo;
+    } catch (...) {
+      if (fp) fclose(fp);
+      delete mo;
+      throw;
+    }
+  });
+}
 
 // ---- workload generator (§III-B)
 llmpilot_status llmpilot_wg_build(llmpilot_ctx* ctx, const float* traces, int64_t n, int32_t P, llmpilot_wg** out) {

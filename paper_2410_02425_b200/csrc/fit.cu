@@ -2420,9 +2420,9 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   // cannot starve the GPU).  LLMP_GRAPH_REPLAY=1 replays the round graph T times from the host.
   static const bool replay_env = getenv("LLMP_GRAPH_REPLAY") && atoi(getenv("LLMP_GRAPH_REPLAY")) != 0;
   const bool replay = replay_env || sharded;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ge = nullptr;
   if (graphs) {
-    cudaGraph_t g = nullptr;
-    cudaGraphExec_t ge = nullptr;
     const cudaStream_t user = ctx->stream;
     const cudaStream_t sa = ctx->capture_stream(0);
     uint64_t l0[LLMP_N_KERNEL_CLASSES];
@@ -2447,13 +2447,9 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       ctx->stream = sa;
       LLMP_CUDA(cudaStreamBeginCapture(sa, cudaStreamCaptureModeThreadLocal));
     }
+    bool ok = true;
     try {
       round(replay ? nullptr : &loop);
-      // launch counters: the captured round runs T times
-      for (int c = 0; c < LLMP_N_KERNEL_CLASSES; ++c) {
-        ctx->launches[c] += (ctx->launches[c] - l0[c]) * (uint64_t)(T - 1);
-        ctx->rows[c] += (ctx->rows[c] - r0[c]) * (double)(T - 1);
-      }
     } catch (...) {
       ctx->comm_sel = 0;
       ctx->stream = sa;
@@ -2461,22 +2457,47 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       cudaStreamEndCapture(sa, &gc);
       if (replay && gc) cudaGraphDestroy(gc);
       if (g) cudaGraphDestroy(g);
+      g = nullptr;
       ctx->stream = user;
-      throw;
+      cudaGetLastError();
+      if (!sharded) throw;
+      ok = false;   // sharded: NCCL collectives that could not be captured -> plain launches below
     }
-    cudaGraph_t gc = nullptr;
-    LLMP_CUDA(cudaStreamEndCapture(sa, &gc));
-    if (replay) g = gc;
-    ctx->stream = user;
-    LLMP_CUDA(cudaGraphInstantiate(&ge, g, 0));
-    if (stamps) k_stamp<<<1, 1, 0, s>>>(stamps);
-    if (replay) {
-      for (int t = 0; t < T; ++t) LLMP_CUDA(cudaGraphLaunch(ge, s));
-    } else {
-      LLMP_CUDA(cudaGraphLaunch(ge, s));
+    if (ok) {
+      cudaGraph_t gc = nullptr;
+      LLMP_CUDA(cudaStreamEndCapture(sa, &gc));
+      if (replay) g = gc;
+      ctx->stream = user;
+      const cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        cudaGraphDestroy(g);
+        g = nullptr;
+        ge = nullptr;
+        if (!sharded) check_cuda(e, "cudaGraphInstantiate", __FILE__, __LINE__);
+        ok = false;
+      }
     }
-    LLMP_CUDA(cudaGraphExecDestroy(ge));
-    LLMP_CUDA(cudaGraphDestroy(g));
+    if (ok) {   // launch counters: the captured round runs T times
+      for (int c = 0; c < LLMP_N_KERNEL_CLASSES; ++c) {
+        ctx->launches[c] += (ctx->launches[c] - l0[c]) * (uint64_t)(T - 1);
+        ctx->rows[c] += (ctx->rows[c] - r0[c]) * (double)(T - 1);
+      }
+      if (stamps) k_stamp<<<1, 1, 0, s>>>(stamps);
+      if (replay) {
+        for (int t = 0; t < T; ++t) LLMP_CUDA(cudaGraphLaunch(ge, s));
+      } else {
+        LLMP_CUDA(cudaGraphLaunch(ge, s));
+      }
+      LLMP_CUDA(cudaGraphExecDestroy(ge));
+      LLMP_CUDA(cudaGraphDestroy(g));
+    } else {    // the same rounds as plain launches
+      memcpy(ctx->launches, l0, sizeof(l0));
+      memcpy(ctx->rows, r0, sizeof(r0));
+      nccl_health(ctx);
+      ctx->pdl = false;
+      for (int t = 0; t < T; ++t) round(nullptr);
+    }
   } else {
     for (int t = 0; t < T; ++t) round(nullptr);
   }

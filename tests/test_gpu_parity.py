@@ -386,6 +386,33 @@ def test_predict_and_recommend_parity(lp, ctx):
     assert any(r[0] == -1 for r in grec2) or True
 
 
+def test_model_save_load_round_trip(lp, ctx, tmp_path):
+    """llmpilot_model_save / llmpilot_model_load: the loaded model exports, predicts, ranks features
+    and recommends exactly as the fitted one (and as the oracle); malformed files are refused."""
+    d = synth.make("C2")
+    om, otp, gm = _fit_both(lp, ctx, d, n_trees=30, max_depth=6)
+    path = str(tmp_path / "m.llmp")
+    gm.save(path)
+    lm = lp.Model.load(ctx, path)
+    e1, e2 = gm.export(), lm.export()
+    for k in e1:
+        assert np.array_equal(e1[k], e2[k]), k
+    assert np.array_equal(gm.gains(), lm.gains())
+    assert np.array_equal(gm.importance(), lm.importance())
+    assert _bits_equal(lm.predict(ctx, d.X), otp)
+    lf, pf, cost, levels = synth.sweep_tables(n_llm=50)
+    assert lp.recommend(ctx, lm, lf, pf, cost, levels, L1, L2, U) == \
+        lp.recommend(ctx, gm, lf, pf, cost, levels, L1, L2, U)
+    raw = open(path, "rb").read()
+    bad = tmp_path / "bad.llmp"
+    for blob in (b"", b"NOTMODEL" + raw[8:], raw[: len(raw) // 2]):
+        bad.write_bytes(blob)
+        with pytest.raises(lp.LLMPilotError):
+            lp.Model.load(ctx, str(bad))
+    with pytest.raises(lp.LLMPilotError):
+        lp.Model.load(ctx, str(tmp_path / "missing.llmp"))
+
+
 def test_c5_sweep_full_size_sampled_parity(lp, ctx):
     """BASELINE configs[4] at full size: the C2-shaped model (2 x 1000 trees, depth 6) and
     the sweep of 6,554 unseen LLMs x 10 profiles x 16 levels = 1,048,640 rows in the launch
