@@ -250,6 +250,7 @@ void llmpilot_hparams_default(llmpilot_hparams* hp) {
 llmpilot_status llmpilot_bin(llmpilot_ctx* ctx, const float* X, int64_t n, int32_t F, int32_t max_bin,
                              const llmpilot_cuts* cuts_in, llmpilot_cuts** cuts_out, uint8_t* codes_out) {
   return guarded([&] {
+    llmp::NvtxRange nvtx_("llmpilot_bin");
     LLMP_REQUIRE(ctx && X, "NULL argument");
     LLMP_REQUIRE(n >= 1 && F >= 1 && F <= llmp::kMaxF, "bad sizes");
     LLMP_REQUIRE(!codes_out || llmp::is_device_ptr(codes_out), "codes_out must be a device buffer");
@@ -309,6 +310,7 @@ void llmpilot_cuts_free(llmpilot_cuts* cuts) { delete cuts; }
 llmpilot_status llmpilot_fit(llmpilot_ctx* ctx, const llmpilot_dataset* ds, const llmpilot_hparams* hp, float L1,
                              float L2, llmpilot_model** out) {
   return guarded([&] {
+    llmp::NvtxRange nvtx_("llmpilot_fit");
     LLMP_REQUIRE(ctx && ds && hp && out, "NULL argument");
     set_device(&ctx->c);
     ResolvedDataset r;
@@ -423,6 +425,7 @@ llmpilot_status llmpilot_model_save(const llmpilot_model* m, const char* path) {
 
 llmpilot_status llmpilot_model_load(llmpilot_ctx* ctx, const char* path, llmpilot_model** out) {
   return guarded([&] {
+    llmp::NvtxRange nvtx_("llmpilot_model_load");
     LLMP_REQUIRE(ctx && path && out, "NULL argument");
     FILE* fp = fopen(path, "rb");
     LLMP_REQUIRE(fp != nullptr, std::string("cannot open ") + path);
@@ -542,6 +545,7 @@ void llmpilot_wg_free(llmpilot_wg* w) { delete w; }
 
 llmpilot_status llmpilot_predict(llmpilot_ctx* ctx, const llmpilot_model* m, const float* X, int64_t n, float* out) {
   return guarded([&] {
+    llmp::NvtxRange nvtx_("llmpilot_predict");
     LLMP_REQUIRE(ctx && m && X && out, "NULL argument");
     LLMP_REQUIRE(n >= 0, "n must be >= 0");
     if (n == 0) return;
@@ -564,6 +568,7 @@ llmpilot_status llmpilot_recommend(llmpilot_ctx* ctx, const llmpilot_model* m, c
                                    int32_t n_levels, float L1, float L2, int64_t U, llmpilot_rec* out,
                                    float* pred_out) {
   return guarded([&] {
+    llmp::NvtxRange nvtx_("llmpilot_recommend");
     LLMP_REQUIRE(ctx && m && out && prof_cost && user_levels, "NULL argument");
     LLMP_REQUIRE(n_llm >= 0 && n_prof >= 1 && n_levels >= 1, "bad sizes");
     LLMP_REQUIRE(F_llm >= 0 && F_prof >= 0 && F_llm + F_prof + 1 == m->m.F, "F_llm + F_prof + 1 must equal the model's F");
@@ -603,6 +608,7 @@ llmpilot_status llmpilot_cv_leave_one_llm_out(llmpilot_ctx* ctx, const llmpilot_
                                               const llmpilot_hparams* grid, int32_t n_grid, float L1, float L2,
                                               int64_t U, const double* prof_cost, llmpilot_cv_report** out) {
   return guarded([&] {
+    llmp::NvtxRange nvtx_("llmpilot_cv_leave_one_llm_out");
     LLMP_REQUIRE(ctx && ds && grid && prof_cost && out, "NULL argument");
     LLMP_REQUIRE(ds->n_llm >= 2 && ds->n_prof >= 1, "need n_llm >= 2 and n_prof >= 1");
     LLMP_REQUIRE(ds->llm_id && ds->profile_id, "llm_id and profile_id are required");

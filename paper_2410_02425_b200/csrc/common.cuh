@@ -10,9 +10,20 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/llmpilot.h"
 
 namespace llmp {
+
+// NVTX range (header-only NVTX3: a no-op unless a tool such as nsys or ncu --nvtx attaches): every
+// C-ABI entry point, the fit phases, and per tree / level when the tree loop runs as plain launches
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 constexpr int kMaxF = 32;        // features per row (codes padded to 32 bytes = one DRAM sector)
 constexpr int kBins = 256;       // histogram bins per feature (u8 codes)

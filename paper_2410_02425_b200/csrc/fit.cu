@@ -25,6 +25,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <memory>
 
 #include "bulk.cuh"
 #include "internal.cuh"
@@ -2046,7 +2047,14 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   // diagnostics (LLMP_FIT_PHASES=1): host-synchronised phase times on stderr
   static const bool phases = getenv("LLMP_FIT_PHASES") && atoi(getenv("LLMP_FIT_PHASES")) != 0;
   auto ph_t0 = std::chrono::steady_clock::now();
+  std::unique_ptr<NvtxRange> ph_range(new NvtxRange("validate"));
   auto phase = [&](const char* name) {
+    ph_range.reset();
+    static const char* const next_of[][2] = {{"validate", "weights"}, {"weights", "cuts+codes"}, {"cuts+codes", "state"},
+                                             {"state", "base"}, {"base", "tree loop"}, {"loop", "to_host"},
+                                             {"to_host", "upload"}};
+    for (const auto& nx : next_of)
+      if (!strcmp(nx[0], name)) ph_range.reset(new NvtxRange(nx[1]));
     if (!phases) return;
     LLMP_CUDA(cudaStreamSynchronize(ctx->stream));
     const auto t1 = std::chrono::steady_clock::now();
@@ -2353,7 +2361,10 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     for (int q = 0; q < ny; ++q) allreduce_sum_i64(ctx, fp.t[q].H[0], SLOT);
     nccl_group_end(ctx);
     split(fp, ny, 0);
+    static const char* const level_name[] = {"level 0", "level 1", "level 2", "level 3", "level 4",
+                                             "level 5", "level 6", "level 7", "level 8", "level 9"};
     for (int d = 1; d < D; ++d) {
+      NvtxRange lr(level_name[d]);
       const int tiles_d = (int)((n + PT_TILE - 1) / PT_TILE) + (1 << (d - 1));
       // persistent tile loop (upper bound of the level's tile count: one partial tile per parent)
       LLMP_LAUNCH_PDL(ctx, KC_PARTITION, ny * n, k_part, dim3(std::min(tiles_d, PT_CTAS_PER_SM / ny * ctx->sms), ny),
@@ -2496,10 +2507,16 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       memcpy(ctx->rows, r0, sizeof(r0));
       nccl_health(ctx);
       ctx->pdl = false;
-      for (int t = 0; t < T; ++t) round(nullptr);
+      for (int t = 0; t < T; ++t) {
+        NvtxRange tr("tree");
+        round(nullptr);
+      }
     }
   } else {
-    for (int t = 0; t < T; ++t) round(nullptr);
+    for (int t = 0; t < T; ++t) {
+      NvtxRange tr("tree");
+      round(nullptr);
+    }
   }
 
   if (stamps) {   // diagnostics: per-round device durations
