@@ -185,6 +185,40 @@ def test_fit_parity_ragged_sizes(lp, ctx, n):
     assert _bits_equal(otp, gm.train_pred(d.n))
 
 
+def _degenerate(case):
+    import copy
+    d = copy.deepcopy(synth.make_s1(5000, seed=4))
+    w = d.w.copy()
+    if case == "constant_y":
+        d.y[:] = np.float32(1.5)
+    elif case == "constant_features":
+        d.X[:, 3] = np.float32(7)
+        d.X[:, 10] = np.float32(-2)
+    elif case == "zero_weights":
+        w[:] = 0
+    elif case == "half_zero_weights":
+        w[::2] = 0
+    elif case == "single_feature":
+        d.X = np.ascontiguousarray(d.X[:, 31:32])
+        d.users_col = 0
+    elif case == "all_rows_equal":
+        d.X[:] = np.float32(0)
+    return d, w
+
+
+@pytest.mark.parametrize("case", ["constant_y", "constant_features", "zero_weights", "half_zero_weights",
+                                  "single_feature", "all_rows_equal"])
+def test_fit_parity_degenerate_inputs(lp, ctx, case):
+    """Degenerate data the method must handle: no split has positive gain (constant y, all rows
+    equal, all weights zero — every tree is a single leaf), constant columns (never split on),
+    a single feature (the users column only) and rows with zero weight (h = 0)."""
+    d, w = _degenerate(case)
+    om, otp, gm = _fit_both(lp, ctx, d, w=w, n_trees=5, max_depth=4, use_eq4_weights=0)
+    _assert_same_model(om, gm.export(), case)
+    assert _bits_equal(otp, gm.train_pred(d.n))
+    assert _bits_equal(oracle.predict(om, d.X), gm.predict(ctx, d.X))
+
+
 def test_fit_sequential_mode_and_root_speculation(lp, ctx):
     """Instrumented mode runs the two ensembles one after the other with plain launches (the
     NCCL path does too); it must give the oracle's model like the concurrent graph replay.  The
