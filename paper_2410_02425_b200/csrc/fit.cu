@@ -110,6 +110,7 @@ struct FitArgs {
   const float* w_base;  // RF: the rows' weights before the bootstrap (w then holds the current tree's)
   int* fq;              // fold-in work queue of the level histogram (k_hist3): [0] head, [1] tail, slots
   const uint32_t* cmask;  // [n/32 batches][32 lanes] precomputed change masks (k_cmask), or null
+  int64_t* hroot;         // h_fixed: the root's q_h histogram (tree-invariant, DESIGN R38), saved at tree 0
   int nn;
   FeatBest* fbest;            // [2^(D-1)][32] per-(node, feature) best split of the current level
   unsigned long long* units;  // device counters of rows processed per kernel class (instrumentation)
@@ -575,7 +576,9 @@ __device__ __forceinline__ void red2(uint32_t addr, int32_t g, uint32_t h) {
   asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(addr), "r"(h), "n"(H2_HH) : "memory");
 }
 
-template <int MODE, int DC = 0>   // DC: compile-time tree depth of the fused update's routing (0 = a.D)
+// DC: compile-time tree depth of the fused update's routing (0 = a.D); HF (fused update only): the
+// root's q_h channel is tree-invariant (DESIGN R38) and copied from a.hroot, so only q_g is histogrammed
+template <int MODE, int DC = 0, bool HF = false>
 __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const int d, const int t_in, const DbgArgs dbg) {
   pdl_wait();
   const FitArgs& a = fp.t[blockIdx.y];
@@ -815,22 +818,22 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
         if (ucol >= 0 && valid) {   // users column, row-parallel into the dense per-bin histogram
           const uint32_t ua = sub + (uint32_t)myrow[ucol] * 4u;
           asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(ua), "r"(qg) : "memory");
-          asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(ua), "r"(qh), "n"(kBins * 4) : "memory");
+          if (!HF) asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(ua), "r"(qh), "n"(kBins * 4) : "memory");
         }
         // inclusive prefix sums of the pairs over the batch's rows
         int32_t pg = qg;
-        uint32_t ph = qh;
+        uint32_t ph = HF ? 0u : qh;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const int32_t ug = __shfl_up_sync(0xffffffffu, pg, o);
-          const uint32_t uh = __shfl_up_sync(0xffffffffu, ph, o);
+          const uint32_t uh = HF ? 0u : __shfl_up_sync(0xffffffffu, ph, o);
           if (lane >= o) {
             pg += ug;
             ph += uh;
           }
         }
         const int32_t tot_g = __shfl_sync(0xffffffffu, pg, 31);
-        const uint32_t tot_h = __shfl_sync(0xffffffffu, ph, 31);
+        const uint32_t tot_h = HF ? 0u : __shfl_sync(0xffffffffu, ph, 31);
         // ---- feature side
         uint32_t M = pre ? (fresh ? bmask & ~1u : bmask) : warp_transpose32(m, lane);
         if (fresh) {
@@ -845,11 +848,12 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
         while (__any_sync(0xffffffffu, Ml != 0u)) {
           const int r = __ffs(Ml) - 1;
           const int32_t pgr = __shfl_sync(0xffffffffu, pg, (r - 1) & 31);
-          const uint32_t phr = __shfl_sync(0xffffffffu, ph, (r - 1) & 31);
+          const uint32_t phr = HF ? 0u : __shfl_sync(0xffffffffu, ph, (r - 1) & 31);
           if (Ml) {
             const int32_t vg = r ? pgr : 0;
             const uint32_t vh = r ? phr : 0u;
-            red2(sgb + cur, acc_g + (vg - bg), acc_h + (vh - bh));
+            if (HF) asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(sgb + cur), "r"(acc_g + (vg - bg)) : "memory");
+            else red2(sgb + cur, acc_g + (vg - bg), acc_h + (vh - bh));
             acc_g = 0;
             acc_h = 0;
             bg = vg;
@@ -880,7 +884,7 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
               for (int j = 0; j < 4; ++j) {
                 const int hl = 8 * j + 7 - q, hf = 4 * q + j;
                 if ((hm & (1u << hl)) && valid)
-                  red2(sgb + (((cw[q] >> (8 * j)) & 0xffu) * H2_PAD + (uint32_t)hf) * 4u, qg, qh);
+                  red2(sgb + (((cw[q] >> (8 * j)) & 0xffu) * H2_PAD + (uint32_t)hf) * 4u, qg, HF ? 0u : qh);
               }
             }
           }
@@ -904,7 +908,7 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
         const uint32_t h = sh[b * H2_PAD + f];
         if (g != 0 || h != 0) {
           atomicAdd(reinterpret_cast<unsigned long long*>(&Hg[f * kBins + b]), (unsigned long long)(long long)g);
-          atomicAdd(reinterpret_cast<unsigned long long*>(&Hh[f * kBins + b]), (unsigned long long)h);
+          if (!HF) atomicAdd(reinterpret_cast<unsigned long long*>(&Hh[f * kBins + b]), (unsigned long long)h);
           sg[b * H2_PAD + f] = 0;
           sh[b * H2_PAD + f] = 0;
         }
@@ -948,7 +952,12 @@ __global__ void __launch_bounds__(256) k_cmask(const uint8_t* codes, int64_t n, 
 
 // the fused update kernel for a depth: compile-time routing depth for the configs' depths (6, 8)
 using Hist2Kernel = void (*)(const FitPair, const int, const int, const DbgArgs);
-static Hist2Kernel updroot2_kernel(int D) {
+static Hist2Kernel updroot2_kernel(int D, bool hf) {
+  if (hf) {
+    if (D == 8) return k_hist2<HM_UPDROOT, 8, true>;
+    if (D == 6) return k_hist2<HM_UPDROOT, 6, true>;
+    return k_hist2<HM_UPDROOT, 0, true>;
+  }
   if (D == 8) return k_hist2<HM_UPDROOT, 8>;
   if (D == 6) return k_hist2<HM_UPDROOT, 6>;
   return k_hist2<HM_UPDROOT, 0>;
@@ -1485,6 +1494,11 @@ __device__ __forceinline__ bool split_feature(const FitArgs& a, const int d, con
       h8[2 * q] = hv[q].x;
       h8[2 * q + 1] = hv[q].y;
     }
+  }
+  if (d == 0 && a.hroot && t == 0) {   // h_fixed: keep tree 0's root q_h histogram (R38)
+    longlong2* hs = reinterpret_cast<longlong2*>(a.hroot + f * kBins + lane * 8);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) hs[q] = make_longlong2(h8[2 * q], h8[2 * q + 1]);
   }
 #pragma unroll
   for (int q = 1; q < 8; ++q) {
@@ -2165,6 +2179,12 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
               d_cm.as<uint32_t>());
   const uint32_t* cmask = d_cm.as<uint32_t>();
   static const int hist1 = hist1_mask();
+  // R38: with h = w on every row of every tree (no row subsampling, not a random forest) the root's
+  // q_h histogram is the same for every tree; the fused update then builds only the q_g channel and
+  // the round copies q_h from tree 0's (unsharded: a sharded root is summed across ranks afterwards)
+  static const bool hfix_env = !(getenv("LLMP_HFIX") && atoi(getenv("LLMP_HFIX")) == 0);
+  const bool hfix = hfix_env && fused && !sharded && hp.subsample >= 1.0f && hp.model == 0 && !(hist1 & 4) &&
+                    upd_kernel() == 2;
   const int lvk = level_kernel();
   // split evaluation folded into k_hist3 (LLMP_FOLD=1; unsharded only: no all-reduce between the
   // histogram and the split).  Measured slower than the separate k_split3 launch (107 vs 55 + 14 us per
@@ -2219,6 +2239,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     a.fq = ctx->workspace("fold_q" + sx, (size_t)FQ_INTS * 4).as<int>();
     if (a.rf) a.w = ctx->workspace("rf_w" + sx, (size_t)n * 4).as<float>();   // per-tree bootstrap weights
     a.cmask = cmask;
+    a.hroot = hfix ? ctx->workspace("hroot" + sx, (size_t)kHistBins * 8).as<int64_t>() : nullptr;
     a.nn = nn;
     a.units = ctx->d_units;
     a.fbest = reinterpret_cast<FeatBest*>(ctx->workspace("featbest" + sx, (size_t)half_max * 32 * 48).p);
@@ -2269,7 +2290,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   ensure_smem_attr((const void*)k_hist3<HM_LEVEL, true>, H3_SMEM);
   // the fused update kernels' dynamic shared memory depends on the depth (the tree they route)
   ensure_smem_attr((const void*)k_hist<HM_UPDROOT>, HIST_SMEM + updroot_tree_smem(D));
-  const Hist2Kernel k_upd2 = updroot2_kernel(D);
+  const Hist2Kernel k_upd2 = updroot2_kernel(D, hfix);
   ensure_smem_attr((const void*)k_upd2, H2_SMEM + updroot_tree_smem(D));
   const Upd3Kernel k_up3 = upd3_kernel(D);
   ensure_smem_attr((const void*)k_up3, U3_SMEM + updroot_tree_smem(D));
@@ -2381,7 +2402,15 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     // RF: tree t+1's bootstrap weights, read by the update's gradients (and the next root rebuild)
     if (rf) LLMP_LAUNCH_PDL(ctx, KC_MISC, ny * n, k_rf_weights, dim3(rfw_grid, ny), 256, 0, fp, 1);
     if (fused) {   // update tree t + root histogram of tree t+1 (into the now free root slot)
-      for (int q = 0; q < ny; ++q) LLMP_CUDA(cudaMemsetAsync(fp.t[q].H[0], 0, (size_t)SLOT * 8, st));
+      for (int q = 0; q < ny; ++q) {
+        if (hfix) {   // q_g channel zeroed, q_h channel = tree 0's (R38)
+          LLMP_CUDA(cudaMemsetAsync(fp.t[q].H[0], 0, (size_t)kHistBins * 8, st));
+          LLMP_CUDA(cudaMemcpyAsync(fp.t[q].H[0] + kHistBins, fp.t[q].hroot, (size_t)kHistBins * 8,
+                                    cudaMemcpyDeviceToDevice, st));
+        } else {
+          LLMP_CUDA(cudaMemsetAsync(fp.t[q].H[0], 0, (size_t)SLOT * 8, st));
+        }
+      }
       if (hist1 & 4)
         LLMP_LAUNCH(ctx, KC_UPDATE, ny * n, k_hist<HM_UPDROOT>, hg, HIST_THREADS, HIST_SMEM + updroot_tree_smem(D), fp,
                     0, 0, nodbg);
