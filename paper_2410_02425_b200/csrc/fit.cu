@@ -1334,10 +1334,21 @@ __global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitPa
     const int64_t o = (int64_t)(t - s_tile_pref[j]) * PT_TILE;
     const int len = (int)min((int64_t)PT_TILE, cnt_j - o);
     const uint32_t* rin = rin_all + s_pp[j].start + o;
+    if (d == 1) {
 #pragma unroll
-    for (int q = 0; q < PT_ITEMS; ++q) {
-      const int k = q * PT_THREADS + tid;
-      r[q] = k < len ? ((d == 1) ? (uint32_t)(o + k) : rin[k]) : 0u;
+      for (int q = 0; q < PT_ITEMS; ++q) {   // identity (a tail's rows past the parent read row 0)
+        const int k = q * PT_THREADS + tid;
+        r[q] = k < len ? (uint32_t)(o + k) : 0u;
+      }
+    } else if (len == PT_TILE) {
+#pragma unroll
+      for (int q = 0; q < PT_ITEMS; ++q) r[q] = rin[q * PT_THREADS + tid];
+    } else {
+#pragma unroll
+      for (int q = 0; q < PT_ITEMS; ++q) {
+        const int k = q * PT_THREADS + tid;
+        r[q] = k < len ? rin[k] : 0u;
+      }
     }
   };
   uint32_t ridx[PT_ITEMS], nridx[PT_ITEMS];
@@ -1354,14 +1365,23 @@ __global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitPa
     const int len = (int)min((int64_t)PT_TILE, cnt_j - o);
     const int f = pp.f, b = pp.b;
     const uint8_t* col = a.codesT + (size_t)f * a.ldT;
+    const bool full = len == PT_TILE;   // every tile but a parent's last: no row predicates
     uint32_t code[PT_ITEMS];
 #pragma unroll
     for (int q = 0; q < PT_ITEMS; ++q) code[q] = __ldg(col + ridx[q]);
+    if (full) {
 #pragma unroll
-    for (int q = 0; q < PT_ITEMS; ++q) {
-      const int k = q * PT_THREADS + tid;
-      const unsigned mw = __ballot_sync(0xffffffffu, k < len && code[q] <= (uint32_t)b);
-      if (lane == 0) bits[q * (PT_THREADS / 32) + warp] = mw;
+      for (int q = 0; q < PT_ITEMS; ++q) {
+        const unsigned mw = __ballot_sync(0xffffffffu, code[q] <= (uint32_t)b);
+        if (lane == 0) bits[q * (PT_THREADS / 32) + warp] = mw;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < PT_ITEMS; ++q) {
+        const int k = q * PT_THREADS + tid;
+        const unsigned mw = __ballot_sync(0xffffffffu, k < len && code[q] <= (uint32_t)b);
+        if (lane == 0) bits[q * (PT_THREADS / 32) + warp] = mw;
+      }
     }
     load_rows(t + gridDim.x, nridx, jnext);   // in flight across the reservation below
     __syncthreads();
@@ -1394,14 +1414,26 @@ __global__ void __launch_bounds__(PT_THREADS, PT_CTAS_PER_SM) k_part(const FitPa
     __syncthreads();
     const int64_t lbase = start_j + s_lb;                // left rows: lbase + (lefts before the row)
     const int64_t rtop = start_j + cnt_j - s_rb;         // right rows: rtop + (rights before the row)
+    if (full) {
+      uint32_t* const lp = rout + lbase;
+      uint32_t* const rp = rout + rtop;
 #pragma unroll
-    for (int q = 0; q < PT_ITEMS; ++q) {
-      const int k = q * PT_THREADS + tid;
-      if (k < len) {
+      for (int q = 0; q < PT_ITEMS; ++q) {
+        const int k = q * PT_THREADS + tid;
         const uint32_t mw = bits[q * (PT_THREADS / 32) + warp];
         const int pre = s_pre[q * (PT_THREADS / 32) + warp] + __popc(mw & lt);   // lefts before row k
-        const bool left = (mw >> lane) & 1u;
-        rout[left ? lbase + pre : rtop + (k - pre)] = ridx[q];
+        *(((mw >> lane) & 1u) ? lp + pre : rp + (k - pre)) = ridx[q];
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < PT_ITEMS; ++q) {
+        const int k = q * PT_THREADS + tid;
+        if (k < len) {
+          const uint32_t mw = bits[q * (PT_THREADS / 32) + warp];
+          const int pre = s_pre[q * (PT_THREADS / 32) + warp] + __popc(mw & lt);   // lefts before row k
+          const bool left = (mw >> lane) & 1u;
+          rout[left ? lbase + pre : rtop + (k - pre)] = ridx[q];
+        }
       }
     }
 #pragma unroll
