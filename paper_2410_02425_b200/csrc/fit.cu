@@ -1460,8 +1460,15 @@ constexpr int SP3_CLUSTER = 32 / SP3_WARPS;   // 8 CTAs = the node's 32 features
 // histogram (sibling = parent - built, exact int64, written back for the next level), prefix scan,
 // fp64 gains with the monotone veto, best (loss desc, b asc).  Lane 0 receives the result in r.
 // Returns false when the node does not exist (its parent did not split).
+// the node's scalars split_feature loaded, reused by the node's decision (split_node): one fewer
+// dependent round trip to global memory in the last-arriving warp
+struct NodeScalars {
+  double lo, hi;
+  int t;
+  uint32_t mgb, mhb;
+};
 __device__ __forceinline__ bool split_feature(const FitArgs& a, const int d, const int k, const int f, const int lane,
-                                              FeatBest& r, const int side_in = -1) {
+                                              FeatBest& r, const int side_in = -1, NodeScalars* ns = nullptr) {
   const LevelView& V = a.lv[d];
   const int j = k >> 1;                                     // parent (level d-1)
   // ---- independent loads, all issued up front
@@ -1477,6 +1484,7 @@ __device__ __forceinline__ bool split_feature(const FitArgs& a, const int d, con
     return false;
   }
   const uint32_t mgb = a.maxg[t], mhb = a.maxh[t];
+  if (ns) *ns = NodeScalars{lo, hi, t, mgb, mhb};
   int64_t* Hself;
   int64_t g8[8], h8[8];
   if (d == 0) {
@@ -1621,11 +1629,12 @@ __device__ __forceinline__ bool split_feature(const FitArgs& a, const int d, con
 // the node's decision (O6 argmax over features, O7 children, O8 leaves), by one warp: lane l holds
 // feature l's result
 __device__ __forceinline__ void split_node(const FitArgs& a, const int d, const int k, const int lane, int rvalid,
-                                           int rb, double rloss, int64_t rGL, int64_t rHL, int64_t rG, int64_t rH) {
+                                           int rb, double rloss, int64_t rGL, int64_t rHL, int64_t rG, int64_t rH,
+                                           const NodeScalars* ns = nullptr) {
   const LevelView& V = a.lv[d];
-  const int t = *a.d_tree;
-  const double lo = (d == 0) ? -INFINITY : V.lo[k], hi = (d == 0) ? INFINITY : V.hi[k];
-  const int eg = exp_of(__uint_as_float(a.maxg[t])), eh = exp_of(__uint_as_float(a.maxh[t]));
+  const int t = ns ? ns->t : *a.d_tree;
+  const double lo = ns ? ns->lo : (d == 0) ? -INFINITY : V.lo[k], hi = ns ? ns->hi : (d == 0) ? INFINITY : V.hi[k];
+  const int eg = exp_of(__uint_as_float(ns ? ns->mgb : a.maxg[t])), eh = exp_of(__uint_as_float(ns ? ns->mhb : a.maxh[t]));
   const double sgi = exp2i(eg - a.K), shi = exp2i(eh - a.K);
   const double lambda = a.lambda, mcw = a.mcw;
   double ml = rvalid ? rloss : -INFINITY;
@@ -1709,7 +1718,8 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitPair fp, con
   const int f = (blockIdx.x % SP3_CLUSTER) * SP3_WARPS + warp;
   const LevelView& V = a.lv[d];
   FeatBest r;
-  if (!split_feature(a, d, k, f, lane, r)) return;
+  NodeScalars ns;
+  if (!split_feature(a, d, k, f, lane, r, -1, &ns)) return;
   if (lane == 0) {
     if (CL) s_fb[warp] = r;
     else a.fbest[(size_t)k * 32 + f] = r;
@@ -1753,7 +1763,7 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitPair fp, con
     rH = rf->Hq;
     if (lane == 0) V.done[k] = 0;
   }
-  split_node(a, d, k, lane, rvalid, rb, rloss, rGL, rHL, rG, rH);
+  split_node(a, d, k, lane, rvalid, rb, rloss, rGL, rHL, rG, rH, &ns);
 }
 
 #include "hist3.cuh"
