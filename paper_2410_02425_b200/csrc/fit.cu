@@ -110,7 +110,7 @@ struct FitArgs {
   const float* w_base;  // RF: the rows' weights before the bootstrap (w then holds the current tree's)
   int* fq;              // fold-in work queue of the level histogram (k_hist3): [0] head, [1] tail, slots
   const uint32_t* cmask;  // [n/32 batches][32 lanes] precomputed change masks (k_cmask), or null
-  int64_t* hroot;         // h_fixed: the root's q_h histogram (tree-invariant, DESIGN R38), saved at tree 0
+  int64_t* hroot;         // h_fixed: the root's q_h histogram (tree-invariant), saved at tree 0
   int nn;
   FeatBest* fbest;            // [2^(D-1)][32] per-(node, feature) best split of the current level
   unsigned long long* units;  // device counters of rows processed per kernel class (instrumentation)
@@ -577,7 +577,7 @@ __device__ __forceinline__ void red2(uint32_t addr, int32_t g, uint32_t h) {
 }
 
 // DC: compile-time tree depth of the fused update's routing (0 = a.D); HF (fused update only): the
-// root's q_h channel is tree-invariant (DESIGN R38) and copied from a.hroot, so only q_g is histogrammed
+// root's q_h channel is tree-invariant and copied from a.hroot, so only q_g is histogrammed
 template <int MODE, int DC = 0, bool HF = false>
 __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const int d, const int t_in, const DbgArgs dbg) {
   pdl_wait();
@@ -1535,7 +1535,7 @@ __device__ __forceinline__ bool split_feature(const FitArgs& a, const int d, con
       h8[2 * q + 1] = hv[q].y;
     }
   }
-  if (d == 0 && a.hroot && t == 0) {   // h_fixed: keep tree 0's root q_h histogram (R38)
+  if (d == 0 && a.hroot && t == 0) {   // h_fixed: keep tree 0's root q_h histogram
     longlong2* hs = reinterpret_cast<longlong2*>(a.hroot + f * kBins + lane * 8);
 #pragma unroll
     for (int q = 0; q < 4; ++q) hs[q] = make_longlong2(h8[2 * q], h8[2 * q + 1]);
@@ -2221,7 +2221,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
               d_cm.as<uint32_t>());
   const uint32_t* cmask = d_cm.as<uint32_t>();
   static const int hist1 = hist1_mask();
-  // R38: with h = w on every row of every tree (no row subsampling, not a random forest) the root's
+  // with h = w on every row of every tree (no row subsampling, not a random forest) the root's
   // q_h histogram is the same for every tree; the fused update then builds only the q_g channel and
   // the round copies q_h from tree 0's (unsharded: a sharded root is summed across ranks afterwards)
   static const bool hfix_env = !(getenv("LLMP_HFIX") && atoi(getenv("LLMP_HFIX")) == 0);
@@ -2445,7 +2445,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     if (rf) LLMP_LAUNCH_PDL(ctx, KC_MISC, ny * n, k_rf_weights, dim3(rfw_grid, ny), 256, 0, fp, 1);
     if (fused) {   // update tree t + root histogram of tree t+1 (into the now free root slot)
       for (int q = 0; q < ny; ++q) {
-        if (hfix) {   // q_g channel zeroed, q_h channel = tree 0's (R38)
+        if (hfix) {   // q_g channel zeroed, q_h channel = tree 0's
           LLMP_CUDA(cudaMemsetAsync(fp.t[q].H[0], 0, (size_t)kHistBins * 8, st));
           LLMP_CUDA(cudaMemcpyAsync(fp.t[q].H[0] + kHistBins, fp.t[q].hroot, (size_t)kHistBins * 8,
                                     cudaMemcpyDeviceToDevice, st));
