@@ -30,7 +30,10 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-os.environ.setdefault("NCCL_DEBUG", "WARN")   # rank 0's stdout carries exactly one JSON line
+# rank 0's stdout carries exactly one JSON line: NCCL logs (including the "NCCL version" line it
+# prints at the WARN level) go to stderr
+os.environ.setdefault("NCCL_DEBUG", "WARN")
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 import numpy as np  # noqa: E402
 
