@@ -2223,10 +2223,11 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   static const int hist1 = hist1_mask();
   // with h = w on every row of every tree (no row subsampling, not a random forest) the root's
   // q_h histogram is the same for every tree; the fused update then builds only the q_g channel and
-  // the round copies q_h from tree 0's (unsharded: a sharded root is summed across ranks afterwards)
+  // the round copies q_h from tree 0's.  Sharded: the root slot is summed across ranks after the
+  // update, and tree 0's saved q_h channel is already the global one, so rank 0 contributes it and the
+  // other ranks zeros (an exact integer sum either way)
   static const bool hfix_env = !(getenv("LLMP_HFIX") && atoi(getenv("LLMP_HFIX")) == 0);
-  const bool hfix = hfix_env && fused && !sharded && hp.subsample >= 1.0f && hp.model == 0 && !(hist1 & 4) &&
-                    upd_kernel() == 2;
+  const bool hfix = hfix_env && fused && hp.subsample >= 1.0f && hp.model == 0 && !(hist1 & 4) && upd_kernel() == 2;
   const int lvk = level_kernel();
   // split evaluation folded into k_hist3 (LLMP_FOLD=1; unsharded only: no all-reduce between the
   // histogram and the split).  Measured slower than the separate k_split3 launch (107 vs 55 + 14 us per
@@ -2445,7 +2446,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     if (rf) LLMP_LAUNCH_PDL(ctx, KC_MISC, ny * n, k_rf_weights, dim3(rfw_grid, ny), 256, 0, fp, 1);
     if (fused) {   // update tree t + root histogram of tree t+1 (into the now free root slot)
       for (int q = 0; q < ny; ++q) {
-        if (hfix) {   // q_g channel zeroed, q_h channel = tree 0's
+        if (hfix && (!sharded || ctx->rank == 0)) {   // q_g channel zeroed, q_h channel = tree 0's
           LLMP_CUDA(cudaMemsetAsync(fp.t[q].H[0], 0, (size_t)kHistBins * 8, st));
           LLMP_CUDA(cudaMemcpyAsync(fp.t[q].H[0] + kHistBins, fp.t[q].hroot, (size_t)kHistBins * 8,
                                     cudaMemcpyDeviceToDevice, st));
