@@ -200,8 +200,15 @@ __global__ void __launch_bounds__(H3_THREADS, 1) k_hist3(const FitPair fp, const
   for (int j = 0; j < 8; ++j) um[j] = (ucol >= 0 && (ucol >> 2) == j) ? ~(0xffu << (8 * (ucol & 3))) : 0xffffffffu;
   const uint32_t uoff = ucol >= 0 ? h3_half(lane, ucol >> 4) + (uint32_t)(ucol & 15) : 0u;   // own row's users byte
 
-  int pc = 0;
-  while (pc + 1 < np && s_vstart[pc + 1] <= v0) ++pc;
+  int pc = 0;   // first piece ending after v0 (binary search: deep levels have up to 2 x 512 pieces)
+  {
+    int hi = np - 1;
+    while (pc < hi) {
+      const int mid = (pc + hi) >> 1;
+      if (s_vstart[mid + 1] <= v0) pc = mid + 1;
+      else hi = mid;
+    }
+  }
   for (; pc < np && s_vstart[pc] < v1; ++pc) {
     const int64_t s0 = max(v0, s_vstart[pc]), s1 = min(v1, s_vstart[pc + 1]);
     if (s0 >= s1) continue;
