@@ -577,11 +577,18 @@ __device__ __forceinline__ void red2(uint32_t addr, int32_t g, uint32_t h) {
 }
 
 // DC: compile-time tree depth of the fused update's routing (0 = a.D); HF (fused update only): the
-// root's q_h channel is tree-invariant and copied from a.hroot, so only q_g is histogrammed
-template <int MODE, int DC = 0, bool HF = false>
+// root's q_h channel is tree-invariant and copied from a.hroot, so only q_g is histogrammed.
+// DUAL (fused update only, with the q_h channel tree-invariant): BOTH ensembles in one pass over the rows —
+// each row's code row, change-mask word and weight are loaded and staged once, the row is routed through
+// both ensembles' trees t, and the histogram's second channel holds ensemble 1's q_g instead of
+// ensemble 0's q_h (the run walk over the shared change mask serves both), flushed into ensemble 1's
+// root slot
+template <int MODE, int DC = 0, bool HF = false, bool DUAL = false>
 __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const int d, const int t_in, const DbgArgs dbg) {
+  static_assert(!DUAL || (MODE == HM_UPDROOT && !HF), "DUAL: fused update, two q_g channels");
   pdl_wait();
-  const FitArgs& a = fp.t[blockIdx.y];
+  const FitArgs& a = fp.t[DUAL ? 0 : blockIdx.y];
+  const FitArgs& a1 = fp.t[1];   // DUAL: ensemble 1
   const int t = (MODE == HM_ROOT || MODE == HM_UPDROOT) ? *a.d_tree : t_in;   // graph replays: tree index from the device
   if (MODE == HM_ROOT && !root_needed(a, t)) return;   // built speculatively by the previous update pass
   const bool has_next = (MODE == HM_UPDROOT) ? (t + 1 < a.T) : true;
@@ -610,16 +617,24 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
   uint16_t* s_rt = reinterpret_cast<uint16_t*>(smem + H2_SMEM);
   float* s_lv = reinterpret_cast<float*>(smem + H2_SMEM + (a.nn + 1));   // 2^D depth-D slots
   const int n_int = (a.nn - 1) / 2;   // 2^D - 1 slots above depth D
+  // DUAL: ensemble 1's table right after ensemble 0's (6 * 2^D bytes each)
+  uint16_t* s_rt1 = reinterpret_cast<uint16_t*>(smem + H2_SMEM + 3 * (a.nn + 1));
+  float* s_lv1 = reinterpret_cast<float*>(smem + H2_SMEM + 4 * (a.nn + 1));
   if (MODE == HM_UPDROOT) {
-    const size_t to = (size_t)t * a.nn;
-    for (int i = tid; i < a.nn; i += H2_THREADS) {
-      const int f = a.tfeat[to + i];
-      if (i < n_int) {
-        s_rt[i] = (uint16_t)(f >= 0 ? ((uint32_t)f | ((uint32_t)(a.tbin[to + i] & 0xff) << 8)) : (255u << 8));
-      }
-      if (f == -1) {   // leaf at depth d = floor(log2(i + 1))
-        const int dl = 31 - __clz(i + 1);
-        s_lv[((i + 1) << (a.D - dl)) - 1 - n_int] = a.tval[to + i];
+    for (int q = 0; q < (DUAL ? 2 : 1); ++q) {
+      const FitArgs& aq = q ? a1 : a;
+      uint16_t* rt = q ? s_rt1 : s_rt;
+      float* lv = q ? s_lv1 : s_lv;
+      const size_t to = (size_t)t * aq.nn;
+      for (int i = tid; i < aq.nn; i += H2_THREADS) {
+        const int f = aq.tfeat[to + i];
+        if (i < n_int) {
+          rt[i] = (uint16_t)(f >= 0 ? ((uint32_t)f | ((uint32_t)(aq.tbin[to + i] & 0xff) << 8)) : (255u << 8));
+        }
+        if (f == -1) {   // leaf at depth d = floor(log2(i + 1))
+          const int dl = 31 - __clz(i + 1);
+          lv[((i + 1) << (aq.D - dl)) - 1 - n_int] = aq.tval[to + i];
+        }
       }
     }
   }
@@ -679,16 +694,22 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
   const int64_t v1 = (blockIdx.x + 1 == gridDim.x) ? S : ((S * (blockIdx.x + 1) / gridDim.x) & am);
   if (v0 >= v1) return;
   if (tid == 0 && MODE != HM_DEBUG && a.units)
-    atomicAdd(&a.units[MODE == HM_ROOT ? KC_HIST_ROOT : MODE == HM_UPDROOT ? KC_UPDATE : KC_HIST], (unsigned long long)(v1 - v0));
+    atomicAdd(&a.units[MODE == HM_ROOT ? KC_HIST_ROOT : MODE == HM_UPDROOT ? KC_UPDATE : KC_HIST],
+              (unsigned long long)(v1 - v0) * (DUAL ? 2 : 1));
 
   // quantisation scales for ROOT (tree t): q = rint(v * 2^(K-e))
   // (HM_UPDROOT: tree t+1's pairs with tree t's exponents — the speculation described at k_hist)
-  double scale_g = 0.0, scale_h = 0.0;
+  double scale_g = 0.0, scale_h = 0.0, scale_g1 = 0.0, scale_h1 = 0.0;
   if (MODE == HM_ROOT || MODE == HM_UPDROOT) {
     scale_g = exp2i(a.K - exp_of(__uint_as_float(a.maxg[t])));
     scale_h = exp2i(a.K - exp_of(__uint_as_float(a.maxh[t])));
   }
+  if (DUAL) {
+    scale_g1 = exp2i(a1.K - exp_of(__uint_as_float(a1.maxg[t])));
+    scale_h1 = exp2i(a1.K - exp_of(__uint_as_float(a1.maxh[t])));
+  }
   float mg = 0.f, mh = 0.f;   // HM_UPDROOT: tree t+1's max |g|, max h
+  float mg1 = 0.f, mh1 = 0.f;   // DUAL: ensemble 1's
   int64_t* Hbase = (MODE == HM_DEBUG) ? dbg.out : a.H[d & 1];
   const uint32_t* sr_in = (MODE == HM_LEVEL) ? a.sr[d & 1] : nullptr;
   const uint32_t sgb = (uint32_t)__cvta_generic_to_shared(sg);
@@ -703,7 +724,7 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
     int64_t s0 = max(v0, s_vstart[pc]), s1 = min(v1, s_vstart[pc + 1]);
     if (s0 >= s1) continue;
     int64_t* Hg = Hbase + (size_t)s_slot[pc] * SLOT;
-    int64_t* Hh = Hg + kHistBins;
+    int64_t* Hh = DUAL ? a1.H[0] : Hg + kHistBins;   // DUAL: second channel = ensemble 1's root q_g
     const int64_t poff = s_pstart[pc] - s_vstart[pc];   // physical position = virtual + poff
     for (int64_t c0 = s0; c0 < s1; c0 += HIST_CHUNK) {
       const int64_t c1 = min(s1, c0 + HIST_CHUNK);
@@ -717,6 +738,7 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
       uint4 nc0 = make_uint4(0, 0, 0, 0), nc1 = nc0;
       uint32_t ngp = 0, nri = 0, nmask = 0;
       float ny = 0.f, nw = 0.f, np_ = 0.f;
+      float ny1 = 0.f, np1 = 0.f;   // DUAL: ensemble 1's target and prediction
       auto load_ridx = [&](int64_t vb) {
         const int64_t vi = vb + lane;
         if (MODE == HM_LEVEL && vi < w1) nri = sr_in[vi + poff];
@@ -731,6 +753,10 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
             ny = a.y[ridx];
             nw = a.w[ridx];
             np_ = a.p[ridx];
+            if (DUAL) {
+              ny1 = a1.y[ridx];
+              np1 = a1.p[ridx];
+            }
           } else if (MODE == HM_LEVEL) {
             ridx = nri;
             ngp = a.gp_root[ridx];
@@ -753,6 +779,7 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
         const int cnt = (int)min((int64_t)32, w1 - base);
         const bool valid = lane < cnt;
         uint32_t gp = ngp;
+        uint32_t gp1 = 0;   // DUAL: ensemble 1's packed pair
         if (MODE == HM_ROOT && valid) {
           const int64_t ridx = base + lane + poff;
           float g, h;
@@ -794,6 +821,25 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
             gp = pack_gp(quantize(g, scale_g), quantize(h, scale_h));
             a.gp_root[ridx] = gp;
           }
+          if (DUAL) {   // the same row through ensemble 1's tree t
+            int k1 = 0;
+#pragma unroll
+            for (int s2 = 0; s2 < (DC ? DC : kMaxDepth); ++s2)
+              if (DC || s2 < D) {
+                const uint32_t w = s_rt1[k1];
+                k1 = 2 * k1 + 1 + ((uint32_t)myrow[w & 0xffu] > (w >> 8) ? 1 : 0);
+              }
+            const float pn1 = __fadd_rn(np1, s_lv1[k1 - n_int]);
+            a1.p[ridx] = pn1;
+            if (has_next) {
+              float g, h;
+              grad_pair(a1, t + 1, a1.row_offset + ridx, ny1, nw, pn1, g, h);
+              mg1 = fmaxf(mg1, fabsf(g));
+              mh1 = fmaxf(mh1, h);
+              gp1 = pack_gp(quantize(g, scale_g1), quantize(h, scale_h1));
+              a1.gp_root[ridx] = gp1;
+            }
+          }
         }
         __syncwarp();
         const uint4 cc0 = nc0, cc1 = nc1;   // this batch's row (the prefetch below overwrites nc*)
@@ -814,7 +860,7 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
               (byte_ne_hi(cc1.z ^ pv1.z) >> 6) | (byte_ne_hi(cc1.w ^ pv1.w) >> 7);
         }
         const int32_t qg = valid ? gp_g(gp) : 0;
-        const uint32_t qh = valid ? (uint32_t)gp_h(gp) : 0u;
+        const uint32_t qh = valid ? (DUAL ? (uint32_t)gp_g(gp1) : (uint32_t)gp_h(gp)) : 0u;
         if (ucol >= 0 && valid) {   // users column, row-parallel into the dense per-bin histogram
           const uint32_t ua = sub + (uint32_t)myrow[ucol] * 4u;
           asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(ua), "r"(qg) : "memory");
@@ -908,7 +954,11 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
         const uint32_t h = sh[b * H2_PAD + f];
         if (g != 0 || h != 0) {
           atomicAdd(reinterpret_cast<unsigned long long*>(&Hg[f * kBins + b]), (unsigned long long)(long long)g);
-          if (!HF) atomicAdd(reinterpret_cast<unsigned long long*>(&Hh[f * kBins + b]), (unsigned long long)h);
+          if (DUAL)   // ensemble 1's q_g: signed
+            atomicAdd(reinterpret_cast<unsigned long long*>(&Hh[f * kBins + b]),
+                      (unsigned long long)(long long)(int32_t)h);
+          else if (!HF)
+            atomicAdd(reinterpret_cast<unsigned long long*>(&Hh[f * kBins + b]), (unsigned long long)h);
           sg[b * H2_PAD + f] = 0;
           sh[b * H2_PAD + f] = 0;
         }
@@ -924,6 +974,16 @@ __global__ void __launch_bounds__(H2_THREADS, 2) k_hist2(const FitPair fp, const
     if (lane == 0) {
       atomicMax(&a.maxg[t + 1], __float_as_uint(mg));
       atomicMax(&a.maxh[t + 1], __float_as_uint(mh));
+    }
+    if (DUAL) {
+      for (int o = 16; o > 0; o >>= 1) {
+        mg1 = fmaxf(mg1, __shfl_xor_sync(0xffffffffu, mg1, o));
+        mh1 = fmaxf(mh1, __shfl_xor_sync(0xffffffffu, mh1, o));
+      }
+      if (lane == 0) {
+        atomicMax(&a1.maxg[t + 1], __float_as_uint(mg1));
+        atomicMax(&a1.maxh[t + 1], __float_as_uint(mh1));
+      }
     }
   }
 }
@@ -952,7 +1012,12 @@ __global__ void __launch_bounds__(256) k_cmask(const uint8_t* codes, int64_t n, 
 
 // the fused update kernel for a depth: compile-time routing depth for the configs' depths (6, 8)
 using Hist2Kernel = void (*)(const FitPair, const int, const int, const DbgArgs);
-static Hist2Kernel updroot2_kernel(int D, bool hf) {
+static Hist2Kernel updroot2_kernel(int D, bool hf, bool dual = false) {
+  if (dual) {
+    if (D == 8) return k_hist2<HM_UPDROOT, 8, false, true>;
+    if (D == 6) return k_hist2<HM_UPDROOT, 6, false, true>;
+    return k_hist2<HM_UPDROOT, 0, false, true>;
+  }
   if (hf) {
     if (D == 8) return k_hist2<HM_UPDROOT, 8, true>;
     if (D == 6) return k_hist2<HM_UPDROOT, 6, true>;
@@ -2335,6 +2400,12 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   ensure_smem_attr((const void*)k_hist<HM_UPDROOT>, HIST_SMEM + updroot_tree_smem(D));
   const Hist2Kernel k_upd2 = updroot2_kernel(D, hfix);
   ensure_smem_attr((const void*)k_upd2, H2_SMEM + updroot_tree_smem(D));
+  // both ensembles' fused update in one pass (LLMP_DUAL=0 keeps one pass per ensemble):
+  // needs the tree-invariant q_h channel, one weight vector and the k_hist2 update kernel
+  static const bool dual_env = !(getenv("LLMP_DUAL") && atoi(getenv("LLMP_DUAL")) == 0);
+  const bool dual = dual_env && hfix && A[0].w == A[1].w && upd_kernel() == 2;
+  const Hist2Kernel k_upd2d = updroot2_kernel(D, false, true);
+  ensure_smem_attr((const void*)k_upd2d, H2_SMEM + updroot_tree_smem(D));
   const Upd3Kernel k_up3 = upd3_kernel(D);
   ensure_smem_attr((const void*)k_up3, U3_SMEM + updroot_tree_smem(D));
   const int updk = upd_kernel();
@@ -2444,7 +2515,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     }
     // RF: tree t+1's bootstrap weights, read by the update's gradients (and the next root rebuild)
     if (rf) LLMP_LAUNCH_PDL(ctx, KC_MISC, ny * n, k_rf_weights, dim3(rfw_grid, ny), 256, 0, fp, 1);
-    if (fused) {   // update tree t + root histogram of tree t+1 (into the now free root slot)
+    if (fused && !dual) {   // update tree t + root histogram of tree t+1 (into the now free root slot)
       for (int q = 0; q < ny; ++q) {
         if (hfix && (!sharded || ctx->rank == 0)) {   // q_g channel zeroed, q_h channel = tree 0's
           LLMP_CUDA(cudaMemsetAsync(fp.t[q].H[0], 0, (size_t)kHistBins * 8, st));
@@ -2461,9 +2532,25 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
         LLMP_LAUNCH_PDL(ctx, KC_UPDATE, ny * n, k_up3, hu3, U3_THREADS, U3_SMEM + updroot_tree_smem(D), fp);
       else
         LLMP_LAUNCH_PDL(ctx, KC_UPDATE, ny * n, k_upd2, hg, H2_THREADS, H2_SMEM + updroot_tree_smem(D), fp, 0, 0, nodbg);
-    } else {
+    } else if (!fused) {
       LLMP_LAUNCH(ctx, KC_UPDATE, ny * n, k_update, dim3(std::max(1, upd_grid * ny / 2), ny), UPD_THREADS, 0, fp);
     }
+  };
+  // dual: the update of tree t + root histograms of trees t+1 of BOTH ensembles, one pass over the rows
+  // (after both ensembles' levels: the branches have joined)
+  auto dual_update = [&]() {
+    const cudaStream_t st = ctx->stream;
+    for (int q = 0; q < 2; ++q) {   // q_g channel zeroed, q_h channel = tree 0's (rank 0; zeros elsewhere)
+      if (!sharded || ctx->rank == 0) {
+        LLMP_CUDA(cudaMemsetAsync(FP.t[q].H[0], 0, (size_t)kHistBins * 8, st));
+        LLMP_CUDA(cudaMemcpyAsync(FP.t[q].H[0] + kHistBins, FP.t[q].hroot, (size_t)kHistBins * 8,
+                                  cudaMemcpyDeviceToDevice, st));
+      } else {
+        LLMP_CUDA(cudaMemsetAsync(FP.t[q].H[0], 0, (size_t)SLOT * 8, st));
+      }
+    }
+    const dim3 hg1((unsigned)std::min<int64_t>(ctx->sms * 2, std::max<int64_t>(1, (n + 2047) / 2048)), 1);
+    LLMP_LAUNCH_PDL(ctx, KC_UPDATE, 2 * n, k_upd2d, hg1, H2_THREADS, H2_SMEM + updroot_tree_smem(D), FP, 0, 0, nodbg);
   };
   // both ensembles' trees t: two concurrent graph branches (default on one GPU: one ensemble's
   // latency-bound split / partition kernels overlap the other's streaming kernels; 592 vs 652 ms
@@ -2491,6 +2578,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
     } else {
       trees(FP, 2);
     }
+    if (dual) dual_update();
     // next tree's gradient maxima of both targets (contiguous; past slots are already equal on
     // every rank, future ones 0)
     allreduce_max_u32(ctx, A[0].maxg, (size_t)4 * (T + 1));

@@ -23,9 +23,15 @@
 // Rows whose codes all equal the previous row's cost no feature-side work at all, so a batch costs
 // ~65 warp-instructions plus ~17 per flagged row (k_hist: ~390 per batch).  Zero-skipping int64
 // atomics flush the shared histogram into the node slot after each chunk.
-constexpr int H3_THREADS = 512;
+#ifndef LLMP_H3_THREADS
+#define LLMP_H3_THREADS 512
+#endif
+#ifndef LLMP_H3_AHEAD
+#define LLMP_H3_AHEAD 4
+#endif
+constexpr int H3_THREADS = LLMP_H3_THREADS;
 constexpr int H3_WARPS = H3_THREADS / 32;
-constexpr int H3_AHEAD = 4;                           // gathers issued this many batches ahead of their use
+constexpr int H3_AHEAD = LLMP_H3_AHEAD;                          // gathers issued this many batches ahead of their use
 constexpr int H3_STAGES = H3_AHEAD + 2;               // ring: b+AHEAD issued while b is processed, b-1 kept
 constexpr int H3_GP = 32 * 32;                        // stage offset of the 32 packed pairs
 constexpr int H3_STAGE = H3_GP + 32 * 4;              // 32 code rows (32 B, halves swizzled) + pairs

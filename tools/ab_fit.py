@@ -43,8 +43,15 @@ def child(trees, reps, llms):
     ctx.set_timing(1)
     m = lp.fit(ctx, X, y, hp, d.users_col, li, pi, d.n_llm, d.n_prof, 100.0, 50.0)
     st = ctx.stats()["classes"]
+    # digest of the model (variants must agree bit for bit)
+    import hashlib
+    import numpy as np
+    e = m.export()
+    h = hashlib.sha1()
+    for k in ("feat", "val", "thr", "base"):
+        h.update(np.ascontiguousarray(np.asarray(e[k])).tobytes())
     m.free()
-    print(json.dumps({"ms": out, "rows_hist_root": st.get("hist_root", {}).get("rows", 0),
+    print(json.dumps({"ms": out, "digest": h.hexdigest()[:12], "rows_hist_root": st.get("hist_root", {}).get("rows", 0),
                       "rows_hist_level": st.get("hist_level", {}).get("rows", 0)}))
 
 
