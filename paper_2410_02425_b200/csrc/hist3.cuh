@@ -215,159 +215,220 @@ __global__ void __launch_bounds__(H3_THREADS, 1) k_hist3(const FitPair fp, const
       else hi = mid;
     }
   }
-  for (; pc < np && s_vstart[pc] < v1; ++pc) {
-    const int64_t s0 = max(v0, s_vstart[pc]), s1 = min(v1, s_vstart[pc + 1]);
-    if (s0 >= s1) continue;
+  // The CTA's work is a sequence of segments (piece, <= HIST_CHUNK-row chunk), each split evenly over
+  // the warps and flushed between two barriers.  A warp's gather pipeline does not drain at a segment
+  // boundary: once its rows of segment s are processed it issues the row-index loads and the first
+  // H3_AHEAD gathers of its rows of segment s+1 into the (now free) ring, and only then waits at the
+  // barrier that precedes segment s's flush — so the next segment's first gathers overlap the wait for
+  // the slowest warp and the flush (deep levels: several short segments per CTA).
+  struct Seg {
+    int pc;              // piece
+    int64_t c0, c1;      // virtual range of the chunk
+    int64_t rbase;       // physical position of the warp's first row
+    int nb, rem;         // the warp's batches; batch b holds this lane's row iff 32 b < rem
+    const uint32_t* sr;  // the piece's row indices (level d's segments) and packed pairs
+    const uint32_t* gpr;
+  };
+  auto seg_make = [&](int p_, int64_t c0_) {
+    Seg g;
+    g.pc = p_;
+    const int64_t s1_ = min(v1, s_vstart[p_ + 1]);
+    g.c0 = c0_;
+    g.c1 = min(s1_, c0_ + HIST_CHUNK);
+    const int64_t clen = g.c1 - g.c0;
+    const int64_t w0 = g.c0 + clen * warp / H3_WARPS, w1 = g.c0 + clen * (warp + 1) / H3_WARPS;
+    g.nb = (int)((w1 - w0 + 31) >> 5);
+    g.rem = (int)(w1 - w0) - lane;
+    g.rbase = w0 + (s_pstart[p_] - s_vstart[p_]);   // physical position = virtual + (pstart - vstart)
+    const FitArgs& ag = fp.t[s_tg[p_]];
+    g.sr = (MODE == HM_LEVEL) ? ag.sr[d & 1] : nullptr;
+    g.gpr = ag.gp_root;
+    return g;
+  };
+  // the segment after g (pc = -1: none)
+  auto seg_next = [&](const Seg& g) {
+    const int64_t s1_ = min(v1, s_vstart[g.pc + 1]);
+    if (g.c1 < s1_) return seg_make(g.pc, g.c1);
+    for (int p_ = g.pc + 1; p_ < np && s_vstart[p_] < v1; ++p_) {
+      const int64_t a0_ = max(v0, s_vstart[p_]), a1_ = min(v1, s_vstart[p_ + 1]);
+      if (a0_ < a1_) return seg_make(p_, a0_);
+    }
+    Seg none;
+    none.pc = -1;
+    none.c0 = none.c1 = 0;
+    none.rbase = 0;
+    none.nb = 0;
+    none.rem = 0;
+    none.sr = nullptr;
+    none.gpr = nullptr;
+    return none;
+  };
+  // row-index loads are never predicated (a predicated load feeds a select that would wait for it):
+  // rows past the range read the warp range's first row index instead (unused)
+  auto ridx_of = [&](const Seg& g, int b) -> uint32_t {
+    const int64_t pi = g.rbase + ((32 * b < g.rem) ? 32 * b + lane : 0);
+    if (MODE == HM_LEVEL) return g.sr[pi];
+    return dbg.idx ? (uint32_t)dbg.idx[pi] : (uint32_t)pi;
+  };
+  auto issue = [&](const Seg& g, int b, int stage, uint32_t ri) {   // gathers of batch b into `stage` (one commit group)
+    if (32 * b < g.rem) {
+      const uint32_t st = ring + (uint32_t)(stage * H3_STAGE);
+      const uint8_t* src = a0.codes + (size_t)ri * kMaxF;
+      cp_async16(st + h3_half(lane, 0), src);
+      cp_async16(st + h3_half(lane, 1), src + 16);
+      if (MODE == HM_LEVEL) cp_async4(st + H3_GP + lane * 4, g.gpr + ri);
+      else sts32(st + H3_GP + lane * 4, pack_gp(dbg.qg[ri], dbg.qh[ri]));
+    }
+    cp_async_commit();
+  };
+  // gathers run H3_AHEAD batches ahead of their use, row indices H3_STAGES batches ahead of their
+  // gathers (a register ring; the loop is unrolled by H3_STAGES, so every stage and ring index is a
+  // compile-time constant and no copy waits on a load)
+  uint32_t R[H3_STAGES];
+  auto prologue = [&](const Seg& g) {
+    if (g.nb > 0) {
+#pragma unroll
+      for (int k = 0; k < H3_AHEAD; ++k) issue(g, k, k, ridx_of(g, k));
+#pragma unroll
+      for (int k = 0; k < H3_STAGES; ++k) R[k] = ridx_of(g, H3_AHEAD + k);
+    }
+  };
+  Seg cs;
+  cs.pc = -1;
+  if (pc < np && s_vstart[pc] < v1) {
+    const int64_t a0_ = max(v0, s_vstart[pc]);
+    if (a0_ < min(v1, s_vstart[pc + 1])) cs = seg_make(pc, a0_);
+    else {
+      Seg t0;
+      t0.pc = pc;
+      t0.c1 = min(v1, s_vstart[pc + 1]);
+      cs = seg_next(t0);
+    }
+  }
+  if (v0 < v1 && cs.pc >= 0) prologue(cs);
+  while (cs.pc >= 0) {
+    const int pc = cs.pc;
     const FitArgs& a = fp.t[s_tg[pc]];
     int64_t* Hg = ((MODE == HM_DEBUG) ? dbg.out : a.H[d & 1]) + (size_t)s_slot[pc] * SLOT;
     int64_t* Hh = Hg + kHistBins;
-    const uint32_t* sr_in = (MODE == HM_LEVEL) ? a.sr[d & 1] : nullptr;
-    const int64_t poff = s_pstart[pc] - s_vstart[pc];   // physical position = virtual + poff
-    for (int64_t c0 = s0; c0 < s1; c0 += HIST_CHUNK) {
-      const int64_t c1 = min(s1, c0 + HIST_CHUNK);
-      const int64_t clen = c1 - c0;
-      const int64_t w0 = c0 + clen * warp / H3_WARPS, w1 = c0 + clen * (warp + 1) / H3_WARPS;
-      const int nb = (int)((w1 - w0 + 31) >> 5);
-      const int rem = (int)(w1 - w0) - lane;   // batch b holds this lane's row iff 32 b < rem
-      // row-index loads are never predicated (a predicated load feeds a select that would wait for
-      // it): rows past the range read the warp range's first row index instead (unused)
-      const int64_t rbase = w0 + poff;
-      auto ridx_of = [&](int b) -> uint32_t {
-        const int64_t pi = rbase + ((32 * b < rem) ? 32 * b + lane : 0);
-        if (MODE == HM_LEVEL) return sr_in[pi];
-        return dbg.idx ? (uint32_t)dbg.idx[pi] : (uint32_t)pi;
-      };
-      auto issue = [&](int b, int stage, uint32_t ri) {   // gathers of batch b into `stage` (one commit group)
-        if (32 * b < rem) {
-          const uint32_t st = ring + (uint32_t)(stage * H3_STAGE);
-          const uint8_t* src = a.codes + (size_t)ri * kMaxF;
-          cp_async16(st + h3_half(lane, 0), src);
-          cp_async16(st + h3_half(lane, 1), src + 16);
-          if (MODE == HM_LEVEL) cp_async4(st + H3_GP + lane * 4, a.gp_root + ri);
-          else sts32(st + H3_GP + lane * 4, pack_gp(dbg.qg[ri], dbg.qh[ri]));
-        }
-        cp_async_commit();
-      };
-      uint32_t cur = 0;          // feature side: byte offset of the pending run's (bin, f) cell
-      int32_t acc_g = 0;         // its sums from earlier batches
-      uint32_t acc_h = 0;
-      bool fresh = true;
-      if (nb > 0) {
-        // gathers run H3_AHEAD batches ahead of their use, row indices H3_STAGES batches ahead of
-        // their gathers (a register ring; the loop is unrolled by H3_STAGES, so every stage and ring
-        // index is a compile-time constant and no copy waits on a load)
-        uint32_t R[H3_STAGES];
+    const int nb = cs.nb;
+    const int rem = cs.rem;
+    uint32_t cur = 0;          // feature side: byte offset of the pending run's (bin, f) cell
+    int32_t acc_g = 0;         // its sums from earlier batches
+    uint32_t acc_h = 0;
+    bool fresh = true;
+    if (nb > 0) {
+      for (int bb = 0; bb < nb; bb += H3_STAGES) {
 #pragma unroll
-        for (int k = 0; k < H3_AHEAD; ++k) issue(k, k, ridx_of(k));
-#pragma unroll
-        for (int k = 0; k < H3_STAGES; ++k) R[k] = ridx_of(H3_AHEAD + k);
-        for (int bb = 0; bb < nb; bb += H3_STAGES) {
-#pragma unroll
-          for (int k = 0; k < H3_STAGES; ++k) {
-            const int b = bb + k;
-            if (b >= nb) break;
-            __syncwarp();            // the stage being refilled (batch b-2's) is fully consumed
-            issue(b + H3_AHEAD, (k + H3_AHEAD) % H3_STAGES, R[k]);
-            R[k] = ridx_of(b + H3_AHEAD + H3_STAGES);
-            cp_async_wait<H3_AHEAD>();   // batch b has landed (b+1 .. b+AHEAD may be in flight)
-            __syncwarp();
-            const uint32_t st = ring + (uint32_t)(k * H3_STAGE);
-            const bool valid = 32 * b < rem;
-            // ---- row side: does row `lane` differ from its predecessor in any (non-users) feature?
-            const uint4 c0v = lds128(st + h3_half(lane, 0)), c1v = lds128(st + h3_half(lane, 1));
-            const uint32_t pst = lane ? st : ring + (uint32_t)(((k + H3_STAGES - 1) % H3_STAGES) * H3_STAGE);
-            const int pr = lane ? lane - 1 : 31;
-            const uint4 p0 = lds128(pst + h3_half(pr, 0)), p1 = lds128(pst + h3_half(pr, 1));
-            const uint32_t dx = ((c0v.x ^ p0.x) & um[0]) | ((c0v.y ^ p0.y) & um[1]) | ((c0v.z ^ p0.z) & um[2]) |
-                                ((c0v.w ^ p0.w) & um[3]) | ((c1v.x ^ p1.x) & um[4]) | ((c1v.y ^ p1.y) & um[5]) |
-                                ((c1v.z ^ p1.z) & um[6]) | ((c1v.w ^ p1.w) & um[7]);
-            unsigned B = __ballot_sync(0xffffffffu, valid && (dx != 0u || (fresh && lane == 0)));
-            const uint32_t gp = valid ? lds32(st + H3_GP + lane * 4) : 0u;
-            const int32_t qg = gp_g(gp);
-            const uint32_t qh = (uint32_t)gp_h(gp);
-            if (ucol >= 0 && valid) {   // users column, row-parallel into the dense per-bin histogram
-              const uint32_t ua = sub + lds8(st + uoff) * 4u;
-              asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(ua), "r"(qg) : "memory");
-              asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(ua), "r"(qh), "n"(kBins * 4) : "memory");
-            }
-            // ---- feature side: walk the flagged rows only; the sum of the batch's rows before a
-            // flagged row r (lanes < r) is one warp reduction per channel
-            if (fresh) {   // the first row starts every lane's run
-              cur = (lds8(st + foff0) * 32u + (uint32_t)lane) * 4u;
-              fresh = false;
-              B &= ~1u;
-            }
-            int32_t bg = 0;          // sum of the batch's rows before the pending run's first row
-            uint32_t bh = 0;
-            // two flagged rows per step: both rows' code loads and prefix reductions are issued
-            // before either update (the updates are a short dependent chain per lane)
-            while (B) {
-              const int r1 = __ffs(B) - 1;
-              B &= B - 1u;
-              const bool two = B != 0u;
-              const int r2 = two ? __ffs(B) - 1 : r1;
-              B &= B - 1u;
-              const uint32_t c1 = lds8(st + (uint32_t)(r1 * 32) + (((r1 >> 2) & 1) ? foff1 : foff0));
-              const uint32_t c2 = lds8(st + (uint32_t)(r2 * 32) + (((r2 >> 2) & 1) ? foff1 : foff0));
-              const int32_t vg1 = (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)(lane < r1 ? qg : 0));
-              const uint32_t vh1 = __reduce_add_sync(0xffffffffu, lane < r1 ? qh : 0u);
-              const int32_t vg2 = (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)(lane < r2 ? qg : 0));
-              const uint32_t vh2 = __reduce_add_sync(0xffffffffu, lane < r2 ? qh : 0u);
-              const uint32_t na1 = (c1 * 32u + (uint32_t)lane) * 4u;
-              if (active && na1 != cur) {
-                red2_h3(sgb + cur, acc_g + (vg1 - bg), acc_h + (vh1 - bh));
-                acc_g = 0;
-                acc_h = 0;
-                bg = vg1;
-                bh = vh1;
-                cur = na1;
-              }
-              const uint32_t na2 = (c2 * 32u + (uint32_t)lane) * 4u;
-              if (two && active && na2 != cur) {
-                red2_h3(sgb + cur, acc_g + (vg2 - bg), acc_h + (vh2 - bh));
-                acc_g = 0;
-                acc_h = 0;
-                bg = vg2;
-                bh = vh2;
-                cur = na2;
-              }
-            }
-            acc_g += (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)qg) - bg;
-            acc_h += __reduce_add_sync(0xffffffffu, qh) - bh;
+        for (int k = 0; k < H3_STAGES; ++k) {
+          const int b = bb + k;
+          if (b >= nb) break;
+          __syncwarp();            // the stage being refilled (batch b-2's) is fully consumed
+          issue(cs, b + H3_AHEAD, (k + H3_AHEAD) % H3_STAGES, R[k]);
+          R[k] = ridx_of(cs, b + H3_AHEAD + H3_STAGES);
+          cp_async_wait<H3_AHEAD>();   // batch b has landed (b+1 .. b+AHEAD may be in flight)
+          __syncwarp();
+          const uint32_t st = ring + (uint32_t)(k * H3_STAGE);
+          const bool valid = 32 * b < rem;
+          // ---- row side: does row `lane` differ from its predecessor in any (non-users) feature?
+          const uint4 c0v = lds128(st + h3_half(lane, 0)), c1v = lds128(st + h3_half(lane, 1));
+          const uint32_t pst = lane ? st : ring + (uint32_t)(((k + H3_STAGES - 1) % H3_STAGES) * H3_STAGE);
+          const int pr = lane ? lane - 1 : 31;
+          const uint4 p0 = lds128(pst + h3_half(pr, 0)), p1 = lds128(pst + h3_half(pr, 1));
+          const uint32_t dx = ((c0v.x ^ p0.x) & um[0]) | ((c0v.y ^ p0.y) & um[1]) | ((c0v.z ^ p0.z) & um[2]) |
+                              ((c0v.w ^ p0.w) & um[3]) | ((c1v.x ^ p1.x) & um[4]) | ((c1v.y ^ p1.y) & um[5]) |
+                              ((c1v.z ^ p1.z) & um[6]) | ((c1v.w ^ p1.w) & um[7]);
+          unsigned B = __ballot_sync(0xffffffffu, valid && (dx != 0u || (fresh && lane == 0)));
+          const uint32_t gp = valid ? lds32(st + H3_GP + lane * 4) : 0u;
+          const int32_t qg = gp_g(gp);
+          const uint32_t qh = (uint32_t)gp_h(gp);
+          if (ucol >= 0 && valid) {   // users column, row-parallel into the dense per-bin histogram
+            const uint32_t ua = sub + lds8(st + uoff) * 4u;
+            asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(ua), "r"(qg) : "memory");
+            asm volatile("red.shared.add.u32 [%0+%2], %1;" ::"r"(ua), "r"(qh), "n"(kBins * 4) : "memory");
           }
+          // ---- feature side: walk the flagged rows only; the sum of the batch's rows before a
+          // flagged row r (lanes < r) is one warp reduction per channel
+          if (fresh) {   // the first row starts every lane's run
+            cur = (lds8(st + foff0) * 32u + (uint32_t)lane) * 4u;
+            fresh = false;
+            B &= ~1u;
+          }
+          int32_t bg = 0;          // sum of the batch's rows before the pending run's first row
+          uint32_t bh = 0;
+          // two flagged rows per step: both rows' code loads and prefix reductions are issued
+          // before either update (the updates are a short dependent chain per lane)
+          while (B) {
+            const int r1 = __ffs(B) - 1;
+            B &= B - 1u;
+            const bool two = B != 0u;
+            const int r2 = two ? __ffs(B) - 1 : r1;
+            B &= B - 1u;
+            const uint32_t c1 = lds8(st + (uint32_t)(r1 * 32) + (((r1 >> 2) & 1) ? foff1 : foff0));
+            const uint32_t c2 = lds8(st + (uint32_t)(r2 * 32) + (((r2 >> 2) & 1) ? foff1 : foff0));
+            const int32_t vg1 = (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)(lane < r1 ? qg : 0));
+            const uint32_t vh1 = __reduce_add_sync(0xffffffffu, lane < r1 ? qh : 0u);
+            const int32_t vg2 = (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)(lane < r2 ? qg : 0));
+            const uint32_t vh2 = __reduce_add_sync(0xffffffffu, lane < r2 ? qh : 0u);
+            const uint32_t na1 = (c1 * 32u + (uint32_t)lane) * 4u;
+            if (active && na1 != cur) {
+              red2_h3(sgb + cur, acc_g + (vg1 - bg), acc_h + (vh1 - bh));
+              acc_g = 0;
+              acc_h = 0;
+              bg = vg1;
+              bh = vh1;
+              cur = na1;
+            }
+            const uint32_t na2 = (c2 * 32u + (uint32_t)lane) * 4u;
+            if (two && active && na2 != cur) {
+              red2_h3(sgb + cur, acc_g + (vg2 - bg), acc_h + (vh2 - bh));
+              acc_g = 0;
+              acc_h = 0;
+              bg = vg2;
+              bh = vh2;
+              cur = na2;
+            }
+          }
+          acc_g += (int32_t)__reduce_add_sync(0xffffffffu, (uint32_t)qg) - bg;
+          acc_h += __reduce_add_sync(0xffffffffu, qh) - bh;
         }
       }
-      if (active && !fresh && (acc_g | (int32_t)acc_h)) red2_h3(sgb + cur, acc_g, acc_h);
-      cp_async_wait<0>();
-      __syncthreads();
-      int32_t* sg = reinterpret_cast<int32_t*>(smem);
-      uint32_t* sh = reinterpret_cast<uint32_t*>(smem + H3_HH);
-      int32_t* sug = reinterpret_cast<int32_t*>(smem + H3_U_OFF);
-      uint32_t* suh = reinterpret_cast<uint32_t*>(smem + H3_U_OFF + kBins * 4);
-      if (ucol >= 0) {   // the users column's cells (never written by its lane) from the dense histogram
-        for (int b = tid; b < kBins; b += H3_THREADS) {
-          sg[b * 32 + ucol] = sug[b];
-          sh[b * 32 + ucol] = suh[b];
-          sug[b] = 0;
-          suh[b] = 0;
-        }
-        __syncthreads();
-      }
-      // flush: zero-skipping int64 atomics into the node histogram ([f][b] layout)
-      for (int i = tid; i < kHistBins; i += H3_THREADS) {
-        const int32_t g = sg[i];
-        const uint32_t h = sh[i];
-        if (g != 0 || h != 0) {
-          const int b = i >> 5, f = i & 31;
-          atomicAdd(reinterpret_cast<unsigned long long*>(&Hg[f * kBins + b]), (unsigned long long)(long long)g);
-          atomicAdd(reinterpret_cast<unsigned long long*>(&Hh[f * kBins + b]), (unsigned long long)h);
-          sg[i] = 0;
-          sh[i] = 0;
-        }
+    }
+    if (active && !fresh && (acc_g | (int32_t)acc_h)) red2_h3(sgb + cur, acc_g, acc_h);
+    // the next segment's first gathers go out before the barrier (the ring is free once every lane
+    // has read its last batch)
+    const Seg ns = seg_next(cs);
+    __syncwarp();
+    if (ns.pc >= 0) prologue(ns);
+    else cp_async_wait<0>();
+    __syncthreads();
+    int32_t* sg = reinterpret_cast<int32_t*>(smem);
+    uint32_t* sh = reinterpret_cast<uint32_t*>(smem + H3_HH);
+    int32_t* sug = reinterpret_cast<int32_t*>(smem + H3_U_OFF);
+    uint32_t* suh = reinterpret_cast<uint32_t*>(smem + H3_U_OFF + kBins * 4);
+    if (ucol >= 0) {   // the users column's cells (never written by its lane) from the dense histogram
+      for (int b = tid; b < kBins; b += H3_THREADS) {
+        sg[b * 32 + ucol] = sug[b];
+        sh[b * 32 + ucol] = suh[b];
+        sug[b] = 0;
+        suh[b] = 0;
       }
       __syncthreads();
     }
-    if (MODE == HM_LEVEL && fold) {
+    // flush: zero-skipping int64 atomics into the node histogram ([f][b] layout)
+    for (int i = tid; i < kHistBins; i += H3_THREADS) {
+      const int32_t g = sg[i];
+      const uint32_t h = sh[i];
+      if (g != 0 || h != 0) {
+        const int b = i >> 5, f = i & 31;
+        atomicAdd(reinterpret_cast<unsigned long long*>(&Hg[f * kBins + b]), (unsigned long long)(long long)g);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&Hh[f * kBins + b]), (unsigned long long)h);
+        sg[i] = 0;
+        sh[i] = 0;
+      }
+    }
+    __syncthreads();
+    if (MODE == HM_LEVEL && fold && ns.pc != pc) {
       // this CTA's contribution to the piece is flushed: the CTA completing the count of CTAs that
       // cover the piece evaluates the split of the piece's parent
       const FitArgs& ap = fp.t[s_tg[pc]];
@@ -401,6 +462,7 @@ __global__ void __launch_bounds__(H3_THREADS, 1) k_hist3(const FitPair fp, const
         atomicExch(&fq[2 + slot], pc + 1);
       }
     }
+    cs = ns;
   }
   if (MODE == HM_LEVEL && fold) {
     // this CTA's histogram work is done: evaluate queued pieces until every non-empty piece is taken

@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B of several environment settings on the bench fit leg (interleaved, 2 rounds), after a parity subset
-#   bash tools/_ab_multi.sh NAME "PYTEST_K" "ENV_A" "ENV_B" ...
+#   bash tools/_ab_multi.sh NAME "PYTEST_K" "ENV_A" "ENV_B" ...   ("AB_ROOT=_abv/X": another build, tools/build_variant.sh)
 NAME=$1; K=$2; shift 2
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${NAME}_build.log 2>&1
@@ -8,7 +8,9 @@ if [ -n "$K" ]; then timeout 1200 python -m pytest tests/test_gpu_parity.py -q -
 rm -f gpurun_out/${NAME}_ab.txt
 for R in 1 2; do
 for E in "$@"; do
-  env $E timeout 600 python bench.py --steps 5 --warmup 3 --no-cv --no-c5 --no-rf --no-wg --no-cpu-baseline --no-e2e 2>gpurun_out/${NAME}_b.err | tail -1 > gpurun_out/${NAME}_b.json
+  B=bench.py
+  case "$E" in AB_ROOT=*) AR=${E#AB_ROOT=}; cp bench.py $AR/; ln -sfn $(pwd)/profiles $AR/profiles; B=$AR/bench.py;; esac
+  env $E timeout 600 python $B --steps 5 --warmup 3 --no-cv --no-c5 --no-rf --no-wg --no-cpu-baseline --no-e2e 2>gpurun_out/${NAME}_b.err | tail -1 > gpurun_out/${NAME}_b.json
   python - "$E" "$NAME" <<'PY' >> gpurun_out/${NAME}_ab.txt
 import json,sys
 try:

@@ -1,6 +1,7 @@
 #!/bin/bash
 # Build a variant of libllmpilot.so with extra nvcc flags for fit.cu into _abv/NAME (a package copy
-# that tools/ab_fit.py loads with AB_ROOT=_abv/NAME):  bash tools/build_variant.sh NAME "-DFOO=1 ..."
+# that tools/ab_fit.py loads with AB_ROOT=_abv/NAME):  bash tools/build_variant.sh NAME "-DFOO=1 ..." [GITREV]
+# (GITREV: take csrc/ from that commit instead of the working tree)
 set -e
 NAME=$1; FL=$2
 R=$(cd "$(dirname "$0")/.." && pwd)
@@ -9,9 +10,15 @@ mkdir -p $D/paper_2410_02425_b200/build
 cp $R/paper_2410_02425_b200/__init__.py $D/paper_2410_02425_b200/
 ln -sfn $R/synth $D/synth
 ln -sfn $R/oracle $D/oracle
+SRC=$R/paper_2410_02425_b200/csrc
+if [ -n "$3" ]; then
+  SRC=$D/paper_2410_02425_b200/csrc; rm -rf $SRC
+  (cd $R && git archive $3 paper_2410_02425_b200/csrc | tar -x -C $D)
+  ln -sfn $R/include $D/include
+fi
 NV=/usr/local/cuda/bin/nvcc
 $NV -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --fmad=false -Xcompiler -fPIC -I $R/include $FL \
-  -c $R/paper_2410_02425_b200/csrc/fit.cu -o $D/paper_2410_02425_b200/build/fit.o
+  -c $SRC/fit.cu -o $D/paper_2410_02425_b200/build/fit.o
 OBJS=$(ls $R/paper_2410_02425_b200/build/*.o | grep -v '/fit.o$')
 $NV -gencode arch=compute_100a,code=sm_100a -shared -o $D/paper_2410_02425_b200/libllmpilot.so $D/paper_2410_02425_b200/build/fit.o $OBJS -ldl
 echo built $D
