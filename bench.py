@@ -49,8 +49,9 @@ BYTES_PER_UNIT = {
     "partition": 9.0,     # row index read + 1 B split-feature code + row index written (the tile
                           # design reads the row index twice: 13 B moved, 9 B algorithmic)
     "hist_level": 40.0,   # 32 B code row + 4 B packed pair (both gathered by row index) + 4 B row index
-    "update": 52.0,       # fused update of tree t + root histogram of tree t+1 (k_hist<UPDROOT>):
-                          # 32 B code row + y, w, p read (12 B) + p and the packed pair written (8 B)
+    "update": 34.0,       # fused update of tree t + root histograms of trees t+1, BOTH ensembles in one
+                          # pass (k_hist2<UPDROOT, DUAL>), per row and ensemble: (32 B code row + w) / 2
+                          # + y, p read (8 B) + p and the packed pair written (8 B); 52 B with LLMP_DUAL=0
     "codes": 192.0,       # 128 B f32 row read + 32 B row-major + 32 B column-major codes written
 }
 
