@@ -1280,12 +1280,17 @@ __device__ __forceinline__ void parent_prefixes(const FitArgs& a, int d, int* s_
     tl[q] = 0;
     rl[q] = 0;
     if (j < NP) {
+      // every load unconditional (one round trip; the entries of parents that did not split are
+      // in bounds and ignored)
       const int f = P.split_f[j];
+      const int sb = P.split_b[j];
+      const int64_t st = (d == 1) ? 0 : P.start[j];
+      const int64_t ct = (d == 1) ? a.n : P.cnt[j];
       PartParent pp;
       pp.f = f;
-      pp.b = f >= 0 ? P.split_b[j] : 0;
-      pp.start = (d == 1) ? 0 : P.start[j];
-      pp.cnt = (f < 0) ? 0 : (d == 1) ? a.n : P.cnt[j];
+      pp.b = f >= 0 ? sb : 0;
+      pp.start = st;
+      pp.cnt = (f < 0) ? 0 : ct;
       s_pp[j] = pp;
       if (f >= 0) {
         rl[q] = pp.cnt;

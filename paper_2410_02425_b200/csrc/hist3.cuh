@@ -126,53 +126,72 @@ __global__ void __launch_bounds__(H3_THREADS, 1) k_hist3(const FitPair fp, const
   }
   // ---- piece list (virtual concatenation of the rows to histogram)
   if (MODE == HM_LEVEL) {
+    // both ensembles' parents at once (entry e = tg * NP + j; thread tid takes entries 2 tid and
+    // 2 tid + 1, E = ny * NP <= 2 * 512): every load is issued unconditionally, so the list costs one
+    // round trip to global memory and one block scan
     const int NP = 1 << (d - 1);
+    const int E = ny * NP;
     __shared__ int64_t s_wsum[H3_WARPS];
-    int64_t base = 0;
-    for (int tg = 0; tg < ny; ++tg) {
-      const FitArgs& a = fp.t[tg];
-      const LevelView& P = a.lv[d - 1];
-      const LevelView& C = a.lv[d];
-      int64_t len = 0, pst = 0;
-      int side_of = 0;
-      if (tid < NP && P.split_f[tid] >= 0) {
-        const int64_t nL = C.cnt[2 * tid], nR = C.cnt[2 * tid + 1];
-        const int side = a.built_by_h ? C.built[tid] : (nL <= nR) ? 0 : 1;   // smaller child (rows; hessian when sharded)
-        side_of = side;
-        len = C.cnt[2 * tid + side];
-        const int64_t ps = (d == 1) ? 0 : P.start[tid], cl = C.cnt[2 * tid];   // k_part: left child first
-        pst = side ? ps + cl : ps;
-        if (blockIdx.x == 0) {
-          C.built[tid] = side;
-          C.start[2 * tid] = ps;
-          C.start[2 * tid + 1] = ps + cl;
+    int64_t len2[2], pst2[2];
+    int side2[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int e = 2 * tid + q;
+      len2[q] = 0;
+      pst2[q] = 0;
+      side2[q] = 0;
+      if (e < E) {
+        const int tg = e >= NP ? 1 : 0, j = e - tg * NP;
+        const FitArgs& a = fp.t[tg];
+        const LevelView& P = a.lv[d - 1];
+        const LevelView& C = a.lv[d];
+        const int pf = P.split_f[j];
+        const int64_t nL = C.cnt[2 * j], nR = C.cnt[2 * j + 1];
+        const int bh = a.built_by_h ? C.built[j] : 0;
+        const int64_t ps = (d == 1) ? 0 : P.start[j];
+        if (pf >= 0) {
+          const int side = a.built_by_h ? bh : (nL <= nR) ? 0 : 1;   // smaller child (rows; hessian when sharded)
+          side2[q] = side;
+          len2[q] = side ? nR : nL;
+          pst2[q] = side ? ps + nL : ps;   // k_part: left child first
+          if (blockIdx.x == 0) {
+            C.built[j] = side;
+            C.start[2 * j] = ps;
+            C.start[2 * j + 1] = ps + nL;
+          }
         }
       }
-      int64_t v = len;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += u;
+    }
+    const int64_t mine = len2[0] + len2[1];
+    int64_t v = mine;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
+    }
+    if (lane == 31) s_wsum[warp] = v;
+    __syncthreads();
+    int64_t woff = 0, tot = 0;
+    for (int w2 = 0; w2 < H3_WARPS; ++w2) {
+      if (w2 < warp) woff += s_wsum[w2];
+      tot += s_wsum[w2];
+    }
+    int64_t ex = woff + v - mine;   // rows of the entries before 2 tid
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int e = 2 * tid + q;
+      if (e < E) {
+        const int tg = e >= NP ? 1 : 0;
+        s_vstart[e] = ex;
+        s_pstart[e] = pst2[q];
+        s_slot[e] = (int16_t)(e - tg * NP);
+        s_tg[e] = (int8_t)tg;
+        s_side[e] = (int8_t)side2[q];
       }
-      if (lane == 31) s_wsum[warp] = v;
-      __syncthreads();
-      int64_t woff = base, tot = base;
-      for (int w2 = 0; w2 < H3_WARPS; ++w2) {
-        if (w2 < warp) woff += s_wsum[w2];
-        tot += s_wsum[w2];
-      }
-      if (tid < NP) {
-        s_vstart[tg * NP + tid] = woff + v - len;
-        s_pstart[tg * NP + tid] = pst;
-        s_slot[tg * NP + tid] = (int16_t)tid;
-        s_tg[tg * NP + tid] = (int8_t)tg;
-        s_side[tg * NP + tid] = (int8_t)side_of;
-      }
-      base = tot;
-      __syncthreads();   // s_wsum is reused by the next ensemble
+      ex += len2[q];
     }
     if (tid == 0) {
-      s_vstart[ny * NP] = base;
-      s_np = ny * NP;
+      s_vstart[E] = tot;
+      s_np = E;
     }
   } else if (tid == 0) {
     s_np = 1;
