@@ -2518,6 +2518,21 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
       nccl_group_end(ctx);
       if (!fold) split(fp, ny, d);
     }
+    if (dual) {
+      // the dual update (after the join) accumulates tree t+1's root q_g into the root slot: reset it
+      // here, at the end of this ensemble's own branch (its last split has consumed the level-0 slot),
+      // so the reset overlaps the other branch instead of sitting between the join and the update.
+      // q_g channel zeroed, q_h channel = tree 0's (rank 0; zeros on the other ranks)
+      for (int q = 0; q < ny; ++q) {
+        if (!sharded || ctx->rank == 0) {
+          LLMP_CUDA(cudaMemsetAsync(fp.t[q].H[0], 0, (size_t)kHistBins * 8, st));
+          LLMP_CUDA(cudaMemcpyAsync(fp.t[q].H[0] + kHistBins, fp.t[q].hroot, (size_t)kHistBins * 8,
+                                    cudaMemcpyDeviceToDevice, st));
+        } else {
+          LLMP_CUDA(cudaMemsetAsync(fp.t[q].H[0], 0, (size_t)SLOT * 8, st));
+        }
+      }
+    }
     // RF: tree t+1's bootstrap weights, read by the update's gradients (and the next root rebuild)
     if (rf) LLMP_LAUNCH_PDL(ctx, KC_MISC, ny * n, k_rf_weights, dim3(rfw_grid, ny), 256, 0, fp, 1);
     if (fused && !dual) {   // update tree t + root histogram of tree t+1 (into the now free root slot)
@@ -2543,17 +2558,7 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   };
   // dual: the update of tree t + root histograms of trees t+1 of BOTH ensembles, one pass over the rows
   // (after both ensembles' levels: the branches have joined)
-  auto dual_update = [&]() {
-    const cudaStream_t st = ctx->stream;
-    for (int q = 0; q < 2; ++q) {   // q_g channel zeroed, q_h channel = tree 0's (rank 0; zeros elsewhere)
-      if (!sharded || ctx->rank == 0) {
-        LLMP_CUDA(cudaMemsetAsync(FP.t[q].H[0], 0, (size_t)kHistBins * 8, st));
-        LLMP_CUDA(cudaMemcpyAsync(FP.t[q].H[0] + kHistBins, FP.t[q].hroot, (size_t)kHistBins * 8,
-                                  cudaMemcpyDeviceToDevice, st));
-      } else {
-        LLMP_CUDA(cudaMemsetAsync(FP.t[q].H[0], 0, (size_t)SLOT * 8, st));
-      }
-    }
+  auto dual_update = [&]() {   // (the root slots were reset at the end of each branch)
     const dim3 hg1((unsigned)std::min<int64_t>(ctx->sms * 2, std::max<int64_t>(1, (n + 2047) / 2048)), 1);
     LLMP_LAUNCH_PDL(ctx, KC_UPDATE, 2 * n, k_upd2d, hg1, H2_THREADS, H2_SMEM + updroot_tree_smem(D), FP, 0, 0, nodbg);
   };
