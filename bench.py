@@ -263,11 +263,13 @@ def bench_c5(lp, ctx, stream, dev, args, rank, world):
                         " depth 6), LLMs split over %d rank(s), per-LLM results all-gathered" %
                         (n_total, pf.shape[0], len(levels), total_rows, world),
             "value": total_rows / (ms / 1000.0), "unit": "rows/s", "ms_per_step": ms, "rows": total_rows,
-            "rows_per_rank": rows, "node_visits_per_s": visits / (ms / 1000.0),
+            "rows_per_rank": rows, "row_node_visits_per_s": visits / (ms / 1000.0),
             "recommend_call_ms": call_ms,
-            "node_visits_per_row": 2 * 1000 * 6,
+            "row_node_visits_per_row": 2 * 1000 * 6,
             "note": "the predictor routes on bin codes through fixed-depth trees: SM-issue bound, not HBM "
-                    "(DESIGN.md §6); node visits/s against the issue-rate bound there"}
+                    "(DESIGN.md §6). With <= 32 user levels the grid predictor walks each tree once per "
+                    "(LLM, profile) pair carrying the set of levels, so row_node_visits_per_s counts the "
+                    "per-row definition's visits (2 x 1000 x 6 per row), not the walks executed"}
 
 
 def bench_rf_traces(lp, ctx, stream, dev, args):

@@ -116,6 +116,108 @@ __global__ void __launch_bounds__(PC_THREADS) k_predict(const PredArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Recommendation grid predictor: the rows of a sweep are the Cartesian product
+// (LLM i) x (profile g) x (user level lv), and within one (i, g) pair only the users column varies.
+// The user levels are strictly increasing (the API requires it), so their codes are non-decreasing
+// and a split "users code <= b" sends exactly the levels lv < t_b left, t_b = #{lv : code_lv <= b}:
+// the levels that reach any node form a contiguous range.  One thread per (pair, ensemble) walks
+// each tree once per distinct leaf: starting from the lowest level not yet placed, lo, it descends
+// with the range [lo, hi) (a split on another feature sends the whole range the pair's way; a users
+// split narrows hi to t_b when lo < t_b and goes left, else goes right), adds the leaf value to
+// levels lo .. hi-1 and continues from lo = hi.  Every row still gets base + its leaf values in tree
+// order with one fp32 rounding per tree: the same bits as k_predict.
+constexpr int PG_THREADS = 128;
+constexpr int PG_TREE_SMEM = 24576;
+__host__ __device__ constexpr int pg_smem(int nl) {
+  return PG_THREADS * PC_RSTRIDE + 256 + nl * PG_THREADS * 4 + PG_TREE_SMEM;
+}
+
+template <int DC>
+__global__ void __launch_bounds__(PG_THREADS) k_predict_grid(const PredArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint8_t* rows = smem;                                     // the pairs' codes
+  uint8_t* lvt = smem + PG_THREADS * PC_RSTRIDE;            // [256] t_b = #{lv : code_lv <= b}
+  float* acc = reinterpret_cast<float*>(lvt + 256);         // [n_levels][PG_THREADS]
+  const int NL = a.n_levels;
+  uint8_t* tabs = reinterpret_cast<uint8_t*>(acc + NL * PG_THREADS);
+  const int tid = threadIdx.x, target = blockIdx.y;
+  const int D = DC ? DC : a.D;
+  const int tb = rtab_bytes(a.D), tin = rtab_inner_bytes(a.D);
+  const int n_int = (1 << a.D) - 1;
+  const int trees_per_chunk = max(1, PG_TREE_SMEM / tb);
+  const int ucol = a.users_col;
+  for (int b = tid; b < 256; b += PG_THREADS) {
+    int t = 0;
+    for (int lv = 0; lv < NL; ++lv) t += a.level_codes[lv] <= b ? 1 : 0;
+    lvt[b] = (uint8_t)t;
+  }
+  const int64_t npairs = a.n / NL;
+  const int FP = a.F_llm + a.F_prof;
+  const float base = target ? a.base1 : a.base0;
+  const uint8_t* tt = a.rtab + (size_t)target * a.T * tb;
+  for (int64_t p0 = (int64_t)blockIdx.x * PG_THREADS; p0 < npairs; p0 += (int64_t)gridDim.x * PG_THREADS) {
+    const int np = (int)min((int64_t)PG_THREADS, npairs - p0);
+    __syncthreads();   // previous pass done with the staged pairs and the accumulators
+    for (int e = tid; e < np * FP; e += PG_THREADS) {   // LLM features, then profile features
+      const int r = e / FP, f = e - r * FP;
+      const int64_t pr = p0 + r;
+      const int64_t i = pr / a.n_prof;
+      const int g = (int)(pr - i * a.n_prof);
+      rows[r * PC_RSTRIDE + f] =
+          f < a.F_llm ? a.llm_codes[i * a.F_llm + f] : a.prof_codes[(int64_t)g * a.F_prof + (f - a.F_llm)];
+    }
+    for (int lv = 0; lv < NL; ++lv) acc[lv * PG_THREADS + tid] = base;
+    const uint8_t* myrow = rows + tid * PC_RSTRIDE;
+    float* myacc = acc + tid;
+    for (int c0 = 0; c0 < a.T; c0 += trees_per_chunk) {
+      const int nt = min(trees_per_chunk, a.T - c0);
+      __syncthreads();
+      if ((tb & 15) == 0) {
+        const uint4* src = reinterpret_cast<const uint4*>(tt + (size_t)c0 * tb);
+        for (int e = tid; e < nt * tb / 16; e += PG_THREADS) reinterpret_cast<uint4*>(tabs)[e] = __ldg(src + e);
+      } else {
+        const uint32_t* s4 = reinterpret_cast<const uint32_t*>(tt + (size_t)c0 * tb);
+        for (int e = tid; e < nt * tb / 4; e += PG_THREADS) reinterpret_cast<uint32_t*>(tabs)[e] = __ldg(s4 + e);
+      }
+      __syncthreads();
+      if (tid < np) {
+        for (int kk = 0; kk < nt; ++kk) {
+          const uint16_t* inode = reinterpret_cast<const uint16_t*>(tabs + kk * tb);
+          const float* lval = reinterpret_cast<const float*>(tabs + kk * tb + tin);
+          int lo = 0;
+          do {   // one descent per distinct leaf, levels in increasing order
+            int hi = NL, k = 0;
+#pragma unroll
+            for (int s2 = 0; s2 < (DC ? DC : kMaxDepth); ++s2)
+              if (DC || s2 < D) {
+                const uint32_t w = inode[k];
+                const uint32_t f = w & 0xffu, b = w >> 8;
+                bool right;
+                if ((int)f == ucol) {   // levels < t_b go left
+                  const int t = lvt[b];
+                  right = lo >= t;
+                  if (!right) hi = min(hi, t);
+                } else {
+                  right = (uint32_t)myrow[f] > b;   // code <= b  <=>  left
+                }
+                k = 2 * k + 1 + (right ? 1 : 0);
+              }
+            const float v = lval[k - n_int];
+            for (int lv = lo; lv < hi; ++lv) myacc[lv * PG_THREADS] = __fadd_rn(myacc[lv * PG_THREADS], v);
+            lo = hi;
+          } while (lo < NL);
+        }
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < np * NL; e += PG_THREADS) {   // row (p0 + r) * NL + lv, rows consecutive
+      const int r = e / NL, lv = e - r * NL;
+      a.out[((p0 + r) * NL + lv) * 2 + target] = acc[lv * PG_THREADS + r];
+    }
+  }
+}
+
 // Device routing tables (see the header comment): per tree the 2^D - 1 node words of the slots above
 // depth D — a split {f, b}, or {0, 255} ("always left") for a leaf and everything below it — then
 // the 2^D leaf values: a leaf k at depth d < D is reached at its leftmost depth-D descendant
@@ -167,6 +269,21 @@ static void launch_predict(Ctx* ctx, const PredArgs& a, bool assemble, int cls) 
   if (dct && a.D == 8) launch_predict_r<4, 8>(ctx, a, assemble, cls);
   else if (dct && a.D == 6) launch_predict_r<4, 6>(ctx, a, assemble, cls);
   else launch_predict_r<4, 0>(ctx, a, assemble, cls);
+}
+
+template <int DC>
+static void launch_predict_grid_d(Ctx* ctx, const PredArgs& a, int64_t npairs) {
+  ensure_smem_attr((const void*)k_predict_grid<DC>, pg_smem(64));
+  const int smem = pg_smem(a.n_levels);
+  const int per_sm = std::max(1, (int)(220000 / (smem + 1024)));
+  const int gx = (int)std::min<int64_t>(std::max<int64_t>((npairs + PG_THREADS - 1) / PG_THREADS, 1),
+                                        (int64_t)ctx->sms * per_sm);
+  LLMP_LAUNCH(ctx, KC_PREDICT, a.n, k_predict_grid<DC>, dim3(gx, 2), PG_THREADS, smem, a);
+}
+static void launch_predict_grid(Ctx* ctx, const PredArgs& a, int64_t npairs) {
+  if (a.D == 8) launch_predict_grid_d<8>(ctx, a, npairs);
+  else if (a.D == 6) launch_predict_grid_d<6>(ctx, a, npairs);
+  else launch_predict_grid_d<0>(ctx, a, npairs);
 }
 
 // codes of a small table whose columns are the model's features col0 .. col0 + ncols - 1
@@ -322,7 +439,11 @@ void recommend_impl(Ctx* ctx, const ModelData& m, const float* llm_feats, int n_
   a.n_levels = n_levels;
   a.users_col = m.users_col;
   a.out = pred;
-  if (n > 0) launch_predict(ctx, a, true, KC_PREDICT);
+  // the grid predictor (tree walks per (LLM, profile) pair, one per distinct leaf) for up to 64 user
+  // levels; LLMP_PRED_GRID=0 keeps the per-row walk
+  static const bool grid_env = !(getenv("LLMP_PRED_GRID") && atoi(getenv("LLMP_PRED_GRID")) == 0);
+  if (n > 0 && grid_env && n_levels <= 64) launch_predict_grid(ctx, a, (int64_t)n_llm * n_prof);
+  else if (n > 0) launch_predict(ctx, a, true, KC_PREDICT);
   argmin_impl(ctx, pred, n_llm, n_prof, n_levels, levels, cost, allowed, L1, L2, U, out);
 }
 

@@ -421,6 +421,40 @@ def test_predict_and_recommend_parity(lp, ctx):
     assert any(r[0] == -1 for r in grec2) or True
 
 
+@pytest.mark.parametrize("depth,levels_kind", [(6, "sorted16"), (7, "sparse16"), (6, "one"), (8, "sorted32"),
+                                               (6, "sorted64"), (6, "sorted70")])
+def test_recommend_grid_predictor_cases(lp, ctx, depth, levels_kind):
+    """The recommend sweep's predictions (per (LLM, profile) pair, one tree descent per distinct leaf
+    carrying the range of user levels, n_levels <= 64; the per-row walk beyond) equal the oracle's
+    predictions of the assembled rows bit for bit, and so do the recommendations: the C5 levels, 16
+    widely spaced levels, a single level, 32 and 64 levels, 70 levels (per-row fallback), compile-time
+    (6, 8) and run-time (7) depths."""
+    d = synth.make("C2")
+    om, otp, gm = _fit_both(lp, ctx, d, n_trees=25, max_depth=depth)
+    lf, pf, cost, lv16 = synth.sweep_tables(n_llm=211, seed=3)
+    rng = np.random.default_rng(depth)
+    if levels_kind == "sorted16":
+        levels = lv16
+    elif levels_kind == "sparse16":
+        levels = np.array([1, 3, 7, 12, 20, 33, 50, 64, 90, 128, 180, 256, 400, 512, 800, 1024], np.int32)
+    elif levels_kind == "one":
+        levels = np.array([8], np.int32)
+    else:
+        k = int(levels_kind[len("sorted"):])
+        levels = np.unique(rng.integers(1, 300, 4 * k))[:k].astype(np.int32)
+        assert len(levels) == k
+    nL, nP, nU = lf.shape[0], pf.shape[0], len(levels)
+    rows = np.concatenate([np.repeat(lf, nP * nU, axis=0), np.tile(np.repeat(pf, nU, axis=0), (nL, 1)),
+                           np.tile(levels.astype(np.float32), nL * nP)[:, None]], axis=1)
+    op = oracle.predict(om, rows)
+    orec = oracle.recommend(op.reshape(nL, nP, nU, 2), levels, cost, L1, L2, U)
+    pred_out = torch.zeros((nL * nP * nU, 2), dtype=torch.float32, device="cuda")
+    grec = lp.recommend(ctx, gm, torch.from_numpy(lf).cuda(), torch.from_numpy(pf).cuda(), cost, levels, L1, L2, U,
+                        pred_out=pred_out)
+    assert _bits_equal(pred_out.cpu().numpy(), op)
+    assert grec == orec
+
+
 def test_model_save_load_round_trip(lp, ctx, tmp_path):
     """llmpilot_model_save / llmpilot_model_load: the loaded model exports, predicts, ranks features
     and recommends exactly as the fitted one (and as the oracle); malformed files are refused."""
