@@ -127,8 +127,14 @@ __global__ void __launch_bounds__(PC_THREADS) k_predict(const PredArgs a) {
 // split narrows hi to t_b when lo < t_b and goes left, else goes right), adds the leaf value to
 // levels lo .. hi-1 and continues from lo = hi.  Every row still gets base + its leaf values in tree
 // order with one fp32 rounding per tree: the same bits as k_predict.
-constexpr int PG_THREADS = 128;
-constexpr int PG_TREE_SMEM = 24576;
+#ifndef LLMP_PG_THREADS
+#define LLMP_PG_THREADS 128
+#endif
+#ifndef LLMP_PG_TREE_SMEM
+#define LLMP_PG_TREE_SMEM 24576
+#endif
+constexpr int PG_THREADS = LLMP_PG_THREADS;
+constexpr int PG_TREE_SMEM = LLMP_PG_TREE_SMEM;
 __host__ __device__ constexpr int pg_smem(int nl) {
   return PG_THREADS * PC_RSTRIDE + 256 + nl * PG_THREADS * 4 + PG_TREE_SMEM;
 }

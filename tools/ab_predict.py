@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def child():
-    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.environ.get("AB_ROOT", ROOT))   # AB_ROOT: another build (tools/build_variant.sh)
     import torch
 
     import paper_2410_02425_b200 as lp

@@ -17,8 +17,12 @@ if [ -n "$3" ]; then
   ln -sfn $R/include $D/include
 fi
 NV=/usr/local/cuda/bin/nvcc
-$NV -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --fmad=false -Xcompiler -fPIC -I $R/include $FL \
-  -c $SRC/fit.cu -o $D/paper_2410_02425_b200/build/fit.o
-OBJS=$(ls $R/paper_2410_02425_b200/build/*.o | grep -v '/fit.o$')
-$NV -gencode arch=compute_100a,code=sm_100a -shared -o $D/paper_2410_02425_b200/libllmpilot.so $D/paper_2410_02425_b200/build/fit.o $OBJS -ldl
+# every translation unit with the variant's flags (in parallel)
+for CU in $SRC/*.cu; do
+  B=$(basename $CU .cu)
+  $NV -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --fmad=false -Xcompiler -fPIC -I $R/include $FL \
+    -c $CU -o $D/paper_2410_02425_b200/build/$B.o &
+done
+wait
+$NV -gencode arch=compute_100a,code=sm_100a -shared -o $D/paper_2410_02425_b200/libllmpilot.so $D/paper_2410_02425_b200/build/*.o -ldl
 echo built $D
