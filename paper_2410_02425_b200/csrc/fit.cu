@@ -1583,8 +1583,10 @@ __device__ __forceinline__ bool split_feature(const FitArgs& a, const int d, con
         g8[2 * q + 1] = pg[q].y - bg2[q].y;
         h8[2 * q] = ph[q].x - bh2[q].x;
         h8[2 * q + 1] = ph[q].y - bh2[q].y;
-        Hs[eg0 + q] = make_longlong2(g8[2 * q], g8[2 * q + 1]);
-        Hs[eh0 + q] = make_longlong2(h8[2 * q], h8[2 * q + 1]);
+        if (d + 1 < a.D) {   // (kept for the next level's sibling subtraction; the last level's is not)
+          Hs[eg0 + q] = make_longlong2(g8[2 * q], g8[2 * q + 1]);
+          Hs[eh0 + q] = make_longlong2(h8[2 * q], h8[2 * q + 1]);
+        }
       }
     }
   }
