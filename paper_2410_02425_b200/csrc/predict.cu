@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(PC_THREADS) k_predict(const PredArgs a) {
 #define LLMP_PG_THREADS 128
 #endif
 #ifndef LLMP_PG_TREE_SMEM
-#define LLMP_PG_TREE_SMEM 24576
+#define LLMP_PG_TREE_SMEM 16384
 #endif
 constexpr int PG_THREADS = LLMP_PG_THREADS;
 constexpr int PG_TREE_SMEM = LLMP_PG_TREE_SMEM;
@@ -197,16 +197,15 @@ __global__ void __launch_bounds__(PG_THREADS) k_predict_grid(const PredArgs a) {
 #pragma unroll
             for (int s2 = 0; s2 < (DC ? DC : kMaxDepth); ++s2)
               if (DC || s2 < D) {
+                // branch-free: every split is "levels below t go left" — t = t_b on the users column,
+                // else NL (the pair's code <= b: the whole range left) or 0 (all right)
                 const uint32_t w = inode[k];
                 const uint32_t f = w & 0xffu, b = w >> 8;
-                bool right;
-                if ((int)f == ucol) {   // levels < t_b go left
-                  const int t = lvt[b];
-                  right = lo >= t;
-                  if (!right) hi = min(hi, t);
-                } else {
-                  right = (uint32_t)myrow[f] > b;   // code <= b  <=>  left
-                }
+                const int tu = lvt[b];
+                const int tc = (uint32_t)myrow[f] <= b ? NL : 0;
+                const int t = (int)f == ucol ? tu : tc;
+                const bool right = lo >= t;
+                hi = right ? hi : min(hi, t);
                 k = 2 * k + 1 + (right ? 1 : 0);
               }
             const float v = lval[k - n_int];

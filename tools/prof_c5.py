@@ -2,7 +2,7 @@
 recommendation over 6,554 unseen LLMs x 10 profiles x 16 levels; per-kernel-class event timings.
     python tools/prof_c5.py [--reps 3]"""
 import argparse, json, os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.environ.get("AB_ROOT", os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import paper_2410_02425_b200 as lp
 import synth
