@@ -422,7 +422,7 @@ def test_predict_and_recommend_parity(lp, ctx):
 
 
 @pytest.mark.parametrize("depth,levels_kind", [(6, "sorted16"), (7, "sparse16"), (6, "one"), (8, "sorted32"),
-                                               (6, "sorted64"), (6, "sorted70")])
+                                               (6, "sorted64"), (6, "sorted70"), (10, "sorted16"), (1, "sparse16")])
 def test_recommend_grid_predictor_cases(lp, ctx, depth, levels_kind):
     """The recommend sweep's predictions (per (LLM, profile) pair, one tree descent per distinct leaf
     carrying the range of user levels, n_levels <= 64; the per-row walk beyond) equal the oracle's
