@@ -2453,10 +2453,15 @@ void fit_impl(Ctx* ctx, const DatasetDev& ds, const llmpilot_hparams& hp, float 
   FP.t[0] = A[0];
   FP.t[1] = A[1];
   static const bool split_cluster = split_cluster_env();
+  // diagnostic (LLMP_SPLIT_TWICE=1): every split launch is issued twice — result-neutral (the second
+  // launch recomputes the same decisions from the same histograms), so the step-time difference is the
+  // marginal cost of the split launches inside the graph
+  static const bool split_twice = getenv("LLMP_SPLIT_TWICE") && atoi(getenv("LLMP_SPLIT_TWICE")) != 0;
   auto split = [&](const FitPair& fp, int ny, int d) {
     const dim3 grid((1 << d) * SP3_CLUSTER, ny);
     if (!split_cluster) {
       LLMP_LAUNCH_PDL(ctx, KC_SPLIT, ny << d, k_split3<false>, grid, SP3_WARPS * 32, 0, fp, d);
+      if (split_twice) LLMP_LAUNCH_PDL(ctx, KC_SPLIT, ny << d, k_split3<false>, grid, SP3_WARPS * 32, 0, fp, d);
       return;
     }
     cudaLaunchConfig_t cfg = {};
