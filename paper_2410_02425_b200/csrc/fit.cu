@@ -1838,6 +1838,7 @@ __global__ void __launch_bounds__(SP3_WARPS * 32) k_split3(const FitPair fp, con
   split_node(a, d, k, lane, rvalid, rb, rloss, rGL, rHL, rG, rH, &ns);
 }
 
+
 #include "hist3.cuh"
 
 using Upd3Kernel = void (*)(const FitPair);

@@ -270,7 +270,8 @@ def _exponent_changes(om, d):
                                  "LLMP_HIST2=0", "LLMP_HIST2=7",
                                  "LLMP_PAIRED=1", "LLMP_GRAPH_REPLAY=1", "LLMP_HIST_SWAR=0", "LLMP_PRED_DC=0", "LLMP_PDL=0",
                                  "LLMP_LEVEL=1", "LLMP_LEVEL=2", "LLMP_UPD=3", "LLMP_PAIRED=1 LLMP_UPD=3", "LLMP_FOLD=1", "LLMP_FOLD=1 LLMP_PAIRED=1", "LLMP_HFIX=0",
-                                 "LLMP_DUAL=0", "LLMP_DUAL=0 LLMP_PAIRED=1", "LLMP_GRAPH_REPLAY=1 LLMP_PAIRED=1"])
+                                 "LLMP_DUAL=0", "LLMP_DUAL=0 LLMP_PAIRED=1", "LLMP_GRAPH_REPLAY=1 LLMP_PAIRED=1",
+                                 "LLMP_SPLIT_TWICE=1"])
 def test_kernel_variants(lp, env):
     """Every selectable kernel variant gives the oracle's models (own process: the switches are
     read once per process)."""
