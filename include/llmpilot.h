@@ -147,7 +147,9 @@ void llmpilot_hparams_default(llmpilot_hparams* hp); /* n_trees 100, depth 6, bi
                                                          seed 0, eq4 1, monotone 1, model 0 (GBDT),
                                                          max_features 1, rf_bootstrap 1, tree_method 0 */
 
-/* Quantile binning: per-feature cuts from a deterministic strided sample of at
+/* Quantile binning for the histogram tree method ("the number of bins for the histogram
+ * tree method" is one of the tuned HPs; the exact method's cuts are every distinct value; DESIGN.md
+ * R14, oracle O2): per-feature cuts from a deterministic strided sample of at
  * most 2^20 rows, then code(x) = #{cuts <= x}.  X: n x F (host or device).  cuts_in != NULL
  * reuses existing cuts; else cuts are computed from X and returned in *cuts_out (may be NULL).
  * codes_out: caller-owned DEVICE buffer of n x 32 bytes (row-major, features >= F padded with
