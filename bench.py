@@ -267,8 +267,8 @@ def bench_c5(lp, ctx, stream, dev, args, rank, world):
             "recommend_call_ms": call_ms,
             "row_node_visits_per_row": 2 * 1000 * 6,
             "note": "the predictor routes on bin codes through fixed-depth trees: SM-issue bound, not HBM "
-                    "(DESIGN.md §6). With <= 32 user levels the grid predictor walks each tree once per "
-                    "(LLM, profile) pair carrying the set of levels, so row_node_visits_per_s counts the "
+                    "(DESIGN.md §6). With <= 64 user levels the grid predictor walks each tree once per "
+                    "(LLM, profile) pair carrying the range of levels, so row_node_visits_per_s counts the "
                     "per-row definition's visits (2 x 1000 x 6 per row), not the walks executed"}
 
 
