@@ -611,7 +611,7 @@ def main():
         h1 = time.perf_counter()
         if record is not None:
             e1.record(stream)
-        recs = lp.recommend(ctx, m, lfx, pfx, cost, levels, L1, L2, U)
+        recs = lp.recommend(ctx, m, lfx, pfx, cost, levels, L1, L2, U, as_array=True)   # one structured copy, not a Python list
         h2 = time.perf_counter()
         if record is not None:
             e2.record(stream)

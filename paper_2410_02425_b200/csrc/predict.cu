@@ -427,7 +427,10 @@ void recommend_impl(Ctx* ctx, const ModelData& m, const float* llm_feats, int n_
                 c_prof.as<uint8_t>(), flag.as<int>());
   LLMP_LAUNCH(ctx, KC_RECOMMEND, 0, k_table_codes, 1, 256, 0, d_lvf.as<float>(), (int64_t)n_levels, 1, m.users_col, cuts,
               ncuts, c_lv.as<uint8_t>(), flag.as<int>());
-  check_flag(ctx, flag, "feature tables hold a non-finite value");
+  // a caller's device pred_out must not be written on bad input: check before predicting; otherwise the
+  // check rides on argmin's final synchronisation (one host round trip less; no output leaves on error)
+  const bool early_check = pred_out_dev != nullptr;
+  if (early_check) check_flag(ctx, flag, "feature tables hold a non-finite value");
   PredArgs a{};
   a.rtab = m.d_nodes.as<uint8_t>();
   a.T = m.T;
@@ -450,6 +453,7 @@ void recommend_impl(Ctx* ctx, const ModelData& m, const float* llm_feats, int n_
   if (n > 0 && grid_env && n_levels <= 64) launch_predict_grid(ctx, a, (int64_t)n_llm * n_prof);
   else if (n > 0) launch_predict(ctx, a, true, KC_PREDICT);
   argmin_impl(ctx, pred, n_llm, n_prof, n_levels, levels, cost, allowed, L1, L2, U, out);
+  if (!early_check) check_flag(ctx, flag, "feature tables hold a non-finite value");
 }
 
 }  // namespace llmp
