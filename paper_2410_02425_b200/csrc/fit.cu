@@ -2068,11 +2068,26 @@ __global__ void k_validate(const float* X, const float* y, const int32_t* llm, c
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     bool bad = !isfinite(y[2 * i]) || !isfinite(y[2 * i + 1]);
     if (w && !(isfinite(w[i]) && w[i] >= 0.0f)) bad = true;   // explicit weights: finite and >= 0
-    for (int f = 0; f < F; ++f) bad |= !isfinite(X[i * F + f]);
     if (llm && (llm[i] < 0 || llm[i] >= n_llm)) bad = true;
     if (prof && (prof[i] < 0 || prof[i] >= n_prof)) bad = true;
     if (bad) atomicOr(flag, 1);
   }
+  // X as one flat array of n * F floats, coalesced 16-byte loads (X is cudaMalloc'ed or a torch
+  // tensor: 16-byte aligned when its base is; a scalar head and tail otherwise)
+  const int64_t m = n * (int64_t)F;
+  const int64_t head = (int64_t)((16 - (reinterpret_cast<uintptr_t>(X) & 15)) & 15) / 4;
+  const int64_t h = min(head, m);
+  const int64_t nv = (m - h) / 4;
+  const float4* X4 = reinterpret_cast<const float4*>(X + h);
+  bool badx = false;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nv; e += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldg(X4 + e);
+    badx |= !(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w));
+  }
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gt < h && !isfinite(X[gt])) badx = true;                    // unaligned head
+  if (gt < m - h - 4 * nv && !isfinite(X[h + 4 * nv + gt])) badx = true;   // tail
+  if (badx) atomicOr(flag, 1);
 }
 
 __global__ void k_weights_max(const float* y, const int32_t* llm, const int32_t* prof, int64_t n, int n_prof, double L1,

@@ -625,6 +625,29 @@ def test_errors(lp, ctx):
     with pytest.raises(lp.LLMPilotError, match="EINVAL"):
         lp.fit(ctx, d.X, d.y, lp.hparams(n_trees=2, grad_bits=15), d.users_col, d.llm_id, d.prof_id, d.n_llm,
                d.n_prof)
+    # a non-finite value anywhere in X (first, last, an inner element; X viewed flat by the validation
+    # kernel), from host and from a device tensor at an odd offset (unaligned base)
+    for pos, val in (((0, 0), np.inf), ((d.X.shape[0] - 1, d.X.shape[1] - 1), np.nan), ((17, 5), -np.inf)):
+        Xb = d.X.copy()
+        Xb[pos] = val
+        with pytest.raises(lp.LLMPilotError, match="EINVAL"):
+            lp.fit(ctx, Xb, d.y, lp.hparams(n_trees=2), d.users_col, d.llm_id, d.prof_id, d.n_llm, d.n_prof)
+    big = torch.from_numpy(np.concatenate([np.zeros(1, np.float32), d.X.ravel()])).cuda()
+    Xoff = big[1:].view(d.X.shape)   # 4-byte offset from a 16-byte aligned allocation
+    Xoff_bad = Xoff.clone()[:, :]
+    m_ok = lp.fit(ctx, Xoff, torch.from_numpy(d.y).cuda(), lp.hparams(n_trees=2, max_depth=2), d.users_col,
+                  torch.from_numpy(d.llm_id).cuda(), torch.from_numpy(d.prof_id).cuda(), d.n_llm, d.n_prof)
+    m_ok.free()
+    big[-1] = float("nan")   # the last element of the unaligned view (the scalar tail)
+    with pytest.raises(lp.LLMPilotError, match="EINVAL"):
+        lp.fit(ctx, Xoff, torch.from_numpy(d.y).cuda(), lp.hparams(n_trees=2), d.users_col,
+               torch.from_numpy(d.llm_id).cuda(), torch.from_numpy(d.prof_id).cuda(), d.n_llm, d.n_prof)
+    big[-1] = 0.0
+    big[1] = float("inf")    # the first element (the scalar head)
+    with pytest.raises(lp.LLMPilotError, match="EINVAL"):
+        lp.fit(ctx, Xoff, torch.from_numpy(d.y).cuda(), lp.hparams(n_trees=2), d.users_col,
+               torch.from_numpy(d.llm_id).cuda(), torch.from_numpy(d.prof_id).cuda(), d.n_llm, d.n_prof)
+    del Xoff_bad
     bad = d.llm_id.copy()
     bad[0] = 99
     with pytest.raises(lp.LLMPilotError, match="EINVAL"):
